@@ -1,0 +1,176 @@
+/* include/tgs.h — C ABI of the B200-native TensorGS forward render path (libtgs.so).
+ *
+ * This is the drop-in boundary for the reference's render entry point
+ *   gsr::render(const std::vector<Gaussian3D>&, const Camera&, const RenderOptions&)
+ *     (reference: proj/include/gsr/render.hpp:30-31, proj/src/render.cpp:7-35)
+ * and its stage API (project_scene projection.hpp:48-50, build_group_entries/sort_entries
+ * binning.hpp:68-73, rasterize_tiles_scalar raster_scalar.hpp:59-62, rasterize_groups_tensor
+ * raster_tensor.hpp:62-65).  Plain pointers and sizes only: no C++ or torch types cross it.
+ * The C++ drop-in (cpp/gsr_render_b200.cpp) and the Python mirror (paper_2605_17855_b200/gsr.py)
+ * both sit on top of these entry points; INTEGRATION.md shows the bindings.
+ *
+ * Every entry point returns a tgs_status; on failure tgs_last_error() describes it.  Status
+ * codes map onto the reference's exception types: VALIDATION -> gsr::ValidationError,
+ * FORMAT -> gsr::FormatError (types.hpp:14-21); CUDA / OOM have no reference counterpart.
+ *
+ * Threading: a tgs_ctx owns one CUDA device and one stream; use a context from one host thread
+ * at a time.  Contexts on different devices run concurrently (multi-GPU camera batches and
+ * screen bands).  There is no CPU fallback: without a usable sm_100
+ * device tgs_ctx_create fails with TGS_ERR_CUDA.
+ */
+#ifndef TGS_H
+#define TGS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TGS_ABI_VERSION 1
+
+typedef enum {
+    TGS_OK = 0,
+    TGS_ERR_VALIDATION = 1, /* gsr::ValidationError */
+    TGS_ERR_FORMAT = 2,     /* gsr::FormatError */
+    TGS_ERR_CUDA = 3,
+    TGS_ERR_OOM = 4
+} tgs_status;
+
+/* gsr::Backend (render.hpp:8) */
+enum { TGS_BACKEND_SCALAR = 0, TGS_BACKEND_TENSOR = 1 };
+/* gsr::PrecisionMode (operands.hpp:13) */
+enum { TGS_MODE_FP32 = 0, TGS_MODE_FP16 = 1 };
+
+/* gsr::Camera (types.hpp:36-49): view is the row-major 4x4 world->camera transform,
+ * view[r*4 + c] == Camera::view(r, c). */
+typedef struct {
+    float view[16];
+    float focal_x, focal_y;
+    int32_t width, height;
+    float near_, far_;
+} tgs_camera;
+
+/* gsr::RenderOptions (render.hpp:10-17) + RasterConstants (raster_scalar.hpp:14-18).
+ * backend: TGS_BACKEND_SCALAR runs the CUDA-core baseline rasterizer (requires group_size 1,
+ * like raster_scalar.cpp:56-57); TGS_BACKEND_TENSOR runs the tcgen05 grouped rasterizer.
+ * mode: both modes run the FP16 hi/lo monomial contraction; the
+ * reference's emulated fp16 operand quantisation is not reproduced.  workers and chunk_len are
+ * accepted for source compatibility; the image does not depend on either (the reference pins
+ * both invariances: acceptance.cpp:227-238, :359-382). */
+typedef struct {
+    int32_t backend;
+    int32_t mode;
+    int32_t group_size; /* 1, 2 or 4 */
+    int32_t workers;    /* >= 1, ignored */
+    int32_t chunk_len;  /* accepted, ignored */
+    float alpha_skip;   /* 1/255 */
+    float alpha_clamp;  /* 0.99 */
+    float t_terminate;  /* 1e-4 */
+} tgs_options;
+
+/* RenderResult counters (render.hpp:19-25) + per-stage device times. */
+typedef struct {
+    uint64_t input, culled, dropped_degenerate; /* ProjectionStats (projection.hpp:40-44) */
+    uint64_t entries;          /* group-level entries N_group */
+    uint64_t tile_appearances; /* sum of mask popcounts N_total */
+    uint64_t visible;          /* projected splats (input - culled - dropped) */
+    float ms_preprocess, ms_binning, ms_sort, ms_raster, ms_total; /* CUDA-event times */
+} tgs_stats;
+
+/* gsr::ProjectedGaussian (projection.hpp:14-23), 44 bytes. */
+typedef struct {
+    float mean2d[2];
+    float conic[3]; /* a, b, c */
+    float color[3];
+    float opacity;
+    float depth;
+    int32_t radius;
+} tgs_projected;
+
+/* gsr::GroupEntry (binning.hpp:41-45), 12 bytes. */
+typedef struct {
+    uint32_t gaussian_index; /* index into the projected (compacted) list */
+    float depth;
+    uint32_t mask; /* bit r*G+c per overlapped member tile */
+} tgs_group_entry;
+
+typedef struct tgs_ctx tgs_ctx;
+typedef struct tgs_scene tgs_scene;
+
+/* Scene records use the .gsb record layout (scene_io.hpp:38-42): per Gaussian
+ *   mean f32x3, scale f32x3, quat f32x4 (w,x,y,z), opacity f32, sh_dc f32x3,
+ *   [sh_rest f32x45 iff sh_degree == 3]
+ * i.e. 14 or 59 floats, contiguous. */
+
+const char* tgs_last_error(void); /* thread-local message of the last failure */
+int tgs_abi_version(void);
+
+tgs_status tgs_ctx_create(int device, tgs_ctx** out);
+void tgs_ctx_destroy(tgs_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) for callers that time with their own events. */
+void* tgs_ctx_stream(tgs_ctx* ctx);
+
+/* Persistent device-resident scene (SoA, float4 planes); amortises marshalling across frames. */
+tgs_status tgs_scene_upload(tgs_ctx* ctx, const float* records, int64_t count, int sh_degree,
+                            tgs_scene** out);
+void tgs_scene_free(tgs_scene* scene);
+
+/* gsr::render equivalent on an uploaded scene: image to a host buffer of width*height*3 floats
+ * (row-major RGB, clamped to [0,1] like ImageBuffer::finalize).  Synchronous. */
+tgs_status tgs_render(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cam,
+                      const tgs_options* opt, float* out_rgb, tgs_stats* stats);
+
+/* gsr::render with the reference's call shape: host records in, host image out (uploads the
+ * scene, renders, downloads).  This is what the C++ drop-in calls. */
+tgs_status tgs_render_records(tgs_ctx* ctx, const float* records, int64_t count, int sh_degree,
+                              const tgs_camera* cam, const tgs_options* opt, float* out_rgb,
+                              tgs_stats* stats);
+
+/* Asynchronous frame on the context stream; the image stays in a device buffer
+ * (tgs_image_device) until the next enqueue.  No host synchronisation. */
+tgs_status tgs_render_enqueue(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cam,
+                              const tgs_options* opt);
+/* Waits for the stream, checks capacity / validation flags, fills stats. If a buffer turned out
+ * too small the frame is re-rendered synchronously with grown buffers. */
+tgs_status tgs_sync(tgs_ctx* ctx, tgs_stats* stats);
+const float* tgs_image_device(tgs_ctx* ctx); /* device pointer, width*height*3 floats */
+
+/* Screen band: group rows [group_row0, group_row1) of the frame, rendered with lists restricted
+ * to those groups (identical to the same rows of the full frame).  out_rgb receives the band's
+ * rows only: (min(H, group_row1*16*G) - group_row0*16*G) * width * 3 floats. */
+tgs_status tgs_render_band(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cam,
+                           const tgs_options* opt, int group_row0, int group_row1, float* out_rgb,
+                           tgs_stats* stats);
+
+/* Camera batch: n frames, out_rgb = n * width * height * 3 floats (all cameras share W,H). */
+tgs_status tgs_render_batch(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cams, int n,
+                            const tgs_options* opt, float* out_rgb, tgs_stats* stats);
+
+/* Readback of the last rendered frame's intermediate products, for parity tests and tooling.
+ * project: ProjectedGaussian list in input order (project_scene). lists: the (group, depth)
+ * sorted GroupEntry array and group_count+1 offsets (sort_entries).  *n receives the count;
+ * nothing is written when cap is too small. */
+tgs_status tgs_read_projected(tgs_ctx* ctx, tgs_projected* out, int64_t cap, int64_t* n);
+tgs_status tgs_read_lists(tgs_ctx* ctx, tgs_group_entry* out, int64_t cap, uint32_t* offsets,
+                          int64_t offsets_cap, int64_t* n);
+
+/* Walked / alpha-contributing pair counts of the last frame (the raster roofline numerator,
+ * DESIGN.md §Roofline); computed by an instrumented pass, not by the timed kernels. */
+tgs_status tgs_count_pairs(tgs_ctx* ctx, uint64_t* walked, uint64_t* blended);
+
+/* Host-side data formats either side of the path (scene_io.cpp). */
+tgs_status tgs_gen_synthetic_scene(uint64_t seed, int count, float extent, float scale_min,
+                                   float scale_max, uint64_t sh_seed, float* out_records);
+/* encode_ppm payload (scene_io.cpp:253-263) of a host RGB float image on the device. */
+tgs_status tgs_encode_u8(tgs_ctx* ctx, const float* rgb_device, int64_t n, uint8_t* out_host);
+
+/* Internal self-test of the tcgen05 operand path: one M=128 x N=32 x K=16 FP16 MMA through the
+ * same smem descriptors / instruction descriptor the rasterizer uses (row-major A[128][16],
+ * B[32][16] as binary16 bit patterns; D[128][32] = A . B^T in FP32). */
+tgs_status tgs_debug_mma(const uint16_t* a_128x16, const uint16_t* b_32x16, float* d_128x32);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TGS_H */

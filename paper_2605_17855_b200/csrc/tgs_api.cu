@@ -1,0 +1,687 @@
+// libtgs host runtime and C ABI (include/tgs.h): contexts, device scenes, the per-frame
+// pipeline (preprocess -> depth presort -> entry scan -> emission -> group sort -> ranges ->
+// raster), capacity management, readback and error mapping.
+//
+// Reference entry point: proj/src/render.cpp:7-35 (gsr::render).  Validation mirrors it:
+// scalar backend requires G == 1 (render.cpp:9-10), workers >= 1 (:11), GroupConfig limits
+// (binning.cpp:22-30), non-positive scales of visible splats (projection.cpp:37) and
+// non-finite/negative depths of binned splats (binning.cpp:78-83) -> TGS_ERR_VALIDATION.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tgs_common.cuh"
+#include "tgs_kernels.cuh"
+
+namespace tgs {
+
+void launch_debug_mma(const uint16_t* a, const uint16_t* b, float* d, cudaStream_t st);
+
+namespace err_state {
+thread_local std::string g_err;
+}
+using err_state::g_err;
+
+tgs_status set_err(tgs_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+tgs_status cuda_fail(cudaError_t e, const char* expr, const char* file, int line) {
+    char buf[512];
+    std::snprintf(buf, sizeof(buf), "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+                  cudaGetErrorString(e), file, line, expr);
+    return set_err(e == cudaErrorMemoryAllocation ? TGS_ERR_OOM : TGS_ERR_CUDA, buf);
+}
+
+// Grow-only device buffer.
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, n);
+        if (e == cudaSuccess) bytes = n;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+}  // namespace tgs
+
+using namespace tgs;
+
+struct tgs_scene;
+struct tgs_ctx;
+
+struct tgs_scene {
+    tgs_ctx* ctx = nullptr;
+    int device = 0;
+    int64_t n = 0;
+    int sh_degree = 0;
+    DBuf planes;  // pos_op | quat | scale_dcr | dc_gb | sh_rest
+    DevScene dev() const {
+        DevScene s;
+        char* b = planes.as<char>();
+        const size_t n4 = (size_t)n * sizeof(float4);
+        s.pos_op = reinterpret_cast<const float4*>(b);
+        s.quat = reinterpret_cast<const float4*>(b + n4);
+        s.scale_dcr = reinterpret_cast<const float4*>(b + 2 * n4);
+        s.dc_gb = reinterpret_cast<const float2*>(b + 3 * n4);
+        s.sh_rest = sh_degree == 3 ? reinterpret_cast<const float4*>(b + 3 * n4 + (size_t)n * sizeof(float2)) : nullptr;
+        s.n = (int)n;
+        s.sh_degree = sh_degree;
+        return s;
+    }
+};
+
+struct tgs_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[6] = {};
+    // per-frame buffers
+    DBuf fc;            // FrameCounters
+    DBuf status;        // look-back status words (preprocess | entry scan)
+    DBuf proj;          // mc | co | col (capacity n)
+    DBuf pre_keys[2], pre_vals[2];
+    DBuf ngroups, eoff;
+    DBuf ent_keys[2], ent_vals[2];
+    DBuf ghist, gid_count, offsets;
+    DBuf image;
+    DBuf scratch_records;
+    FrameCounters* h_fc = nullptr;  // pinned
+    uint32_t capacity = 0;          // entry capacity
+    int64_t proj_cap = 0;
+    // last frame
+    const tgs_scene* last_scene = nullptr;
+    tgs_camera last_cam{};
+    tgs_options last_opt{};
+    GroupGeom last_gg{};
+    int last_band0 = 0, last_band1 = 0;
+    int list_parity = 0;
+    int image_rows = 0;
+    bool pending = false;
+    tgs_scene* scratch_scene = nullptr;
+};
+
+namespace tgs {
+namespace api {
+
+int ceil_log2(int n) {
+    int b = 0;
+    while ((1 << b) < n) ++b;
+    return b;
+}
+
+tgs_status validate_options(const tgs_camera* cam, const tgs_options* opt) {
+    if (!cam || !opt) return set_err(TGS_ERR_VALIDATION, "render: null camera or options");
+    if (opt->backend != TGS_BACKEND_SCALAR && opt->backend != TGS_BACKEND_TENSOR)
+        return set_err(TGS_ERR_VALIDATION, "render: unknown backend");
+    if (opt->backend == TGS_BACKEND_SCALAR && opt->group_size != 1)
+        return set_err(TGS_ERR_VALIDATION, "render: the scalar backend requires group size 1");
+    if (opt->workers < 1) return set_err(TGS_ERR_VALIDATION, "render: workers must be >= 1");
+    if (cam->width <= 0 || cam->height <= 0)
+        return set_err(TGS_ERR_VALIDATION, "GroupConfig: image dimensions must be positive");
+    if (!(opt->group_size == 1 || opt->group_size == 2 || opt->group_size == 4))
+        return set_err(TGS_ERR_VALIDATION, "GroupConfig: supported group sizes are 1x1, 2x2, 4x4");
+    return TGS_OK;
+}
+
+GroupGeom make_geom(int g, int w, int h, int band0, int band1) {
+    GroupGeom gg;
+    gg.g = g;
+    gg.width = w;
+    gg.height = h;
+    gg.tiles_x = (w + kTile - 1) / kTile;
+    gg.tiles_y = (h + kTile - 1) / kTile;
+    gg.groups_x = (gg.tiles_x + g - 1) / g;
+    gg.groups_y = (gg.tiles_y + g - 1) / g;
+    gg.band_gy0 = band0;
+    gg.band_gy1 = band1;
+    gg.n_groups_band = gg.groups_x * (band1 - band0);
+    return gg;
+}
+
+DevCamera make_dev_camera(const tgs_camera* c) {
+    DevCamera d;
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) d.r[i][j] = c->view[i * 4 + j];
+        d.t[i] = c->view[i * 4 + 3];
+    }
+    d.fx = c->focal_x;
+    d.fy = c->focal_y;
+    d.width = c->width;
+    d.height = c->height;
+    d.near_ = c->near_;
+    d.far_ = c->far_;
+    return d;
+}
+
+DevProjected dev_proj(tgs_ctx* ctx) {
+    DevProjected p;
+    float4* b = ctx->proj.as<float4>();
+    p.mc = b;
+    p.co = b + ctx->proj_cap;
+    p.col = b + 2 * ctx->proj_cap;
+    return p;
+}
+
+// Enqueue one frame (or band) on ctx->stream.
+tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cam,
+                         const tgs_options* opt, int band0, int band1) {
+    tgs_status st = validate_options(cam, opt);
+    if (st != TGS_OK) return st;
+    if (!scene || scene->ctx != ctx) return set_err(TGS_ERR_VALIDATION, "render: scene belongs to another context");
+    const GroupGeom full = make_geom(opt->group_size, cam->width, cam->height, 0, 0);
+    if (band1 <= 0) {
+        band0 = 0;
+        band1 = full.groups_y;
+    }
+    if (band0 < 0 || band1 > full.groups_y || band0 >= band1)
+        return set_err(TGS_ERR_VALIDATION, "render_band: group-row band out of range");
+    const GroupGeom gg = make_geom(opt->group_size, cam->width, cam->height, band0, band1);
+    const int n_groups = gg.n_groups_band;
+    if (n_groups > 49152)
+        return set_err(TGS_ERR_VALIDATION, "render: more than 49152 groups in one frame/band; use bands");
+    cudaStream_t s = ctx->stream;
+    const int64_t n = scene->n;
+    const int n_alloc = (int)std::max<int64_t>(n, 1);
+
+    // ---- buffers ----
+    if (ctx->proj_cap < n_alloc) {
+        TGS_CUDA_OK(ctx->proj.ensure((size_t)n_alloc * 3 * sizeof(float4)));
+        ctx->proj_cap = n_alloc;
+    }
+    for (int i = 0; i < 2; ++i) {
+        TGS_CUDA_OK(ctx->pre_keys[i].ensure((size_t)n_alloc * 4));
+        TGS_CUDA_OK(ctx->pre_vals[i].ensure((size_t)n_alloc * 4));
+    }
+    TGS_CUDA_OK(ctx->ngroups.ensure((size_t)n_alloc * 4));
+    TGS_CUDA_OK(ctx->eoff.ensure((size_t)n_alloc * 4));
+    const size_t pre_tiles = (size_t)(n_alloc + 255) / 256, scan_tiles = (size_t)(n_alloc + 2047) / 2048;
+    TGS_CUDA_OK(ctx->status.ensure((pre_tiles + scan_tiles) * 8));
+    const uint32_t cap = std::max<uint32_t>(ctx->capacity, 1u);
+    for (int i = 0; i < 2; ++i) {
+        TGS_CUDA_OK(ctx->ent_keys[i].ensure((size_t)cap * 4));
+        TGS_CUDA_OK(ctx->ent_vals[i].ensure((size_t)cap * 4));
+    }
+    TGS_CUDA_OK(ctx->ghist.ensure((size_t)256 * kSortBlocks * 4));
+    TGS_CUDA_OK(ctx->gid_count.ensure((size_t)n_groups * 4));
+    TGS_CUDA_OK(ctx->offsets.ensure((size_t)(n_groups + 1) * 4));
+    const int row0 = band0 * gg.g * kTile;
+    const int row1 = std::min(cam->height, band1 * gg.g * kTile);
+    TGS_CUDA_OK(ctx->image.ensure((size_t)(row1 - row0) * cam->width * 3 * sizeof(float)));
+
+    FrameCounters* fc = ctx->fc.as<FrameCounters>();
+    unsigned long long* pre_status = ctx->status.as<unsigned long long>();
+    unsigned long long* scan_status = pre_status + pre_tiles;
+    const DevProjected proj = dev_proj(ctx);
+
+    TGS_CUDA_OK(cudaEventRecord(ctx->ev[0], s));
+    TGS_CUDA_OK(cudaMemsetAsync(fc, 0, sizeof(FrameCounters), s));
+    TGS_CUDA_OK(cudaMemsetAsync(pre_status, 0, (pre_tiles + scan_tiles) * 8, s));
+    TGS_CUDA_OK(cudaMemsetAsync(ctx->gid_count.p, 0, (size_t)n_groups * 4, s));
+
+    // 1. preprocess + compaction
+    PreprocessArgs pa;
+    pa.scene = scene->dev();
+    pa.cam = make_dev_camera(cam);
+    pa.out = proj;
+    pa.depth_keys = ctx->pre_keys[0].as<uint32_t>();
+    pa.idx_vals = ctx->pre_vals[0].as<uint32_t>();
+    pa.ngroups = ctx->ngroups.as<uint32_t>();
+    pa.gg = gg;
+    pa.tile_status = pre_status;
+    pa.fc = fc;
+    launch_preprocess(pa, s);
+    TGS_CUDA_OK(cudaGetLastError());
+    TGS_CUDA_OK(cudaEventRecord(ctx->ev[1], s));
+
+    // 2. depth presort (keys: depth bits, values: project_scene index)
+    SortBuffers pb;
+    pb.keys[0] = ctx->pre_keys[0].as<uint32_t>();
+    pb.keys[1] = ctx->pre_keys[1].as<uint32_t>();
+    pb.vals[0] = ctx->pre_vals[0].as<uint32_t>();
+    pb.vals[1] = ctx->pre_vals[1].as<uint32_t>();
+    pb.ghist = ctx->ghist.as<uint32_t>();
+    pb.gid_count = nullptr;
+    const int pr = radix_sort(pb, &fc->visible, 32, 0, false, s);
+    TGS_CUDA_OK(cudaGetLastError());
+
+    // 3. entry counts -> offsets (depth order), 4. emission
+    BinArgs ba;
+    ba.visible = &fc->visible;
+    ba.sval = pb.vals[pr];
+    ba.ngroups = ctx->ngroups.as<uint32_t>();
+    ba.eoff = ctx->eoff.as<uint32_t>();
+    ba.tile_status = scan_status;
+    ba.fc = fc;
+    ba.capacity = ctx->capacity;
+    ba.proj = proj;
+    ba.gg = gg;
+    ba.keys = ctx->ent_keys[0].as<uint32_t>();
+    ba.vals = ctx->ent_vals[0].as<uint32_t>();
+    launch_entry_scan(ba, n_alloc, s);
+    launch_emit(ba, n_alloc, s);
+    TGS_CUDA_OK(cudaGetLastError());
+    TGS_CUDA_OK(cudaEventRecord(ctx->ev[2], s));
+
+    // 5. stable group sort + ranges
+    SortBuffers eb;
+    eb.keys[0] = ctx->ent_keys[0].as<uint32_t>();
+    eb.keys[1] = ctx->ent_keys[1].as<uint32_t>();
+    eb.vals[0] = ctx->ent_vals[0].as<uint32_t>();
+    eb.vals[1] = ctx->ent_vals[1].as<uint32_t>();
+    eb.ghist = ctx->ghist.as<uint32_t>();
+    eb.gid_count = ctx->gid_count.as<uint32_t>();
+    const int er = radix_sort(eb, &fc->n_sort, std::max(1, ceil_log2(n_groups)), n_groups, false, s);
+    launch_offsets_scan(eb.gid_count, ctx->offsets.as<uint32_t>(), n_groups, s);
+    TGS_CUDA_OK(cudaGetLastError());
+    TGS_CUDA_OK(cudaEventRecord(ctx->ev[3], s));
+
+    // 6. raster
+    RasterArgs ra;
+    ra.proj = proj;
+    ra.list = eb.vals[er];
+    ra.offsets = ctx->offsets.as<uint32_t>();
+    ra.gg = gg;
+    ra.image = ctx->image.as<float>();
+    ra.image_row0 = row0;
+    ra.alpha_skip = opt->alpha_skip;
+    ra.alpha_clamp = opt->alpha_clamp;
+    ra.t_terminate = opt->t_terminate;
+    ra.fc = fc;
+    if (opt->backend == TGS_BACKEND_SCALAR)
+        launch_raster_scalar(ra, s);
+    else
+        launch_raster_tensor(ra, ctx->num_sms, s);
+    TGS_CUDA_OK(cudaGetLastError());
+    TGS_CUDA_OK(cudaEventRecord(ctx->ev[4], s));
+    TGS_CUDA_OK(cudaMemcpyAsync(ctx->h_fc, fc, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
+
+    ctx->last_scene = scene;
+    ctx->last_cam = *cam;
+    ctx->last_opt = *opt;
+    ctx->last_gg = gg;
+    ctx->last_band0 = band0;
+    ctx->last_band1 = band1;
+    ctx->list_parity = er;
+    ctx->image_rows = row1 - row0;
+    ctx->pending = true;
+    return TGS_OK;
+}
+
+tgs_status finish_frame(tgs_ctx* ctx, tgs_stats* stats) {
+    TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    ctx->pending = false;
+    const FrameCounters& f = *ctx->h_fc;
+    if (f.overflow) {
+        // entry buffers too small: grow (25% headroom) and re-render this frame
+        const uint64_t need = (uint64_t)f.n_entries + f.n_entries / 4 + 1024;
+        if (need > 0xFFFFFFF0ull) return set_err(TGS_ERR_OOM, "render: more than 2^32 entries in one frame");
+        ctx->capacity = (uint32_t)need;
+        tgs_camera cam = ctx->last_cam;
+        tgs_options opt = ctx->last_opt;
+        tgs_status st = enqueue_frame(ctx, ctx->last_scene, &cam, &opt, ctx->last_band0, ctx->last_band1);
+        if (st != TGS_OK) return st;
+        TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        ctx->pending = false;
+        if (ctx->h_fc->overflow) return set_err(TGS_ERR_OOM, "render: entry capacity overflow after growth");
+    }
+    const FrameCounters& g = *ctx->h_fc;
+    if (g.err_validation & 1u) return set_err(TGS_ERR_VALIDATION, "compute_cov3d: non-positive scale");
+    if (g.err_validation & 2u)
+        return set_err(TGS_ERR_VALIDATION, "sort_entries: an entry has non-finite or negative depth");
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        stats->input = (uint64_t)ctx->last_scene->n;
+        stats->culled = g.culled;
+        stats->dropped_degenerate = g.dropped;
+        stats->entries = g.n_entries;
+        stats->tile_appearances = g.appearances;
+        stats->visible = g.visible;
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+        stats->ms_preprocess = ms;
+        cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]);
+        stats->ms_binning = ms;
+        cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+        stats->ms_sort = ms;
+        cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[4]);
+        stats->ms_raster = ms;
+        cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[4]);
+        stats->ms_total = ms;
+    }
+    return TGS_OK;
+}
+
+__global__ void records_to_planes(const float* __restrict__ rec, int64_t n, int rf, float4* pos_op,
+                                  float4* quat, float4* scale_dcr, float2* dc_gb, float4* sh) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float* p = rec + i * rf;
+        pos_op[i] = make_float4(p[0], p[1], p[2], p[10]);
+        quat[i] = make_float4(p[6], p[7], p[8], p[9]);
+        scale_dcr[i] = make_float4(p[3], p[4], p[5], p[11]);
+        dc_gb[i] = make_float2(p[12], p[13]);
+        if (sh) {
+            for (int k = 0; k < 12; ++k) {
+                float v[4];
+                for (int c = 0; c < 4; ++c) v[c] = (4 * k + c < 45) ? p[14 + 4 * k + c] : 0.0f;
+                sh[(size_t)k * n + i] = make_float4(v[0], v[1], v[2], v[3]);
+            }
+        }
+    }
+}
+
+tgs_status upload_into(tgs_ctx* ctx, tgs_scene* sc, const float* records, int64_t count, int deg) {
+    if (count < 0 || count > (int64_t)0x7fffffff) return set_err(TGS_ERR_VALIDATION, "scene: bad count");
+    if (deg != 0 && deg != 3) return set_err(TGS_ERR_FORMAT, "scene: unsupported sh_degree");
+    const int rf = deg == 3 ? 59 : 14;
+    const int64_t n = count;
+    const size_t n_alloc = (size_t)std::max<int64_t>(n, 1);
+    const size_t bytes = n_alloc * (3 * sizeof(float4) + sizeof(float2)) + (deg == 3 ? n_alloc * 12 * sizeof(float4) : 0);
+    TGS_CUDA_OK(cudaSetDevice(ctx->device));
+    TGS_CUDA_OK(sc->planes.ensure(bytes));
+    sc->ctx = ctx;
+    sc->device = ctx->device;
+    sc->n = n;
+    sc->sh_degree = deg;
+    if (n == 0) return TGS_OK;
+    TGS_CUDA_OK(ctx->scratch_records.ensure((size_t)n * rf * sizeof(float)));
+    TGS_CUDA_OK(cudaMemcpyAsync(ctx->scratch_records.p, records, (size_t)n * rf * sizeof(float),
+                                cudaMemcpyHostToDevice, ctx->stream));
+    const DevScene d = sc->dev();
+    records_to_planes<<<148 * 8, 256, 0, ctx->stream>>>(ctx->scratch_records.as<float>(), n, rf,
+                                                         const_cast<float4*>(d.pos_op), const_cast<float4*>(d.quat),
+                                                         const_cast<float4*>(d.scale_dcr), const_cast<float2*>(d.dc_gb),
+                                                         const_cast<float4*>(d.sh_rest));
+    TGS_CUDA_OK(cudaGetLastError());
+    TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    return TGS_OK;
+}
+
+tgs_status copy_image_to_host(tgs_ctx* ctx, float* out) {
+    const size_t bytes = (size_t)ctx->image_rows * ctx->last_cam.width * 3 * sizeof(float);
+    TGS_CUDA_OK(cudaMemcpyAsync(out, ctx->image.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    return TGS_OK;
+}
+
+}  // namespace api
+}  // namespace tgs
+
+using namespace tgs::api;
+
+extern "C" {
+
+const char* tgs_last_error(void) { return g_err.c_str(); }
+int tgs_abi_version(void) { return TGS_ABI_VERSION; }
+
+tgs_status tgs_ctx_create(int device, tgs_ctx** out) {
+    if (!out) return set_err(TGS_ERR_VALIDATION, "ctx_create: null out");
+    *out = nullptr;
+    int ndev = 0;
+    TGS_CUDA_OK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return set_err(TGS_ERR_CUDA, "ctx_create: no such CUDA device");
+    cudaDeviceProp prop;
+    TGS_CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return set_err(TGS_ERR_CUDA, std::string("ctx_create: libtgs is built for sm_100a; device is ") + prop.name);
+    TGS_CUDA_OK(cudaSetDevice(device));
+    tgs_ctx* c = new tgs_ctx();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    for (int i = 0; e == cudaSuccess && i < 6; ++i) e = cudaEventCreate(&c->ev[i]);
+    if (e == cudaSuccess) e = c->fc.ensure(sizeof(FrameCounters));
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_fc, sizeof(FrameCounters));
+    if (e != cudaSuccess) {
+        tgs_ctx_destroy(c);
+        return cuda_fail(e, "ctx_create", __FILE__, __LINE__);
+    }
+    *out = c;
+    return TGS_OK;
+}
+
+void tgs_ctx_destroy(tgs_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->scratch_scene) tgs_scene_free(c->scratch_scene);
+    DBuf* bufs[] = {&c->fc, &c->status, &c->proj, &c->pre_keys[0], &c->pre_keys[1], &c->pre_vals[0],
+                    &c->pre_vals[1], &c->ngroups, &c->eoff, &c->ent_keys[0], &c->ent_keys[1],
+                    &c->ent_vals[0], &c->ent_vals[1], &c->ghist, &c->gid_count, &c->offsets,
+                    &c->image, &c->scratch_records};
+    for (DBuf* b : bufs) b->release();
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->h_fc) cudaFreeHost(c->h_fc);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+void* tgs_ctx_stream(tgs_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+tgs_status tgs_scene_upload(tgs_ctx* ctx, const float* records, int64_t count, int sh_degree, tgs_scene** out) {
+    if (!ctx || !out || (count > 0 && !records)) return set_err(TGS_ERR_VALIDATION, "scene_upload: null argument");
+    tgs_scene* sc = new tgs_scene();
+    tgs_status st = upload_into(ctx, sc, records, count, sh_degree);
+    if (st != TGS_OK) {
+        sc->planes.release();
+        delete sc;
+        *out = nullptr;
+        return st;
+    }
+    *out = sc;
+    return TGS_OK;
+}
+
+void tgs_scene_free(tgs_scene* sc) {
+    if (!sc) return;
+    cudaSetDevice(sc->device);
+    sc->planes.release();
+    delete sc;
+}
+
+tgs_status tgs_render_enqueue(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cam, const tgs_options* opt) {
+    if (!ctx) return set_err(TGS_ERR_VALIDATION, "render: null context");
+    cudaSetDevice(ctx->device);
+    return enqueue_frame(ctx, scene, cam, opt, 0, 0);
+}
+
+tgs_status tgs_sync(tgs_ctx* ctx, tgs_stats* stats) {
+    if (!ctx) return set_err(TGS_ERR_VALIDATION, "sync: null context");
+    if (!ctx->pending) {
+        TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        return TGS_OK;
+    }
+    return finish_frame(ctx, stats);
+}
+
+const float* tgs_image_device(tgs_ctx* ctx) { return ctx ? ctx->image.as<float>() : nullptr; }
+
+tgs_status tgs_render(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cam, const tgs_options* opt,
+                      float* out_rgb, tgs_stats* stats) {
+    tgs_status st = tgs_render_enqueue(ctx, scene, cam, opt);
+    if (st != TGS_OK) return st;
+    st = finish_frame(ctx, stats);
+    if (st != TGS_OK) return st;
+    return out_rgb ? copy_image_to_host(ctx, out_rgb) : TGS_OK;
+}
+
+tgs_status tgs_render_records(tgs_ctx* ctx, const float* records, int64_t count, int sh_degree,
+                              const tgs_camera* cam, const tgs_options* opt, float* out_rgb, tgs_stats* stats) {
+    if (!ctx) return set_err(TGS_ERR_VALIDATION, "render: null context");
+    tgs_status st = validate_options(cam, opt);
+    if (st != TGS_OK) return st;
+    if (!ctx->scratch_scene) ctx->scratch_scene = new tgs_scene();
+    st = upload_into(ctx, ctx->scratch_scene, records, count, sh_degree);
+    if (st != TGS_OK) return st;
+    return tgs_render(ctx, ctx->scratch_scene, cam, opt, out_rgb, stats);
+}
+
+tgs_status tgs_render_band(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cam, const tgs_options* opt,
+                           int group_row0, int group_row1, float* out_rgb, tgs_stats* stats) {
+    if (!ctx) return set_err(TGS_ERR_VALIDATION, "render_band: null context");
+    if (group_row1 <= group_row0) return set_err(TGS_ERR_VALIDATION, "render_band: empty band");
+    cudaSetDevice(ctx->device);
+    tgs_status st = enqueue_frame(ctx, scene, cam, opt, group_row0, group_row1);
+    if (st != TGS_OK) return st;
+    st = finish_frame(ctx, stats);
+    if (st != TGS_OK) return st;
+    return out_rgb ? copy_image_to_host(ctx, out_rgb) : TGS_OK;
+}
+
+tgs_status tgs_render_batch(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cams, int n,
+                            const tgs_options* opt, float* out_rgb, tgs_stats* stats) {
+    if (!ctx || !cams || n < 0) return set_err(TGS_ERR_VALIDATION, "render_batch: bad arguments");
+    tgs_stats acc{};
+    for (int i = 0; i < n; ++i) {
+        if (cams[i].width != cams[0].width || cams[i].height != cams[0].height)
+            return set_err(TGS_ERR_VALIDATION, "render_batch: all cameras must share width/height");
+        tgs_stats one{};
+        const size_t px = (size_t)cams[i].width * cams[i].height * 3;
+        tgs_status st = tgs_render(ctx, scene, &cams[i], opt, out_rgb ? out_rgb + px * i : nullptr, &one);
+        if (st != TGS_OK) return st;
+        acc.input += one.input;
+        acc.culled += one.culled;
+        acc.dropped_degenerate += one.dropped_degenerate;
+        acc.entries += one.entries;
+        acc.tile_appearances += one.tile_appearances;
+        acc.visible += one.visible;
+        acc.ms_preprocess += one.ms_preprocess;
+        acc.ms_binning += one.ms_binning;
+        acc.ms_sort += one.ms_sort;
+        acc.ms_raster += one.ms_raster;
+        acc.ms_total += one.ms_total;
+    }
+    if (stats) *stats = acc;
+    return TGS_OK;
+}
+
+tgs_status tgs_read_projected(tgs_ctx* ctx, tgs_projected* out, int64_t cap, int64_t* n) {
+    if (!ctx || !n) return set_err(TGS_ERR_VALIDATION, "read_projected: null argument");
+    if (!ctx->last_scene) return set_err(TGS_ERR_VALIDATION, "read_projected: no frame rendered yet");
+    const int64_t v = ctx->h_fc->visible;
+    *n = v;
+    if (!out || cap < v || v == 0) return TGS_OK;
+    std::vector<float4> h((size_t)v * 3);
+    const DevProjected p = dev_proj(ctx);
+    TGS_CUDA_OK(cudaMemcpy(h.data(), p.mc, (size_t)v * sizeof(float4), cudaMemcpyDeviceToHost));
+    TGS_CUDA_OK(cudaMemcpy(h.data() + v, p.co, (size_t)v * sizeof(float4), cudaMemcpyDeviceToHost));
+    TGS_CUDA_OK(cudaMemcpy(h.data() + 2 * v, p.col, (size_t)v * sizeof(float4), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < v; ++i) {
+        const float4 mc = h[i], co = h[v + i], col = h[2 * v + i];
+        tgs_projected& o = out[i];
+        o.mean2d[0] = mc.x;
+        o.mean2d[1] = mc.y;
+        o.conic[0] = mc.z;
+        o.conic[1] = mc.w;
+        o.conic[2] = co.x;
+        o.opacity = co.y;
+        o.depth = co.z;
+        std::memcpy(&o.radius, &co.w, 4);
+        o.color[0] = col.x;
+        o.color[1] = col.y;
+        o.color[2] = col.z;
+    }
+    return TGS_OK;
+}
+
+tgs_status tgs_read_lists(tgs_ctx* ctx, tgs_group_entry* out, int64_t cap, uint32_t* offsets,
+                          int64_t offsets_cap, int64_t* n) {
+    if (!ctx || !n) return set_err(TGS_ERR_VALIDATION, "read_lists: null argument");
+    if (!ctx->last_scene) return set_err(TGS_ERR_VALIDATION, "read_lists: no frame rendered yet");
+    const int64_t m = ctx->h_fc->n_entries;
+    const int ng = ctx->last_gg.n_groups_band;
+    *n = m;
+    if (!out || cap < m || !offsets || offsets_cap < ng + 1) return TGS_OK;
+    TGS_CUDA_OK(cudaMemcpy(offsets, ctx->offsets.p, (size_t)(ng + 1) * 4, cudaMemcpyDeviceToHost));
+    if (m == 0) return TGS_OK;
+    DBuf tmp;
+    TGS_CUDA_OK(tmp.ensure((size_t)m * sizeof(tgs_group_entry)));
+    launch_lists_readback(ctx->ent_vals[ctx->list_parity].as<uint32_t>(), ctx->offsets.as<uint32_t>(), ng,
+                          dev_proj(ctx), ctx->last_gg, tmp.as<tgs_group_entry>(), ctx->stream);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, tmp.p, (size_t)m * sizeof(tgs_group_entry), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    tmp.release();
+    if (e != cudaSuccess) return cuda_fail(e, "read_lists", __FILE__, __LINE__);
+    return TGS_OK;
+}
+
+tgs_status tgs_count_pairs(tgs_ctx* ctx, uint64_t* walked, uint64_t* blended) {
+    if (!ctx || !walked || !blended) return set_err(TGS_ERR_VALIDATION, "count_pairs: null argument");
+    if (!ctx->last_scene) return set_err(TGS_ERR_VALIDATION, "count_pairs: no frame rendered yet");
+    FrameCounters* fc = ctx->fc.as<FrameCounters>();
+    TGS_CUDA_OK(cudaMemsetAsync(&fc->walked, 0, 2 * sizeof(unsigned long long), ctx->stream));
+    RasterArgs ra;
+    ra.proj = dev_proj(ctx);
+    ra.list = ctx->ent_vals[ctx->list_parity].as<uint32_t>();
+    ra.offsets = ctx->offsets.as<uint32_t>();
+    ra.gg = ctx->last_gg;
+    ra.image = nullptr;
+    ra.image_row0 = 0;
+    ra.alpha_skip = ctx->last_opt.alpha_skip;
+    ra.alpha_clamp = ctx->last_opt.alpha_clamp;
+    ra.t_terminate = ctx->last_opt.t_terminate;
+    ra.fc = fc;
+    launch_count_pairs(ra, ctx->stream);
+    TGS_CUDA_OK(cudaGetLastError());
+    unsigned long long h[2];
+    TGS_CUDA_OK(cudaMemcpyAsync(h, &fc->walked, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    *walked = h[0];
+    *blended = h[1];
+    return TGS_OK;
+}
+
+tgs_status tgs_encode_u8(tgs_ctx* ctx, const float* rgb_device, int64_t n, uint8_t* out_host) {
+    if (!ctx || !rgb_device || !out_host || n < 0) return set_err(TGS_ERR_VALIDATION, "encode_u8: bad arguments");
+    DBuf tmp;
+    TGS_CUDA_OK(tmp.ensure((size_t)std::max<int64_t>(n, 1)));
+    launch_encode_u8(rgb_device, n, tmp.as<uint8_t>(), ctx->stream);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_host, tmp.p, (size_t)n, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    tmp.release();
+    if (e != cudaSuccess) return cuda_fail(e, "encode_u8", __FILE__, __LINE__);
+    return TGS_OK;
+}
+
+// Internal self-test of the tcgen05 operand descriptors (tests/test_gpu_tcgen05.py).
+tgs_status tgs_debug_mma(const uint16_t* a_host_128x16, const uint16_t* b_host_32x16, float* d_host_128x32) {
+    DBuf da, db, dd;
+    TGS_CUDA_OK(da.ensure(128 * 16 * 2));
+    TGS_CUDA_OK(db.ensure(32 * 16 * 2));
+    TGS_CUDA_OK(dd.ensure(128 * 32 * 4));
+    TGS_CUDA_OK(cudaMemcpy(da.p, a_host_128x16, 128 * 16 * 2, cudaMemcpyHostToDevice));
+    TGS_CUDA_OK(cudaMemcpy(db.p, b_host_32x16, 32 * 16 * 2, cudaMemcpyHostToDevice));
+    launch_debug_mma(da.as<uint16_t>(), db.as<uint16_t>(), dd.as<float>(), 0);
+    TGS_CUDA_OK(cudaGetLastError());
+    TGS_CUDA_OK(cudaDeviceSynchronize());
+    TGS_CUDA_OK(cudaMemcpy(d_host_128x32, dd.p, 128 * 32 * 4, cudaMemcpyDeviceToHost));
+    da.release();
+    db.release();
+    dd.release();
+    return TGS_OK;
+}
+
+}  // extern "C"

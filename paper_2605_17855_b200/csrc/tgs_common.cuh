@@ -1,0 +1,138 @@
+// Shared device-side definitions of libtgs (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "../../include/tgs.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libtgs is written for sm_100a (B200) only"
+#endif
+
+namespace tgs {
+
+constexpr int kTile = 16;  // binning.hpp:11 kTileSize
+
+// Camera parameters as the preprocess kernel consumes them (row-major R, t).
+struct DevCamera {
+    float r[3][3];
+    float t[3];
+    float fx, fy;
+    int width, height;
+    float near_, far_;
+};
+
+// Device scene: SoA float4 planes, coalesced 16/8-byte loads per Gaussian.
+struct DevScene {
+    const float4* pos_op;     // mean.xyz, opacity
+    const float4* quat;       // w, x, y, z
+    const float4* scale_dcr;  // scale.xyz, sh_dc.r
+    const float2* dc_gb;      // sh_dc.g, sh_dc.b
+    const float4* sh_rest;    // 12 planes of n float4 (coefficients 4p..4p+3), or null
+    int n;
+    int sh_degree;
+};
+
+// Projected splats, indexed by the compacted (project_scene output) index.
+struct DevProjected {
+    float4* mc;   // mean2d.x, mean2d.y, conic_a, conic_b
+    float4* co;   // conic_c, opacity, depth, radius (int bits)
+    float4* col;  // color r, g, b, 0
+};
+
+// Device counters / flags of one frame (zeroed per frame).
+struct FrameCounters {
+    unsigned long long culled;
+    unsigned long long dropped;
+    unsigned long long appearances;
+    unsigned int visible;           // compacted count
+    unsigned int n_entries;         // emitted entries (may exceed capacity -> overflow)
+    unsigned int n_sort;            // entries handed to the group sort (0 on overflow)
+    unsigned int err_validation;    // non-positive scale (projection.cpp:37) / bad depth (binning.cpp:78-83)
+    unsigned int overflow;          // entry capacity exceeded
+    unsigned int tile_counter;      // decoupled look-back tile ticket (preprocess)
+    unsigned int scan_tile_counter; // decoupled look-back tile ticket (entry scan)
+    unsigned int group_counter;     // persistent raster scheduler ticket
+    unsigned long long walked;      // instrumented pair counters (tgs_count_pairs)
+    unsigned long long blended;
+};
+
+// Group geometry (GroupConfig, binning.hpp:15-31) with an optional band of group rows.
+struct GroupGeom {
+    int g;          // tiles per group side
+    int width, height;
+    int tiles_x, tiles_y;
+    int groups_x, groups_y;
+    int band_gy0, band_gy1;  // group rows [gy0, gy1) are binned; others dropped
+    int n_groups_band;       // groups_x * (gy1 - gy0)
+};
+
+// Exact IEEE single operations (no FMA contraction) for the bit-exact stages.
+__device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fdiv(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float fsqrt(float a) { return __fsqrt_rn(a); }
+// Eigen fixed-size 3-term reduction order: e0 + (e1 + e2).
+__device__ __forceinline__ float sum3(float e0, float e1, float e2) { return fadd(e0, fadd(e1, e2)); }
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// binning.cpp:32-44 tiles_overlapped, clipped to the tile grid. Same float ops as the reference:
+// floor((mean - r) / 16), division by 16 is exact.
+__device__ __forceinline__ void tile_rect(float mx, float my, int radius, int tiles_x, int tiles_y,
+                                          int& x0, int& y0, int& x1, int& y1) {
+    const float r = (float)radius;
+    x0 = (int)floorf(__fdiv_rn(__fsub_rn(mx, r), 16.0f));
+    x1 = (int)floorf(__fdiv_rn(__fadd_rn(mx, r), 16.0f));
+    y0 = (int)floorf(__fdiv_rn(__fsub_rn(my, r), 16.0f));
+    y1 = (int)floorf(__fdiv_rn(__fadd_rn(my, r), 16.0f));
+    x0 = max(x0, 0);
+    y0 = max(y0, 0);
+    x1 = min(x1, tiles_x - 1);
+    y1 = min(y1, tiles_y - 1);
+}
+
+// Group-rect of a splat (restricted to the band), returns number of groups (0 = no entries).
+__device__ __forceinline__ int group_rect(float mx, float my, int radius, const GroupGeom& gg,
+                                          int& tx0, int& ty0, int& tx1, int& ty1, int& gx0,
+                                          int& gy0, int& gx1, int& gy1) {
+    tile_rect(mx, my, radius, gg.tiles_x, gg.tiles_y, tx0, ty0, tx1, ty1);
+    if (tx1 < tx0 || ty1 < ty0) return 0;
+    gx0 = tx0 / gg.g;
+    gx1 = tx1 / gg.g;
+    gy0 = max(ty0 / gg.g, gg.band_gy0);
+    gy1 = min(ty1 / gg.g, gg.band_gy1 - 1);
+    if (gy1 < gy0) return 0;
+    return (gx1 - gx0 + 1) * (gy1 - gy0 + 1);
+}
+
+// Member-tile mask of group (gx, gy) for tile rect [tx0..tx1]x[ty0..ty1] (binning.cpp:56-65).
+__device__ __forceinline__ uint32_t group_mask(int gx, int gy, int g, int tx0, int ty0, int tx1,
+                                               int ty1) {
+    const int a0 = max(tx0, gx * g), a1 = min(tx1, gx * g + g - 1);
+    const int b0 = max(ty0, gy * g), b1 = min(ty1, gy * g + g - 1);
+    uint32_t m = 0;
+    for (int ty = b0; ty <= b1; ++ty)
+        for (int tx = a0; tx <= a1; ++tx) m |= 1u << ((ty - gy * g) * g + (tx - gx * g));
+    return m;
+}
+
+}  // namespace tgs
+
+#define TGS_CUDA_OK(expr)                                                   \
+    do {                                                                    \
+        cudaError_t _e = (expr);                                            \
+        if (_e != cudaSuccess) return tgs::cuda_fail(_e, #expr, __FILE__, __LINE__); \
+    } while (0)

@@ -1,0 +1,226 @@
+// Hand-written stable LSD radix sort (north_star 2) for u32 keys + u32 values with a
+// device-resident item count (no host round trip inside a frame / CUDA graph).
+//
+// Reference semantics it realises: std::stable_sort on (group_id << 32) | f32_bits(depth) with
+// ties in emission order (proj/src/binning.cpp:86-91).  The path sorts twice:
+//   1. presort of visible splats by depth bits (values = project_scene index) — 32-bit keys;
+//   2. stable sort of the emitted (group id, index) entries by group id only.
+// Emission happens in presorted order, so (2) yields (group, depth, index) order == the
+// reference's list, bit for bit (tests/test_gpu_parity.py checks full list equality).
+//
+// Per pass (reduce-then-scan, fixed grid of kSortBlocks blocks, each owning a contiguous range):
+//   hist    : per-block digit histogram (smem atomics); the first gid pass also accumulates the
+//             per-group counts that become the list offsets;
+//   scan    : one block scans the [digit][block] matrix;
+//   scatter : stable block-local ranking — each warp ranks 32 items per step with
+//             __match_any_sync against warp-private running digit counters, a block-wide
+//             per-digit prefix across warps orders the warps, then every item is written to
+//             its global slot.
+#include "tgs_common.cuh"
+#include "tgs_kernels.cuh"
+
+namespace tgs {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kSteps = 8;                              // 32-item steps per warp per tile
+constexpr int kTileItems = kThreads * kSteps;          // 2048
+
+__device__ __forceinline__ void block_range(uint32_t count, uint32_t& begin, uint32_t& end) {
+    const uint32_t per = ((count + kSortBlocks - 1) / kSortBlocks + kTileItems - 1) / kTileItems * kTileItems;
+    begin = min(count, per * blockIdx.x);
+    end = min(count, begin + per);
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(kThreads) hist_kernel(const uint32_t* __restrict__ keys,
+                                                        const uint32_t* count_ptr, int shift,
+                                                        uint32_t* __restrict__ ghist,
+                                                        uint32_t* __restrict__ gid_count,
+                                                        int n_groups) {
+    constexpr int R = 1 << BITS;
+    extern __shared__ uint32_t sh[];  // R digit bins (+ n_groups gid bins when gid_count)
+    uint32_t* dh = sh;
+    uint32_t* gh = sh + R;
+    const bool full = gid_count != nullptr;
+    for (int d = threadIdx.x; d < R; d += kThreads) dh[d] = 0;
+    if (full)
+        for (int g = threadIdx.x; g < n_groups; g += kThreads) gh[g] = 0;
+    __syncthreads();
+    uint32_t begin, end;
+    block_range(*count_ptr, begin, end);
+    if (full) {
+        for (uint32_t i = begin + threadIdx.x; i < end; i += kThreads) atomicAdd(&gh[keys[i]], 1u);
+        __syncthreads();
+        for (int g = threadIdx.x; g < n_groups; g += kThreads) {
+            const uint32_t c = gh[g];
+            if (c) {
+                atomicAdd(&dh[(g >> shift) & (R - 1)], c);
+                atomicAdd(&gid_count[g], c);
+            }
+        }
+    } else {
+        for (uint32_t i = begin + threadIdx.x; i < end; i += kThreads)
+            atomicAdd(&dh[(keys[i] >> shift) & (R - 1)], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < R; d += kThreads) ghist[d * kSortBlocks + blockIdx.x] = dh[d];
+}
+
+// Exclusive scan of n u32 in place, one block of 1024 threads.
+__global__ void __launch_bounds__(1024) scan_inplace_kernel(uint32_t* data, int n) {
+    __shared__ uint32_t warp_tot[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int base = 0; base < n; base += 1024 * 4) {
+        uint32_t v[4], s = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = base + threadIdx.x * 4 + k;
+            v[k] = i < n ? data[i] : 0u;
+            s += v[k];
+        }
+        uint32_t incl = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) warp_tot[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = warp_tot[lane], wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += t;
+            }
+            warp_tot[lane] = wi - w;
+        }
+        __syncthreads();
+        uint32_t run = carry + warp_tot[warp] + incl - s;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = base + threadIdx.x * 4 + k;
+            if (i < n) data[i] = run;
+            run += v[k];
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = run;
+        __syncthreads();
+    }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(kThreads) scatter_kernel(
+    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
+    uint32_t* __restrict__ vout, const uint32_t* count_ptr, int shift,
+    const uint32_t* __restrict__ ghist, bool write_keys) {
+    constexpr int R = 1 << BITS;
+    __shared__ uint32_t blk_off[R];
+    __shared__ uint32_t wcnt[kWarps][R];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int d = threadIdx.x; d < R; d += kThreads) blk_off[d] = ghist[d * kSortBlocks + blockIdx.x];
+    uint32_t begin, end;
+    block_range(*count_ptr, begin, end);
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t tile = begin; tile < end; tile += kTileItems) {
+        for (int d = lane; d < R; d += 32) wcnt[warp][d] = 0;
+        __syncwarp();
+        uint32_t k[kSteps], v[kSteps], rk[kSteps];
+#pragma unroll
+        for (int s = 0; s < kSteps; ++s) {
+            const uint32_t i = tile + warp * (32 * kSteps) + s * 32 + lane;
+            const bool valid = i < end;
+            k[s] = valid ? kin[i] : 0u;
+            v[s] = valid ? vin[i] : 0u;
+            const uint32_t d = (k[s] >> shift) & (R - 1);
+            const uint32_t key = valid ? d : (uint32_t)(R + lane);  // invalid lanes match nobody
+            const uint32_t peers = __match_any_sync(0xffffffffu, key);
+            uint32_t before = 0;
+            if (valid) before = wcnt[warp][d];
+            __syncwarp();
+            if (valid && (31 - __clz(peers)) == lane) wcnt[warp][d] = before + __popc(peers);
+            rk[s] = before + __popc(peers & lt);
+            if (!valid) rk[s] = 0xffffffffu;
+            __syncwarp();
+        }
+        __syncthreads();
+        for (int d = threadIdx.x; d < R; d += kThreads) {
+            uint32_t run = blk_off[d];
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t c = wcnt[w][d];
+                wcnt[w][d] = run;
+                run += c;
+            }
+            blk_off[d] = run;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < kSteps; ++s) {
+            if (rk[s] != 0xffffffffu) {
+                const uint32_t d = (k[s] >> shift) & (R - 1);
+                const uint32_t pos = wcnt[warp][d] + rk[s];
+                if (write_keys) kout[pos] = k[s];
+                vout[pos] = v[s];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int BITS>
+void run_pass(SortBuffers& b, int src, const uint32_t* count, int shift, int n_groups,
+              bool first_gid_pass, bool write_keys, cudaStream_t st) {
+    const int R = 1 << BITS;
+    size_t smem = R * sizeof(uint32_t);
+    uint32_t* gidc = nullptr;
+    if (first_gid_pass) {
+        gidc = b.gid_count;
+        smem += (size_t)n_groups * sizeof(uint32_t);
+        cudaFuncSetAttribute(hist_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    hist_kernel<BITS><<<kSortBlocks, kThreads, smem, st>>>(b.keys[src], count, shift, b.ghist, gidc,
+                                                           n_groups);
+    scan_inplace_kernel<<<1, 1024, 0, st>>>(b.ghist, R * kSortBlocks);
+    scatter_kernel<BITS><<<kSortBlocks, kThreads, 0, st>>>(b.keys[src], b.vals[src], b.keys[src ^ 1],
+                                                           b.vals[src ^ 1], count, shift, b.ghist,
+                                                           write_keys);
+}
+
+typedef void (*PassFn)(SortBuffers&, int, const uint32_t*, int, int, bool, bool, cudaStream_t);
+const PassFn kPass[9] = {nullptr,        run_pass<1>, run_pass<2>, run_pass<3>, run_pass<4>,
+                         run_pass<5>,    run_pass<6>, run_pass<7>, run_pass<8>};
+
+}  // namespace
+
+int radix_sort(SortBuffers& b, const uint32_t* count, int nbits, int n_groups, bool want_keys_last,
+               cudaStream_t st) {
+    if (nbits < 1) nbits = 1;
+    const int passes = (nbits + 7) / 8;
+    const int per = (nbits + passes - 1) / passes;
+    int src = 0, shift = 0;
+    for (int p = 0; p < passes; ++p) {
+        const int bits = (p == passes - 1) ? nbits - shift : per;
+        const bool last = p == passes - 1;
+        kPass[bits](b, src, count, shift, n_groups, p == 0 && b.gid_count != nullptr,
+                    !last || want_keys_last, st);
+        src ^= 1;
+        shift += bits;
+    }
+    return src;
+}
+
+void launch_offsets_scan(const uint32_t* counts, uint32_t* offsets, int n, cudaStream_t st) {
+    // offsets[0..n]: copy counts into offsets[0..n-1], offsets[n] = 0, exclusive scan n+1 values
+    cudaMemcpyAsync(offsets, counts, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
+    cudaMemsetAsync(offsets + n, 0, sizeof(uint32_t), st);
+    scan_inplace_kernel<<<1, 1024, 0, st>>>(offsets, n + 1);
+}
+
+}  // namespace tgs

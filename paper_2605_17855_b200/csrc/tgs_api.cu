@@ -103,7 +103,7 @@ struct tgs_ctx {
     DBuf pre_keys[2], pre_vals[2];
     DBuf ngroups, eoff;
     DBuf ent_keys[2], ent_vals[2];
-    DBuf ghist, gid_count, offsets;
+    DBuf ghist, gid_count, offsets, order;
     DBuf image;
     DBuf scratch_records;
     FrameCounters* h_fc = nullptr;  // pinned
@@ -225,6 +225,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     TGS_CUDA_OK(ctx->ghist.ensure((size_t)256 * kSortBlocks * 4));
     TGS_CUDA_OK(ctx->gid_count.ensure((size_t)n_groups * 4));
     TGS_CUDA_OK(ctx->offsets.ensure((size_t)(n_groups + 1) * 4));
+    TGS_CUDA_OK(ctx->order.ensure((size_t)n_groups * 4));
     const int row0 = band0 * gg.g * kTile;
     const int row1 = std::min(cam->height, band1 * gg.g * kTile);
     TGS_CUDA_OK(ctx->image.ensure((size_t)(row1 - row0) * cam->width * 3 * sizeof(float)));
@@ -293,6 +294,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     eb.gid_count = ctx->gid_count.as<uint32_t>();
     const int er = radix_sort(eb, &fc->n_sort, std::max(1, ceil_log2(n_groups)), n_groups, false, s);
     launch_offsets_scan(eb.gid_count, ctx->offsets.as<uint32_t>(), n_groups, s);
+    launch_group_order(ctx->offsets.as<uint32_t>(), n_groups, ctx->order.as<int>(), s);
     TGS_CUDA_OK(cudaGetLastError());
     TGS_CUDA_OK(cudaEventRecord(ctx->ev[3], s));
 
@@ -301,6 +303,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     ra.proj = proj;
     ra.list = eb.vals[er];
     ra.offsets = ctx->offsets.as<uint32_t>();
+    ra.order = ctx->order.as<int>();
     ra.gg = gg;
     ra.image = ctx->image.as<float>();
     ra.image_row0 = row0;
@@ -467,7 +470,7 @@ void tgs_ctx_destroy(tgs_ctx* c) {
     if (c->scratch_scene) tgs_scene_free(c->scratch_scene);
     DBuf* bufs[] = {&c->fc, &c->status, &c->proj, &c->pre_keys[0], &c->pre_keys[1], &c->pre_vals[0],
                     &c->pre_vals[1], &c->ngroups, &c->eoff, &c->ent_keys[0], &c->ent_keys[1],
-                    &c->ent_vals[0], &c->ent_vals[1], &c->ghist, &c->gid_count, &c->offsets,
+                    &c->ent_vals[0], &c->ent_vals[1], &c->ghist, &c->gid_count, &c->offsets, &c->order,
                     &c->image, &c->scratch_records};
     for (DBuf* b : bufs) b->release();
     for (auto& e : c->ev)
@@ -636,6 +639,7 @@ tgs_status tgs_count_pairs(tgs_ctx* ctx, uint64_t* walked, uint64_t* blended) {
     ra.proj = dev_proj(ctx);
     ra.list = ctx->ent_vals[ctx->list_parity].as<uint32_t>();
     ra.offsets = ctx->offsets.as<uint32_t>();
+    ra.order = nullptr;
     ra.gg = ctx->last_gg;
     ra.image = nullptr;
     ra.image_row0 = 0;

@@ -175,7 +175,38 @@ __global__ void encode_u8_kernel(const float* __restrict__ rgb, int64_t n, uint8
     }
 }
 
+// Longest-processing-time-first schedule (bucketed): both rasterisers take groups from this order,
+// so the heaviest lists start first and the tail of the persistent grid is short lists.
+__global__ void __launch_bounds__(1024) group_order_kernel(const uint32_t* __restrict__ offsets, int n,
+                                                           int* __restrict__ order) {
+    __shared__ uint32_t cnt[33];
+    if (threadIdx.x < 33) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int g = threadIdx.x; g < n; g += blockDim.x) {
+        const uint32_t len = offsets[g + 1] - offsets[g];
+        atomicAdd(&cnt[__clz(len + 1u)], 1u);  // key 0 = longest bucket
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int k = 0; k < 33; ++k) {
+            const uint32_t c = cnt[k];
+            cnt[k] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (int g = threadIdx.x; g < n; g += blockDim.x) {
+        const uint32_t len = offsets[g + 1] - offsets[g];
+        order[atomicAdd(&cnt[__clz(len + 1u)], 1u)] = g;
+    }
+}
+
 }  // namespace
+
+void launch_group_order(const uint32_t* offsets, int n_groups, int* order, cudaStream_t st) {
+    if (n_groups > 0) group_order_kernel<<<1, 1024, 0, st>>>(offsets, n_groups, order);
+}
 
 void launch_entry_scan(const BinArgs& a, int max_items, cudaStream_t st) {
     const int blocks = (max_items + kScanTile - 1) / kScanTile;

@@ -61,6 +61,7 @@ struct RasterArgs {
     DevProjected proj;
     const uint32_t* list;     // sorted compacted indices
     const uint32_t* offsets;  // [n_groups + 1]
+    const int* order;         // group processing order (longest lists first) or null
     GroupGeom gg;
     float* image;             // H x W x 3 (band rows only when banded)
     int image_row0;           // first image row stored in `image`
@@ -68,6 +69,8 @@ struct RasterArgs {
     FrameCounters* fc;
 };
 void launch_raster_scalar(const RasterArgs& a, cudaStream_t st);
+// LPT schedule for the rasterisers: groups bucketed by floor(log2(list length)), longest first.
+void launch_group_order(const uint32_t* offsets, int n_groups, int* order, cudaStream_t st);
 void launch_raster_tensor(const RasterArgs& a, int num_sms, cudaStream_t st);
 // Instrumented walk: counts walked / alpha-contributing pairs (reference semantics, G=1 lists).
 void launch_count_pairs(const RasterArgs& a, cudaStream_t st);

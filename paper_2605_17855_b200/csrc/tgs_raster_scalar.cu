@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256) raster_scalar_kernel(RasterArgs a) {
     __shared__ float4 s_gc[kBatch];   // q3=-c/2*log2e, opacity, r, g
     __shared__ float s_b[kBatch];     // b
     const GroupGeom& gg = a.gg;
-    const int tile = blockIdx.x;
+    const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
     const int tx = tile % gg.tiles_x, ty = tile / gg.tiles_x + gg.band_gy0;  // G == 1: group == tile
     const int px = tx * kTile + (threadIdx.x & 15);
     const int py = ty * kTile + (threadIdx.x >> 4);

@@ -48,13 +48,18 @@ struct Cfg {
     static constexpr int TILES = G * G;
     static constexpr int MT = 2 * TILES;                      // 128-pixel M-tiles
     static constexpr int N = (G == 4) ? 16 : 32;              // splats per chunk (MMA N)
-    static constexpr int STAGES = (G == 4) ? 1 : 2;
-    static constexpr int COLS_USED = STAGES * MT * N;
+    static constexpr int TS = (G == 4) ? 1 : 2;               // TMEM accumulator stages
+    static constexpr int SS = 3;                              // smem (operand + epilogue data) stages
+    static constexpr int COLS_USED = TS * MT * N;
     static constexpr int TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
                                      : COLS_USED <= 256 ? 256 : 512;
-    static constexpr int EPI = (G == 1) ? 8 : 16;             // epilogue warps
-    static constexpr int PPT = MT * 4 / EPI;                  // pixels per epilogue thread
-    static constexpr int THREADS = (EPI + 2) * 32;
+    static constexpr int EPI = (G == 1) ? 4 : (G == 2) ? 8 : 16;  // epilogue warps
+    static constexpr int PPT = MT * 4 / EPI;                  // pixels per epilogue thread (2, 4, 8)
+    static constexpr int PB = PPT < 4 ? PPT : 4;              // pixels blended together (ILP)
+    static constexpr int JB = 32 / PB;                        // splat columns per TMEM load block
+    static constexpr int PROD = (G == 1) ? 1 : 4;             // producer warps
+    static constexpr int TPP = TILES / PROD;                  // tiles per producer warp
+    static constexpr int THREADS = (EPI + PROD + 1) * 32;
     static constexpr int CTAS_PER_SM = 512 / TMEM_COLS;
     static constexpr int B_BYTES = N * 32;                    // one tile's B operand
 };
@@ -66,14 +71,16 @@ struct ChunkHeader {
 
 template <int G>
 struct Smem {
-    alignas(128) uint8_t a[256 * 32];                                        // pixel monomials
-    alignas(128) uint8_t b[Cfg<G>::STAGES][Cfg<G>::TILES][Cfg<G>::B_BYTES];  // splat rows
-    float4 epi[Cfg<G>::STAGES][Cfg<G>::N];                                   // r, g, b, min(clamp, o)
-    ChunkHeader hdr[Cfg<G>::STAGES];
-    int alive[Cfg<G>::STAGES];
-    uint64_t full[Cfg<G>::STAGES];      // producer -> MMA
-    uint64_t tfull[Cfg<G>::STAGES];     // MMA -> epilogue (tcgen05.commit)
-    uint64_t done[Cfg<G>::STAGES];      // epilogue -> producer (stage reusable)
+    alignas(128) uint8_t a[256 * 32];                                     // pixel monomials
+    alignas(128) uint8_t b[Cfg<G>::SS][Cfg<G>::TILES][Cfg<G>::B_BYTES];   // splat rows
+    float4 epi[Cfg<G>::SS][Cfg<G>::N];                                    // r, g, b, min(clamp, o)
+    ChunkHeader hdr[Cfg<G>::SS];
+    int alive_tag[Cfg<G>::SS];        // max over epilogue warps of (chunk << 1 | any pixel alive)
+    int gq[2];                        // group ticket broadcast to producer warps
+    uint64_t full[Cfg<G>::SS];        // producers -> MMA          (count PROD)
+    uint64_t done[Cfg<G>::SS];        // epilogue -> producers     (count EPI): smem stage reusable
+    uint64_t tfull[Cfg<G>::TS];       // MMA -> epilogue           (tcgen05.commit)
+    uint64_t tempty[Cfg<G>::TS];      // epilogue -> MMA           (count EPI): TMEM stage drained
     uint32_t tmem_base;
 };
 
@@ -87,6 +94,49 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Coefficient row of one splat for one tile (centre (ox, oy)) as FP16 hi/lo halves.
+__device__ __forceinline__ void make_row(bool ok, float mx, float my, float qa, float qb, float qc, float lo2,
+                                         float ox, float oy, uint4& r0, uint4& r1) {
+    float w[6];
+    if (ok) {
+        const float dx = mx - ox, dy = my - oy;
+        const float ha = 0.5f * qa, hc = 0.5f * qc;
+        w[0] = -ha * kLog2e;
+        w[1] = -qb * kLog2e;
+        w[2] = -hc * kLog2e;
+        w[3] = fmaf(qa, dx, qb * dy) * kLog2e;
+        w[4] = fmaf(qb, dx, qc * dy) * kLog2e;
+        const float quad = fmaf(ha * dx, dx, fmaf(qb * dx, dy, hc * dy * dy));
+        w[5] = fmaf(-quad, kLog2e, lo2);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) ok = ok && fabsf(w[k]) <= 16384.0f;
+    }
+    if (ok) {
+        float h[6], l[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            h[k] = __half2float(__float2half_rn(w[k]));
+            l[k] = w[k] - h[k];
+        }
+        r0.x = pack_half2(h[0], h[1]);
+        r0.y = pack_half2(h[2], h[3]);
+        r0.z = pack_half2(h[4], h[5]);
+        r0.w = pack_half2(l[0], l[1]);
+        r1.x = pack_half2(l[2], l[3]);
+        r1.y = pack_half2(l[4], l[5]);
+    } else {
+        r0 = make_uint4(0u, 0u, pack_half2(0.0f, kNeverRow), 0u);
+        r1.x = 0u;
+        r1.y = 0u;
+    }
+    r1.z = 0u;
+    r1.w = 0u;
+}
+
 template <int G>
 __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(RasterArgs a) {
     using C = Cfg<G>;
@@ -95,10 +145,10 @@ __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(Raste
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const GroupGeom& gg = a.gg;
     const int n_groups = gg.n_groups_band;
+    constexpr int kProd0 = C::EPI, kMma = C::EPI + C::PROD;
 
     // ---- setup: A operand, barriers, TMEM ----------------------------------------------------
-    if (threadIdx.x < 256) {
-        const int p = threadIdx.x;
+    for (int p = threadIdx.x; p < 256; p += blockDim.x) {
         const float ux = (float)(p & 15) - 7.5f, uy = (float)(p >> 4) - 7.5f;
         const float phi[6] = {ux * ux, ux * uy, uy * uy, ux, uy, 1.0f};
         uint4 lo, hi;
@@ -114,36 +164,46 @@ __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(Raste
         *reinterpret_cast<uint4*>(sm.a + core_off(p, 1)) = hi;
     }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < C::STAGES; ++s) {
-            ptx::mbar_init(&sm.full[s], 1);
-            ptx::mbar_init(&sm.tfull[s], 1);
+        for (int s = 0; s < C::SS; ++s) {
+            ptx::mbar_init(&sm.full[s], C::PROD);
             ptx::mbar_init(&sm.done[s], C::EPI);
-            sm.alive[s] = 0;
+            sm.alive_tag[s] = -1;
+        }
+        for (int s = 0; s < C::TS; ++s) {
+            ptx::mbar_init(&sm.tfull[s], 1);
+            ptx::mbar_init(&sm.tempty[s], C::EPI);
         }
         ptx::mbar_fence_init();
     }
-    if (warp == C::EPI + 1) ptx::tmem_alloc<C::TMEM_COLS>(&sm.tmem_base);
+    if (warp == kMma) ptx::tmem_alloc<C::TMEM_COLS>(&sm.tmem_base);
     ptx::fence_proxy_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
-    if (warp == C::EPI) {
-        // ================================ producer ===========================================
-        const float L = a.alpha_skip;
+    if (warp >= kProd0 && warp < kMma) {
+        // ================================ producers ==========================================
+        // Producer warp p builds the coefficient rows of tiles [p*TPP, (p+1)*TPP) for all N splats
+        // of the chunk (lane = splat); warp 0 also writes the epilogue data and the header.
+        const int p = warp - kProd0;
+        const float skip = a.alpha_skip;
         uint32_t c = 0;
+        int slot = 0;
         for (;;) {
-            int g = 0;
-            if (lane == 0) g = (int)atomicAdd(&a.fc->group_counter, 1u);
-            g = __shfl_sync(0xffffffffu, g, 0);
-            if (g >= n_groups) break;
+            if (p == 0 && lane == 0) {
+                const int t = (int)atomicAdd(&a.fc->group_counter, 1u);
+                sm.gq[slot] = t < n_groups ? (a.order ? a.order[t] : t) : -1;
+            }
+            if (C::PROD > 1) named_bar_sync(1, C::PROD * 32); else __syncwarp();
+            const int g = sm.gq[slot];
+            slot ^= 1;
+            if (g < 0) break;
             const int gx = g % gg.groups_x, gy = g / gg.groups_x + gg.band_gy0;
             const uint32_t begin = a.offsets[g], end = a.offsets[g + 1];
             const uint32_t nchunks = end > begin ? (end - begin + C::N - 1) / C::N : 1u;
             for (uint32_t ch = 0; ch < nchunks; ++ch, ++c) {
-                const int s = (int)(c % C::STAGES);
-                // prefetch this lane's splat before waiting for the stage
+                const int s = (int)(c % C::SS);
                 const uint32_t e = begin + ch * C::N + (uint32_t)lane;
                 const bool valid = lane < C::N && e < end;
                 float4 mc = make_float4(0, 0, 0, 0), co = mc, col = mc;
@@ -151,77 +211,42 @@ __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(Raste
                     const uint32_t idx = a.list[e];
                     mc = a.proj.mc[idx];
                     co = a.proj.co[idx];
-                    col = a.proj.col[idx];
+                    if (p == 0) col = a.proj.col[idx];
                 }
-                if (c >= (uint32_t)C::STAGES) {
-                    ptx::mbar_wait(&sm.done[s], ((c / C::STAGES) - 1) & 1);
-                    const int alive = sm.alive[s];
-                    __syncwarp();
-                    if (lane == 0) sm.alive[s] = 0;
-                    // chunk c-STAGES belonged to this group and left nothing alive: retire
-                    if (ch >= (uint32_t)C::STAGES && !alive) break;
+                if (c >= (uint32_t)C::SS) {
+                    ptx::mbar_wait(&sm.done[s], ((c / C::SS) - 1) & 1);
+                    const int tag = sm.alive_tag[s];
+                    // the last chunk of this group in this stage left no pixel alive: retire
+                    if (ch >= (uint32_t)C::SS && tag == (int)((c - C::SS) << 1)) break;
                 }
-                // per-tile coefficient rows of this lane's splat
                 int tx0 = 0, ty0 = 0, tx1 = -1, ty1 = -1;
-                float c_o = 0.0f;
+                float c_o = 0.0f, lo2 = 0.0f;
                 if (valid) {
                     tile_rect(mc.x, mc.y, __float_as_int(co.w), gg.tiles_x, gg.tiles_y, tx0, ty0, tx1, ty1);
                     c_o = fminf(a.alpha_clamp, co.y);
+                    lo2 = lg2_approx(co.y);
                 }
-                const bool can = valid && !(c_o < L);
-                const double qa = mc.z, qb = mc.w, qc = co.x;
-                const double lo2 = can ? (double)lg2_approx(co.y) : 0.0;
+                const bool can = valid && !(c_o < skip);
 #pragma unroll
-                for (int t = 0; t < C::TILES; ++t) {
+                for (int tt = 0; tt < C::TPP; ++tt) {
+                    const int t = p * C::TPP + tt;
                     const int tcx = gx * G + (t % G), tcy = gy * G + (t / G);
-                    float w[6];
-                    bool row_ok = can && tcx >= tx0 && tcx <= tx1 && tcy >= ty0 && tcy <= ty1;
-                    if (row_ok) {
-                        const double mx = (double)mc.x - (double)(tcx * kTile + 8);
-                        const double my = (double)mc.y - (double)(tcy * kTile + 8);
-                        const double L2E = 1.4426950408889634;
-                        w[0] = (float)(-0.5 * qa * L2E);
-                        w[1] = (float)(-qb * L2E);
-                        w[2] = (float)(-0.5 * qc * L2E);
-                        w[3] = (float)((qa * mx + qb * my) * L2E);
-                        w[4] = (float)((qb * mx + qc * my) * L2E);
-                        w[5] = (float)(-(0.5 * qa * mx * mx + qb * mx * my + 0.5 * qc * my * my) * L2E + lo2);
-#pragma unroll
-                        for (int k = 0; k < 6; ++k) row_ok = row_ok && fabsf(w[k]) <= 16384.0f;
-                    }
+                    const bool row_ok = can && tcx >= tx0 && tcx <= tx1 && tcy >= ty0 && tcy <= ty1;
                     uint4 r0, r1;
-                    if (row_ok) {
-                        float h[6], l[6];
-#pragma unroll
-                        for (int k = 0; k < 6; ++k) {
-                            h[k] = __half2float(__float2half_rn(w[k]));
-                            l[k] = w[k] - h[k];
-                        }
-                        r0.x = pack_half2(h[0], h[1]);
-                        r0.y = pack_half2(h[2], h[3]);
-                        r0.z = pack_half2(h[4], h[5]);
-                        r0.w = pack_half2(l[0], l[1]);
-                        r1.x = pack_half2(l[2], l[3]);
-                        r1.y = pack_half2(l[4], l[5]);
-                    } else {
-                        r0.x = 0u;
-                        r0.y = 0u;
-                        r0.z = pack_half2(0.0f, kNeverRow);
-                        r0.w = 0u;
-                        r1.x = 0u;
-                        r1.y = 0u;
-                    }
-                    r1.z = 0u;
-                    r1.w = 0u;
+                    make_row(row_ok, mc.x, mc.y, mc.z, mc.w, co.x, lo2, (float)(tcx * kTile + 8),
+                             (float)(tcy * kTile + 8), r0, r1);
                     if (lane < C::N) {
                         *reinterpret_cast<uint4*>(&sm.b[s][t][core_off(lane, 0)]) = r0;
                         *reinterpret_cast<uint4*>(&sm.b[s][t][core_off(lane, 1)]) = r1;
                     }
                 }
-                if (lane < C::N) sm.epi[s][lane] = make_float4(col.x, col.y, col.z, c_o);
-                if (lane == 0) {
-                    sm.hdr[s].gid = g;
-                    sm.hdr[s].n_valid = (int)min((uint32_t)C::N, end > begin + ch * C::N ? end - begin - ch * C::N : 0u);
+                if (p == 0) {
+                    if (lane < C::N) sm.epi[s][lane] = make_float4(col.x, col.y, col.z, c_o);
+                    if (lane == 0) {
+                        sm.hdr[s].gid = g;
+                        sm.hdr[s].n_valid =
+                            (int)min((uint32_t)C::N, end > begin + ch * C::N ? end - begin - ch * C::N : 0u);
+                    }
                 }
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
@@ -229,21 +254,24 @@ __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(Raste
             }
         }
         // end of stream
-        const int s = (int)(c % C::STAGES);
-        if (c >= (uint32_t)C::STAGES) ptx::mbar_wait(&sm.done[s], ((c / C::STAGES) - 1) & 1);
+        const int s = (int)(c % C::SS);
+        if (c >= (uint32_t)C::SS) ptx::mbar_wait(&sm.done[s], ((c / C::SS) - 1) & 1);
         if (lane == 0) {
-            sm.hdr[s].gid = -1;
-            sm.hdr[s].n_valid = 0;
+            if (p == 0) {
+                sm.hdr[s].gid = -1;
+                sm.hdr[s].n_valid = 0;
+            }
             ptx::mbar_arrive(&sm.full[s]);
         }
         __syncwarp();
-    } else if (warp == C::EPI + 1) {
+    } else if (warp == kMma) {
         // ================================ MMA issuer ==========================================
         constexpr uint32_t idesc = ptx::idesc_f16(128, C::N);
         const uint32_t a_base = ptx::smem_u32(sm.a);
         for (uint32_t c = 0;; ++c) {
-            const int s = (int)(c % C::STAGES);
-            ptx::mbar_wait(&sm.full[s], (c / C::STAGES) & 1);
+            const int s = (int)(c % C::SS), ts = (int)(c % C::TS);
+            ptx::mbar_wait(&sm.full[s], (c / C::SS) & 1);
+            if (c >= (uint32_t)C::TS) ptx::mbar_wait(&sm.tempty[ts], ((c / C::TS) - 1) & 1);
             ptx::tc_fence_after();
             const ChunkHeader h = sm.hdr[s];
             if (lane == 0) {
@@ -252,11 +280,11 @@ __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(Raste
                     for (int m = 0; m < C::MT; ++m) {
                         const uint64_t ad = ptx::smem_desc(a_base + (uint32_t)(m & 1) * 4096u, 128, 256);
                         const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[s][m >> 1][0]), 128, 256);
-                        ptx::mma_f16_ss(tmem + (uint32_t)(s * C::MT * C::N + m * C::N), ad, bd, idesc, 0u);
+                        ptx::mma_f16_ss(tmem + (uint32_t)(ts * C::MT * C::N + m * C::N), ad, bd, idesc, 0u);
                     }
-                    ptx::mma_commit(&sm.tfull[s]);
+                    ptx::mma_commit(&sm.tfull[ts]);
                 } else {
-                    ptx::mbar_arrive(&sm.tfull[s]);
+                    ptx::mbar_arrive(&sm.tfull[ts]);
                 }
             }
             __syncwarp();
@@ -264,24 +292,30 @@ __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(Raste
         }
     } else {
         // ================================ epilogue ============================================
-        const int q = warp & 3;  // TMEM lane quadrant of this warp
-        int mtile[C::PPT];
-        int prow[C::PPT], pcol[C::PPT];
+        // warp w: TMEM lane quadrant q = w % 4; M-tiles m_k = w/4 + k * EPI/4 (k < PPT), which for
+        // G = 2 gives every thread one pixel in each of the 4 member tiles (balanced work per warp,
+        // PB = 4 independent blend chains per thread).
+        const int q = warp & 3;
+        const int mg = warp >> 2;
+        int prow[C::PPT], pcol[C::PPT], ptile[C::PPT], pm[C::PPT];
 #pragma unroll
         for (int k = 0; k < C::PPT; ++k) {
-            mtile[k] = (warp >> 2) + k * (C::EPI / 4);
-            const int p = (mtile[k] & 1) * 128 + q * 32 + lane;  // pixel within its tile
-            prow[k] = p >> 4;
-            pcol[k] = p & 15;
+            const int m = mg + k * (C::EPI / 4);
+            const int pix = (m & 1) * 128 + q * 32 + lane;  // pixel within its tile
+            pm[k] = m;
+            prow[k] = pix >> 4;
+            pcol[k] = pix & 15;
+            ptile[k] = m >> 1;
         }
         float T[C::PPT], cr[C::PPT], cg[C::PPT], cb[C::PPT], thr[C::PPT];
         int px[C::PPT], py[C::PPT];
         bool inside[C::PPT];
         const float L = log2f(a.alpha_skip);
+        const float tterm = a.t_terminate;
         int cur = -1;
         for (uint32_t c = 0;; ++c) {
-            const int s = (int)(c % C::STAGES);
-            ptx::mbar_wait(&sm.tfull[s], (c / C::STAGES) & 1);
+            const int s = (int)(c % C::SS), ts = (int)(c % C::TS);
+            ptx::mbar_wait(&sm.tfull[ts], (c / C::TS) & 1);
             ptx::tc_fence_after();
             const ChunkHeader h = sm.hdr[s];
             if (h.gid != cur) {
@@ -300,7 +334,7 @@ __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(Raste
                 const int gx = cur % gg.groups_x, gy = cur / gg.groups_x + gg.band_gy0;
 #pragma unroll
                 for (int k = 0; k < C::PPT; ++k) {
-                    const int t = mtile[k] >> 1;
+                    const int t = ptile[k];
                     const int tx = gx * G + (t % G), ty = gy * G + (t / G);
                     px[k] = tx * kTile + pcol[k];
                     py[k] = ty * kTile + prow[k];
@@ -313,41 +347,91 @@ __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(Raste
             bool any = false;
 #pragma unroll
             for (int k = 0; k < C::PPT; ++k) any = any || thr[k] != kInf;
-            const bool warp_alive = __any_sync(0xffffffffu, any);
-            if (h.n_valid > 0 && warp_alive) {
-                constexpr int PP = C::PPT >= 2 ? 2 : 1;  // pixels blended together (ILP)
+            const bool work = h.n_valid > 0 && __any_sync(0xffffffffu, any);
+            const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ts * C::MT * C::N);
+            // D is consumed in blocks of PB pixels x JB splats (32 registers); the TMEM stage is
+            // released as soon as the warp's last block is in registers.
+            constexpr int NBLK = (C::PPT / C::PB) * (C::N / C::JB);
 #pragma unroll
-                for (int k0 = 0; k0 < C::PPT; k0 += PP) {
-                    uint32_t d[PP][C::N];
+            for (int blk = 0; blk < NBLK; ++blk) {
+                const int k0 = (blk / (C::N / C::JB)) * C::PB;
+                const int j0 = (blk % (C::N / C::JB)) * C::JB;
+                uint32_t d[C::PB][C::JB];
+                if (work) {
 #pragma unroll
-                    for (int kk = 0; kk < PP; ++kk) {
-                        const uint32_t col0 = (uint32_t)(s * C::MT * C::N + mtile[k0 + kk] * C::N);
-#pragma unroll
-                        for (int j0 = 0; j0 < C::N; j0 += 16)
-                            ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + col0 + j0, &d[kk][j0]);
+                    for (int kk = 0; kk < C::PB; ++kk) {
+                        const uint32_t ad = lane_base + (uint32_t)(pm[k0 + kk] * C::N + j0);
+                        if constexpr (C::JB == 16) ptx::tmem_ld16(ad, d[kk]); else ptx::tmem_ld8(ad, d[kk]);
                     }
                     ptx::tmem_wait_ld();
 #pragma unroll
-                    for (int kk = 0; kk < PP; ++kk)
+                    for (int kk = 0; kk < C::PB; ++kk) {
+                        if constexpr (C::JB == 16) ptx::reg_fence16(d[kk]); else ptx::reg_fence8(d[kk]);
+                    }
+                }
+                if (blk == NBLK - 1) {
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&sm.tempty[ts]);
+                }
+                if (!work) continue;
+                // Speculative pass: blend every splat with D >= thr without the per-splat
+                // termination test (no loop-carried compare chain); T only decreases, so
+                // T_end < t_terminate <=> the pixel terminated inside this block, in which case
+                // the block is replayed exactly below (at most once per pixel per group).
+                float T0[C::PB], r0[C::PB], g0[C::PB], b0[C::PB];
 #pragma unroll
-                        for (int j0 = 0; j0 < C::N; j0 += 16) ptx::reg_fence16(&d[kk][j0]);
+                for (int kk = 0; kk < C::PB; ++kk) {
+                    T0[kk] = T[k0 + kk];
+                    r0[kk] = cr[k0 + kk];
+                    g0[kk] = cg[k0 + kk];
+                    b0[kk] = cb[k0 + kk];
+                }
 #pragma unroll
-                    for (int j = 0; j < C::N; ++j) {
-                        const float4 ej = sm.epi[s][j];
+                for (int jj = 0; jj < C::JB; ++jj) {
+                    bool tk[C::PB], anyt = false;
 #pragma unroll
-                        for (int kk = 0; kk < PP; ++kk) {
+                    for (int kk = 0; kk < C::PB; ++kk) {
+                        tk[kk] = __uint_as_float(d[kk][jj]) >= thr[k0 + kk];
+                        anyt = anyt || tk[kk];
+                    }
+                    if (anyt) {
+                        const float4 ej = sm.epi[s][j0 + jj];
+#pragma unroll
+                        for (int kk = 0; kk < C::PB; ++kk) {
                             const int k = k0 + kk;
-                            const float dv = __uint_as_float(d[kk][j]);
-                            if (dv >= thr[k]) {
-                                const float al = fminf(ej.w, ex2_approx(dv));
-                                const float wt = T[k] * al;
+                            const float al = tk[kk] ? fminf(ej.w, ex2_approx(__uint_as_float(d[kk][jj]))) : 0.0f;
+                            const float wt = T[k] * al;
+                            cr[k] = fmaf(wt, ej.x, cr[k]);
+                            cg[k] = fmaf(wt, ej.y, cg[k]);
+                            cb[k] = fmaf(wt, ej.z, cb[k]);
+                            T[k] -= wt;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int kk = 0; kk < C::PB; ++kk) {
+                    const int k = k0 + kk;
+                    if (T[k] < tterm) {  // terminated inside the block: exact replay
+                        T[k] = T0[kk];
+                        cr[k] = r0[kk];
+                        cg[k] = g0[kk];
+                        cb[k] = b0[kk];
+                        bool stop = false;
+#pragma unroll
+                        for (int jj = 0; jj < C::JB; ++jj) {
+                            const float dv = __uint_as_float(d[kk][jj]);
+                            if (!stop && dv >= thr[k]) {
+                                const float4 ej = sm.epi[s][j0 + jj];
+                                const float wt = T[k] * fminf(ej.w, ex2_approx(dv));
                                 cr[k] = fmaf(wt, ej.x, cr[k]);
                                 cg[k] = fmaf(wt, ej.y, cg[k]);
                                 cb[k] = fmaf(wt, ej.z, cb[k]);
-                                T[k] = T[k] - wt;
-                                if (T[k] < a.t_terminate) thr[k] = kInf;
+                                T[k] -= wt;
+                                stop = T[k] < tterm;
                             }
                         }
+                        thr[k] = kInf;
                     }
                 }
             }
@@ -355,10 +439,9 @@ __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(Raste
 #pragma unroll
             for (int k = 0; k < C::PPT; ++k) any = any || thr[k] != kInf;
             const bool still = __any_sync(0xffffffffu, any);
-            ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if (still) sm.alive[s] = 1;
+                atomicMax(&sm.alive_tag[s], (int)((c << 1) | (still ? 1u : 0u)));
                 ptx::mbar_arrive(&sm.done[s]);
             }
         }
@@ -367,7 +450,7 @@ __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(Raste
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    if (warp == C::EPI + 1) ptx::tmem_dealloc<C::TMEM_COLS>(tmem);
+    if (warp == kMma) ptx::tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
 template <int G>

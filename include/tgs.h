@@ -159,6 +159,11 @@ tgs_status tgs_read_lists(tgs_ctx* ctx, tgs_group_entry* out, int64_t cap, uint3
  * DESIGN.md §Roofline); computed by an instrumented pass, not by the timed kernels. */
 tgs_status tgs_count_pairs(tgs_ctx* ctx, uint64_t* walked, uint64_t* blended);
 
+/* Per tile of the last frame (band-local, row-major): how many entries of the tile's
+ * mask-filtered list the slowest pixel walked before terminating (the tile's trip).  Tooling for
+ * load-balance analysis; *n receives the tile count. */
+tgs_status tgs_tile_trips(tgs_ctx* ctx, uint32_t* trips, int64_t cap, int64_t* n);
+
 /* Host-side data formats either side of the path (scene_io.cpp). */
 tgs_status tgs_gen_synthetic_scene(uint64_t seed, int count, float extent, float scale_min,
                                    float scale_max, uint64_t sh_seed, float* out_records);
@@ -169,6 +174,10 @@ tgs_status tgs_encode_u8(tgs_ctx* ctx, const float* rgb_device, int64_t n, uint8
  * same smem descriptors / instruction descriptor the rasterizer uses (row-major A[128][16],
  * B[32][16] as binary16 bit patterns; D[128][32] = A . B^T in FP32). */
 tgs_status tgs_debug_mma(const uint16_t* a_128x16, const uint16_t* b_32x16, float* d_128x32);
+/* Internal microbenchmark of the rasterizer's chunk hand-off protocol (producer -> MMA ->
+ * epilogue): device cycles for `chunks` chunks with no blending work; mode bits: 1 issue MMAs,
+ * 2 tcgen05.ld the accumulators, 4 producer proxy fence. */
+tgs_status tgs_debug_pipeline(int chunks, int mode, long long* cycles);
 
 #ifdef __cplusplus
 }

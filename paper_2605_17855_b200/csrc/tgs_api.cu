@@ -225,7 +225,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     TGS_CUDA_OK(ctx->ghist.ensure((size_t)256 * kSortBlocks * 4));
     TGS_CUDA_OK(ctx->gid_count.ensure((size_t)n_groups * 4));
     TGS_CUDA_OK(ctx->offsets.ensure((size_t)(n_groups + 1) * 4));
-    TGS_CUDA_OK(ctx->order.ensure((size_t)n_groups * 4));
+    TGS_CUDA_OK(ctx->order.ensure((size_t)gg.tiles_x * gg.tiles_y * 4));
     const int row0 = band0 * gg.g * kTile;
     const int row1 = std::min(cam->height, band1 * gg.g * kTile);
     TGS_CUDA_OK(ctx->image.ensure((size_t)(row1 - row0) * cam->width * 3 * sizeof(float)));
@@ -294,7 +294,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     eb.gid_count = ctx->gid_count.as<uint32_t>();
     const int er = radix_sort(eb, &fc->n_sort, std::max(1, ceil_log2(n_groups)), n_groups, false, s);
     launch_offsets_scan(eb.gid_count, ctx->offsets.as<uint32_t>(), n_groups, s);
-    launch_group_order(ctx->offsets.as<uint32_t>(), n_groups, ctx->order.as<int>(), s);
+    launch_tile_order(ctx->offsets.as<uint32_t>(), gg, ctx->order.as<int>(), s);
     TGS_CUDA_OK(cudaGetLastError());
     TGS_CUDA_OK(cudaEventRecord(ctx->ev[3], s));
 
@@ -311,6 +311,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     ra.alpha_clamp = opt->alpha_clamp;
     ra.t_terminate = opt->t_terminate;
     ra.fc = fc;
+    ra.tile_trip = nullptr;
     if (opt->backend == TGS_BACKEND_SCALAR)
         launch_raster_scalar(ra, s);
     else
@@ -630,6 +631,38 @@ tgs_status tgs_read_lists(tgs_ctx* ctx, tgs_group_entry* out, int64_t cap, uint3
     return TGS_OK;
 }
 
+tgs_status tgs_tile_trips(tgs_ctx* ctx, uint32_t* trips, int64_t cap, int64_t* n) {
+    if (!ctx || !n) return set_err(TGS_ERR_VALIDATION, "tile_trips: null argument");
+    if (!ctx->last_scene) return set_err(TGS_ERR_VALIDATION, "tile_trips: no frame rendered yet");
+    const GroupGeom& gg = ctx->last_gg;
+    const int tiles = gg.tiles_x * (gg.band_gy1 - gg.band_gy0) * gg.g;
+    *n = tiles;
+    if (!trips || cap < tiles) return TGS_OK;
+    DBuf tmp;
+    TGS_CUDA_OK(tmp.ensure((size_t)tiles * 4));
+    FrameCounters* fc = ctx->fc.as<FrameCounters>();
+    RasterArgs ra;
+    ra.proj = dev_proj(ctx);
+    ra.list = ctx->ent_vals[ctx->list_parity].as<uint32_t>();
+    ra.offsets = ctx->offsets.as<uint32_t>();
+    ra.order = nullptr;
+    ra.gg = gg;
+    ra.image = nullptr;
+    ra.image_row0 = 0;
+    ra.alpha_skip = ctx->last_opt.alpha_skip;
+    ra.alpha_clamp = ctx->last_opt.alpha_clamp;
+    ra.t_terminate = ctx->last_opt.t_terminate;
+    ra.fc = fc;
+    ra.tile_trip = tmp.as<uint32_t>();
+    launch_count_pairs(ra, ctx->stream);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(trips, tmp.p, (size_t)tiles * 4, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    tmp.release();
+    if (e != cudaSuccess) return cuda_fail(e, "tile_trips", __FILE__, __LINE__);
+    return TGS_OK;
+}
+
 tgs_status tgs_count_pairs(tgs_ctx* ctx, uint64_t* walked, uint64_t* blended) {
     if (!ctx || !walked || !blended) return set_err(TGS_ERR_VALIDATION, "count_pairs: null argument");
     if (!ctx->last_scene) return set_err(TGS_ERR_VALIDATION, "count_pairs: no frame rendered yet");
@@ -647,6 +680,7 @@ tgs_status tgs_count_pairs(tgs_ctx* ctx, uint64_t* walked, uint64_t* blended) {
     ra.alpha_clamp = ctx->last_opt.alpha_clamp;
     ra.t_terminate = ctx->last_opt.t_terminate;
     ra.fc = fc;
+    ra.tile_trip = nullptr;
     launch_count_pairs(ra, ctx->stream);
     TGS_CUDA_OK(cudaGetLastError());
     unsigned long long h[2];

@@ -175,17 +175,21 @@ __global__ void encode_u8_kernel(const float* __restrict__ rgb, int64_t n, uint8
     }
 }
 
-// Longest-processing-time-first schedule (bucketed): both rasterisers take groups from this order,
-// so the heaviest lists start first and the tail of the persistent grid is short lists.
-__global__ void __launch_bounds__(1024) group_order_kernel(const uint32_t* __restrict__ offsets, int n,
-                                                           int* __restrict__ order) {
+// Longest-processing-time-first schedule (bucketed): the rasterisers take tiles in this order, so
+// tiles with the longest group lists start first and the tail of the persistent grid is short.
+// Work estimate of a tile = length of its group's list.
+__global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __restrict__ offsets, GroupGeom gg,
+                                                          int n_tiles, int* __restrict__ order) {
     __shared__ uint32_t cnt[33];
     if (threadIdx.x < 33) cnt[threadIdx.x] = 0;
     __syncthreads();
-    for (int g = threadIdx.x; g < n; g += blockDim.x) {
-        const uint32_t len = offsets[g + 1] - offsets[g];
-        atomicAdd(&cnt[__clz(len + 1u)], 1u);  // key 0 = longest bucket
-    }
+    const int trow0 = gg.band_gy0 * gg.g;
+    auto key = [&](int t) {
+        const int tx = t % gg.tiles_x, ty = t / gg.tiles_x + trow0;
+        const int gid = (ty / gg.g - gg.band_gy0) * gg.groups_x + tx / gg.g;
+        return __clz(offsets[gid + 1] - offsets[gid] + 1u);  // 0 = longest bucket
+    };
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&cnt[key(t)], 1u);
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t run = 0;
@@ -196,16 +200,15 @@ __global__ void __launch_bounds__(1024) group_order_kernel(const uint32_t* __res
         }
     }
     __syncthreads();
-    for (int g = threadIdx.x; g < n; g += blockDim.x) {
-        const uint32_t len = offsets[g + 1] - offsets[g];
-        order[atomicAdd(&cnt[__clz(len + 1u)], 1u)] = g;
-    }
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) order[atomicAdd(&cnt[key(t)], 1u)] = t;
 }
 
 }  // namespace
 
-void launch_group_order(const uint32_t* offsets, int n_groups, int* order, cudaStream_t st) {
-    if (n_groups > 0) group_order_kernel<<<1, 1024, 0, st>>>(offsets, n_groups, order);
+void launch_tile_order(const uint32_t* offsets, const GroupGeom& gg, int* order, cudaStream_t st) {
+    const int trows = min(gg.tiles_y, gg.band_gy1 * gg.g) - gg.band_gy0 * gg.g;
+    const int n_tiles = gg.tiles_x * trows;
+    if (n_tiles > 0) tile_order_kernel<<<1, 1024, 0, st>>>(offsets, gg, n_tiles, order);
 }
 
 void launch_entry_scan(const BinArgs& a, int max_items, cudaStream_t st) {

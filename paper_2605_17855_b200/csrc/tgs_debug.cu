@@ -1,0 +1,124 @@
+// Microbenchmark of the rasterizer's chunk hand-off protocol (producer -> MMA -> epilogue ->
+// producer) with no blending work, to measure per-chunk pipeline latency on the device.
+// Exposed as tgs_debug_pipeline (include/tgs.h, internal).
+#include "tgs_common.cuh"
+#include "tgs_kernels.cuh"
+#include "tgs_ptx.cuh"
+
+namespace tgs {
+namespace {
+
+constexpr int kDbgSS = 4, kDbgTS = 2, kDbgEpi = 4;
+
+struct DbgSmem {
+    alignas(128) uint8_t a[256 * 32];
+    alignas(128) uint8_t b[kDbgSS][32 * 32];
+    uint64_t full[kDbgSS], done[kDbgSS], tfull[kDbgTS], tempty[kDbgTS];
+    uint32_t tmem_base;
+};
+
+// mode bit 0: issue the MMAs; bit 1: epilogue tcgen05.ld's the accumulators; bit 2: producer fences
+__global__ void __launch_bounds__(192, 1) debug_pipeline_kernel(int chunks, int mode, long long* out) {
+    __shared__ DbgSmem sm;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 256 * 32 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sm.a)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < kDbgSS * 32 * 32 / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(&sm.b[0][0])[i] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kDbgSS; ++s) {
+            ptx::mbar_init(&sm.full[s], 1);
+            ptx::mbar_init(&sm.done[s], kDbgEpi);
+        }
+        for (int s = 0; s < kDbgTS; ++s) {
+            ptx::mbar_init(&sm.tfull[s], 1);
+            ptx::mbar_init(&sm.tempty[s], kDbgEpi);
+        }
+        ptx::mbar_fence_init();
+    }
+    if (warp == 5) ptx::tmem_alloc<128>(&sm.tmem_base);
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+    const long long t0 = clock64();
+    if (warp == 4) {
+        for (int c = 0; c < chunks; ++c) {
+            const int s = c % kDbgSS;
+            if (c >= kDbgSS) ptx::mbar_wait(&sm.done[s], ((c / kDbgSS) - 1) & 1);
+            if (mode & 4) ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&sm.full[s]);
+        }
+    } else if (warp == 5) {
+        const uint32_t idesc = ptx::idesc_f16(128, 32);
+        const uint32_t a_base = ptx::smem_u32(sm.a);
+        for (int c = 0; c < chunks; ++c) {
+            const int s = c % kDbgSS, ts = c % kDbgTS;
+            ptx::mbar_wait(&sm.full[s], (c / kDbgSS) & 1);
+            if (c >= kDbgTS) ptx::mbar_wait(&sm.tempty[ts], ((c / kDbgTS) - 1) & 1);
+            ptx::tc_fence_after();
+            if (lane == 0) {
+                if (mode & 1) {
+                    const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[s][0]), 128, 256);
+                    ptx::mma_f16_ss(tmem + ts * 64, ptx::smem_desc(a_base, 128, 256), bd, idesc, 0u);
+                    ptx::mma_f16_ss(tmem + ts * 64 + 32, ptx::smem_desc(a_base + 4096, 128, 256), bd, idesc, 0u);
+                    ptx::mma_commit(&sm.tfull[ts]);
+                } else {
+                    ptx::mbar_arrive(&sm.tfull[ts]);
+                }
+            }
+            __syncwarp();
+        }
+    } else {
+        float acc = 0.0f;
+        for (int c = 0; c < chunks; ++c) {
+            const int s = c % kDbgSS, ts = c % kDbgTS;
+            ptx::mbar_wait(&sm.tfull[ts], (c / kDbgTS) & 1);
+            ptx::tc_fence_after();
+            if (mode & 2) {
+                uint32_t d[2][16];
+                const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16) + ts * 64;
+                ptx::tmem_ld16(base, d[0]);
+                ptx::tmem_ld16(base + 32, d[1]);
+                ptx::tmem_wait_ld();
+                ptx::reg_fence16(d[0]);
+                ptx::reg_fence16(d[1]);
+                acc += __uint_as_float(d[0][lane & 15]) + __uint_as_float(d[1][3]);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                ptx::mbar_arrive(&sm.tempty[ts]);
+                ptx::mbar_arrive(&sm.done[s]);
+            }
+        }
+        if (acc == 12345.0f) out[3] = 1;
+    }
+    const long long t1 = clock64();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == 5) ptx::tmem_dealloc<128>(tmem);
+    if (threadIdx.x == 0) out[0] = t1 - t0;
+}
+
+}  // namespace
+
+cudaError_t debug_pipeline(int chunks, int mode, long long* cycles) {
+    long long* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 4 * sizeof(long long));
+    if (e != cudaSuccess) return e;
+    debug_pipeline_kernel<<<1, 192>>>(chunks, mode, d);
+    e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(cycles, d, sizeof(long long), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e;
+}
+
+}  // namespace tgs
+
+extern "C" tgs_status tgs_debug_pipeline(int chunks, int mode, long long* cycles) {
+    const cudaError_t e = tgs::debug_pipeline(chunks, mode, cycles);
+    return e == cudaSuccess ? TGS_OK : TGS_ERR_CUDA;
+}

@@ -67,10 +67,11 @@ struct RasterArgs {
     int image_row0;           // first image row stored in `image`
     float alpha_skip, alpha_clamp, t_terminate;
     FrameCounters* fc;
+    uint32_t* tile_trip;      // optional (count_pairs): per tile, entries of its list walked until done
 };
 void launch_raster_scalar(const RasterArgs& a, cudaStream_t st);
-// LPT schedule for the rasterisers: groups bucketed by floor(log2(list length)), longest first.
-void launch_group_order(const uint32_t* offsets, int n_groups, int* order, cudaStream_t st);
+// LPT schedule for the rasterisers: tiles bucketed by floor(log2(group list length)), longest first.
+void launch_tile_order(const uint32_t* offsets, const GroupGeom& gg, int* order, cudaStream_t st);
 void launch_raster_tensor(const RasterArgs& a, int num_sms, cudaStream_t st);
 // Instrumented walk: counts walked / alpha-contributing pairs (reference semantics, G=1 lists).
 void launch_count_pairs(const RasterArgs& a, cudaStream_t st);

@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256) raster_scalar_kernel(RasterArgs a) {
     __shared__ float4 s_gc[kBatch];   // q3=-c/2*log2e, opacity, r, g
     __shared__ float s_b[kBatch];     // b
     const GroupGeom& gg = a.gg;
-    const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
+    const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;  // LPT order, as the tensor path
     const int tx = tile % gg.tiles_x, ty = tile / gg.tiles_x + gg.band_gy0;  // G == 1: group == tile
     const int px = tx * kTile + (threadIdx.x & 15);
     const int py = ty * kTile + (threadIdx.x >> 4);
@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(256) count_pairs_kernel(RasterArgs a) {
     const int py = ty * kTile + (threadIdx.x >> 4);
     const int gid = (ty / gg.g - gg.band_gy0) * gg.groups_x + tx / gg.g;
     unsigned long long walked = 0, blended = 0;
+    uint32_t trip = 0;  // position in the tile's (mask-filtered) list where this pixel stopped
     if (px < gg.width && py < gg.height && ty < gg.tiles_y) {
         const float fx = (float)px + 0.5f, fy = (float)py + 0.5f;
         float T = 1.0f;
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(256) count_pairs_kernel(RasterArgs a) {
             int x0, y0, x1, y1;
             tile_rect(mc.x, mc.y, __float_as_int(co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1, y1);
             if (tx < x0 || tx > x1 || ty < y0 || ty > y1) continue;
+            ++trip;
             const float dx = __fsub_rn(fx, mc.x), dy = __fsub_rn(fy, mc.y);
             float acc = 0.0f;
             acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(-0.5f, mc.z), __fmul_rn(dx, dx)));
@@ -123,6 +125,14 @@ __global__ void __launch_bounds__(256) count_pairs_kernel(RasterArgs a) {
     if ((threadIdx.x & 31) == 0) {
         atomicAdd(&a.fc->walked, walked);
         atomicAdd(&a.fc->blended, blended);
+    }
+    if (a.tile_trip) {
+        __shared__ uint32_t s_trip;
+        if (threadIdx.x == 0) s_trip = 0;
+        __syncthreads();
+        atomicMax(&s_trip, trip);
+        __syncthreads();
+        if (threadIdx.x == 0) a.tile_trip[blockIdx.x] = s_trip;
     }
 }
 

@@ -20,20 +20,28 @@
 // mask filter — the epilogue has no per-tile branch.  Any row with |w| > 16384 cannot contribute
 // to its tile (the +0.3 dilation bounds the conic) and gets the same row.
 //
-// CTA = one group at a time (persistent over groups):
-//   warps [0, EPI)  epilogue: each thread owns PPT pixels (TMEM lane = pixel), tcgen05.ld's its
-//                   D rows and runs the ordered blend on CUDA cores + MUFU ex2;
-//   warp EPI        producer: gathers the chunk's splats (one per lane), derives the per-tile
-//                   coefficient rows (hi/lo FP16) into smem — the chunk is staged once and
-//                   shared by all G*G tiles (north_star 4);
-//   warp EPI+1      TMEM owner + MMA issuer: one tcgen05.mma per 128-pixel M-tile per chunk,
-//                   tcgen05.commit -> epilogue.
+// CTA = one 16x16 tile at a time, persistent over tiles (longest group lists first), several CTAs
+// per SM so the hardware balances tiles of unequal depth:
+//   warps 0-3  epilogue: TMEM lane quadrant q = warp; each thread owns two pixels of the tile
+//              (rows 2q + lane/16 and 8 + 2q + lane/16), tcgen05.ld's its D rows and runs the
+//              ordered blend on CUDA cores + MUFU ex2;
+//   warp 4     producer: streams the tile's G x G group list (north_star 4: group lists are
+//              G^2-fold shorter to bin and sort, reference binning.cpp:46-74), gathers 32 splats
+//              per step, keeps those whose mask has this tile (warp ballot compaction, so no MMA
+//              column or blend slot is spent on another tile's splats), derives the
+//              tile-centred coefficient rows (FP16 hi/lo) into smem;
+//   warp 5     TMEM owner + MMA issuer: two tcgen05.mma (M=128 pixels, N=32 splats, K=16) per
+//              chunk, tcgen05.commit -> epilogue.
 // A (pixel monomials) is identical for every tile, built once per CTA (256 rows x 32 B).
-// Chunks flow through STAGES smem/TMEM stages guarded by mbarriers; the chunk header carries
-// the group id, so group boundaries need no extra synchronisation.
+// Chunks flow through SS smem stages and one TMEM stage (drained into registers before the
+// blend, so the next MMA overlaps it), guarded by mbarriers; chunk headers carry the tile, so
+// tile boundaries need no extra synchronisation.  A tile retires as soon as its 4 epilogue warps
+// report all pixels terminated.
 #include "tgs_common.cuh"
 #include "tgs_kernels.cuh"
 #include "tgs_ptx.cuh"
+
+#include <algorithm>
 
 namespace tgs {
 
@@ -43,46 +51,42 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kNeverRow = -30000.0f;
 constexpr float kInf = __builtin_huge_valf();
 
-template <int G>
-struct Cfg {
-    static constexpr int TILES = G * G;
-    static constexpr int MT = 2 * TILES;                      // 128-pixel M-tiles
-    static constexpr int N = (G == 4) ? 16 : 32;              // splats per chunk (MMA N)
-    static constexpr int TS = (G == 4) ? 1 : 2;               // TMEM accumulator stages
-    static constexpr int SS = 3;                              // smem (operand + epilogue data) stages
-    static constexpr int COLS_USED = TS * MT * N;
-    static constexpr int TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
-                                     : COLS_USED <= 256 ? 256 : 512;
-    static constexpr int EPI = (G == 1) ? 4 : (G == 2) ? 8 : 16;  // epilogue warps
-    static constexpr int PPT = MT * 4 / EPI;                  // pixels per epilogue thread (2, 4, 8)
-    static constexpr int PB = PPT < 4 ? PPT : 4;              // pixels blended together (ILP)
-    static constexpr int JB = 32 / PB;                        // splat columns per TMEM load block
-    static constexpr int PROD = (G == 1) ? 1 : 4;             // producer warps
-    static constexpr int TPP = TILES / PROD;                  // tiles per producer warp
-    static constexpr int THREADS = (EPI + PROD + 1) * 32;
-    static constexpr int CTAS_PER_SM = 512 / TMEM_COLS;
-    static constexpr int B_BYTES = N * 32;                    // one tile's B operand
-};
+constexpr int kN = 32;          // splats per chunk (MMA N)
+constexpr int kSS = 4;          // smem stages
+constexpr int kEpi = 4;         // epilogue warps
+constexpr int kThreads = (kEpi + 2) * 32;
+constexpr int kTS = 2;          // TMEM accumulator stages
+constexpr int kTmemCols = 128;  // kTS x 2 M-tiles x 32 columns
+constexpr int kCtasPerSm = 4;
 
 struct ChunkHeader {
-    int gid;      // band-local group id, -1 = end of stream
-    int n_valid;  // splats in the chunk (0: empty group)
+    int seq;      // per-CTA tile sequence number, -1 = end of stream
+    int tile;     // band-local tile index
+    int n_valid;  // splats in the chunk (0: tile without contributing splats)
 };
 
-template <int G>
 struct Smem {
-    alignas(128) uint8_t a[256 * 32];                                     // pixel monomials
-    alignas(128) uint8_t b[Cfg<G>::SS][Cfg<G>::TILES][Cfg<G>::B_BYTES];   // splat rows
-    float4 epi[Cfg<G>::SS][Cfg<G>::N];                                    // r, g, b, min(clamp, o)
-    ChunkHeader hdr[Cfg<G>::SS];
-    int alive_tag[Cfg<G>::SS];        // max over epilogue warps of (chunk << 1 | any pixel alive)
-    int gq[2];                        // group ticket broadcast to producer warps
-    uint64_t full[Cfg<G>::SS];        // producers -> MMA          (count PROD)
-    uint64_t done[Cfg<G>::SS];        // epilogue -> producers     (count EPI): smem stage reusable
-    uint64_t tfull[Cfg<G>::TS];       // MMA -> epilogue           (tcgen05.commit)
-    uint64_t tempty[Cfg<G>::TS];      // epilogue -> MMA           (count EPI): TMEM stage drained
+    alignas(128) uint8_t a[256 * 32];      // pixel monomials (both M-tiles)
+    alignas(128) uint8_t b[kSS][kN * 32];  // splat coefficient rows
+    float4 epi[kSS][kN];                   // r, g, b, min(alpha_clamp, opacity)
+    ChunkHeader hdr[kSS];
+    int dead_seq[kEpi];                    // last tile seq whose pixels (per warp) all terminated
+    uint64_t full[kSS];                    // producer -> MMA
+    uint64_t done[kSS];                    // epilogue -> producer (count kEpi)
+    uint64_t tfull[kTS];                   // MMA -> epilogue (tcgen05.commit)
+    uint64_t tempty[kTS];                  // epilogue -> MMA (count kEpi)
     uint32_t tmem_base;
 };
+
+// Pixel owned by TMEM lane l (0..127) of M-tile m (0/1): epilogue warp q = l/32 owns the 8x8
+// quadrant (q%2, q/2) of the tile, lane j = l%32 the column j%8 of rows 4m + j/8 inside it, so a
+// thread's two pixels are 4 rows apart and a splat footprint touches as few warps as possible.
+__device__ __forceinline__ int lane_pixel(int m, int l) {
+    const int q = l >> 5, j = l & 31;
+    const int x = (q & 1) * 8 + (j & 7);
+    const int y = (q >> 1) * 8 + m * 4 + (j >> 3);
+    return y * 16 + x;
+}
 
 // byte offset of (row, k-half) in a K-major no-swizzle operand: 8x16B core matrices
 __device__ __forceinline__ uint32_t core_off(int row, int khalf) {
@@ -94,11 +98,7 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-__device__ __forceinline__ void named_bar_sync(int id, int threads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
-// Coefficient row of one splat for one tile (centre (ox, oy)) as FP16 hi/lo halves.
+// Coefficient row of one splat for the tile centred at (ox, oy), as FP16 hi/lo halves.
 __device__ __forceinline__ void make_row(bool ok, float mx, float my, float qa, float qb, float qc, float lo2,
                                          float ox, float oy, uint4& r0, uint4& r1) {
     float w[6];
@@ -137,19 +137,26 @@ __device__ __forceinline__ void make_row(bool ok, float mx, float my, float qa, 
     r1.w = 0u;
 }
 
-template <int G>
-__global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(RasterArgs a) {
-    using C = Cfg<G>;
+__device__ __forceinline__ void write_row(Smem& sm, int s, int slot, const uint4& r0, const uint4& r1) {
+    *reinterpret_cast<uint4*>(&sm.b[s][core_off(slot, 0)]) = r0;
+    *reinterpret_cast<uint4*>(&sm.b[s][core_off(slot, 1)]) = r1;
+}
+
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) raster_tensor_kernel(RasterArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    Smem<G>& sm = *reinterpret_cast<Smem<G>*>(smem_raw);
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const GroupGeom& gg = a.gg;
-    const int n_groups = gg.n_groups_band;
-    constexpr int kProd0 = C::EPI, kMma = C::EPI + C::PROD;
+    const int G = gg.g;
+    const int trow0 = gg.band_gy0 * G;                                  // first tile row of the band
+    const int trows = min(gg.tiles_y, gg.band_gy1 * G) - trow0;
+    const int n_tiles = gg.tiles_x * trows;
+    constexpr int kProd = kEpi, kMma = kEpi + 1;
 
     // ---- setup: A operand, barriers, TMEM ----------------------------------------------------
     for (int p = threadIdx.x; p < 256; p += blockDim.x) {
-        const float ux = (float)(p & 15) - 7.5f, uy = (float)(p >> 4) - 7.5f;
+        const int pix = lane_pixel(p >> 7, p & 127);  // A row p feeds TMEM lane p%128 of M-tile p/128
+        const float ux = (float)(pix & 15) - 7.5f, uy = (float)(pix >> 4) - 7.5f;
         const float phi[6] = {ux * ux, ux * uy, uy * uy, ux, uy, 1.0f};
         uint4 lo, hi;
         lo.x = pack_half2(phi[0], phi[1]);
@@ -164,212 +171,249 @@ __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(Raste
         *reinterpret_cast<uint4*>(sm.a + core_off(p, 1)) = hi;
     }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < C::SS; ++s) {
-            ptx::mbar_init(&sm.full[s], C::PROD);
-            ptx::mbar_init(&sm.done[s], C::EPI);
-            sm.alive_tag[s] = -1;
+        for (int s = 0; s < kSS; ++s) {
+            ptx::mbar_init(&sm.full[s], 1);
+            ptx::mbar_init(&sm.done[s], kEpi);
         }
-        for (int s = 0; s < C::TS; ++s) {
+        for (int s = 0; s < kTS; ++s) {
             ptx::mbar_init(&sm.tfull[s], 1);
-            ptx::mbar_init(&sm.tempty[s], C::EPI);
+            ptx::mbar_init(&sm.tempty[s], kEpi);
         }
+        for (int w = 0; w < kEpi; ++w) sm.dead_seq[w] = -1;
         ptx::mbar_fence_init();
     }
-    if (warp == kMma) ptx::tmem_alloc<C::TMEM_COLS>(&sm.tmem_base);
+    if (warp == kMma) ptx::tmem_alloc<kTmemCols>(&sm.tmem_base);
     ptx::fence_proxy_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
-    if (warp >= kProd0 && warp < kMma) {
-        // ================================ producers ==========================================
-        // Producer warp p builds the coefficient rows of tiles [p*TPP, (p+1)*TPP) for all N splats
-        // of the chunk (lane = splat); warp 0 also writes the epilogue data and the header.
-        const int p = warp - kProd0;
+    if (warp == kProd) {
+        // ================================ producer ===========================================
         const float skip = a.alpha_skip;
-        uint32_t c = 0;
-        int slot = 0;
-        for (;;) {
-            if (p == 0 && lane == 0) {
-                const int t = (int)atomicAdd(&a.fc->group_counter, 1u);
-                sm.gq[slot] = t < n_groups ? (a.order ? a.order[t] : t) : -1;
-            }
-            if (C::PROD > 1) named_bar_sync(1, C::PROD * 32); else __syncwarp();
-            const int g = sm.gq[slot];
-            slot ^= 1;
-            if (g < 0) break;
-            const int gx = g % gg.groups_x, gy = g / gg.groups_x + gg.band_gy0;
-            const uint32_t begin = a.offsets[g], end = a.offsets[g + 1];
-            const uint32_t nchunks = end > begin ? (end - begin + C::N - 1) / C::N : 1u;
-            for (uint32_t ch = 0; ch < nchunks; ++ch, ++c) {
-                const int s = (int)(c % C::SS);
-                const uint32_t e = begin + ch * C::N + (uint32_t)lane;
-                const bool valid = lane < C::N && e < end;
-                float4 mc = make_float4(0, 0, 0, 0), co = mc, col = mc;
-                if (valid) {
-                    const uint32_t idx = a.list[e];
-                    mc = a.proj.mc[idx];
-                    co = a.proj.co[idx];
-                    if (p == 0) col = a.proj.col[idx];
+        uint32_t c = 0;     // chunks emitted so far
+        int seq = 0;        // tiles started by this CTA
+        const uint32_t lt = (1u << lane) - 1u;
+        for (;; ++seq) {
+            int t = 0;
+            if (lane == 0) t = (int)atomicAdd(&a.fc->group_counter, 1u);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= n_tiles) break;
+            const int tile = a.order ? a.order[t] : t;
+            const int tx = tile % gg.tiles_x, ty = tile / gg.tiles_x + trow0;
+            const int gid = (ty / G - gg.band_gy0) * gg.groups_x + tx / G;
+            const uint32_t begin = a.offsets[gid], end = a.offsets[gid + 1];
+            const float ox = (float)(tx * kTile + 8), oy = (float)(ty * kTile + 8);
+            int fill = 0;                 // rows placed in the open chunk
+            bool open = false;            // a stage is open for this tile
+            bool emitted = false;         // at least one chunk of this tile emitted
+            int s = 0;
+            // Software-pipelined gather: list indices two batches ahead, splat records one
+            // batch ahead, so the dependent idx -> record loads overlap the row building.
+            const uint32_t nb = (end - begin + 31u) / 32u;
+            auto ld_idx = [&](uint32_t b) -> uint32_t {
+                const uint32_t e = begin + b * 32u + (uint32_t)lane;
+                return (b < nb && e < end) ? __ldg(&a.list[e]) : 0xffffffffu;
+            };
+            struct Rec { float4 mc, co, col; uint32_t idx; };
+            auto ld_rec = [&](uint32_t idx) -> Rec {
+                Rec r;
+                r.idx = idx;
+                if (idx != 0xffffffffu) {
+                    r.mc = __ldg(&a.proj.mc[idx]);
+                    r.co = __ldg(&a.proj.co[idx]);
+                    r.col = __ldg(&a.proj.col[idx]);
+                } else {
+                    r.mc = r.co = r.col = make_float4(0, 0, 0, 0);
                 }
-                if (c >= (uint32_t)C::SS) {
-                    ptx::mbar_wait(&sm.done[s], ((c / C::SS) - 1) & 1);
-                    const int tag = sm.alive_tag[s];
-                    // the last chunk of this group in this stage left no pixel alive: retire
-                    if (ch >= (uint32_t)C::SS && tag == (int)((c - C::SS) << 1)) break;
-                }
-                int tx0 = 0, ty0 = 0, tx1 = -1, ty1 = -1;
-                float c_o = 0.0f, lo2 = 0.0f;
-                if (valid) {
-                    tile_rect(mc.x, mc.y, __float_as_int(co.w), gg.tiles_x, gg.tiles_y, tx0, ty0, tx1, ty1);
-                    c_o = fminf(a.alpha_clamp, co.y);
-                    lo2 = lg2_approx(co.y);
-                }
-                const bool can = valid && !(c_o < skip);
+                return r;
+            };
+            uint32_t idx_next2 = ld_idx(1);
+            Rec nxt = ld_rec(ld_idx(0));
+            for (uint32_t bi = 0; bi < nb; ++bi) {
+                const Rec cur = nxt;
+                nxt = ld_rec(idx_next2);
+                idx_next2 = ld_idx(bi + 2);
+                // retire as soon as every epilogue warp reported the tile terminated
+                if (emitted) {
+                    int dmin = ((volatile int*)sm.dead_seq)[0];
 #pragma unroll
-                for (int tt = 0; tt < C::TPP; ++tt) {
-                    const int t = p * C::TPP + tt;
-                    const int tcx = gx * G + (t % G), tcy = gy * G + (t / G);
-                    const bool row_ok = can && tcx >= tx0 && tcx <= tx1 && tcy >= ty0 && tcy <= ty1;
-                    uint4 r0, r1;
-                    make_row(row_ok, mc.x, mc.y, mc.z, mc.w, co.x, lo2, (float)(tcx * kTile + 8),
-                             (float)(tcy * kTile + 8), r0, r1);
-                    if (lane < C::N) {
-                        *reinterpret_cast<uint4*>(&sm.b[s][t][core_off(lane, 0)]) = r0;
-                        *reinterpret_cast<uint4*>(&sm.b[s][t][core_off(lane, 1)]) = r1;
-                    }
+                    for (int w = 1; w < kEpi; ++w) dmin = min(dmin, ((volatile int*)sm.dead_seq)[w]);
+                    if (dmin >= seq) break;
                 }
-                if (p == 0) {
-                    if (lane < C::N) sm.epi[s][lane] = make_float4(col.x, col.y, col.z, c_o);
+                bool keep = false;
+                if (cur.idx != 0xffffffffu) {
+                    int x0, y0, x1, y1;
+                    tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1, y1);
+                    keep = tx >= x0 && tx <= x1 && ty >= y0 && ty <= y1 && !(fminf(a.alpha_clamp, cur.co.y) < skip);
+                }
+                const uint32_t km = __ballot_sync(0xffffffffu, keep);
+                if (km == 0u) continue;
+                const int nk = __popc(km);
+                const int rank = __popc(km & lt);
+                uint4 r0, r1;
+                float4 epi_v = make_float4(0, 0, 0, 0);
+                if (keep) {
+                    make_row(true, cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox, oy,
+                             r0, r1);
+                    epi_v = make_float4(cur.col.x, cur.col.y, cur.col.z, fminf(a.alpha_clamp, cur.co.y));
+                }
+                if (!open) {
+                    s = (int)(c % kSS);
+                    if (c >= (uint32_t)kSS) ptx::mbar_wait(&sm.done[s], ((c / kSS) - 1) & 1);
+                    open = true;
+                    fill = 0;
+                }
+                const int room = kN - fill;
+                if (keep && rank < room) {
+                    write_row(sm, s, fill + rank, r0, r1);
+                    sm.epi[s][fill + rank] = epi_v;
+                }
+                if (nk >= room) {
+                    // chunk full: publish it and open the next one for the remaining ranks
                     if (lane == 0) {
-                        sm.hdr[s].gid = g;
-                        sm.hdr[s].n_valid =
-                            (int)min((uint32_t)C::N, end > begin + ch * C::N ? end - begin - ch * C::N : 0u);
+                        sm.hdr[s].seq = seq;
+                        sm.hdr[s].tile = tile;
+                        sm.hdr[s].n_valid = kN;
                     }
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&sm.full[s]);
+                    ++c;
+                    emitted = true;
+                    s = (int)(c % kSS);
+                    if (c >= (uint32_t)kSS) ptx::mbar_wait(&sm.done[s], ((c / kSS) - 1) & 1);
+                    if (keep && rank >= room) {
+                        write_row(sm, s, rank - room, r0, r1);
+                        sm.epi[s][rank - room] = epi_v;
+                    }
+                    fill = nk - room;
+                } else {
+                    fill += nk;
+                }
+            }
+            // close the tile: pad and publish the partial chunk (or an empty one so the
+            // epilogue still writes the tile)
+            if (open && (fill > 0 || !emitted)) {
+                if (lane >= fill) {
+                    uint4 r0, r1;
+                    make_row(false, 0, 0, 0, 0, 0, 0, 0, 0, r0, r1);
+                    write_row(sm, s, lane, r0, r1);
+                }
+                if (lane == 0) {
+                    sm.hdr[s].seq = seq;
+                    sm.hdr[s].tile = tile;
+                    sm.hdr[s].n_valid = fill;
                 }
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&sm.full[s]);
+                ++c;
+            } else if (!open) {
+                s = (int)(c % kSS);
+                if (c >= (uint32_t)kSS) ptx::mbar_wait(&sm.done[s], ((c / kSS) - 1) & 1);
+                if (lane == 0) {
+                    sm.hdr[s].seq = seq;
+                    sm.hdr[s].tile = tile;
+                    sm.hdr[s].n_valid = 0;
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&sm.full[s]);
+                ++c;
             }
         }
         // end of stream
-        const int s = (int)(c % C::SS);
-        if (c >= (uint32_t)C::SS) ptx::mbar_wait(&sm.done[s], ((c / C::SS) - 1) & 1);
+        const int s = (int)(c % kSS);
+        if (c >= (uint32_t)kSS) ptx::mbar_wait(&sm.done[s], ((c / kSS) - 1) & 1);
         if (lane == 0) {
-            if (p == 0) {
-                sm.hdr[s].gid = -1;
-                sm.hdr[s].n_valid = 0;
-            }
+            sm.hdr[s].seq = -1;
+            sm.hdr[s].tile = -1;
+            sm.hdr[s].n_valid = 0;
             ptx::mbar_arrive(&sm.full[s]);
         }
         __syncwarp();
     } else if (warp == kMma) {
         // ================================ MMA issuer ==========================================
-        constexpr uint32_t idesc = ptx::idesc_f16(128, C::N);
+        constexpr uint32_t idesc = ptx::idesc_f16(128, kN);
         const uint32_t a_base = ptx::smem_u32(sm.a);
         for (uint32_t c = 0;; ++c) {
-            const int s = (int)(c % C::SS), ts = (int)(c % C::TS);
-            ptx::mbar_wait(&sm.full[s], (c / C::SS) & 1);
-            if (c >= (uint32_t)C::TS) ptx::mbar_wait(&sm.tempty[ts], ((c / C::TS) - 1) & 1);
+            const int s = (int)(c % kSS), ts = (int)(c % kTS);
+            ptx::mbar_wait(&sm.full[s], (c / kSS) & 1);
+            if (c >= (uint32_t)kTS) ptx::mbar_wait(&sm.tempty[ts], ((c / kTS) - 1) & 1);
             ptx::tc_fence_after();
             const ChunkHeader h = sm.hdr[s];
             if (lane == 0) {
-                if (h.gid >= 0 && h.n_valid > 0) {
-#pragma unroll
-                    for (int m = 0; m < C::MT; ++m) {
-                        const uint64_t ad = ptx::smem_desc(a_base + (uint32_t)(m & 1) * 4096u, 128, 256);
-                        const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[s][m >> 1][0]), 128, 256);
-                        ptx::mma_f16_ss(tmem + (uint32_t)(ts * C::MT * C::N + m * C::N), ad, bd, idesc, 0u);
-                    }
+                if (h.seq >= 0 && h.n_valid > 0) {
+                    const uint32_t dcol = tmem + (uint32_t)(ts * 2 * kN);
+                    const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[s][0]), 128, 256);
+                    ptx::mma_f16_ss(dcol, ptx::smem_desc(a_base, 128, 256), bd, idesc, 0u);
+                    ptx::mma_f16_ss(dcol + (uint32_t)kN, ptx::smem_desc(a_base + 4096u, 128, 256), bd, idesc, 0u);
                     ptx::mma_commit(&sm.tfull[ts]);
                 } else {
                     ptx::mbar_arrive(&sm.tfull[ts]);
                 }
             }
             __syncwarp();
-            if (h.gid < 0) break;
+            if (h.seq < 0) break;
         }
     } else {
         // ================================ epilogue ============================================
-        // warp w: TMEM lane quadrant q = w % 4; M-tiles m_k = w/4 + k * EPI/4 (k < PPT), which for
-        // G = 2 gives every thread one pixel in each of the 4 member tiles (balanced work per warp,
-        // PB = 4 independent blend chains per thread).
-        const int q = warp & 3;
-        const int mg = warp >> 2;
-        int prow[C::PPT], pcol[C::PPT], ptile[C::PPT], pm[C::PPT];
-#pragma unroll
-        for (int k = 0; k < C::PPT; ++k) {
-            const int m = mg + k * (C::EPI / 4);
-            const int pix = (m & 1) * 128 + q * 32 + lane;  // pixel within its tile
-            pm[k] = m;
-            prow[k] = pix >> 4;
-            pcol[k] = pix & 15;
-            ptile[k] = m >> 1;
-        }
-        float T[C::PPT], cr[C::PPT], cg[C::PPT], cb[C::PPT], thr[C::PPT];
-        int px[C::PPT], py[C::PPT];
-        bool inside[C::PPT];
+        const int q = warp;
+        const int p0 = lane_pixel(0, q * 32 + lane), p1 = lane_pixel(1, q * 32 + lane);
+        const int prow[2] = {p0 >> 4, p1 >> 4};
+        const int pcol = p0 & 15;
+        float T[2], cr[2], cg[2], cb[2], thr[2];
+        int px = 0, py[2] = {0, 0};
+        bool inside[2] = {false, false};
         const float L = log2f(a.alpha_skip);
         const float tterm = a.t_terminate;
         int cur = -1;
+        bool reported = false;
         for (uint32_t c = 0;; ++c) {
-            const int s = (int)(c % C::SS), ts = (int)(c % C::TS);
-            ptx::mbar_wait(&sm.tfull[ts], (c / C::TS) & 1);
+            const int s = (int)(c % kSS), ts = (int)(c % kTS);
+            ptx::mbar_wait(&sm.tfull[ts], (c / kTS) & 1);
             ptx::tc_fence_after();
             const ChunkHeader h = sm.hdr[s];
-            if (h.gid != cur) {
+            if (h.seq != cur) {
                 if (cur >= 0) {
 #pragma unroll
-                    for (int k = 0; k < C::PPT; ++k)
+                    for (int k = 0; k < 2; ++k)
                         if (inside[k]) {
-                            float* o = a.image + ((size_t)(py[k] - a.image_row0) * gg.width + px[k]) * 3;
+                            float* o = a.image + ((size_t)(py[k] - a.image_row0) * gg.width + px) * 3;
                             o[0] = fminf(fmaxf(cr[k], 0.0f), 1.0f);
                             o[1] = fminf(fmaxf(cg[k], 0.0f), 1.0f);
                             o[2] = fminf(fmaxf(cb[k], 0.0f), 1.0f);
                         }
                 }
-                if (h.gid < 0) break;
-                cur = h.gid;
-                const int gx = cur % gg.groups_x, gy = cur / gg.groups_x + gg.band_gy0;
+                if (h.seq < 0) break;
+                cur = h.seq;
+                reported = false;
+                const int tx = h.tile % gg.tiles_x, ty = h.tile / gg.tiles_x + trow0;
+                px = tx * kTile + pcol;
 #pragma unroll
-                for (int k = 0; k < C::PPT; ++k) {
-                    const int t = ptile[k];
-                    const int tx = gx * G + (t % G), ty = gy * G + (t / G);
-                    px[k] = tx * kTile + pcol[k];
+                for (int k = 0; k < 2; ++k) {
                     py[k] = ty * kTile + prow[k];
-                    inside[k] = tx < gg.tiles_x && ty < gg.tiles_y && px[k] < gg.width && py[k] < gg.height;
+                    inside[k] = px < gg.width && py[k] < gg.height;
                     T[k] = 1.0f;
                     cr[k] = cg[k] = cb[k] = 0.0f;
                     thr[k] = inside[k] ? L : kInf;
                 }
             }
-            bool any = false;
+            const bool work = h.n_valid > 0 && __any_sync(0xffffffffu, thr[0] != kInf || thr[1] != kInf);
+            const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ts * 2 * kN);
 #pragma unroll
-            for (int k = 0; k < C::PPT; ++k) any = any || thr[k] != kInf;
-            const bool work = h.n_valid > 0 && __any_sync(0xffffffffu, any);
-            const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ts * C::MT * C::N);
-            // D is consumed in blocks of PB pixels x JB splats (32 registers); the TMEM stage is
-            // released as soon as the warp's last block is in registers.
-            constexpr int NBLK = (C::PPT / C::PB) * (C::N / C::JB);
-#pragma unroll
-            for (int blk = 0; blk < NBLK; ++blk) {
-                const int k0 = (blk / (C::N / C::JB)) * C::PB;
-                const int j0 = (blk % (C::N / C::JB)) * C::JB;
-                uint32_t d[C::PB][C::JB];
+            for (int blk = 0; blk < 2; ++blk) {
+                const int j0 = blk * 16;
+                uint32_t d[2][16];
                 if (work) {
-#pragma unroll
-                    for (int kk = 0; kk < C::PB; ++kk) {
-                        const uint32_t ad = lane_base + (uint32_t)(pm[k0 + kk] * C::N + j0);
-                        if constexpr (C::JB == 16) ptx::tmem_ld16(ad, d[kk]); else ptx::tmem_ld8(ad, d[kk]);
-                    }
+                    ptx::tmem_ld16(lane_base + (uint32_t)j0, d[0]);
+                    ptx::tmem_ld16(lane_base + (uint32_t)(kN + j0), d[1]);
                     ptx::tmem_wait_ld();
-#pragma unroll
-                    for (int kk = 0; kk < C::PB; ++kk) {
-                        if constexpr (C::JB == 16) ptx::reg_fence16(d[kk]); else ptx::reg_fence8(d[kk]);
-                    }
+                    ptx::reg_fence16(d[0]);
+                    ptx::reg_fence16(d[1]);
                 }
-                if (blk == NBLK - 1) {
+                if (blk == 1) {  // TMEM drained into registers: the next MMA may overwrite it
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&sm.tempty[ts]);
@@ -377,50 +421,46 @@ __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(Raste
                 if (!work) continue;
                 // Speculative pass: blend every splat with D >= thr without the per-splat
                 // termination test (no loop-carried compare chain); T only decreases, so
-                // T_end < t_terminate <=> the pixel terminated inside this block, in which case
-                // the block is replayed exactly below (at most once per pixel per group).
-                float T0[C::PB], r0[C::PB], g0[C::PB], b0[C::PB];
+                // T_end < t_terminate <=> the pixel terminated inside this block, which is then
+                // replayed exactly (at most once per pixel per tile).
+                float T0[2], r0[2], g0[2], b0[2];
 #pragma unroll
-                for (int kk = 0; kk < C::PB; ++kk) {
-                    T0[kk] = T[k0 + kk];
-                    r0[kk] = cr[k0 + kk];
-                    g0[kk] = cg[k0 + kk];
-                    b0[kk] = cb[k0 + kk];
+                for (int k = 0; k < 2; ++k) {
+                    T0[k] = T[k];
+                    r0[k] = cr[k];
+                    g0[k] = cg[k];
+                    b0[k] = cb[k];
                 }
 #pragma unroll
-                for (int jj = 0; jj < C::JB; ++jj) {
-                    bool tk[C::PB], anyt = false;
-#pragma unroll
-                    for (int kk = 0; kk < C::PB; ++kk) {
-                        tk[kk] = __uint_as_float(d[kk][jj]) >= thr[k0 + kk];
-                        anyt = anyt || tk[kk];
-                    }
-                    if (anyt) {
+                for (int jj = 0; jj < 16; ++jj) {
+                    const float dA = __uint_as_float(d[0][jj]), dB = __uint_as_float(d[1][jj]);
+                    const bool ta = dA >= thr[0], tb = dB >= thr[1];
+                    if (ta || tb) {
                         const float4 ej = sm.epi[s][j0 + jj];
-#pragma unroll
-                        for (int kk = 0; kk < C::PB; ++kk) {
-                            const int k = k0 + kk;
-                            const float al = tk[kk] ? fminf(ej.w, ex2_approx(__uint_as_float(d[kk][jj]))) : 0.0f;
-                            const float wt = T[k] * al;
-                            cr[k] = fmaf(wt, ej.x, cr[k]);
-                            cg[k] = fmaf(wt, ej.y, cg[k]);
-                            cb[k] = fmaf(wt, ej.z, cb[k]);
-                            T[k] -= wt;
-                        }
+                        const float aA = ta ? fminf(ej.w, ex2_approx(dA)) : 0.0f;
+                        const float aB = tb ? fminf(ej.w, ex2_approx(dB)) : 0.0f;
+                        const float wA = T[0] * aA, wB = T[1] * aB;
+                        cr[0] = fmaf(wA, ej.x, cr[0]);
+                        cg[0] = fmaf(wA, ej.y, cg[0]);
+                        cb[0] = fmaf(wA, ej.z, cb[0]);
+                        cr[1] = fmaf(wB, ej.x, cr[1]);
+                        cg[1] = fmaf(wB, ej.y, cg[1]);
+                        cb[1] = fmaf(wB, ej.z, cb[1]);
+                        T[0] -= wA;
+                        T[1] -= wB;
                     }
                 }
 #pragma unroll
-                for (int kk = 0; kk < C::PB; ++kk) {
-                    const int k = k0 + kk;
+                for (int k = 0; k < 2; ++k) {
                     if (T[k] < tterm) {  // terminated inside the block: exact replay
-                        T[k] = T0[kk];
-                        cr[k] = r0[kk];
-                        cg[k] = g0[kk];
-                        cb[k] = b0[kk];
+                        T[k] = T0[k];
+                        cr[k] = r0[k];
+                        cg[k] = g0[k];
+                        cb[k] = b0[k];
                         bool stop = false;
 #pragma unroll
-                        for (int jj = 0; jj < C::JB; ++jj) {
-                            const float dv = __uint_as_float(d[kk][jj]);
+                        for (int jj = 0; jj < 16; ++jj) {
+                            const float dv = __uint_as_float(d[k][jj]);
                             if (!stop && dv >= thr[k]) {
                                 const float4 ej = sm.epi[s][j0 + jj];
                                 const float wt = T[k] * fminf(ej.w, ex2_approx(dv));
@@ -435,48 +475,33 @@ __global__ void __launch_bounds__(Cfg<G>::THREADS, 1) raster_tensor_kernel(Raste
                     }
                 }
             }
-            any = false;
-#pragma unroll
-            for (int k = 0; k < C::PPT; ++k) any = any || thr[k] != kInf;
-            const bool still = __any_sync(0xffffffffu, any);
+            // report this warp's pixels terminated (once per tile) so the producer can retire
+            const bool dead = !__any_sync(0xffffffffu, thr[0] != kInf || thr[1] != kInf);
             __syncwarp();
             if (lane == 0) {
-                atomicMax(&sm.alive_tag[s], (int)((c << 1) | (still ? 1u : 0u)));
+                if (dead && !reported) ((volatile int*)sm.dead_seq)[q] = cur;
                 ptx::mbar_arrive(&sm.done[s]);
             }
+            reported = reported || dead;
         }
     }
 
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    if (warp == kMma) ptx::tmem_dealloc<C::TMEM_COLS>(tmem);
-}
-
-template <int G>
-void launch_g(const RasterArgs& a, int num_sms, cudaStream_t st) {
-    using C = Cfg<G>;
-    // Dynamic smem is padded so that exactly CTAS_PER_SM CTAs fit on an SM: TMEM columns are the
-    // binding resource and a CTA that cannot allocate would otherwise spin.
-    size_t smem = sizeof(Smem<G>) + 1024;
-    const size_t min_smem = (size_t)(228 * 1024) / (C::CTAS_PER_SM + 1) + 1024;
-    if (smem < min_smem) smem = min_smem;
-    cudaFuncSetAttribute(raster_tensor_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int n = a.gg.n_groups_band;
-    int grid = num_sms * C::CTAS_PER_SM;
-    if (grid > n) grid = n;
-    if (grid > 0) raster_tensor_kernel<G><<<grid, C::THREADS, smem, st>>>(a);
+    if (warp == kMma) ptx::tmem_dealloc<kTmemCols>(tmem);
 }
 
 }  // namespace
 
 void launch_raster_tensor(const RasterArgs& a, int num_sms, cudaStream_t st) {
-    if (a.gg.g == 1)
-        launch_g<1>(a, num_sms, st);
-    else if (a.gg.g == 2)
-        launch_g<2>(a, num_sms, st);
-    else
-        launch_g<4>(a, num_sms, st);
+    const size_t smem = sizeof(Smem) + 1024;
+    cudaFuncSetAttribute(raster_tensor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int trows = std::min(a.gg.tiles_y, a.gg.band_gy1 * a.gg.g) - a.gg.band_gy0 * a.gg.g;
+    const int n_tiles = a.gg.tiles_x * trows;
+    int grid = num_sms * kCtasPerSm;
+    if (grid > n_tiles) grid = n_tiles;
+    if (grid > 0) raster_tensor_kernel<<<grid, kThreads, smem, st>>>(a);
 }
 
 }  // namespace tgs

@@ -1,0 +1,10 @@
+"""Per-chunk latency of the producer -> MMA -> epilogue hand-off (no blending work)."""
+import ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_17855_b200 import _lib
+lib = _lib.load()
+for mode in range(8):
+    cyc = C.c_longlong()
+    n = 4000
+    assert lib.tgs_debug_pipeline(n, mode, C.byref(cyc)) == 0, _lib.last_error()
+    print(f"mode {mode} (mma={mode&1} ld={mode>>1&1} fence={mode>>2&1}): {cyc.value / n:8.1f} cycles/chunk")

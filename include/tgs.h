@@ -178,6 +178,9 @@ tgs_status tgs_debug_mma(const uint16_t* a_128x16, const uint16_t* b_32x16, floa
  * epilogue): device cycles for `chunks` chunks with no blending work; mode bits: 1 issue MMAs,
  * 2 tcgen05.ld the accumulators, 4 producer proxy fence. */
 tgs_status tgs_debug_pipeline(int chunks, int mode, long long* cycles);
+/* Internal probe of the tcgen05.mma issue/commit rate: n MMAs (M=128, N=ncols in {16,32,64},
+ * K=16), a commit every per_commit MMAs (waited for when wait_each); device cycles. */
+tgs_status tgs_debug_mma_rate(int n, int per_commit, int wait_each, int ncols, long long* cycles);
 
 #ifdef __cplusplus
 }

@@ -65,6 +65,7 @@ SIGNATURES = {
     "tgs_encode_u8": (c_status, [P, P, C.c_int64, P]),
     "tgs_debug_mma": (c_status, [P, P, P]),
     "tgs_debug_pipeline": (c_status, [C.c_int, C.c_int, C.POINTER(C.c_longlong)]),
+    "tgs_debug_mma_rate": (c_status, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_longlong)]),
 }
 
 

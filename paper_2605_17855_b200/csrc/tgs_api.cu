@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -294,7 +295,10 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     eb.gid_count = ctx->gid_count.as<uint32_t>();
     const int er = radix_sort(eb, &fc->n_sort, std::max(1, ceil_log2(n_groups)), n_groups, false, s);
     launch_offsets_scan(eb.gid_count, ctx->offsets.as<uint32_t>(), n_groups, s);
-    launch_tile_order(ctx->offsets.as<uint32_t>(), gg, ctx->order.as<int>(), s);
+    {
+        const int per = gg.g == 4 ? 4 : 1;  // G=4 groups are rasterised as 2x2-tile quarters
+        launch_unit_order(ctx->offsets.as<uint32_t>(), n_groups * per, per, ctx->order.as<int>(), s);
+    }
     TGS_CUDA_OK(cudaGetLastError());
     TGS_CUDA_OK(cudaEventRecord(ctx->ev[3], s));
 
@@ -312,7 +316,9 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     ra.t_terminate = opt->t_terminate;
     ra.fc = fc;
     ra.tile_trip = nullptr;
-    if (opt->backend == TGS_BACKEND_SCALAR)
+    static const bool skip_raster = std::getenv("TGS_DEBUG_SKIP_RASTER") != nullptr;  // bisection aid
+    if (skip_raster) {
+    } else if (opt->backend == TGS_BACKEND_SCALAR)
         launch_raster_scalar(ra, s);
     else
         launch_raster_tensor(ra, ctx->num_sms, s);

@@ -175,21 +175,19 @@ __global__ void encode_u8_kernel(const float* __restrict__ rgb, int64_t n, uint8
     }
 }
 
-// Longest-processing-time-first schedule (bucketed): the rasterisers take tiles in this order, so
-// tiles with the longest group lists start first and the tail of the persistent grid is short.
-// Work estimate of a tile = length of its group's list.
-__global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __restrict__ offsets, GroupGeom gg,
-                                                          int n_tiles, int* __restrict__ order) {
+// Longest-processing-time-first schedule (bucketed): the rasterisers take work units (G=1:
+// tiles; G=2: groups; G=4: quarter groups) in this order, so units with the longest lists start
+// first and the tail of the persistent grid is short.  Work estimate = the unit's list length.
+__global__ void __launch_bounds__(1024) unit_order_kernel(const uint32_t* __restrict__ offsets, int n_units,
+                                                          int per_group, int* __restrict__ order) {
     __shared__ uint32_t cnt[33];
     if (threadIdx.x < 33) cnt[threadIdx.x] = 0;
     __syncthreads();
-    const int trow0 = gg.band_gy0 * gg.g;
-    auto key = [&](int t) {
-        const int tx = t % gg.tiles_x, ty = t / gg.tiles_x + trow0;
-        const int gid = (ty / gg.g - gg.band_gy0) * gg.groups_x + tx / gg.g;
+    auto key = [&](int u) {
+        const int gid = u / per_group;
         return __clz(offsets[gid + 1] - offsets[gid] + 1u);  // 0 = longest bucket
     };
-    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&cnt[key(t)], 1u);
+    for (int t = threadIdx.x; t < n_units; t += blockDim.x) atomicAdd(&cnt[key(t)], 1u);
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t run = 0;
@@ -200,15 +198,13 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __rest
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) order[atomicAdd(&cnt[key(t)], 1u)] = t;
+    for (int t = threadIdx.x; t < n_units; t += blockDim.x) order[atomicAdd(&cnt[key(t)], 1u)] = t;
 }
 
 }  // namespace
 
-void launch_tile_order(const uint32_t* offsets, const GroupGeom& gg, int* order, cudaStream_t st) {
-    const int trows = min(gg.tiles_y, gg.band_gy1 * gg.g) - gg.band_gy0 * gg.g;
-    const int n_tiles = gg.tiles_x * trows;
-    if (n_tiles > 0) tile_order_kernel<<<1, 1024, 0, st>>>(offsets, gg, n_tiles, order);
+void launch_unit_order(const uint32_t* offsets, int n_units, int per_group, int* order, cudaStream_t st) {
+    if (n_units > 0) unit_order_kernel<<<1, 1024, 0, st>>>(offsets, n_units, per_group, order);
 }
 
 void launch_entry_scan(const BinArgs& a, int max_items, cudaStream_t st) {

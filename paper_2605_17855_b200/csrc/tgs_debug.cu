@@ -8,7 +8,7 @@
 namespace tgs {
 namespace {
 
-constexpr int kDbgSS = 4, kDbgTS = 2, kDbgEpi = 4;
+constexpr int kDbgSS = 8, kDbgTS = 4, kDbgEpi = 4;
 
 struct DbgSmem {
     alignas(128) uint8_t a[256 * 32];
@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(192, 1) debug_pipeline_kernel(int chunks, int 
         }
         ptx::mbar_fence_init();
     }
-    if (warp == 5) ptx::tmem_alloc<128>(&sm.tmem_base);
+    if (warp == 5) ptx::tmem_alloc<256>(&sm.tmem_base);
     ptx::fence_proxy_async_smem();
     ptx::tc_fence_before();
     __syncthreads();
@@ -99,11 +99,109 @@ __global__ void __launch_bounds__(192, 1) debug_pipeline_kernel(int chunks, int 
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    if (warp == 5) ptx::tmem_dealloc<128>(tmem);
+    if (warp == 5) ptx::tmem_dealloc<256>(tmem);
+    if (threadIdx.x == 0) out[0] = t1 - t0;
+}
+
+// MMA issue-rate probe: one thread issues n tcgen05.mma (M=128, N=ncols, K=16, A and B from
+// smem) into rotating TMEM columns, committing to an mbarrier every `per_commit` MMAs and
+// waiting for that commit before continuing when `wait_each` is set; reports total cycles.
+__global__ void __launch_bounds__(128, 1) debug_mma_rate_kernel(int n, int per_commit, int wait_each, int ncols,
+                                                                 long long* out) {
+    const int variant = per_commit >> 16;  // 0 SS no-swizzle, 1 A in TMEM, 2 SS 32B-swizzle, 3 M=64
+    per_commit &= 0xffff;
+    __shared__ __align__(128) uint8_t sa[128 * 32];
+    __shared__ __align__(128) uint8_t sb[64 * 32];
+    __shared__ uint64_t bar, bar_end;
+    __shared__ uint32_t tbase;
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 128 * 32 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sa)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < 64 * 32 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sb)[i] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bar, 1);
+        ptx::mbar_init(&bar_end, 1);
+        ptx::mbar_fence_init();
+    }
+    if (warp == 0) ptx::tmem_alloc<512>(&tbase);
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tm = tbase;
+    long long t0 = clock64(), t1 = t0;
+    if (variant == 4) {  // warp-uniform issue: whole warp 0 runs the loop, one elected lane issues
+        if (warp == 0) {
+            const uint32_t idesc = ncols == 16 ? ptx::idesc_f16(128, 16) : ncols == 64 ? ptx::idesc_f16(128, 64)
+                                                                               : ptx::idesc_f16(128, 32);
+            const uint64_t ad = ptx::smem_desc(ptx::smem_u32(sa), 128, 256);
+            const uint64_t bd = ptx::smem_desc(ptx::smem_u32(sb), 128, 256);
+            uint32_t phase = 0;
+            int pending = 0;
+            for (int i = 0; i < n; ++i) {
+                ptx::mma_f16_ss_elect(tm + 8u + (uint32_t)((i * ncols) & 255), ad, bd, idesc, 0u);
+                if (++pending == per_commit) {
+                    ptx::mma_commit_elect(&bar);
+                    pending = 0;
+                    if (wait_each) {
+                        ptx::mbar_wait(&bar, phase);
+                        phase ^= 1;
+                    }
+                }
+            }
+            ptx::mma_commit_elect(&bar_end);
+            ptx::mbar_wait(&bar_end, 0);
+            t1 = clock64();
+        }
+    } else if (threadIdx.x == 0) {
+        const int mm = variant == 3 ? 64 : 128;
+        const uint32_t idesc = ncols == 16 ? ptx::idesc_f16(mm, 16) : ncols == 64 ? ptx::idesc_f16(mm, 64)
+                                                                           : ptx::idesc_f16(mm, 32);
+        uint64_t ad = ptx::smem_desc(ptx::smem_u32(sa), 128, 256);
+        uint64_t bd = ptx::smem_desc(ptx::smem_u32(sb), 128, 256);
+        if (variant == 2) {  // SWIZZLE_32B (layout type 6): 8 rows x 32 B atoms, SBO 256 B
+            ad = ptx::smem_desc(ptx::smem_u32(sa), 16, 256) | (6ull << 61);
+            bd = ptx::smem_desc(ptx::smem_u32(sb), 16, 256) | (6ull << 61);
+        }
+        uint32_t phase = 0;
+        int pending = 0;
+        for (int i = 0; i < n; ++i) {
+            const uint32_t dcol = tm + 8u + (uint32_t)((i * ncols) & 255);
+            if (variant == 1)
+                ptx::mma_f16_ts(dcol, tm, bd, idesc, 0u);  // A = TMEM columns 0..7
+            else
+                ptx::mma_f16_ss(dcol, ad, bd, idesc, 0u);
+            if (++pending == per_commit) {
+                ptx::mma_commit(&bar);
+                pending = 0;
+                if (wait_each) {
+                    ptx::mbar_wait(&bar, phase);
+                    phase ^= 1;
+                }
+            }
+        }
+        ptx::mma_commit(&bar_end);  // arrives when every MMA above has completed
+        ptx::mbar_wait(&bar_end, 0);
+        t1 = clock64();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == 0) ptx::tmem_dealloc<512>(tm);
     if (threadIdx.x == 0) out[0] = t1 - t0;
 }
 
 }  // namespace
+
+cudaError_t debug_mma_rate(int n, int per_commit, int wait_each, int ncols, long long* cycles) {
+    long long* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(long long));
+    if (e != cudaSuccess) return e;
+    debug_mma_rate_kernel<<<1, 128>>>(n, per_commit, wait_each, ncols, d);
+    e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(cycles, d, sizeof(long long), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e;
+}
 
 cudaError_t debug_pipeline(int chunks, int mode, long long* cycles) {
     long long* d = nullptr;
@@ -117,6 +215,11 @@ cudaError_t debug_pipeline(int chunks, int mode, long long* cycles) {
 }
 
 }  // namespace tgs
+
+extern "C" tgs_status tgs_debug_mma_rate(int n, int per_commit, int wait_each, int ncols, long long* cycles) {
+    const cudaError_t e = tgs::debug_mma_rate(n, per_commit, wait_each, ncols, cycles);
+    return e == cudaSuccess ? TGS_OK : TGS_ERR_CUDA;
+}
 
 extern "C" tgs_status tgs_debug_pipeline(int chunks, int mode, long long* cycles) {
     const cudaError_t e = tgs::debug_pipeline(chunks, mode, cycles);

@@ -70,8 +70,9 @@ struct RasterArgs {
     uint32_t* tile_trip;      // optional (count_pairs): per tile, entries of its list walked until done
 };
 void launch_raster_scalar(const RasterArgs& a, cudaStream_t st);
-// LPT schedule for the rasterisers: tiles bucketed by floor(log2(group list length)), longest first.
-void launch_tile_order(const uint32_t* offsets, const GroupGeom& gg, int* order, cudaStream_t st);
+// LPT schedule for the rasterisers: work units (tile / group / quarter group, per_group units per
+// group list) bucketed by floor(log2(list length)), longest first.
+void launch_unit_order(const uint32_t* offsets, int n_units, int per_group, int* order, cudaStream_t st);
 void launch_raster_tensor(const RasterArgs& a, int num_sms, cudaStream_t st);
 // Instrumented walk: counts walked / alpha-contributing pairs (reference semantics, G=1 lists).
 void launch_count_pairs(const RasterArgs& a, cudaStream_t st);

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <cstdio>
 
 namespace tgs {
 namespace ptx {
@@ -23,14 +24,60 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
                  : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    // try_wait without a suspend-time hint: the hardware's own bounded wait, re-polled
+    const uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
-        "r"(parity), "r"(0x989680u)  // suspend-time hint: sleep until the phase flips, don't spin
+        "r"(parity), "r"(0x989680u)  // suspend-time hint: sleep until the phase flips
         : "memory");
+}
+
+// Bounded wait: a deadlock (a protocol bug) must become a reported kernel error, never a hung
+// GPU.  After ~4e9 cycles (~2 s) the waiter prints where it is stuck and traps.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    // try_wait with a suspend-time hint: the thread sleeps in hardware until the phase completes
+    // or ~20 us pass, so waiting warps do not steal issue slots from working ones
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(20000u)
+        : "memory");
+    return ok != 0;
+}
+static __device__ __noinline__ void watchdog_trap(const char* what, int a0, int a1) {
+    if ((threadIdx.x & 31) == 0)
+        printf("libtgs watchdog: block %d thread %d stuck in %s (%d, %d)\n", (int)blockIdx.x, (int)threadIdx.x, what,
+           a0, a1);
+    __trap();
+}
+// Warp-wide bounded wait: lane 0 polls (hardware-suspending try_wait), then the warp
+// reconverges, so no lane reaches a .sync.aligned tcgen05 op / elect.sync / vote while others
+// are still in the loop.  Memory ordering for the other lanes comes from __syncwarp.
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, const char* what, int a0, int a1) {
+    if ((threadIdx.x & 31) == 0 && !mbar_try(bar, parity)) {
+        const long long t0 = clock64();
+        for (uint32_t i = 1;; ++i) {
+            if (mbar_try(bar, parity)) break;
+            if ((i & 255u) == 0u && clock64() - t0 > 4000000000ll) watchdog_trap(what, a0, a1);
+        }
+    }
+    __syncwarp();
 }
 
 // generic-proxy smem writes -> visible to the async proxy (tensor core operand reads)
@@ -88,6 +135,37 @@ __device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t adesc, uint
         : "memory");
 }
 
+// Warp-collective forms: the whole warp executes them with warp-uniform operands (so they stay
+// in uniform registers) and one elected lane issues the instruction.
+__device__ __forceinline__ void mma_f16_ss_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
+// A operand from TMEM (a_tmem: lanes 0..M-1, K/2 32-bit columns), B from shared memory.
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -113,6 +191,10 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
                    "=r"(r[7])
                  : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld1(uint32_t taddr, uint32_t& r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+}
+__device__ __forceinline__ void reg_fence1(uint32_t& r) { asm volatile("" : "+r"(r)); }
 __device__ __forceinline__ void reg_fence8(uint32_t* r) {
     asm volatile("" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]));
 }

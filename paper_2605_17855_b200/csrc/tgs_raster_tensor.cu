@@ -1,42 +1,44 @@
 // Tensorized, cross-tile-grouped rasterizer (north_star 3 + 4) on the 5th-gen tensor cores.
 //
-// Reference semantics: proj/src/raster_tensor.cpp:64-160 (rasterize_group_impl) — a group of
-// G x G tiles walks its depth-sorted list chunk by chunk; every live member tile consumes the
-// chunk's entries whose mask has its bit, in list order; per pixel the power feeds
-// alpha_of/blend (raster_scalar.hpp:40-55) until T < t_terminate; tiles/groups retire early.
+// Reference semantics: proj/src/raster_tensor.cpp:64-160 (rasterize_group_impl) — one CTA per
+// tile group walks the group's depth-sorted list chunk by chunk; every live member tile consumes
+// the chunk's entries whose mask has its bit, in list order; per pixel the power feeds
+// alpha_of/blend (raster_scalar.hpp:40-55) until T < t_terminate; tiles retire early
+// (:93-96, :107, :138-141) and the group exits when all member tiles are done.  The paper's
+// design: the chunk is staged in shared memory ONCE per group and reused by
+// all member tiles.
 //
 // B200 formulation.  The reference builds a pixel operand per Gaussian row
 // (raster_tensor.cpp:118-123), which no hardware MMA can do.  Here the power is expanded around
-// each tile's centre o:  u = pixel - o, m = mean - o,
+// the centre o of the 2x2-tile unit:  u = pixel - o, m = mean - o,
 //     log2(e) * power + log2(opacity) = w . phi(u),
-//     phi(u) = [ux^2, ux*uy, uy^2, ux, uy, 1]                      (pixel side, exact in FP16)
+//     phi(u) = [ux^2, ux*uy, uy^2, ux, uy, 1]          (pixel side, exact in FP16: |u| <= 15.5)
 //     w      = log2e * [-a/2, -b, -c/2, a mx + b my, b mx + c my,
-//                       -(a mx^2/2 + b mx my + c my^2/2)] + [0,0,0,0,0, log2 o]  (splat side)
-// and w is carried as an FP16 hi/lo pair, so K = 6 (hi) + 6 (lo) + 4 zero lanes = 16:
-//     D[pixel][splat] = A[pixel][0:16] . B[splat][0:16]      (one tcgen05.mma, M=128, K=16)
-// gives the ex2 argument directly: alpha = min(min(alpha_clamp, o), ex2(D)), skip D < log2(skip).
-// Splats outside a tile's mask (binning.cpp:56-65), rows past the list end and splats whose
-// min(clamp, o) < alpha_skip get the row "D = -30000", so the alpha-skip test also realises the
-// mask filter — the epilogue has no per-tile branch.  Any row with |w| > 16384 cannot contribute
-// to its tile (the +0.3 dilation bounds the conic) and gets the same row.
+//                       -(a mx^2/2 + b mx my + c my^2/2)] + [0,0,0,0,0, log2 o]   (splat side)
+// carried as an FP16 hi/lo pair (K lanes 0-5 hi, 6-11 lo).  K lanes 12-15 realise the paper's
+// tile-membership mask (binning.cpp:56-65, raster_tensor.cpp:24-38) inside the contraction: the
+// pixel row of member tile t has a one-hot 1.0 in lane 12+t, the splat row has 0 there when the
+// splat overlaps tile t and -30000 otherwise.  So ONE K=16 FP16 MMA per (M-tile, chunk) gives
+//     D[pixel][splat] = log2(alpha_unclamped)  (or <= -30000 for a non-member tile)
+// and the epilogue needs no per-tile branch: alpha = min(ex2(D), min(alpha_clamp, o)), skip iff
+// D < log2(alpha_skip) — which also realises the positive-power clamp (raster_scalar.hpp:41).
 //
-// CTA = one 16x16 tile at a time, persistent over tiles (longest group lists first), several CTAs
-// per SM so the hardware balances tiles of unequal depth:
-//   warps 0-3  epilogue: TMEM lane quadrant q = warp; each thread owns two pixels of the tile
-//              (rows 2q + lane/16 and 8 + 2q + lane/16), tcgen05.ld's its D rows and runs the
-//              ordered blend on CUDA cores + MUFU ex2;
-//   warp 4     producer: streams the tile's G x G group list (north_star 4: group lists are
-//              G^2-fold shorter to bin and sort, reference binning.cpp:46-74), gathers 32 splats
-//              per step, keeps those whose mask has this tile (warp ballot compaction, so no MMA
-//              column or blend slot is spent on another tile's splats), derives the
-//              tile-centred coefficient rows (FP16 hi/lo) into smem;
-//   warp 5     TMEM owner + MMA issuer: two tcgen05.mma (M=128 pixels, N=32 splats, K=16) per
-//              chunk, tcgen05.commit -> epilogue.
-// A (pixel monomials) is identical for every tile, built once per CTA (256 rows x 32 B).
-// Chunks flow through SS smem stages and one TMEM stage (drained into registers before the
-// blend, so the next MMA overlaps it), guarded by mbarriers; chunk headers carry the tile, so
-// tile boundaries need no extra synchronisation.  A tile retires as soon as its 4 epilogue warps
-// report all pixels terminated.
+// CTA (persistent, one per SM) = one unit of 2x2 tiles at a time (G=2: the group; G=4: a
+// quarter group; G=1: a single tile with SLOTS = 1), units in longest-list-first order:
+//   warps 0-7  epilogue: warp w reads TMEM lane quadrant q = w%4 of the M-tiles (2t + w/4),
+//              t = 0..SLOTS-1, so each thread owns one pixel in each member tile (slot t); the
+//              ordered blend runs on CUDA cores + MUFU ex2; a retired tile drops out of every
+//              warp at once;
+//   warp 8     producer: streams the unit's list in 32-entry batches (prefetched two ahead),
+//              gathers the splats once, drops entries whose member tiles are all retired or
+//              that can never reach alpha_skip (ballot compaction keeps list order), and writes
+//              the unit-centred coefficient rows (+ mask lanes) and blend data into an smem stage;
+//   warp 9     TMEM owner + MMA issuer: per chunk one tcgen05.mma (M=128, N=32, K=16) per live
+//              M-tile into a TMEM stage (2 stages x 2*SLOTS M-tiles x 32 columns), then
+//              tcgen05.commit -> epilogue.
+// The pixel operand A (2*SLOTS M-tiles x 128 rows x 32 B) is identical for every unit and is
+// built once per CTA.  Stages are guarded by mbarriers; chunk headers carry the unit sequence
+// number, so unit boundaries need no extra synchronisation.
 #include "tgs_common.cuh"
 #include "tgs_kernels.cuh"
 #include "tgs_ptx.cuh"
@@ -51,41 +53,62 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kNeverRow = -30000.0f;
 constexpr float kInf = __builtin_huge_valf();
 
-constexpr int kN = 32;          // splats per chunk (MMA N)
-constexpr int kSS = 4;          // smem stages
-constexpr int kEpi = 4;         // epilogue warps
-constexpr int kThreads = (kEpi + 2) * 32;
-constexpr int kTS = 2;          // TMEM accumulator stages
-constexpr int kTmemCols = 128;  // kTS x 2 M-tiles x 32 columns
-constexpr int kCtasPerSm = 4;
+constexpr int kN = 32;  // splats per chunk (MMA N)
+constexpr int kSS = 4;  // smem stages
+constexpr int kTS = 2;  // TMEM accumulator stages
 
 struct ChunkHeader {
-    int seq;      // per-CTA tile sequence number, -1 = end of stream
-    int tile;     // band-local tile index
-    int n_valid;  // splats in the chunk (0: tile without contributing splats)
+    int seq;      // per-CTA unit sequence number, -1 = end of stream
+    int unit;     // unit index (order-resolved)
+    int n_valid;  // splats in the chunk (0: unit without contributing splats)
+    int live;     // member tiles live when the chunk was produced (MMA skips the others)
+    int chunk;    // chunk number (protocol self-check)
 };
 
+// Roles: SLOTS member tiles per unit -> 2*SLOTS M=128 tiles.  Each epilogue warp owns SPW
+// (slot) pixel blocks: lane quadrant q = warp % 4 (the TMEM lanes it may read) of M-tiles
+// 2*(k0+i) + half, i < SPW; so each thread owns one pixel in SPW member tiles.
+template <int SLOTS>
+struct Roles {
+    static constexpr int kMT = 2 * SLOTS;
+    static constexpr int kSPW = SLOTS == 1 ? 1 : 2;            // slots (member tiles) per warp
+    static constexpr int kEpiWarps = 8 * SLOTS / kSPW;         // 16 (G>=2) or 8 (G=1)
+    static constexpr int kThreads = (kEpiWarps + 2) * 32;
+    static constexpr int kProd = kEpiWarps, kMma = kEpiWarps + 1;
+};
+
+template <int SLOTS>
 struct Smem {
-    alignas(128) uint8_t a[256 * 32];      // pixel monomials (both M-tiles)
-    alignas(128) uint8_t b[kSS][kN * 32];  // splat coefficient rows
-    float4 epi[kSS][kN];                   // r, g, b, min(alpha_clamp, opacity)
+    static constexpr int kMT = 2 * SLOTS;
+    alignas(128) uint8_t a[kMT][128 * 32];   // pixel monomial rows (K-major, no swizzle)
+    alignas(128) uint8_t b[kSS][kN * 32];    // splat coefficient rows
+    float4 epi[kSS][kN];                     // r, g, b, min(alpha_clamp, opacity)
     ChunkHeader hdr[kSS];
-    int dead_seq[kEpi];                    // last tile seq whose pixels (per warp) all terminated
-    uint64_t full[kSS];                    // producer -> MMA
-    uint64_t done[kSS];                    // epilogue -> producer (count kEpi)
-    uint64_t tfull[kTS];                   // MMA -> epilogue (tcgen05.commit)
-    uint64_t tempty[kTS];                  // epilogue -> MMA (count kEpi)
+    alignas(16) int wdone[16];               // chunks each epilogue warp has completed
+    alignas(16) int dead[16];                // (seq << 4) | retired member tiles, per warp
+    uint64_t full[kSS];                      // producer -> MMA
+    uint64_t tfull[kTS];                     // MMA -> epilogue (tcgen05.commit)
+    // Releases are monotonic counters compared with absolute targets (no mbarrier phase
+    // aliasing): done_cnt[s] = warps that finished a chunk on smem stage s; a TMEM stage is free
+    // once every epilogue warp's wdone passed the chunk that used it.
+    unsigned int done_cnt[kSS];
     uint32_t tmem_base;
 };
 
-// Pixel owned by TMEM lane l (0..127) of M-tile m (0/1): epilogue warp q = l/32 owns the 8x8
-// quadrant (q%2, q/2) of the tile, lane j = l%32 the column j%8 of rows 4m + j/8 inside it, so a
-// thread's two pixels are 4 rows apart and a splat footprint touches as few warps as possible.
-__device__ __forceinline__ int lane_pixel(int m, int l) {
-    const int q = l >> 5, j = l & 31;
-    const int x = (q & 1) * 8 + (j & 7);
-    const int y = (q >> 1) * 8 + m * 4 + (j >> 3);
-    return y * 16 + x;
+template <int SLOTS>
+constexpr uint32_t tmem_cols() {
+    constexpr int c = kTS * 2 * SLOTS * kN;
+    return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
+}
+
+// Pixel (relative to the unit's top-left) of TMEM lane l of M-tile m = 2*slot + half: the lane
+// quadrant q = l/32 is an 8x4 block of the half tile, so an epilogue warp's 32 pixels are
+// spatially compact and a splat footprint touches few warps.
+__device__ __forceinline__ void lane_pixel(int m, int l, int& x, int& y) {
+    const int slot = m >> 1, half = m & 1;
+    const int q = l >> 5, i = l & 31;
+    x = (slot & 1) * 16 + (q & 1) * 8 + (i & 7);
+    y = (slot >> 1) * 16 + half * 8 + (q >> 1) * 4 + (i >> 3);
 }
 
 // byte offset of (row, k-half) in a K-major no-swizzle operand: 8x16B core matrices
@@ -98,66 +121,131 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// Coefficient row of one splat for the tile centred at (ox, oy), as FP16 hi/lo halves.
-__device__ __forceinline__ void make_row(bool ok, float mx, float my, float qa, float qb, float qc, float lo2,
-                                         float ox, float oy, uint4& r0, uint4& r1) {
+// Coefficient row of one splat for a unit centred at (ox, oy): FP16 hi/lo halves of w plus the
+// four member-tile mask lanes.  Returns false when |w| exceeds the FP16 hi/lo range: such a
+// splat cannot reach alpha_skip anywhere in the unit (|u| <= 15.5 and the +0.3 dilation bounds
+// the conic by 1/0.3), so it is dropped.
+__device__ __forceinline__ bool make_row(float mx, float my, float qa, float qb, float qc, float lo2, float ox,
+                                         float oy, uint32_t cover, uint4& r0, uint4& r1) {
     float w[6];
-    if (ok) {
-        const float dx = mx - ox, dy = my - oy;
-        const float ha = 0.5f * qa, hc = 0.5f * qc;
-        w[0] = -ha * kLog2e;
-        w[1] = -qb * kLog2e;
-        w[2] = -hc * kLog2e;
-        w[3] = fmaf(qa, dx, qb * dy) * kLog2e;
-        w[4] = fmaf(qb, dx, qc * dy) * kLog2e;
-        const float quad = fmaf(ha * dx, dx, fmaf(qb * dx, dy, hc * dy * dy));
-        w[5] = fmaf(-quad, kLog2e, lo2);
+    const float dx = mx - ox, dy = my - oy;
+    const float ha = 0.5f * qa, hc = 0.5f * qc;
+    w[0] = -ha * kLog2e;
+    w[1] = -qb * kLog2e;
+    w[2] = -hc * kLog2e;
+    w[3] = fmaf(qa, dx, qb * dy) * kLog2e;
+    w[4] = fmaf(qb, dx, qc * dy) * kLog2e;
+    const float quad = fmaf(ha * dx, dx, fmaf(qb * dx, dy, hc * dy * dy));
+    w[5] = fmaf(-quad, kLog2e, lo2);
+    bool ok = true;
+    float h[6], l[6];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) ok = ok && fabsf(w[k]) <= 16384.0f;
+    for (int k = 0; k < 6; ++k) {
+        ok = ok && fabsf(w[k]) <= 16384.0f;
+        h[k] = __half2float(__float2half_rn(w[k]));
+        l[k] = w[k] - h[k];
     }
-    if (ok) {
-        float h[6], l[6];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            h[k] = __half2float(__float2half_rn(w[k]));
-            l[k] = w[k] - h[k];
-        }
-        r0.x = pack_half2(h[0], h[1]);
-        r0.y = pack_half2(h[2], h[3]);
-        r0.z = pack_half2(h[4], h[5]);
-        r0.w = pack_half2(l[0], l[1]);
-        r1.x = pack_half2(l[2], l[3]);
-        r1.y = pack_half2(l[4], l[5]);
-    } else {
-        r0 = make_uint4(0u, 0u, pack_half2(0.0f, kNeverRow), 0u);
-        r1.x = 0u;
-        r1.y = 0u;
-    }
-    r1.z = 0u;
-    r1.w = 0u;
+    const float m0 = (cover & 1u) ? 0.0f : kNeverRow, m1 = (cover & 2u) ? 0.0f : kNeverRow;
+    const float m2 = (cover & 4u) ? 0.0f : kNeverRow, m3 = (cover & 8u) ? 0.0f : kNeverRow;
+    r0.x = pack_half2(h[0], h[1]);
+    r0.y = pack_half2(h[2], h[3]);
+    r0.z = pack_half2(h[4], h[5]);
+    r0.w = pack_half2(l[0], l[1]);
+    r1.x = pack_half2(l[2], l[3]);
+    r1.y = pack_half2(l[4], l[5]);
+    r1.z = pack_half2(m0, m1);
+    r1.w = pack_half2(m2, m3);
+    return ok;
 }
 
-__device__ __forceinline__ void write_row(Smem& sm, int s, int slot, const uint4& r0, const uint4& r1) {
+// 0xffffffff if a >= b else 0 (opaque to CSE, so the blend's own compare stays a predicate)
+__device__ __forceinline__ uint32_t fset_ge(float a, float b) {
+    uint32_t r;
+    asm volatile("set.ge.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
+    return r;
+}
+
+__device__ __forceinline__ unsigned int ld_volatile_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(ptx::smem_u32(p)) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ int4 ld_volatile_v4(const int* p) {
+    int4 v;
+    asm volatile("ld.volatile.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(ptx::smem_u32(p)));
+    return v;
+}
+
+// Never-contributing padding row (tail of a partial chunk).
+__device__ __forceinline__ void never_row(uint4& r0, uint4& r1) {
+    r0 = make_uint4(0u, 0u, pack_half2(0.0f, kNeverRow), 0u);
+    r1 = make_uint4(0u, 0u, 0u, 0u);
+}
+
+template <int SLOTS>
+__device__ __forceinline__ void write_row(Smem<SLOTS>& sm, int s, int slot, const uint4& r0, const uint4& r1) {
     *reinterpret_cast<uint4*>(&sm.b[s][core_off(slot, 0)]) = r0;
     *reinterpret_cast<uint4*>(&sm.b[s][core_off(slot, 1)]) = r1;
 }
 
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) raster_tensor_kernel(RasterArgs a) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+// Unit geometry: the unit's top-left tile, the group whose list it walks, member-tile liveness.
+struct UnitGeom {
+    int tx0, ty0;   // top-left tile of the unit (absolute tile coords)
+    int gid;        // band-local group id
+    uint32_t live;  // member tiles inside the tile grid
+};
+
+template <int SLOTS>
+__device__ __forceinline__ UnitGeom unit_geom(const GroupGeom& gg, int unit) {
+    UnitGeom u;
+    if (SLOTS == 1) {  // G == 1: unit == tile == group
+        const int gx = unit % gg.groups_x, gy = unit / gg.groups_x + gg.band_gy0;
+        u.tx0 = gx;
+        u.ty0 = gy;
+        u.gid = unit;
+        u.live = 1u;
+        return u;
+    }
+    // G == 2: unit == group; G == 4: unit == quarter (2x2 tiles) of a group
+    const int per = (gg.g == 4) ? 4 : 1;
+    const int grp = unit / per, quarter = unit % per;
+    const int gx = grp % gg.groups_x, gy = grp / gg.groups_x + gg.band_gy0;
+    u.tx0 = gx * gg.g + (quarter & 1) * 2;
+    u.ty0 = gy * gg.g + (quarter >> 1) * 2;
+    u.gid = grp;
+    u.live = 0u;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+        if (u.tx0 + (t & 1) < gg.tiles_x && u.ty0 + (t >> 1) < gg.tiles_y) u.live |= 1u << t;
+    return u;
+}
+
+template <int SLOTS>
+__global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kernel(RasterArgs a) {
+    using R = Roles<SLOTS>;
+    constexpr int kMT = R::kMT, SPW = R::kSPW, kEpiWarps = R::kEpiWarps;
+    constexpr int kProd = R::kProd, kMma = R::kMma;
+    constexpr int kColsPerStage = kMT * kN;
+    constexpr uint32_t kTmemCols = tmem_cols<SLOTS>();
+    // No-swizzle K-major operands only need 16-byte alignment (descriptor addresses are >> 4).
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    Smem<SLOTS>& sm = *reinterpret_cast<Smem<SLOTS>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const GroupGeom& gg = a.gg;
-    const int G = gg.g;
-    const int trow0 = gg.band_gy0 * G;                                  // first tile row of the band
-    const int trows = min(gg.tiles_y, gg.band_gy1 * G) - trow0;
-    const int n_tiles = gg.tiles_x * trows;
-    constexpr int kProd = kEpi, kMma = kEpi + 1;
+    const int n_units = (SLOTS == 1 || gg.g == 2) ? gg.n_groups_band : gg.n_groups_band * 4;
+    const float centre = SLOTS == 1 ? 8.0f : 16.0f;
 
-    // ---- setup: A operand, barriers, TMEM ----------------------------------------------------
-    for (int p = threadIdx.x; p < 256; p += blockDim.x) {
-        const int pix = lane_pixel(p >> 7, p & 127);  // A row p feeds TMEM lane p%128 of M-tile p/128
-        const float ux = (float)(pix & 15) - 7.5f, uy = (float)(pix >> 4) - 7.5f;
+    // ---- setup: A operand (pixel monomials + tile one-hot), barriers, TMEM -----------------
+    for (int p = threadIdx.x; p < kMT * 128; p += blockDim.x) {
+        const int m = p >> 7, l = p & 127;
+        int x, y;
+        lane_pixel(m, l, x, y);
+        const float ux = (float)x + 0.5f - centre, uy = (float)y + 0.5f - centre;
         const float phi[6] = {ux * ux, ux * uy, uy * uy, ux, uy, 1.0f};
+        const int t = m >> 1;
         uint4 lo, hi;
         lo.x = pack_half2(phi[0], phi[1]);
         lo.y = pack_half2(phi[2], phi[3]);
@@ -165,21 +253,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) raster_tensor_kernel(Ras
         lo.w = pack_half2(phi[0], phi[1]);
         hi.x = pack_half2(phi[2], phi[3]);
         hi.y = pack_half2(phi[4], phi[5]);
-        hi.z = 0u;
-        hi.w = 0u;
-        *reinterpret_cast<uint4*>(sm.a + core_off(p, 0)) = lo;
-        *reinterpret_cast<uint4*>(sm.a + core_off(p, 1)) = hi;
+        hi.z = pack_half2(t == 0 ? 1.0f : 0.0f, t == 1 ? 1.0f : 0.0f);
+        hi.w = pack_half2(t == 2 ? 1.0f : 0.0f, t == 3 ? 1.0f : 0.0f);
+        *reinterpret_cast<uint4*>(&sm.a[m][core_off(l, 0)]) = lo;
+        *reinterpret_cast<uint4*>(&sm.a[m][core_off(l, 1)]) = hi;
+    }
+    if (threadIdx.x < 16) {
+        sm.wdone[threadIdx.x] = threadIdx.x < kEpiWarps ? 0 : 0x7fffffff;
+        sm.dead[threadIdx.x] = -1;
     }
     if (threadIdx.x == 0) {
         for (int s = 0; s < kSS; ++s) {
             ptx::mbar_init(&sm.full[s], 1);
-            ptx::mbar_init(&sm.done[s], kEpi);
+            sm.done_cnt[s] = 0;
         }
-        for (int s = 0; s < kTS; ++s) {
-            ptx::mbar_init(&sm.tfull[s], 1);
-            ptx::mbar_init(&sm.tempty[s], kEpi);
-        }
-        for (int w = 0; w < kEpi; ++w) sm.dead_seq[w] = -1;
+        for (int s = 0; s < kTS; ++s) ptx::mbar_init(&sm.tfull[s], 1);
         ptx::mbar_fence_init();
     }
     if (warp == kMma) ptx::tmem_alloc<kTmemCols>(&sm.tmem_base);
@@ -191,32 +279,63 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) raster_tensor_kernel(Ras
 
     if (warp == kProd) {
         // ================================ producer ===========================================
-        const float skip = a.alpha_skip;
-        uint32_t c = 0;     // chunks emitted so far
-        int seq = 0;        // tiles started by this CTA
+        const float skip = a.alpha_skip, clampv = a.alpha_clamp;
+        uint32_t c = 0;  // chunks emitted so far
         const uint32_t lt = (1u << lane) - 1u;
-        for (;; ++seq) {
+        auto open_stage = [&](uint32_t cc) {
+            // stage cc % kSS is free once every epilogue warp finished chunk cc - kSS (lane 0
+            // polls, the warp reconverges after)
+            const int s = (int)(cc % kSS);
+            if (cc >= (uint32_t)kSS && lane == 0) {
+                const unsigned int need = (unsigned int)kEpiWarps * (cc / kSS);
+                if (ld_volatile_u32(&sm.done_cnt[s]) < need) {
+                    const long long t0 = clock64();
+                    while (ld_volatile_u32(&sm.done_cnt[s]) < need) {
+                        __nanosleep(32);
+                        if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producer/done", (int)cc, s);
+                    }
+                }
+            }
+            __syncwarp();
+            return s;
+        };
+        auto publish = [&](int s, int seq, int unit, int n_valid, uint32_t live) {
+            if (lane == 0) {
+                sm.hdr[s].seq = seq;
+                sm.hdr[s].unit = unit;
+                sm.hdr[s].n_valid = n_valid;
+                sm.hdr[s].live = (int)live;
+                sm.hdr[s].chunk = (int)c;
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&sm.full[s]);
+            __syncwarp();
+        };
+        for (int seq = 0;; ++seq) {
             int t = 0;
             if (lane == 0) t = (int)atomicAdd(&a.fc->group_counter, 1u);
             t = __shfl_sync(0xffffffffu, t, 0);
-            if (t >= n_tiles) break;
-            const int tile = a.order ? a.order[t] : t;
-            const int tx = tile % gg.tiles_x, ty = tile / gg.tiles_x + trow0;
-            const int gid = (ty / G - gg.band_gy0) * gg.groups_x + tx / G;
-            const uint32_t begin = a.offsets[gid], end = a.offsets[gid + 1];
-            const float ox = (float)(tx * kTile + 8), oy = (float)(ty * kTile + 8);
-            int fill = 0;                 // rows placed in the open chunk
-            bool open = false;            // a stage is open for this tile
-            bool emitted = false;         // at least one chunk of this tile emitted
+            if (t >= n_units) break;
+            const int unit = a.order ? a.order[t] : t;
+            const UnitGeom ug = unit_geom<SLOTS>(gg, unit);
+            const uint32_t begin = a.offsets[ug.gid], end = a.offsets[ug.gid + 1];
+            const float ox = (float)(ug.tx0 * kTile) + centre, oy = (float)(ug.ty0 * kTile) + centre;
+            int fill = 0;          // rows placed in the open chunk
+            bool open = false;     // a stage is open for this unit
+            bool emitted = false;  // at least one chunk of this unit emitted
+            uint32_t live = ug.live;
             int s = 0;
-            // Software-pipelined gather: list indices two batches ahead, splat records one
-            // batch ahead, so the dependent idx -> record loads overlap the row building.
+            // software-pipelined gather: list indices two batches ahead, records one ahead
             const uint32_t nb = (end - begin + 31u) / 32u;
             auto ld_idx = [&](uint32_t b) -> uint32_t {
                 const uint32_t e = begin + b * 32u + (uint32_t)lane;
                 return (b < nb && e < end) ? __ldg(&a.list[e]) : 0xffffffffu;
             };
-            struct Rec { float4 mc, co, col; uint32_t idx; };
+            struct Rec {
+                float4 mc, co, col;
+                uint32_t idx;
+            };
             auto ld_rec = [&](uint32_t idx) -> Rec {
                 Rec r;
                 r.idx = idx;
@@ -231,59 +350,72 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) raster_tensor_kernel(Ras
             };
             uint32_t idx_next2 = ld_idx(1);
             Rec nxt = ld_rec(ld_idx(0));
+
             for (uint32_t bi = 0; bi < nb; ++bi) {
                 const Rec cur = nxt;
                 nxt = ld_rec(idx_next2);
                 idx_next2 = ld_idx(bi + 2);
-                // retire as soon as every epilogue warp reported the tile terminated
-                if (emitted) {
-                    int dmin = ((volatile int*)sm.dead_seq)[0];
+                if (emitted) {  // drop member tiles whose pixels all terminated (all owner warps)
+                    uint32_t retired = 0xfu;
 #pragma unroll
-                    for (int w = 1; w < kEpi; ++w) dmin = min(dmin, ((volatile int*)sm.dead_seq)[w]);
-                    if (dmin >= seq) break;
+                    for (int w4 = 0; w4 < kEpiWarps; w4 += 4) {
+                        const int4 d = ld_volatile_v4(&sm.dead[w4]);
+                        const int dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int w = w4 + j;
+                            const uint32_t owned = ((1u << SPW) - 1u) << ((w >> 3) * SPW);
+                            retired &= ((dd[j] >> 4) == seq ? (uint32_t)(dd[j] & 15) : 0u) | (0xfu & ~owned);
+                        }
+                    }
+                    // sm.dead is written concurrently by the epilogue warps: take lane 0's view so
+                    // the whole warp makes the same decision (lanes may read it at different times)
+                    retired = __shfl_sync(0xffffffffu, retired, 0);
+                    live &= ~retired;
+                    if (live == 0u) break;
                 }
                 bool keep = false;
+                uint4 r0, r1;
+                float4 epi_v = make_float4(0, 0, 0, 0);
                 if (cur.idx != 0xffffffffu) {
                     int x0, y0, x1, y1;
-                    tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1, y1);
-                    keep = tx >= x0 && tx <= x1 && ty >= y0 && ty <= y1 && !(fminf(a.alpha_clamp, cur.co.y) < skip);
+                    tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1,
+                              y1);
+                    uint32_t cover = 0;
+#pragma unroll
+                    for (int k = 0; k < SLOTS; ++k) {
+                        const int tx = ug.tx0 + (k & 1), ty = ug.ty0 + (k >> 1);
+                        if (tx >= x0 && tx <= x1 && ty >= y0 && ty <= y1) cover |= 1u << k;
+                    }
+                    cover &= live;
+                    const float cj = fminf(clampv, cur.co.y);
+                    if (cover != 0u && !(cj < skip)) {
+                        keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox,
+                                        oy, cover, r0, r1);
+                        epi_v = make_float4(cur.col.x, cur.col.y, cur.col.z, cj);
+                    }
                 }
                 const uint32_t km = __ballot_sync(0xffffffffu, keep);
                 if (km == 0u) continue;
+
                 const int nk = __popc(km);
                 const int rank = __popc(km & lt);
-                uint4 r0, r1;
-                float4 epi_v = make_float4(0, 0, 0, 0);
-                if (keep) {
-                    make_row(true, cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox, oy,
-                             r0, r1);
-                    epi_v = make_float4(cur.col.x, cur.col.y, cur.col.z, fminf(a.alpha_clamp, cur.co.y));
-                }
                 if (!open) {
-                    s = (int)(c % kSS);
-                    if (c >= (uint32_t)kSS) ptx::mbar_wait(&sm.done[s], ((c / kSS) - 1) & 1);
+                    s = open_stage(c);
                     open = true;
                     fill = 0;
                 }
+                // place the kept ranks (nk <= 32 = kN, so a batch spills into at most one new chunk)
                 const int room = kN - fill;
                 if (keep && rank < room) {
                     write_row(sm, s, fill + rank, r0, r1);
                     sm.epi[s][fill + rank] = epi_v;
                 }
-                if (nk >= room) {
-                    // chunk full: publish it and open the next one for the remaining ranks
-                    if (lane == 0) {
-                        sm.hdr[s].seq = seq;
-                        sm.hdr[s].tile = tile;
-                        sm.hdr[s].n_valid = kN;
-                    }
-                    ptx::fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&sm.full[s]);
+                if (nk >= room) {  // chunk full: publish it, open the next for the remaining ranks
+                    publish(s, seq, unit, kN, live);
                     ++c;
                     emitted = true;
-                    s = (int)(c % kSS);
-                    if (c >= (uint32_t)kSS) ptx::mbar_wait(&sm.done[s], ((c / kSS) - 1) & 1);
+                    s = open_stage(c);
                     if (keep && rank >= room) {
                         write_row(sm, s, rank - room, r0, r1);
                         sm.epi[s][rank - room] = epi_v;
@@ -293,94 +425,116 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) raster_tensor_kernel(Ras
                     fill += nk;
                 }
             }
-            // close the tile: pad and publish the partial chunk (or an empty one so the
-            // epilogue still writes the tile)
+            // close the unit: pad and publish the partial chunk (or an empty one so the
+            // epilogue still writes the unit's pixels)
             if (open && (fill > 0 || !emitted)) {
-                if (lane >= fill) {
+                if (lane >= fill && lane < kN) {
                     uint4 r0, r1;
-                    make_row(false, 0, 0, 0, 0, 0, 0, 0, 0, r0, r1);
+                    never_row(r0, r1);
                     write_row(sm, s, lane, r0, r1);
                 }
-                if (lane == 0) {
-                    sm.hdr[s].seq = seq;
-                    sm.hdr[s].tile = tile;
-                    sm.hdr[s].n_valid = fill;
-                }
-                ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&sm.full[s]);
+                publish(s, seq, unit, fill, live);
                 ++c;
             } else if (!open) {
-                s = (int)(c % kSS);
-                if (c >= (uint32_t)kSS) ptx::mbar_wait(&sm.done[s], ((c / kSS) - 1) & 1);
-                if (lane == 0) {
-                    sm.hdr[s].seq = seq;
-                    sm.hdr[s].tile = tile;
-                    sm.hdr[s].n_valid = 0;
-                }
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&sm.full[s]);
+                s = open_stage(c);
+                publish(s, seq, unit, 0, live);
                 ++c;
             }
         }
-        // end of stream
-        const int s = (int)(c % kSS);
-        if (c >= (uint32_t)kSS) ptx::mbar_wait(&sm.done[s], ((c / kSS) - 1) & 1);
-        if (lane == 0) {
-            sm.hdr[s].seq = -1;
-            sm.hdr[s].tile = -1;
-            sm.hdr[s].n_valid = 0;
-            ptx::mbar_arrive(&sm.full[s]);
-        }
-        __syncwarp();
+        const int s = open_stage(c);  // end of stream
+        publish(s, -1, -1, 0, 0u);
     } else if (warp == kMma) {
         // ================================ MMA issuer ==========================================
         constexpr uint32_t idesc = ptx::idesc_f16(128, kN);
-        const uint32_t a_base = ptx::smem_u32(sm.a);
+        const uint32_t a_base = ptx::smem_u32(&sm.a[0][0]);
         for (uint32_t c = 0;; ++c) {
             const int s = (int)(c % kSS), ts = (int)(c % kTS);
-            ptx::mbar_wait(&sm.full[s], (c / kSS) & 1);
-            if (c >= (uint32_t)kTS) ptx::mbar_wait(&sm.tempty[ts], ((c / kTS) - 1) & 1);
-            ptx::tc_fence_after();
-            const ChunkHeader h = sm.hdr[s];
-            if (lane == 0) {
-                if (h.seq >= 0 && h.n_valid > 0) {
-                    const uint32_t dcol = tmem + (uint32_t)(ts * 2 * kN);
-                    const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[s][0]), 128, 256);
-                    ptx::mma_f16_ss(dcol, ptx::smem_desc(a_base, 128, 256), bd, idesc, 0u);
-                    ptx::mma_f16_ss(dcol + (uint32_t)kN, ptx::smem_desc(a_base + 4096u, 128, 256), bd, idesc, 0u);
-                    ptx::mma_commit(&sm.tfull[ts]);
-                } else {
-                    ptx::mbar_arrive(&sm.tfull[ts]);
+            ptx::mbar_wait_wd(&sm.full[s], (c / kSS) & 1, "mma/full", (int)c, s);
+            if (c >= (uint32_t)kTS && lane == 0) {  // every epilogue warp finished chunk c - kTS
+                const int need = (int)(c - kTS + 1);
+                auto released = [&]() {
+                    int mn = 0x7fffffff;
+#pragma unroll
+                    for (int w4 = 0; w4 < 16; w4 += 4) {
+                        const int4 d = ld_volatile_v4(&sm.wdone[w4]);
+                        mn = min(mn, min(min(d.x, d.y), min(d.z, d.w)));
+                    }
+                    return mn >= need;
+                };
+                if (!released()) {
+                    const long long t0 = clock64();
+                    while (!released()) {
+                        __nanosleep(32);
+                        if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("mma/tempty", (int)c, 0);
+                    }
                 }
             }
             __syncwarp();
-            if (h.seq < 0) break;
+            ptx::tc_fence_after();
+            // warp-uniform issue (operands stay uniform; one elected lane issues)
+            const int hseq = __shfl_sync(0xffffffffu, sm.hdr[s].seq, 0);
+            const int hnv = __shfl_sync(0xffffffffu, sm.hdr[s].n_valid, 0);
+            const uint32_t hlive = __shfl_sync(0xffffffffu, (uint32_t)sm.hdr[s].live, 0);
+            const int hch = __shfl_sync(0xffffffffu, sm.hdr[s].chunk, 0);
+            if (hch != (int)c) {
+                if (lane == 0) printf("MMA header mismatch: expected chunk %d found %d (seq %d)\n", (int)c, hch, hseq);
+                __trap();
+            }
+            if (hseq >= 0 && hnv > 0) {
+                const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[s][0]), 128, 256);
+                const uint32_t dcol = tmem + (uint32_t)(ts * kColsPerStage);
+#pragma unroll
+                for (int m = 0; m < kMT; ++m)
+                    if ((hlive >> (m >> 1)) & 1u)
+                        ptx::mma_f16_ss_elect(dcol + (uint32_t)(m * kN),
+                                              ptx::smem_desc(a_base + (uint32_t)(m * 128 * 32), 128, 256), bd, idesc, 0u);
+                ptx::mma_commit_elect(&sm.tfull[ts]);
+            } else if (lane == 0) {
+                ptx::mbar_arrive(&sm.tfull[ts]);
+            }
+            __syncwarp();
+            if (hseq < 0) break;
         }
     } else {
         // ================================ epilogue ============================================
-        const int q = warp;
-        const int p0 = lane_pixel(0, q * 32 + lane), p1 = lane_pixel(1, q * 32 + lane);
-        const int prow[2] = {p0 >> 4, p1 >> 4};
-        const int pcol = p0 & 15;
-        float T[2], cr[2], cg[2], cb[2], thr[2];
-        int px = 0, py[2] = {0, 0};
-        bool inside[2] = {false, false};
+        // warp -> (lane quadrant q, tile half, slots k0 .. k0+SPW-1); slot i of a thread is a
+        // pixel of member tile k0 + i
+        const int q = warp & 3, half = (warp >> 2) & 1, k0 = (warp >> 3) * SPW;
+        int relx[SPW], rely[SPW];
+#pragma unroll
+        for (int k = 0; k < SPW; ++k) lane_pixel(2 * (k0 + k) + half, q * 32 + lane, relx[k], rely[k]);
+        float T[SPW], cr[SPW], cg[SPW], cb[SPW], thr[SPW];
+        int px[SPW], py[SPW];
         const float L = log2f(a.alpha_skip);
         const float tterm = a.t_terminate;
         int cur = -1;
-        bool reported = false;
+        uint32_t alive = 0;     // warp-uniform: slots with a non-terminated pixel
+        uint32_t reported = 0;  // dead slots already published for `cur`
+        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+        // Accumulator registers.  A retired slot skips its tcgen05.ld and keeps stale finite
+        // values, which never pass the D >= thr test because its thr is +inf.
+        uint32_t d[SPW][16];
+#pragma unroll
+        for (int k = 0; k < SPW; ++k)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) d[k][j] = 0u;
         for (uint32_t c = 0;; ++c) {
             const int s = (int)(c % kSS), ts = (int)(c % kTS);
-            ptx::mbar_wait(&sm.tfull[ts], (c / kTS) & 1);
+            // this warp consumed the phase of chunk c - kTS itself, so the parity is unambiguous
+            ptx::mbar_wait_wd(&sm.tfull[ts], (c / kTS) & 1, "epilogue/tfull", (int)c, warp);
             ptx::tc_fence_after();
             const ChunkHeader h = sm.hdr[s];
+            if (h.chunk != (int)c) {
+                if (lane == 0)
+                    printf("EPI w%d header mismatch: expected chunk %d found %d (seq %d)\n", warp, (int)c, h.chunk, h.seq);
+                __trap();
+            }
             if (h.seq != cur) {
                 if (cur >= 0) {
 #pragma unroll
-                    for (int k = 0; k < 2; ++k)
-                        if (inside[k]) {
-                            float* o = a.image + ((size_t)(py[k] - a.image_row0) * gg.width + px) * 3;
+                    for (int k = 0; k < SPW; ++k)
+                        if (px[k] >= 0) {
+                            float* o = a.image + ((size_t)(py[k] - a.image_row0) * gg.width + px[k]) * 3;
                             o[0] = fminf(fmaxf(cr[k], 0.0f), 1.0f);
                             o[1] = fminf(fmaxf(cg[k], 0.0f), 1.0f);
                             o[2] = fminf(fmaxf(cb[k], 0.0f), 1.0f);
@@ -388,101 +542,89 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) raster_tensor_kernel(Ras
                 }
                 if (h.seq < 0) break;
                 cur = h.seq;
-                reported = false;
-                const int tx = h.tile % gg.tiles_x, ty = h.tile / gg.tiles_x + trow0;
-                px = tx * kTile + pcol;
+                reported = 0;
+                const UnitGeom ug = unit_geom<SLOTS>(gg, h.unit);
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    py[k] = ty * kTile + prow[k];
-                    inside[k] = px < gg.width && py[k] < gg.height;
+                for (int k = 0; k < SPW; ++k) {
+                    const int x = ug.tx0 * kTile + relx[k], y = ug.ty0 * kTile + rely[k];
+                    const bool inside = x < gg.width && y < gg.height;
+                    px[k] = inside ? x : -1;
+                    py[k] = y;
                     T[k] = 1.0f;
                     cr[k] = cg[k] = cb[k] = 0.0f;
-                    thr[k] = inside[k] ? L : kInf;
+                    thr[k] = inside ? L : kInf;
                 }
+                alive = 0;
+#pragma unroll
+                for (int k = 0; k < SPW; ++k)
+                    if (__any_sync(0xffffffffu, thr[k] != kInf)) alive |= 1u << k;
             }
-            const bool work = h.n_valid > 0 && __any_sync(0xffffffffu, thr[0] != kInf || thr[1] != kInf);
-            const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ts * 2 * kN);
+            const int nv = h.n_valid;
+            const uint32_t stage_col = (uint32_t)(ts * kColsPerStage);
+            if (nv > 0 && alive != 0u) {
+#pragma unroll 1
+                for (int j0 = 0; j0 < nv; j0 += 16) {
 #pragma unroll
-            for (int blk = 0; blk < 2; ++blk) {
-                const int j0 = blk * 16;
-                uint32_t d[2][16];
-                if (work) {
-                    ptx::tmem_ld16(lane_base + (uint32_t)j0, d[0]);
-                    ptx::tmem_ld16(lane_base + (uint32_t)(kN + j0), d[1]);
+                    for (int k = 0; k < SPW; ++k)
+                        if (alive & (1u << k))
+                            ptx::tmem_ld16(lane_base + stage_col + (uint32_t)((2 * (k0 + k) + half) * kN + j0), d[k]);
                     ptx::tmem_wait_ld();
-                    ptx::reg_fence16(d[0]);
-                    ptx::reg_fence16(d[1]);
-                }
-                if (blk == 1) {  // TMEM drained into registers: the next MMA may overwrite it
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&sm.tempty[ts]);
-                }
-                if (!work) continue;
-                // Speculative pass: blend every splat with D >= thr without the per-splat
-                // termination test (no loop-carried compare chain); T only decreases, so
-                // T_end < t_terminate <=> the pixel terminated inside this block, which is then
-                // replayed exactly (at most once per pixel per tile).
-                float T0[2], r0[2], g0[2], b0[2];
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    T0[k] = T[k];
-                    r0[k] = cr[k];
-                    g0[k] = cg[k];
-                    b0[k] = cb[k];
-                }
+                    for (int k = 0; k < SPW; ++k) ptx::reg_fence16(d[k]);
+                    // Phase 1 (branch-free, 16 independent chains): which of the 16 splats reach
+                    // alpha_skip at any of this warp's pixels -> warp-uniform mask.
+                    uint32_t mk = 0;
 #pragma unroll
-                for (int jj = 0; jj < 16; ++jj) {
-                    const float dA = __uint_as_float(d[0][jj]), dB = __uint_as_float(d[1][jj]);
-                    const bool ta = dA >= thr[0], tb = dB >= thr[1];
-                    if (ta || tb) {
-                        const float4 ej = sm.epi[s][j0 + jj];
-                        const float aA = ta ? fminf(ej.w, ex2_approx(dA)) : 0.0f;
-                        const float aB = tb ? fminf(ej.w, ex2_approx(dB)) : 0.0f;
-                        const float wA = T[0] * aA, wB = T[1] * aB;
-                        cr[0] = fmaf(wA, ej.x, cr[0]);
-                        cg[0] = fmaf(wA, ej.y, cg[0]);
-                        cb[0] = fmaf(wA, ej.z, cb[0]);
-                        cr[1] = fmaf(wB, ej.x, cr[1]);
-                        cg[1] = fmaf(wB, ej.y, cg[1]);
-                        cb[1] = fmaf(wB, ej.z, cb[1]);
-                        T[0] -= wA;
-                        T[1] -= wB;
+                    for (int jj = 0; jj < 16; ++jj) {
+                        uint32_t p = 0;
+#pragma unroll
+                        for (int k = 0; k < SPW; ++k) p |= fset_ge(__uint_as_float(d[k][jj]), thr[k]);
+                        mk |= p & (1u << jj);
                     }
-                }
+                    const uint32_t M = __reduce_or_sync(0xffffffffu, mk);
+                    // Phase 2: ordered blend of the active splats (uniform branches).  A pixel blends
+                    // splat j iff D >= log2(alpha_skip) and it had not terminated before j
+                    // (T >= t_terminate): exactly alpha_of/blend/done (raster_scalar.hpp:40-55,
+                    // raster_scalar.cpp:36-41) — the splat that drives T below t_terminate is
+                    // blended, nothing after it.
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    if (T[k] < tterm) {  // terminated inside the block: exact replay
-                        T[k] = T0[k];
-                        cr[k] = r0[k];
-                        cg[k] = g0[k];
-                        cb[k] = b0[k];
-                        bool stop = false;
+                    for (int jj = 0; jj < 16; ++jj) {
+                        if (M & (1u << jj)) {
+                            const float4 ej = sm.epi[s][j0 + jj];
 #pragma unroll
-                        for (int jj = 0; jj < 16; ++jj) {
-                            const float dv = __uint_as_float(d[k][jj]);
-                            if (!stop && dv >= thr[k]) {
-                                const float4 ej = sm.epi[s][j0 + jj];
-                                const float wt = T[k] * fminf(ej.w, ex2_approx(dv));
+                            for (int k = 0; k < SPW; ++k) {
+                                const float dv = __uint_as_float(d[k][jj]);
+                                const float e2 = fminf(ej.w, ex2_approx(dv));
+                                const float al = (dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f;
+                                const float wt = T[k] * al;
                                 cr[k] = fmaf(wt, ej.x, cr[k]);
                                 cg[k] = fmaf(wt, ej.y, cg[k]);
                                 cb[k] = fmaf(wt, ej.z, cb[k]);
                                 T[k] -= wt;
-                                stop = T[k] < tterm;
                             }
                         }
-                        thr[k] = kInf;
                     }
+#pragma unroll
+                    for (int k = 0; k < SPW; ++k)
+                        if (T[k] < tterm) thr[k] = kInf;
                 }
             }
-            // report this warp's pixels terminated (once per tile) so the producer can retire
-            const bool dead = !__any_sync(0xffffffffu, thr[0] != kInf || thr[1] != kInf);
+            // retire slots whose pixels all terminated; report once per unit
+            uint32_t dead = 0;
+#pragma unroll
+            for (int k = 0; k < SPW; ++k)
+                if (!__any_sync(0xffffffffu, thr[k] != kInf)) dead |= 1u << k;
+            alive &= ~dead;
+            // TMEM stage and smem stage consumed (all tcgen05.ld of this warp completed above)
+            ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if (dead && !reported) ((volatile int*)sm.dead_seq)[q] = cur;
-                ptx::mbar_arrive(&sm.done[s]);
+                if (dead != reported) ((volatile int*)sm.dead)[warp] = (cur << 4) | (int)(dead << k0);
+                __threadfence_block();
+                ((volatile int*)sm.wdone)[warp] = (int)c + 1;
+                atomicAdd(&sm.done_cnt[s], 1u);
             }
-            reported = reported || dead;
+            reported = dead;
         }
     }
 
@@ -492,16 +634,23 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) raster_tensor_kernel(Ras
     if (warp == kMma) ptx::tmem_dealloc<kTmemCols>(tmem);
 }
 
+template <int SLOTS>
+void launch_t(const RasterArgs& a, int num_sms, cudaStream_t st) {
+    const size_t smem = sizeof(Smem<SLOTS>);
+    cudaFuncSetAttribute(raster_tensor_kernel<SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int n_units = (SLOTS == 1 || a.gg.g == 2) ? a.gg.n_groups_band : a.gg.n_groups_band * 4;
+    int grid = num_sms;
+    if (grid > n_units) grid = n_units;
+    if (grid > 0) raster_tensor_kernel<SLOTS><<<grid, Roles<SLOTS>::kThreads, smem, st>>>(a);
+}
+
 }  // namespace
 
 void launch_raster_tensor(const RasterArgs& a, int num_sms, cudaStream_t st) {
-    const size_t smem = sizeof(Smem) + 1024;
-    cudaFuncSetAttribute(raster_tensor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int trows = std::min(a.gg.tiles_y, a.gg.band_gy1 * a.gg.g) - a.gg.band_gy0 * a.gg.g;
-    const int n_tiles = a.gg.tiles_x * trows;
-    int grid = num_sms * kCtasPerSm;
-    if (grid > n_tiles) grid = n_tiles;
-    if (grid > 0) raster_tensor_kernel<<<grid, kThreads, smem, st>>>(a);
+    if (a.gg.g == 1)
+        launch_t<1>(a, num_sms, st);
+    else
+        launch_t<4>(a, num_sms, st);
 }
 
 }  // namespace tgs
@@ -516,7 +665,7 @@ __global__ void __launch_bounds__(128, 1) debug_mma_kernel(const uint16_t* __res
     __shared__ __align__(1024) uint8_t sb[32 * 32];
     __shared__ uint64_t bar;
     __shared__ uint32_t tbase;
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int t = threadIdx.x, warp = t >> 5;
     // row t of A (16 halves) -> core-matrix layout
     for (int kh = 0; kh < 2; ++kh) {
         uint4 v = *reinterpret_cast<const uint4*>(a + t * 16 + kh * 8);
@@ -554,7 +703,6 @@ __global__ void __launch_bounds__(128, 1) debug_mma_kernel(const uint16_t* __res
     __syncthreads();
     ptx::tc_fence_after();
     if (warp == 0) ptx::tmem_dealloc<32>(tm);
-    (void)lane;
 }
 }  // namespace
 

@@ -21,7 +21,7 @@ OBJ = os.path.join(HERE, "_obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
-           "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+           "--expt-relaxed-constexpr", "-Xptxas", "-v"] + os.environ.get("TGS_NVCC_EXTRA", "").split()
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math"]
 
 

@@ -1,0 +1,159 @@
+// gsr_b200.hpp — C++ drop-in for the reference's render entry point on B200 (libtgs.so).
+//
+// Source-compatible re-declaration of the types a caller of the reference uses
+//   gsr::render(const std::vector<Gaussian3D>&, const Camera&, const RenderOptions&)
+//     (reference: proj/include/gsr/render.hpp:8-31, src/render.cpp:7-35)
+// with Gaussian3D / Camera / ImageBuffer / FormatError / ValidationError (types.hpp:14-69),
+// ProjectionStats (projection.hpp:40-44), OpReport (metrics.hpp:49-69), RasterConstants
+// (raster_scalar.hpp:14-18), PrecisionMode (operands.hpp:13).  A program written against the
+// reference's render.hpp compiles against this header unchanged and links libtgs.so instead of
+// the reference's libgsr; the pipeline runs on the GPU behind the C ABI in include/tgs.h.
+//
+// Like the reference, the types hold Eigen values, so the caller's Eigen (>= 3.3, the reference's
+// own dependency, CMakeLists.txt:14) must be on the include path.
+//
+// Differences a caller can observe: images are within the stated FP16
+// tolerance of the reference's fp32 image instead of byte-identical; RenderResult::ops (the
+// emulated-fragment counters of the CPU tensor path) are not produced and stay zero; `workers`
+// and `chunk_len` are validated like the reference and otherwise ignored.
+#pragma once
+
+#include <Eigen/Core>
+#include <Eigen/Geometry>
+
+#include <array>
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <vector>
+
+namespace gsr {
+
+struct FormatError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ValidationError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+/// CUDA failure / out of device memory (no counterpart in the CPU reference).
+struct DeviceError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline constexpr int kShRestCoeffs = 45;
+inline constexpr int kFragmentDim = 16;
+
+struct Gaussian3D {
+    Eigen::Vector3f mean = Eigen::Vector3f::Zero();
+    Eigen::Vector3f scale = Eigen::Vector3f::Ones();
+    Eigen::Quaternionf rotation = Eigen::Quaternionf::Identity();
+    float opacity = 1.0f;
+    Eigen::Vector3f sh_dc = Eigen::Vector3f::Zero();
+    std::optional<std::array<float, kShRestCoeffs>> sh_rest;
+};
+
+struct Camera {
+    Eigen::Matrix4f view = Eigen::Matrix4f::Identity();
+    float focal_x = 0.0f;
+    float focal_y = 0.0f;
+    int width = 0;
+    int height = 0;
+    float near = 0.0f;
+    float far = 0.0f;
+
+    Eigen::Matrix3f rotation() const { return view.topLeftCorner<3, 3>(); }
+    Eigen::Vector3f translation() const { return view.topRightCorner<3, 1>(); }
+    Eigen::Vector3f position() const { return -(rotation().transpose() * translation()); }
+};
+
+struct ImageBuffer {
+    int width = 0;
+    int height = 0;
+    std::vector<float> rgb;
+
+    ImageBuffer() = default;
+    ImageBuffer(int w, int h) : width(w), height(h), rgb(static_cast<size_t>(w) * h * 3, 0.0f) {}
+    float* pixel(int x, int y) { return &rgb[(static_cast<size_t>(y) * width + x) * 3]; }
+    const float* pixel(int x, int y) const { return &rgb[(static_cast<size_t>(y) * width + x) * 3]; }
+    void finalize() {
+        for (float& v : rgb) v = v < 0.0f ? 0.0f : (v > 1.0f ? 1.0f : v);
+    }
+};
+
+enum class PrecisionMode { fp32, fp16 };
+
+struct RasterConstants {
+    float alpha_skip = 1.0f / 255.0f;
+    float alpha_clamp = 0.99f;
+    float t_terminate = 1e-4f;
+};
+
+struct ProjectionStats {
+    std::size_t input = 0;
+    std::size_t culled = 0;
+    std::size_t dropped_degenerate = 0;
+};
+
+struct OpReport {
+    std::uint64_t fragment_ops = 0;
+    std::uint64_t chunk_loads = 0;
+    std::uint64_t skipped_pairs = 0;
+    std::uint64_t used_lanes = 0;
+    std::uint64_t total_lanes = 0;
+    double padding_waste() const {
+        return total_lanes ? 1.0 - static_cast<double>(used_lanes) / static_cast<double>(total_lanes) : 0.0;
+    }
+};
+
+enum class Backend { scalar, tensor };
+
+struct RenderOptions {
+    Backend backend = Backend::tensor;
+    PrecisionMode mode = PrecisionMode::fp32;
+    int group_size = 2;
+    int workers = 1;
+    int chunk_len = kFragmentDim;
+    RasterConstants constants{};
+};
+
+struct RenderResult {
+    ImageBuffer image;
+    ProjectionStats projection;
+    OpReport ops;
+    std::uint64_t entries = 0;
+    std::uint64_t tile_appearances = 0;
+};
+
+/// Drop-in for the reference's gsr::render: uploads the scene, renders on the current B200
+/// (device 0 unless gsr::b200::set_device was called), downloads the image.
+RenderResult render(const std::vector<Gaussian3D>& scene, const Camera& cam, const RenderOptions& opt);
+
+namespace b200 {
+
+/// Device used by gsr::render on this thread (default 0).
+void set_device(int device);
+
+/// Per-stage device times of the last render on this thread (CUDA events, milliseconds).
+struct StageTimes {
+    float preprocess = 0, binning = 0, sort = 0, raster = 0, total = 0;
+};
+StageTimes last_stage_times();
+
+/// Persistent device-resident scene: marshal + upload once, render many cameras.
+class DeviceScene {
+public:
+    explicit DeviceScene(const std::vector<Gaussian3D>& scene, int device = 0);
+    ~DeviceScene();
+    DeviceScene(const DeviceScene&) = delete;
+    DeviceScene& operator=(const DeviceScene&) = delete;
+    RenderResult render(const Camera& cam, const RenderOptions& opt);
+
+private:
+    struct Impl;
+    std::unique_ptr<Impl> impl_;
+};
+
+}  // namespace b200
+}  // namespace gsr

@@ -6,7 +6,7 @@
  * and its stage API (project_scene projection.hpp:48-50, build_group_entries/sort_entries
  * binning.hpp:68-73, rasterize_tiles_scalar raster_scalar.hpp:59-62, rasterize_groups_tensor
  * raster_tensor.hpp:62-65).  Plain pointers and sizes only: no C++ or torch types cross it.
- * The C++ drop-in (cpp/gsr_render_b200.cpp) and the Python mirror (paper_2605_17855_b200/gsr.py)
+ * The C++ drop-in (cpp/gsr_b200.hpp, cpp/gsr_b200.cpp) and the Python mirror (paper_2605_17855_b200/gsr.py)
  * both sit on top of these entry points; INTEGRATION.md shows the bindings.
  *
  * Every entry point returns a tgs_status; on failure tgs_last_error() describes it.  Status

@@ -25,20 +25,19 @@
 //
 // CTA (persistent, one per SM) = one unit of 2x2 tiles at a time (G=2: the group; G=4: a
 // quarter group; G=1: a single tile with SLOTS = 1), units in longest-list-first order:
-//   warps 0-7  epilogue: warp w reads TMEM lane quadrant q = w%4 of the M-tiles (2t + w/4),
-//              t = 0..SLOTS-1, so each thread owns one pixel in each member tile (slot t); the
-//              ordered blend runs on CUDA cores + MUFU ex2; a retired tile drops out of every
-//              warp at once;
-//   warp 8     producer: streams the unit's list in 32-entry batches (prefetched two ahead),
-//              gathers the splats once, drops entries whose member tiles are all retired or
-//              that can never reach alpha_skip (ballot compaction keeps list order), and writes
-//              the unit-centred coefficient rows (+ mask lanes) and blend data into an smem stage;
-//   warp 9     TMEM owner + MMA issuer: per chunk one tcgen05.mma (M=128, N=32, K=16) per live
-//              M-tile into a TMEM stage (2 stages x 2*SLOTS M-tiles x 32 columns), then
-//              tcgen05.commit -> epilogue.
+//   epilogue warps (16; 8 for G=1): warp w reads TMEM lane quadrant q = w%4 of the M-tiles
+//              2*(k0+i) + half (i < SPW = 2), so each thread owns one pixel in two member tiles;
+//              the ordered blend runs on CUDA cores + MUFU ex2; a retired tile drops out at once;
+//   producer warp: streams the unit's list in 32-entry batches (prefetched two ahead), gathers
+//              each splat once per group, drops entries whose member tiles are all retired or
+//              that can never reach alpha_skip (ballot compaction keeps list order), and writes the
+//              unit-centred coefficient rows (+ mask lanes) and blend data into an smem stage;
+//   MMA warp:  TMEM owner; per chunk one tcgen05.mma (M=128, N=32, K=16) per live M-tile into a
+//              TMEM stage (2 stages x 2*SLOTS M-tiles x 32 columns), issued from warp-uniform code
+//              by an elected lane, then tcgen05.commit -> epilogue.
 // The pixel operand A (2*SLOTS M-tiles x 128 rows x 32 B) is identical for every unit and is
-// built once per CTA.  Stages are guarded by mbarriers; chunk headers carry the unit sequence
-// number, so unit boundaries need no extra synchronisation.
+// built once per CTA.  Hand-offs: full[s] (mbarrier), tfull[ts] (tcgen05.commit), and release
+// counters compared against absolute chunk targets; every wait is watchdog-bounded.
 #include "tgs_common.cuh"
 #include "tgs_kernels.cuh"
 #include "tgs_ptx.cuh"

@@ -102,9 +102,10 @@ struct tgs_ctx {
     DBuf status;        // look-back status words (preprocess | entry scan)
     DBuf proj;          // mc | co | col (capacity n)
     DBuf pre_keys[2], pre_vals[2];
-    DBuf ngroups, eoff;
-    DBuf ent_keys[2], ent_vals[2];
-    DBuf ghist, gid_count, offsets, order;
+    DBuf rect, rrect;   // tile rect per compacted splat / per rank
+    DBuf list;          // sorted group lists (compacted indices)
+    DBuf hist, bsum;    // counting-sort [group][chunk] matrix and its scan block sums
+    DBuf ghist, offsets, order;
     DBuf image;
     DBuf scratch_records;
     FrameCounters* h_fc = nullptr;  // pinned
@@ -116,7 +117,6 @@ struct tgs_ctx {
     tgs_options last_opt{};
     GroupGeom last_gg{};
     int last_band0 = 0, last_band1 = 0;
-    int list_parity = 0;
     int image_rows = 0;
     bool pending = false;
     tgs_scene* scratch_scene = nullptr;
@@ -214,17 +214,15 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
         TGS_CUDA_OK(ctx->pre_keys[i].ensure((size_t)n_alloc * 4));
         TGS_CUDA_OK(ctx->pre_vals[i].ensure((size_t)n_alloc * 4));
     }
-    TGS_CUDA_OK(ctx->ngroups.ensure((size_t)n_alloc * 4));
-    TGS_CUDA_OK(ctx->eoff.ensure((size_t)n_alloc * 4));
-    const size_t pre_tiles = (size_t)(n_alloc + 255) / 256, scan_tiles = (size_t)(n_alloc + 2047) / 2048;
-    TGS_CUDA_OK(ctx->status.ensure((pre_tiles + scan_tiles) * 8));
+    TGS_CUDA_OK(ctx->rect.ensure((size_t)n_alloc * sizeof(uint2)));
+    TGS_CUDA_OK(ctx->rrect.ensure((size_t)n_alloc * sizeof(uint2)));
+    const size_t pre_tiles = (size_t)(n_alloc + 255) / 256;
+    TGS_CUDA_OK(ctx->status.ensure(pre_tiles * 8));
     const uint32_t cap = std::max<uint32_t>(ctx->capacity, 1u);
-    for (int i = 0; i < 2; ++i) {
-        TGS_CUDA_OK(ctx->ent_keys[i].ensure((size_t)cap * 4));
-        TGS_CUDA_OK(ctx->ent_vals[i].ensure((size_t)cap * 4));
-    }
+    TGS_CUDA_OK(ctx->list.ensure((size_t)cap * 4));
+    TGS_CUDA_OK(ctx->hist.ensure(bin_hist_elems(n_groups) * 4));
+    TGS_CUDA_OK(ctx->bsum.ensure(std::max(bin_bsum_elems(n_groups), scan_tmp_elems((size_t)256 * kSortBlocks)) * 4));
     TGS_CUDA_OK(ctx->ghist.ensure((size_t)256 * kSortBlocks * 4));
-    TGS_CUDA_OK(ctx->gid_count.ensure((size_t)n_groups * 4));
     TGS_CUDA_OK(ctx->offsets.ensure((size_t)(n_groups + 1) * 4));
     TGS_CUDA_OK(ctx->order.ensure((size_t)gg.tiles_x * gg.tiles_y * 4));
     const int row0 = band0 * gg.g * kTile;
@@ -233,13 +231,11 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
 
     FrameCounters* fc = ctx->fc.as<FrameCounters>();
     unsigned long long* pre_status = ctx->status.as<unsigned long long>();
-    unsigned long long* scan_status = pre_status + pre_tiles;
     const DevProjected proj = dev_proj(ctx);
 
     TGS_CUDA_OK(cudaEventRecord(ctx->ev[0], s));
     TGS_CUDA_OK(cudaMemsetAsync(fc, 0, sizeof(FrameCounters), s));
-    TGS_CUDA_OK(cudaMemsetAsync(pre_status, 0, (pre_tiles + scan_tiles) * 8, s));
-    TGS_CUDA_OK(cudaMemsetAsync(ctx->gid_count.p, 0, (size_t)n_groups * 4, s));
+    TGS_CUDA_OK(cudaMemsetAsync(pre_status, 0, pre_tiles * 8, s));
 
     // 1. preprocess + compaction
     PreprocessArgs pa;
@@ -248,7 +244,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     pa.out = proj;
     pa.depth_keys = ctx->pre_keys[0].as<uint32_t>();
     pa.idx_vals = ctx->pre_vals[0].as<uint32_t>();
-    pa.ngroups = ctx->ngroups.as<uint32_t>();
+    pa.rect = ctx->rect.as<uint2>();
     pa.gg = gg;
     pa.tile_status = pre_status;
     pa.fc = fc;
@@ -264,37 +260,27 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     pb.vals[1] = ctx->pre_vals[1].as<uint32_t>();
     pb.ghist = ctx->ghist.as<uint32_t>();
     pb.gid_count = nullptr;
+    pb.scan_tmp = ctx->bsum.as<uint32_t>();
     const int pr = radix_sort(pb, &fc->visible, 32, 0, false, s);
     TGS_CUDA_OK(cudaGetLastError());
 
-    // 3. entry counts -> offsets (depth order), 4. emission
+    TGS_CUDA_OK(cudaEventRecord(ctx->ev[2], s));
+
+    // 3. binning: stable counting sort of (group, rank) entries -> lists + per-group offsets
     BinArgs ba;
     ba.visible = &fc->visible;
     ba.sval = pb.vals[pr];
-    ba.ngroups = ctx->ngroups.as<uint32_t>();
-    ba.eoff = ctx->eoff.as<uint32_t>();
-    ba.tile_status = scan_status;
+    ba.rect = ctx->rect.as<uint2>();
+    ba.rrect = ctx->rrect.as<uint2>();
+    ba.gg = gg;
+    ba.hist = ctx->hist.as<uint32_t>();
+    ba.bsum = ctx->bsum.as<uint32_t>();
+    ba.offsets = ctx->offsets.as<uint32_t>();
+    ba.list = ctx->list.as<uint32_t>();
     ba.fc = fc;
     ba.capacity = ctx->capacity;
-    ba.proj = proj;
-    ba.gg = gg;
-    ba.keys = ctx->ent_keys[0].as<uint32_t>();
-    ba.vals = ctx->ent_vals[0].as<uint32_t>();
-    launch_entry_scan(ba, n_alloc, s);
-    launch_emit(ba, n_alloc, s);
-    TGS_CUDA_OK(cudaGetLastError());
-    TGS_CUDA_OK(cudaEventRecord(ctx->ev[2], s));
-
-    // 5. stable group sort + ranges
-    SortBuffers eb;
-    eb.keys[0] = ctx->ent_keys[0].as<uint32_t>();
-    eb.keys[1] = ctx->ent_keys[1].as<uint32_t>();
-    eb.vals[0] = ctx->ent_vals[0].as<uint32_t>();
-    eb.vals[1] = ctx->ent_vals[1].as<uint32_t>();
-    eb.ghist = ctx->ghist.as<uint32_t>();
-    eb.gid_count = ctx->gid_count.as<uint32_t>();
-    const int er = radix_sort(eb, &fc->n_sort, std::max(1, ceil_log2(n_groups)), n_groups, false, s);
-    launch_offsets_scan(eb.gid_count, ctx->offsets.as<uint32_t>(), n_groups, s);
+    ba.n_chunks = bin_chunks(n_groups);
+    launch_binning(ba, n_alloc, s);
     {
         const int per = gg.g == 4 ? 4 : 1;  // G=4 groups are rasterised as 2x2-tile quarters
         launch_unit_order(ctx->offsets.as<uint32_t>(), n_groups * per, per, ctx->order.as<int>(), s);
@@ -305,7 +291,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     // 6. raster
     RasterArgs ra;
     ra.proj = proj;
-    ra.list = eb.vals[er];
+    ra.list = ctx->list.as<uint32_t>();
     ra.offsets = ctx->offsets.as<uint32_t>();
     ra.order = ctx->order.as<int>();
     ra.gg = gg;
@@ -332,7 +318,6 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     ctx->last_gg = gg;
     ctx->last_band0 = band0;
     ctx->last_band1 = band1;
-    ctx->list_parity = er;
     ctx->image_rows = row1 - row0;
     ctx->pending = true;
     return TGS_OK;
@@ -371,9 +356,9 @@ tgs_status finish_frame(tgs_ctx* ctx, tgs_stats* stats) {
         cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
         stats->ms_preprocess = ms;
         cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]);
-        stats->ms_binning = ms;
+        stats->ms_sort = ms;  // depth presort (radix)
         cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
-        stats->ms_sort = ms;
+        stats->ms_binning = ms;  // counting sort into group lists + ranges
         cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[4]);
         stats->ms_raster = ms;
         cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[4]);
@@ -476,9 +461,8 @@ void tgs_ctx_destroy(tgs_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->scratch_scene) tgs_scene_free(c->scratch_scene);
     DBuf* bufs[] = {&c->fc, &c->status, &c->proj, &c->pre_keys[0], &c->pre_keys[1], &c->pre_vals[0],
-                    &c->pre_vals[1], &c->ngroups, &c->eoff, &c->ent_keys[0], &c->ent_keys[1],
-                    &c->ent_vals[0], &c->ent_vals[1], &c->ghist, &c->gid_count, &c->offsets, &c->order,
-                    &c->image, &c->scratch_records};
+                    &c->pre_vals[1], &c->rect, &c->rrect, &c->list, &c->hist, &c->bsum, &c->ghist,
+                    &c->offsets, &c->order, &c->image, &c->scratch_records};
     for (DBuf* b : bufs) b->release();
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
@@ -627,7 +611,7 @@ tgs_status tgs_read_lists(tgs_ctx* ctx, tgs_group_entry* out, int64_t cap, uint3
     if (m == 0) return TGS_OK;
     DBuf tmp;
     TGS_CUDA_OK(tmp.ensure((size_t)m * sizeof(tgs_group_entry)));
-    launch_lists_readback(ctx->ent_vals[ctx->list_parity].as<uint32_t>(), ctx->offsets.as<uint32_t>(), ng,
+    launch_lists_readback(ctx->list.as<uint32_t>(), ctx->offsets.as<uint32_t>(), ng,
                           dev_proj(ctx), ctx->last_gg, tmp.as<tgs_group_entry>(), ctx->stream);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(out, tmp.p, (size_t)m * sizeof(tgs_group_entry), cudaMemcpyDeviceToHost, ctx->stream);
@@ -649,7 +633,7 @@ tgs_status tgs_tile_trips(tgs_ctx* ctx, uint32_t* trips, int64_t cap, int64_t* n
     FrameCounters* fc = ctx->fc.as<FrameCounters>();
     RasterArgs ra;
     ra.proj = dev_proj(ctx);
-    ra.list = ctx->ent_vals[ctx->list_parity].as<uint32_t>();
+    ra.list = ctx->list.as<uint32_t>();
     ra.offsets = ctx->offsets.as<uint32_t>();
     ra.order = nullptr;
     ra.gg = gg;
@@ -676,7 +660,7 @@ tgs_status tgs_count_pairs(tgs_ctx* ctx, uint64_t* walked, uint64_t* blended) {
     TGS_CUDA_OK(cudaMemsetAsync(&fc->walked, 0, 2 * sizeof(unsigned long long), ctx->stream));
     RasterArgs ra;
     ra.proj = dev_proj(ctx);
-    ra.list = ctx->ent_vals[ctx->list_parity].as<uint32_t>();
+    ra.list = ctx->list.as<uint32_t>();
     ra.offsets = ctx->offsets.as<uint32_t>();
     ra.order = nullptr;
     ra.gg = ctx->last_gg;

@@ -110,10 +110,11 @@ __device__ __forceinline__ int group_rect(float mx, float my, int radius, const 
                                           int& gy0, int& gx1, int& gy1) {
     tile_rect(mx, my, radius, gg.tiles_x, gg.tiles_y, tx0, ty0, tx1, ty1);
     if (tx1 < tx0 || ty1 < ty0) return 0;
-    gx0 = tx0 / gg.g;
-    gx1 = tx1 / gg.g;
-    gy0 = max(ty0 / gg.g, gg.band_gy0);
-    gy1 = min(ty1 / gg.g, gg.band_gy1 - 1);
+    const int sh = gg.g >> 1;  // G in {1, 2, 4}
+    gx0 = tx0 >> sh;
+    gx1 = tx1 >> sh;
+    gy0 = max(ty0 >> sh, gg.band_gy0);
+    gy1 = min(ty1 >> sh, gg.band_gy1 - 1);
     if (gy1 < gy0) return 0;
     return (gx1 - gx0 + 1) * (gy1 - gy0 + 1);
 }

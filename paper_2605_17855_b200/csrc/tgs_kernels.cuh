@@ -11,7 +11,7 @@ struct PreprocessArgs {
     DevProjected out;
     uint32_t* depth_keys;          // [visible] depth bits (presort keys)
     uint32_t* idx_vals;            // [visible] compacted index (presort values)
-    uint32_t* ngroups;             // [visible] group entries emitted per splat
+    uint2* rect;                   // [visible] tile rect: x0 | x1 << 16, y0 | y1 << 16 (x0 > x1: none)
     GroupGeom gg;
     unsigned long long* tile_status;  // decoupled look-back status words (zeroed per frame)
     FrameCounters* fc;
@@ -24,6 +24,7 @@ struct SortBuffers {
     uint32_t* vals[2];
     uint32_t* ghist;      // [256 * kSortBlocks]
     uint32_t* gid_count;  // [n_groups] (gid sort only)
+    uint32_t* scan_tmp;   // scan_tmp_elems(256 * kSortBlocks) u32
 };
 constexpr int kSortBlocks = 592;  // 4 x 148 SMs
 // Sorts count (device) items of keys[0]/vals[0] by bits [0, nbits); result in keys[r]/vals[r]
@@ -33,24 +34,35 @@ constexpr int kSortBlocks = 592;  // 4 x 148 SMs
 int radix_sort(SortBuffers& b, const uint32_t* count, int nbits, int n_groups, bool want_keys_last,
                cudaStream_t st);
 
-// ---- binning -------------------------------------------------------------------------------
+// ---- binning: stable counting sort of (group, rank) entries ---------------------------------
+// The splats are presorted by (depth, index) (rank order); every warp of the count/scatter grids
+// owns a contiguous rank range ("chunk").  count: per-chunk group histograms via 2D difference
+// arrays; scan: exclusive scan of the [group][chunk] matrix; scatter: each chunk writes its entries
+// at its cursors in rank order.  The result equals std::stable_sort on (group << 32 | depth bits)
+// of the reference (binning.cpp:86-91) entry for entry.
 struct BinArgs {
-    const uint32_t* visible;     // &fc->visible
-    const uint32_t* sval;        // presorted compacted indices (rank order)
-    const uint32_t* ngroups;     // per compacted index
-    uint32_t* eoff;              // [visible] exclusive entry offsets (rank order)
-    unsigned long long* tile_status;
-    FrameCounters* fc;
-    uint32_t capacity;           // entry buffer capacity
-    DevProjected proj;
+    const uint32_t* visible;     // &fc->visible (device-side count)
+    const uint32_t* sval;        // rank -> compacted index
+    const uint2* rect;           // compacted index -> tile rect
+    uint2* rrect;                // rank -> tile rect
     GroupGeom gg;
-    uint32_t* keys;              // out: gid
-    uint32_t* vals;              // out: compacted idx
+    uint32_t* hist;              // [n_groups_band * n_chunks], scanned in place
+    uint32_t* bsum;              // scan block sums (+1)
+    uint32_t* offsets;           // [n_groups_band + 1]
+    uint32_t* list;              // [capacity] output entries (compacted indices)
+    FrameCounters* fc;
+    uint32_t capacity;
+    int n_chunks;
 };
-void launch_entry_scan(const BinArgs& a, int max_items, cudaStream_t st);
-void launch_emit(const BinArgs& a, int max_items, cudaStream_t st);
-// offsets[0..n] = exclusive scan of counts[0..n-1]; offsets[n] = total.
-void launch_offsets_scan(const uint32_t* counts, uint32_t* offsets, int n, cudaStream_t st);
+// chunk count for a band of n_groups groups (bounds the histogram matrix)
+int bin_chunks(int n_groups);
+size_t bin_hist_elems(int n_groups);   // hist length
+size_t bin_bsum_elems(int n_groups);   // bsum length
+void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st);
+// In-place exclusive scan of n u32 (multi-block: block sums, one-block scan of the sums, apply);
+// tmp holds scan_tmp_elems(n) u32 and ends with the total.
+size_t scan_tmp_elems(size_t n);
+void launch_exclusive_scan(uint32_t* x, size_t n, uint32_t* tmp, cudaStream_t st);
 
 // Sorted lists -> GroupEntry array (for readback).
 void launch_lists_readback(const uint32_t* sorted_idx, const uint32_t* offsets, int n_groups,

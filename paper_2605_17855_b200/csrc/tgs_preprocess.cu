@@ -293,7 +293,10 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a)
         a.idx_vals[ci] = ci;
         int tx0, ty0, tx1, ty1, gx0, gy0, gx1, gy1;
         const int ng = group_rect(pr.mx, pr.my, pr.radius, a.gg, tx0, ty0, tx1, ty1, gx0, gy0, gx1, gy1);
-        a.ngroups[ci] = (uint32_t)ng;
+        // tile rectangle (binning.cpp:32-44) for the group counting sort; empty -> x0 > x1
+        a.rect[ci] = (tx1 >= tx0 && ty1 >= ty0)
+                         ? make_uint2((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16))
+                         : make_uint2(0xffffu, 0u);
         if (tx1 >= tx0 && ty1 >= ty0) app = (unsigned long long)(tx1 - tx0 + 1) * (ty1 - ty0 + 1);
         // sort_entries depth validation (binning.cpp:78-83) for splats that emit entries
         if (ng > 0 && !(isfinite(pr.depth) && pr.depth >= 0.0f)) atomicOr(&a.fc->err_validation, 2u);

@@ -69,52 +69,6 @@ __global__ void __launch_bounds__(kThreads) hist_kernel(const uint32_t* __restri
     for (int d = threadIdx.x; d < R; d += kThreads) ghist[d * kSortBlocks + blockIdx.x] = dh[d];
 }
 
-// Exclusive scan of n u32 in place, one block of 1024 threads.
-__global__ void __launch_bounds__(1024) scan_inplace_kernel(uint32_t* data, int n) {
-    __shared__ uint32_t warp_tot[32];
-    __shared__ uint32_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int base = 0; base < n; base += 1024 * 4) {
-        uint32_t v[4], s = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = base + threadIdx.x * 4 + k;
-            v[k] = i < n ? data[i] : 0u;
-            s += v[k];
-        }
-        uint32_t incl = s;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) warp_tot[warp] = incl;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t w = warp_tot[lane], wi = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o) wi += t;
-            }
-            warp_tot[lane] = wi - w;
-        }
-        __syncthreads();
-        uint32_t run = carry + warp_tot[warp] + incl - s;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = base + threadIdx.x * 4 + k;
-            if (i < n) data[i] = run;
-            run += v[k];
-        }
-        __syncthreads();
-        if (threadIdx.x == 1023) carry = run;
-        __syncthreads();
-    }
-}
-
 template <int BITS>
 __global__ void __launch_bounds__(kThreads) scatter_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
@@ -187,7 +141,7 @@ void run_pass(SortBuffers& b, int src, const uint32_t* count, int shift, int n_g
     }
     hist_kernel<BITS><<<kSortBlocks, kThreads, smem, st>>>(b.keys[src], count, shift, b.ghist, gidc,
                                                            n_groups);
-    scan_inplace_kernel<<<1, 1024, 0, st>>>(b.ghist, R * kSortBlocks);
+    launch_exclusive_scan(b.ghist, (size_t)R * kSortBlocks, b.scan_tmp, st);
     scatter_kernel<BITS><<<kSortBlocks, kThreads, 0, st>>>(b.keys[src], b.vals[src], b.keys[src ^ 1],
                                                            b.vals[src ^ 1], count, shift, b.ghist,
                                                            write_keys);
@@ -216,11 +170,5 @@ int radix_sort(SortBuffers& b, const uint32_t* count, int nbits, int n_groups, b
     return src;
 }
 
-void launch_offsets_scan(const uint32_t* counts, uint32_t* offsets, int n, cudaStream_t st) {
-    // offsets[0..n]: copy counts into offsets[0..n-1], offsets[n] = 0, exclusive scan n+1 values
-    cudaMemcpyAsync(offsets, counts, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
-    cudaMemsetAsync(offsets + n, 0, sizeof(uint32_t), st);
-    scan_inplace_kernel<<<1, 1024, 0, st>>>(offsets, n + 1);
-}
 
 }  // namespace tgs

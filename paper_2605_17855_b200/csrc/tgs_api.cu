@@ -99,7 +99,6 @@ struct tgs_ctx {
     cudaEvent_t ev[6] = {};
     // per-frame buffers
     DBuf fc;            // FrameCounters
-    DBuf status;        // look-back status words (preprocess | entry scan)
     DBuf proj;          // mc | co | col (capacity n)
     DBuf pre_keys[2], pre_vals[2];
     DBuf rect, rrect;   // tile rect per compacted splat / per rank
@@ -216,8 +215,6 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     }
     TGS_CUDA_OK(ctx->rect.ensure((size_t)n_alloc * sizeof(uint2)));
     TGS_CUDA_OK(ctx->rrect.ensure((size_t)n_alloc * sizeof(uint2)));
-    const size_t pre_tiles = (size_t)(n_alloc + 255) / 256;
-    TGS_CUDA_OK(ctx->status.ensure(pre_tiles * 8));
     const uint32_t cap = std::max<uint32_t>(ctx->capacity, 1u);
     TGS_CUDA_OK(ctx->list.ensure((size_t)cap * 4));
     TGS_CUDA_OK(ctx->hist.ensure(bin_hist_elems(n_groups) * 4));
@@ -230,12 +227,10 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     TGS_CUDA_OK(ctx->image.ensure((size_t)(row1 - row0) * cam->width * 3 * sizeof(float)));
 
     FrameCounters* fc = ctx->fc.as<FrameCounters>();
-    unsigned long long* pre_status = ctx->status.as<unsigned long long>();
     const DevProjected proj = dev_proj(ctx);
 
     TGS_CUDA_OK(cudaEventRecord(ctx->ev[0], s));
     TGS_CUDA_OK(cudaMemsetAsync(fc, 0, sizeof(FrameCounters), s));
-    TGS_CUDA_OK(cudaMemsetAsync(pre_status, 0, pre_tiles * 8, s));
 
     // 1. preprocess + compaction
     PreprocessArgs pa;
@@ -246,7 +241,6 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     pa.idx_vals = ctx->pre_vals[0].as<uint32_t>();
     pa.rect = ctx->rect.as<uint2>();
     pa.gg = gg;
-    pa.tile_status = pre_status;
     pa.fc = fc;
     launch_preprocess(pa, s);
     TGS_CUDA_OK(cudaGetLastError());
@@ -259,9 +253,9 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     pb.vals[0] = ctx->pre_vals[0].as<uint32_t>();
     pb.vals[1] = ctx->pre_vals[1].as<uint32_t>();
     pb.ghist = ctx->ghist.as<uint32_t>();
-    pb.gid_count = nullptr;
     pb.scan_tmp = ctx->bsum.as<uint32_t>();
-    const int pr = radix_sort(pb, &fc->visible, 32, 0, false, s);
+    // pass 1 covers all n splats and drops the culled ones (key kCulledKey); later passes the kept
+    const int pr = radix_sort(pb, &fc->n_input, &fc->visible, 32, true, false, s);
     TGS_CUDA_OK(cudaGetLastError());
 
     TGS_CUDA_OK(cudaEventRecord(ctx->ev[2], s));
@@ -460,7 +454,7 @@ void tgs_ctx_destroy(tgs_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->scratch_scene) tgs_scene_free(c->scratch_scene);
-    DBuf* bufs[] = {&c->fc, &c->status, &c->proj, &c->pre_keys[0], &c->pre_keys[1], &c->pre_vals[0],
+    DBuf* bufs[] = {&c->fc, &c->proj, &c->pre_keys[0], &c->pre_keys[1], &c->pre_vals[0],
                     &c->pre_vals[1], &c->rect, &c->rrect, &c->list, &c->hist, &c->bsum, &c->ghist,
                     &c->offsets, &c->order, &c->image, &c->scratch_records};
     for (DBuf* b : bufs) b->release();
@@ -570,20 +564,43 @@ tgs_status tgs_render_batch(tgs_ctx* ctx, const tgs_scene* scene, const tgs_came
     return TGS_OK;
 }
 
+namespace tgs {
+namespace api {
+// project_scene's compacted order (projection.cpp:131-139): kept[i] and the compacted index of
+// every input splat, from the per-splat rect words (kCulledRect = not projected).
+tgs_status compaction_map(tgs_ctx* ctx, std::vector<int64_t>& cidx, int64_t& visible) {
+    const int64_t n = ctx->last_scene->n;
+    std::vector<uint2> rect((size_t)n);
+    if (n) TGS_CUDA_OK(cudaMemcpy(rect.data(), ctx->rect.p, (size_t)n * sizeof(uint2), cudaMemcpyDeviceToHost));
+    cidx.assign((size_t)n, -1);
+    visible = 0;
+    for (int64_t i = 0; i < n; ++i)
+        if (!(rect[i].x == kCulledRect && rect[i].y == kCulledRect)) cidx[i] = visible++;
+    return TGS_OK;
+}
+}  // namespace api
+}  // namespace tgs
+
 tgs_status tgs_read_projected(tgs_ctx* ctx, tgs_projected* out, int64_t cap, int64_t* n) {
     if (!ctx || !n) return set_err(TGS_ERR_VALIDATION, "read_projected: null argument");
     if (!ctx->last_scene) return set_err(TGS_ERR_VALIDATION, "read_projected: no frame rendered yet");
     const int64_t v = ctx->h_fc->visible;
     *n = v;
     if (!out || cap < v || v == 0) return TGS_OK;
-    std::vector<float4> h((size_t)v * 3);
+    std::vector<int64_t> cidx;
+    int64_t vis = 0;
+    tgs_status st = compaction_map(ctx, cidx, vis);
+    if (st != TGS_OK) return st;
+    const int64_t N = ctx->last_scene->n;
+    std::vector<float4> h((size_t)N * 3);
     const DevProjected p = dev_proj(ctx);
-    TGS_CUDA_OK(cudaMemcpy(h.data(), p.mc, (size_t)v * sizeof(float4), cudaMemcpyDeviceToHost));
-    TGS_CUDA_OK(cudaMemcpy(h.data() + v, p.co, (size_t)v * sizeof(float4), cudaMemcpyDeviceToHost));
-    TGS_CUDA_OK(cudaMemcpy(h.data() + 2 * v, p.col, (size_t)v * sizeof(float4), cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < v; ++i) {
-        const float4 mc = h[i], co = h[v + i], col = h[2 * v + i];
-        tgs_projected& o = out[i];
+    TGS_CUDA_OK(cudaMemcpy(h.data(), p.mc, (size_t)N * sizeof(float4), cudaMemcpyDeviceToHost));
+    TGS_CUDA_OK(cudaMemcpy(h.data() + N, p.co, (size_t)N * sizeof(float4), cudaMemcpyDeviceToHost));
+    TGS_CUDA_OK(cudaMemcpy(h.data() + 2 * N, p.col, (size_t)N * sizeof(float4), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < N; ++i) {
+        if (cidx[i] < 0) continue;
+        const float4 mc = h[i], co = h[N + i], col = h[2 * N + i];
+        tgs_projected& o = out[cidx[i]];
         o.mean2d[0] = mc.x;
         o.mean2d[1] = mc.y;
         o.conic[0] = mc.z;
@@ -618,6 +635,13 @@ tgs_status tgs_read_lists(tgs_ctx* ctx, tgs_group_entry* out, int64_t cap, uint3
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     tmp.release();
     if (e != cudaSuccess) return cuda_fail(e, "read_lists", __FILE__, __LINE__);
+    // entries reference input indices on the device; the reference's GroupEntry holds the
+    // project_scene (compacted) index
+    std::vector<int64_t> cidx;
+    int64_t vis = 0;
+    tgs_status st = compaction_map(ctx, cidx, vis);
+    if (st != TGS_OK) return st;
+    for (int64_t k = 0; k < m; ++k) out[k].gaussian_index = (uint32_t)cidx[out[k].gaussian_index];
     return TGS_OK;
 }
 

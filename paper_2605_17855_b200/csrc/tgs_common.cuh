@@ -14,6 +14,8 @@
 namespace tgs {
 
 constexpr int kTile = 16;  // binning.hpp:11 kTileSize
+constexpr uint32_t kCulledKey = 0xffffffffu;   // presort key of a culled/dropped splat (dropped by pass 1)
+constexpr uint32_t kCulledRect = 0xffffffffu;  // rect word of a culled/dropped splat
 
 // Camera parameters as the preprocess kernel consumes them (row-major R, t).
 struct DevCamera {
@@ -47,13 +49,12 @@ struct FrameCounters {
     unsigned long long culled;
     unsigned long long dropped;
     unsigned long long appearances;
-    unsigned int visible;           // compacted count
+    unsigned int visible;           // projected (kept) splats
     unsigned int n_entries;         // emitted entries (may exceed capacity -> overflow)
     unsigned int n_sort;            // entries handed to the group sort (0 on overflow)
     unsigned int err_validation;    // non-positive scale (projection.cpp:37) / bad depth (binning.cpp:78-83)
     unsigned int overflow;          // entry capacity exceeded
-    unsigned int tile_counter;      // decoupled look-back tile ticket (preprocess)
-    unsigned int scan_tile_counter; // decoupled look-back tile ticket (entry scan)
+    unsigned int n_input;           // scene size (first presort pass item count)
     unsigned int group_counter;     // persistent raster scheduler ticket
     unsigned long long walked;      // instrumented pair counters (tgs_count_pairs)
     unsigned long long blended;

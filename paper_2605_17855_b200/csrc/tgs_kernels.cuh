@@ -9,11 +9,11 @@ struct PreprocessArgs {
     DevScene scene;
     DevCamera cam;
     DevProjected out;
-    uint32_t* depth_keys;          // [visible] depth bits (presort keys)
-    uint32_t* idx_vals;            // [visible] compacted index (presort values)
-    uint2* rect;                   // [visible] tile rect: x0 | x1 << 16, y0 | y1 << 16 (x0 > x1: none)
+    uint32_t* depth_keys;          // [n] depth bits (presort keys; kCulledKey when not projected)
+    uint32_t* idx_vals;            // [n] input index (presort values)
+    uint2* rect;                   // [n] tile rect: x0 | x1 << 16, y0 | y1 << 16 (x0 > x1: none;
+                                   //     kCulledRect twice: not projected)
     GroupGeom gg;
-    unsigned long long* tile_status;  // decoupled look-back status words (zeroed per frame)
     FrameCounters* fc;
 };
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t st);
@@ -23,16 +23,15 @@ struct SortBuffers {
     uint32_t* keys[2];
     uint32_t* vals[2];
     uint32_t* ghist;      // [256 * kSortBlocks]
-    uint32_t* gid_count;  // [n_groups] (gid sort only)
     uint32_t* scan_tmp;   // scan_tmp_elems(256 * kSortBlocks) u32
 };
 constexpr int kSortBlocks = 592;  // 4 x 148 SMs
-// Sorts count (device) items of keys[0]/vals[0] by bits [0, nbits); result in keys[r]/vals[r]
-// where r is returned (ping-pong parity).  If gid_count != null the first pass also builds the
-// per-key histogram (keys < n_groups).  keys_out_last == false skips writing keys in the last
-// pass (only values are needed downstream).
-int radix_sort(SortBuffers& b, const uint32_t* count, int nbits, int n_groups, bool want_keys_last,
-               cudaStream_t st);
+// Sorts keys[0]/vals[0] by bits [0, nbits); the first pass covers *count_first items and, with
+// drop_first, drops keys equal to kCulledKey; later passes cover *count_rest items (device-side
+// counts).  Result in keys[r]/vals[r], r returned.  want_keys_last == false skips writing keys
+// in the last pass (only values are needed downstream).
+int radix_sort(SortBuffers& b, const uint32_t* count_first, const uint32_t* count_rest, int nbits,
+               bool drop_first, bool want_keys_last, cudaStream_t st);
 
 // ---- binning: stable counting sort of (group, rank) entries ---------------------------------
 // The splats are presorted by (depth, index) (rank order); every warp of the count/scatter grids

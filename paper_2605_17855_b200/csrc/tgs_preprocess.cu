@@ -8,9 +8,9 @@
 // e0 + (e1 + e2) for every 3-term dot product (oracle/eigen_min/Eigen/Core documents it).
 // Colour and conic follow the same discipline, so the whole ProjectedGaussian is bit-exact.
 //
-// Compaction: single-pass decoupled look-back scan over 256-Gaussian tiles (tile tickets from an
-// atomic counter guarantee forward progress), so projected records land at their
-// project_scene index directly with no second pass.
+// Outputs land at the input index: project_scene's order-preserving compaction
+// (projection.cpp:131-139) is realised by the depth presort, which drops culled splats, and by the
+// readback path (tgs_read_projected), which compacts on demand.
 #include "tgs_common.cuh"
 #include "tgs_kernels.cuh"
 
@@ -193,45 +193,18 @@ __device__ __forceinline__ int project_one(const DevScene& s, const DevCamera& c
     return 1;
 }
 
-__device__ __forceinline__ uint32_t lookback_exclusive(unsigned long long* status, int tile,
-                                                       uint32_t aggregate) {
-    // status: bits 62-63 flag (1 = aggregate, 2 = inclusive prefix), bits 0-31 value.
-    constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62;
-    if (tile == 0) {
-        atomicExch(&status[0], kPre | aggregate);
-        return 0;
-    }
-    atomicExch(&status[tile], kAgg | aggregate);
-    uint32_t excl = 0;
-    int t = tile - 1;
-    while (true) {
-        unsigned long long s;
-        do {
-            s = atomicAdd(&status[t], 0ull);
-        } while ((s >> 62) == 0);
-        excl += (uint32_t)(s & 0xffffffffu);
-        if ((s >> 62) == 2) break;
-        --t;
-    }
-    atomicExch(&status[tile], kPre | (unsigned long long)(excl + aggregate));
-    return excl;
-}
-
 constexpr int kPreBlock = 256;
 
+// One thread per input Gaussian, outputs at the INPUT index (no compaction pass: the depth
+// presort drops culled splats, whose key is 0xffffffff, and project_scene's compacted order is
+// only materialised on readback).  Counters are block-aggregated.
 __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a) {
-    __shared__ uint32_t s_tile;
-    __shared__ uint32_t s_warp[kPreBlock / 32];
-    __shared__ uint32_t s_base;
-    __shared__ unsigned long long s_cnt[3];
-    if (threadIdx.x == 0) {
-        s_tile = atomicAdd(&a.fc->tile_counter, 1u);
-        s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
-    }
+    __shared__ unsigned long long s_cnt[4];
+    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.fc->n_input = (unsigned)a.scene.n;
     __syncthreads();
-    const int tile = (int)s_tile;
-    const int i = tile * kPreBlock + threadIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int i = blockIdx.x * kPreBlock + threadIdx.x;
+    const int lane = threadIdx.x & 31;
 
     bool keep = false, culled = false, dropped = false;
     Proj pr;
@@ -261,60 +234,45 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a)
             }
         }
     }
-
-    // block-exclusive scan of keep
-    const unsigned ballot = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) s_warp[warp] = __popc(ballot);
+    unsigned long long app = 0;
+    if (i < a.scene.n) {
+        a.idx_vals[i] = (uint32_t)i;
+        if (keep) {
+            a.out.mc[i] = make_float4(pr.mx, pr.my, pr.a, pr.b);
+            a.out.co[i] = make_float4(pr.c, po.w, pr.depth, __int_as_float(pr.radius));
+            a.out.col[i] = make_float4(pr.r, pr.g, pr.bl, 0.0f);
+            a.depth_keys[i] = __float_as_uint(pr.depth);
+            int tx0, ty0, tx1, ty1, gx0, gy0, gx1, gy1;
+            const int ng = group_rect(pr.mx, pr.my, pr.radius, a.gg, tx0, ty0, tx1, ty1, gx0, gy0, gx1, gy1);
+            // tile rectangle (binning.cpp:32-44) for the group counting sort; empty -> x0 > x1
+            a.rect[i] = (tx1 >= tx0 && ty1 >= ty0)
+                            ? make_uint2((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16))
+                            : make_uint2(0xffffu, 0u);
+            if (tx1 >= tx0 && ty1 >= ty0) app = (unsigned long long)(tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+            // sort_entries depth validation (binning.cpp:78-83) for splats that emit entries
+            if (ng > 0 && !(isfinite(pr.depth) && pr.depth >= 0.0f)) atomicOr(&a.fc->err_validation, 2u);
+        } else {
+            a.depth_keys[i] = kCulledKey;
+            a.rect[i] = make_uint2(kCulledRect, kCulledRect);
+        }
+    }
     const unsigned long long nc = __popc(__ballot_sync(0xffffffffu, culled));
     const unsigned long long nd = __popc(__ballot_sync(0xffffffffu, dropped));
+    const unsigned long long nk = __popc(__ballot_sync(0xffffffffu, keep));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) app += __shfl_xor_sync(0xffffffffu, app, o);
     if (lane == 0) {
         if (nc) atomicAdd(&s_cnt[0], nc);
         if (nd) atomicAdd(&s_cnt[1], nd);
+        if (app) atomicAdd(&s_cnt[2], app);  // tile appearances (render.cpp:19-20)
+        if (nk) atomicAdd(&s_cnt[3], nk);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (int w = 0; w < kPreBlock / 32; ++w) {
-            const uint32_t c = s_warp[w];
-            s_warp[w] = run;
-            run += c;
-        }
-        s_base = lookback_exclusive(a.tile_status, tile, run);
-    }
-    __syncthreads();
-
-    unsigned long long app = 0;
-    if (keep) {
-        const uint32_t ci = s_base + s_warp[warp] + __popc(ballot & ((1u << lane) - 1u));
-        a.out.mc[ci] = make_float4(pr.mx, pr.my, pr.a, pr.b);
-        a.out.co[ci] = make_float4(pr.c, po.w, pr.depth, __int_as_float(pr.radius));
-        a.out.col[ci] = make_float4(pr.r, pr.g, pr.bl, 0.0f);
-        a.depth_keys[ci] = __float_as_uint(pr.depth);
-        a.idx_vals[ci] = ci;
-        int tx0, ty0, tx1, ty1, gx0, gy0, gx1, gy1;
-        const int ng = group_rect(pr.mx, pr.my, pr.radius, a.gg, tx0, ty0, tx1, ty1, gx0, gy0, gx1, gy1);
-        // tile rectangle (binning.cpp:32-44) for the group counting sort; empty -> x0 > x1
-        a.rect[ci] = (tx1 >= tx0 && ty1 >= ty0)
-                         ? make_uint2((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16))
-                         : make_uint2(0xffffu, 0u);
-        if (tx1 >= tx0 && ty1 >= ty0) app = (unsigned long long)(tx1 - tx0 + 1) * (ty1 - ty0 + 1);
-        // sort_entries depth validation (binning.cpp:78-83) for splats that emit entries
-        if (ng > 0 && !(isfinite(pr.depth) && pr.depth >= 0.0f)) atomicOr(&a.fc->err_validation, 2u);
-    }
-    // tile appearances (render.cpp:19-20)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) app += __shfl_xor_sync(0xffffffffu, app, o);
-    if (lane == 0 && app) atomicAdd(&s_cnt[2], app);
     __syncthreads();
     if (threadIdx.x == 0) {
         if (s_cnt[0]) atomicAdd(&a.fc->culled, s_cnt[0]);
         if (s_cnt[1]) atomicAdd(&a.fc->dropped, s_cnt[1]);
         if (s_cnt[2]) atomicAdd(&a.fc->appearances, s_cnt[2]);
-    }
-    if (tile == (a.scene.n + kPreBlock - 1) / kPreBlock - 1 && threadIdx.x == kPreBlock - 1) {
-        // last thread of the last tile knows the inclusive total
-        const uint32_t incl = s_base + s_warp[warp] + __popc(ballot);
-        a.fc->visible = incl;
+        if (s_cnt[3]) atomicAdd(&a.fc->visible, (unsigned)s_cnt[3]);
     }
 }
 

@@ -37,33 +37,16 @@ __device__ __forceinline__ void block_range(uint32_t count, uint32_t& begin, uin
 template <int BITS>
 __global__ void __launch_bounds__(kThreads) hist_kernel(const uint32_t* __restrict__ keys,
                                                         const uint32_t* count_ptr, int shift,
-                                                        uint32_t* __restrict__ ghist,
-                                                        uint32_t* __restrict__ gid_count,
-                                                        int n_groups) {
+                                                        uint32_t* __restrict__ ghist, bool drop) {
     constexpr int R = 1 << BITS;
-    extern __shared__ uint32_t sh[];  // R digit bins (+ n_groups gid bins when gid_count)
-    uint32_t* dh = sh;
-    uint32_t* gh = sh + R;
-    const bool full = gid_count != nullptr;
+    __shared__ uint32_t dh[R];
     for (int d = threadIdx.x; d < R; d += kThreads) dh[d] = 0;
-    if (full)
-        for (int g = threadIdx.x; g < n_groups; g += kThreads) gh[g] = 0;
     __syncthreads();
     uint32_t begin, end;
     block_range(*count_ptr, begin, end);
-    if (full) {
-        for (uint32_t i = begin + threadIdx.x; i < end; i += kThreads) atomicAdd(&gh[keys[i]], 1u);
-        __syncthreads();
-        for (int g = threadIdx.x; g < n_groups; g += kThreads) {
-            const uint32_t c = gh[g];
-            if (c) {
-                atomicAdd(&dh[(g >> shift) & (R - 1)], c);
-                atomicAdd(&gid_count[g], c);
-            }
-        }
-    } else {
-        for (uint32_t i = begin + threadIdx.x; i < end; i += kThreads)
-            atomicAdd(&dh[(keys[i] >> shift) & (R - 1)], 1u);
+    for (uint32_t i = begin + threadIdx.x; i < end; i += kThreads) {
+        const uint32_t k = keys[i];
+        if (!(drop && k == kCulledKey)) atomicAdd(&dh[(k >> shift) & (R - 1)], 1u);
     }
     __syncthreads();
     for (int d = threadIdx.x; d < R; d += kThreads) ghist[d * kSortBlocks + blockIdx.x] = dh[d];
@@ -73,7 +56,7 @@ template <int BITS>
 __global__ void __launch_bounds__(kThreads) scatter_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, const uint32_t* count_ptr, int shift,
-    const uint32_t* __restrict__ ghist, bool write_keys) {
+    const uint32_t* __restrict__ ghist, bool write_keys, bool drop) {
     constexpr int R = 1 << BITS;
     __shared__ uint32_t blk_off[R];
     __shared__ uint32_t wcnt[kWarps][R];
@@ -89,8 +72,8 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(
 #pragma unroll
         for (int s = 0; s < kSteps; ++s) {
             const uint32_t i = tile + warp * (32 * kSteps) + s * 32 + lane;
-            const bool valid = i < end;
-            k[s] = valid ? kin[i] : 0u;
+            k[s] = i < end ? kin[i] : 0u;
+            const bool valid = i < end && !(drop && k[s] == kCulledKey);  // pass 1 drops culled splats
             v[s] = valid ? vin[i] : 0u;
             const uint32_t d = (k[s] >> shift) & (R - 1);
             const uint32_t key = valid ? d : (uint32_t)(R + lane);  // invalid lanes match nobody
@@ -129,32 +112,24 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(
 }
 
 template <int BITS>
-void run_pass(SortBuffers& b, int src, const uint32_t* count, int shift, int n_groups,
-              bool first_gid_pass, bool write_keys, cudaStream_t st) {
+void run_pass(SortBuffers& b, int src, const uint32_t* count, int shift, bool write_keys, bool drop,
+              cudaStream_t st) {
     const int R = 1 << BITS;
-    size_t smem = R * sizeof(uint32_t);
-    uint32_t* gidc = nullptr;
-    if (first_gid_pass) {
-        gidc = b.gid_count;
-        smem += (size_t)n_groups * sizeof(uint32_t);
-        cudaFuncSetAttribute(hist_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
-    hist_kernel<BITS><<<kSortBlocks, kThreads, smem, st>>>(b.keys[src], count, shift, b.ghist, gidc,
-                                                           n_groups);
+    hist_kernel<BITS><<<kSortBlocks, kThreads, 0, st>>>(b.keys[src], count, shift, b.ghist, drop);
     launch_exclusive_scan(b.ghist, (size_t)R * kSortBlocks, b.scan_tmp, st);
     scatter_kernel<BITS><<<kSortBlocks, kThreads, 0, st>>>(b.keys[src], b.vals[src], b.keys[src ^ 1],
                                                            b.vals[src ^ 1], count, shift, b.ghist,
-                                                           write_keys);
+                                                           write_keys, drop);
 }
 
-typedef void (*PassFn)(SortBuffers&, int, const uint32_t*, int, int, bool, bool, cudaStream_t);
+typedef void (*PassFn)(SortBuffers&, int, const uint32_t*, int, bool, bool, cudaStream_t);
 const PassFn kPass[9] = {nullptr,        run_pass<1>, run_pass<2>, run_pass<3>, run_pass<4>,
                          run_pass<5>,    run_pass<6>, run_pass<7>, run_pass<8>};
 
 }  // namespace
 
-int radix_sort(SortBuffers& b, const uint32_t* count, int nbits, int n_groups, bool want_keys_last,
-               cudaStream_t st) {
+int radix_sort(SortBuffers& b, const uint32_t* count_first, const uint32_t* count_rest, int nbits,
+               bool drop_first, bool want_keys_last, cudaStream_t st) {
     if (nbits < 1) nbits = 1;
     const int passes = (nbits + 7) / 8;
     const int per = (nbits + passes - 1) / passes;
@@ -162,8 +137,8 @@ int radix_sort(SortBuffers& b, const uint32_t* count, int nbits, int n_groups, b
     for (int p = 0; p < passes; ++p) {
         const int bits = (p == passes - 1) ? nbits - shift : per;
         const bool last = p == passes - 1;
-        kPass[bits](b, src, count, shift, n_groups, p == 0 && b.gid_count != nullptr,
-                    !last || want_keys_last, st);
+        kPass[bits](b, src, p == 0 ? count_first : count_rest, shift, !last || want_keys_last,
+                    p == 0 && drop_first, st);
         src ^= 1;
         shift += bits;
     }

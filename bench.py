@@ -245,18 +245,29 @@ def main():
     dom = max(stages, key=stages.get)
     n_vis = int(st_last.visible)
     ent = st_t["entries"]
+    # algorithmic bytes per launch of each HBM-bound stage: preprocess reads the
+    # 56-B SH0 record and writes the 64-B projected record (+ rect, key, value); the depth presort
+    # moves (key, value) pairs 4 times; binning writes every 4-B list entry once and reads the
+    # rank-ordered rect (8 B) twice plus the rank->index map (4 B)
+    alg_bytes = {"preprocess": (56 + 64) * N_SPLATS, "sort": 4 * 16 * n_vis, "binning": 4 * ent + 20 * n_vis}
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json"))).get(dom)
+    except Exception:
+        pass
     if dom == "raster":
-        # tensor pipe: 32 issued flops per (pixel, splat) slot of every MMA (K=16 x 2)
+        # tensor pipe: 12 useful flops per walked (pixel, splat) pair (6-term contraction)
         achieved = 12.0 * walked / (st_t["raster"] / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": tflops, "unit": "TFLOP/s",
-                "frac": achieved / tflops, "traffic": None, "kernel": "raster_tensor_kernel<2>",
+                "frac": achieved / tflops, "traffic": traffic, "kernel": "raster_tensor_kernel<4>",
                 "algorithmic": "12 flops per walked pixel-splat pair (6-term contraction)"}
     else:
-        alg = {"preprocess": (56 + 44) * N_SPLATS, "binning": 8 * ent + 12 * n_vis,
-               "sort": 36 * ent}[dom]
-        achieved = alg / (stages[dom] / 1e3) / 1e9
+        achieved = alg_bytes[dom] / (stages[dom] / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": None, "kernel": dom}
+                "traffic": traffic, "kernel": {"binning": "rank_gather + group_count + scan + group_scatter",
+                                               "sort": "depth presort (4 radix passes)",
+                                               "preprocess": "preprocess_kernel"}[dom],
+                "algorithmic_bytes": alg_bytes[dom]}
     roof["peak_source"] = peak_src
     # raster pipes (the kernel the paper targets): FP32 / MUFU work per the survey's model
     sm_mhz = clk.summary().get("sm_mhz") or 1965.0
@@ -323,9 +334,10 @@ def main():
         except Exception as e:  # reported, never fatal for the GPU number
             cpu = {"value": None, "unit": "frames/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
-    # our kernels per frame: preprocess 1, presort 4 x (hist, scan, scatter), entry scan 1, emit 1,
-    # group sort 2 x 3 (11-bit group ids at G=2), offsets scan 1, raster 1
-    launches_per_frame = 1 + 12 + 2 + 6 + 1 + 1
+    # our kernels per frame: preprocess 1; depth presort 4 passes x (hist, 3-kernel digit scan,
+    # scatter); binning: rank gather, group count, 3-kernel scan, offsets, group scatter; unit
+    # order 1; raster 1
+    launches_per_frame = 1 + 4 * 5 + 7 + 1 + 1
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",

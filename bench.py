@@ -183,7 +183,8 @@ def main():
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
 
     # capacity sizing over every camera this rank will render (untimed), then warm-up
-    mine = [cams[(i * world + rank) % N_CAMS] for i in range(args.warmup + args.steps)]
+    from paper_2605_17855_b200 import multigpu
+    mine = [cams[c] for c in multigpu.camera_schedule(N_CAMS, world, rank, args.warmup + args.steps)]
     for c in {id(c): c for c in mine}.values():
         ctx.enqueue(ds, c, opt_t)
         ctx.sync()
@@ -203,11 +204,8 @@ def main():
         ev1.record(stream)
         st_last = ctx.sync()
         torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    ms = multigpu.max_over_ranks(ev0.elapsed_time(ev1), device=torch.device("cuda", local))
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
         dist.barrier()
     frames = args.steps * world
     value = frames / (ms / 1000.0)
@@ -301,11 +299,7 @@ def main():
                                         C.byref(mine[args.warmup + i % args.steps].to_c()), C.byref(oc),
                                         C.cast(out.data_ptr(), _lib.F32P), C.byref(st))
             assert rc == 0, _lib.last_error()
-        dt = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([dt], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+        dt = multigpu.max_over_ranks(time.perf_counter() - t0, device=torch.device("cuda", local))
         e2e = {"value": n_e2e * world / dt, "unit": "frames/s",
                "h2d_bytes_per_step": int(scene.records.nbytes + 88),
                "d2h_bytes_per_step": int(W * H * 3 * 4),

@@ -79,7 +79,7 @@ def load():
     with _LOCK:
         if _LIB is not None:
             return _LIB
-        path = _build.LIB
+        path = os.environ.get("TGS_LIB") or _build.LIB  # TGS_LIB: a variant build (tools/build_variant.py)
         if not os.path.exists(path):
             _build.build()
         lib = C.CDLL(path)

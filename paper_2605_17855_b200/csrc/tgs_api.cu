@@ -105,6 +105,8 @@ struct tgs_ctx {
     DBuf list;          // sorted group lists (compacted indices)
     DBuf hist, bsum;    // counting-sort [group][chunk] matrix and its scan block sums
     DBuf ghist, offsets, order;
+    DBuf ucost;         // per unit, list entries the last frame walked (schedule feedback)
+    uint64_t ucost_key = 0;  // geometry the feedback belongs to (0: none)
     DBuf image;
     DBuf scratch_records;
     FrameCounters* h_fc = nullptr;  // pinned
@@ -222,6 +224,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     TGS_CUDA_OK(ctx->ghist.ensure((size_t)256 * kSortBlocks * 4));
     TGS_CUDA_OK(ctx->offsets.ensure((size_t)(n_groups + 1) * 4));
     TGS_CUDA_OK(ctx->order.ensure((size_t)gg.tiles_x * gg.tiles_y * 4));
+    TGS_CUDA_OK(ctx->ucost.ensure((size_t)gg.tiles_x * gg.tiles_y * 4));
     const int row0 = band0 * gg.g * kTile;
     const int row1 = std::min(cam->height, band1 * gg.g * kTile);
     TGS_CUDA_OK(ctx->image.ensure((size_t)(row1 - row0) * cam->width * 3 * sizeof(float)));
@@ -277,7 +280,14 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     launch_binning(ba, n_alloc, s);
     {
         const int per = gg.g == 4 ? 4 : 1;  // G=4 groups are rasterised as 2x2-tile quarters
-        launch_unit_order(ctx->offsets.as<uint32_t>(), n_groups * per, per, ctx->order.as<int>(), s);
+        // the previous frame's measured walks schedule this one when it had the same unit geometry
+        // (same image, group size, band and backend): a camera path changes slowly
+        const uint64_t key = ((uint64_t)(uint32_t)cam->width << 40) ^ ((uint64_t)(uint32_t)cam->height << 20) ^
+                             ((uint64_t)band0 << 8) ^ ((uint64_t)band1 << 28) ^ ((uint64_t)gg.g << 4) ^
+                             (uint64_t)opt->backend ^ (1ull << 63);
+        const uint32_t* fb = (ctx->ucost_key == key) ? ctx->ucost.as<uint32_t>() : nullptr;
+        launch_unit_order(ctx->offsets.as<uint32_t>(), fb, n_groups * per, per, ctx->order.as<int>(), s);
+        ctx->ucost_key = key;
     }
     TGS_CUDA_OK(cudaGetLastError());
     TGS_CUDA_OK(cudaEventRecord(ctx->ev[3], s));
@@ -296,6 +306,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     ra.t_terminate = opt->t_terminate;
     ra.fc = fc;
     ra.tile_trip = nullptr;
+    ra.unit_cost = ctx->ucost.as<uint32_t>();
     static const bool skip_raster = std::getenv("TGS_DEBUG_SKIP_RASTER") != nullptr;  // bisection aid
     if (skip_raster) {
     } else if (opt->backend == TGS_BACKEND_SCALAR)
@@ -456,7 +467,7 @@ void tgs_ctx_destroy(tgs_ctx* c) {
     if (c->scratch_scene) tgs_scene_free(c->scratch_scene);
     DBuf* bufs[] = {&c->fc, &c->proj, &c->pre_keys[0], &c->pre_keys[1], &c->pre_vals[0],
                     &c->pre_vals[1], &c->rect, &c->rrect, &c->list, &c->hist, &c->bsum, &c->ghist,
-                    &c->offsets, &c->order, &c->image, &c->scratch_records};
+                    &c->offsets, &c->order, &c->ucost, &c->image, &c->scratch_records};
     for (DBuf* b : bufs) b->release();
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
@@ -668,6 +679,7 @@ tgs_status tgs_tile_trips(tgs_ctx* ctx, uint32_t* trips, int64_t cap, int64_t* n
     ra.t_terminate = ctx->last_opt.t_terminate;
     ra.fc = fc;
     ra.tile_trip = tmp.as<uint32_t>();
+    ra.unit_cost = nullptr;
     launch_count_pairs(ra, ctx->stream);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(trips, tmp.p, (size_t)tiles * 4, cudaMemcpyDeviceToHost, ctx->stream);
@@ -695,6 +707,7 @@ tgs_status tgs_count_pairs(tgs_ctx* ctx, uint64_t* walked, uint64_t* blended) {
     ra.t_terminate = ctx->last_opt.t_terminate;
     ra.fc = fc;
     ra.tile_trip = nullptr;
+    ra.unit_cost = nullptr;
     launch_count_pairs(ra, ctx->stream);
     TGS_CUDA_OK(cudaGetLastError());
     unsigned long long h[2];

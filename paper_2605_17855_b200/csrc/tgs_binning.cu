@@ -417,20 +417,30 @@ __global__ void encode_u8_kernel(const float* __restrict__ rgb, int64_t n, uint8
 // Longest-processing-time-first schedule (bucketed): the rasterisers take work units (G=1:
 // tiles; G=2: groups; G=4: quarter groups) in this order, so units with the longest lists start
 // first and the tail of the persistent grid is short.  Work estimate = the unit's list length.
-__global__ void __launch_bounds__(1024) unit_order_kernel(const uint32_t* __restrict__ offsets, int n_units,
+// Longest-processing-time-first order of the rasteriser's work units.  A unit's cost is how much
+// of its list it walks before its pixels terminate, which the list length alone predicts poorly
+// (deep central lists terminate after a few hundred splats, silhouette lists are walked to the
+// end); with `feedback` the cost is the walk measured on the previous frame of the same geometry
+// (temporal coherence of a camera path), else the list length.  Counting sort on a log2 key with
+// 8 buckets per octave; equal keys keep unit order.
+__global__ void __launch_bounds__(1024) unit_order_kernel(const uint32_t* __restrict__ offsets,
+                                                          const uint32_t* __restrict__ feedback, int n_units,
                                                           int per_group, int* __restrict__ order) {
-    __shared__ uint32_t cnt[33];
-    if (threadIdx.x < 33) cnt[threadIdx.x] = 0;
+    constexpr int kBuckets = 264;
+    __shared__ uint32_t cnt[kBuckets];
+    for (int k = threadIdx.x; k < kBuckets; k += blockDim.x) cnt[k] = 0;
     __syncthreads();
     auto key = [&](int u) {
         const int gid = u / per_group;
-        return __clz(offsets[gid + 1] - offsets[gid] + 1u);  // 0 = longest bucket
+        const uint32_t cost = feedback ? feedback[u] : offsets[gid + 1] - offsets[gid];
+        const int b = (int)(log2f((float)cost + 1.0f) * 8.0f);
+        return kBuckets - 1 - min(kBuckets - 1, b);  // 0 = most expensive
     };
     for (int t = threadIdx.x; t < n_units; t += blockDim.x) atomicAdd(&cnt[key(t)], 1u);
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t run = 0;
-        for (int k = 0; k < 33; ++k) {
+        for (int k = 0; k < kBuckets; ++k) {
             const uint32_t c = cnt[k];
             cnt[k] = run;
             run += c;
@@ -442,8 +452,9 @@ __global__ void __launch_bounds__(1024) unit_order_kernel(const uint32_t* __rest
 
 }  // namespace
 
-void launch_unit_order(const uint32_t* offsets, int n_units, int per_group, int* order, cudaStream_t st) {
-    if (n_units > 0) unit_order_kernel<<<1, 1024, 0, st>>>(offsets, n_units, per_group, order);
+void launch_unit_order(const uint32_t* offsets, const uint32_t* feedback, int n_units, int per_group, int* order,
+                       cudaStream_t st) {
+    if (n_units > 0) unit_order_kernel<<<1, 1024, 0, st>>>(offsets, feedback, n_units, per_group, order);
 }
 
 // Warps per count/scatter block: one difference array ((rows+1) x (cols+1) ints) per warp in

@@ -79,11 +79,15 @@ struct RasterArgs {
     float alpha_skip, alpha_clamp, t_terminate;
     FrameCounters* fc;
     uint32_t* tile_trip;      // optional (count_pairs): per tile, entries of its list walked until done
+    uint32_t* unit_cost;      // optional: per unit, list entries walked (next frame's schedule)
 };
 void launch_raster_scalar(const RasterArgs& a, cudaStream_t st);
 // LPT schedule for the rasterisers: work units (tile / group / quarter group, per_group units per
 // group list) bucketed by floor(log2(list length)), longest first.
-void launch_unit_order(const uint32_t* offsets, int n_units, int per_group, int* order, cudaStream_t st);
+// With `feedback` (per unit, entries walked by the previous frame of the same geometry) the cost
+// is the measured walk, else the list length.
+void launch_unit_order(const uint32_t* offsets, const uint32_t* feedback, int n_units, int per_group, int* order,
+                       cudaStream_t st);
 void launch_raster_tensor(const RasterArgs& a, int num_sms, cudaStream_t st);
 // Instrumented walk: counts walked / alpha-contributing pairs (reference semantics, G=1 lists).
 void launch_count_pairs(const RasterArgs& a, cudaStream_t st);

@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(256) raster_scalar_kernel(RasterArgs a) {
     const uint32_t begin = a.offsets[tile], end = a.offsets[tile + 1];
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
     bool done = !inside;
-    for (uint32_t base = begin; base < end; base += kBatch) {
+    uint32_t base = begin;
+    for (; base < end; base += kBatch) {
         if (__syncthreads_count(done) == kBatch) break;
         const uint32_t e = base + threadIdx.x;
         if (e < end) {
@@ -71,6 +72,8 @@ __global__ void __launch_bounds__(256) raster_scalar_kernel(RasterArgs a) {
             }
         }
     }
+    // schedule feedback: list entries this tile walked
+    if (a.unit_cost && threadIdx.x == 0) a.unit_cost[tile] = min(base, end) - begin;
     if (inside) {
         float* o = a.image + ((size_t)(py - a.image_row0) * gg.width + px) * 3;
         o[0] = fminf(fmaxf(cr, 0.0f), 1.0f);

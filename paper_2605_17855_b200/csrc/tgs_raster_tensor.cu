@@ -38,6 +38,7 @@
 // The pixel operand A (2*SLOTS M-tiles x 128 rows x 32 B) is identical for every unit and is
 // built once per CTA.  Hand-offs: full[s] (mbarrier), tfull[ts] (tcgen05.commit), and release
 // counters compared against absolute chunk targets; every wait is watchdog-bounded.
+#include <cstdlib>
 #include "tgs_common.cuh"
 #include "tgs_kernels.cuh"
 #include "tgs_ptx.cuh"
@@ -52,9 +53,47 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kNeverRow = -30000.0f;
 constexpr float kInf = __builtin_huge_valf();
 
-constexpr int kN = 32;  // splats per chunk (MMA N)
-constexpr int kSS = 4;  // smem stages
-constexpr int kTS = 2;  // TMEM accumulator stages
+#ifndef TGS_RASTER_N
+#define TGS_RASTER_N 32
+#endif
+constexpr int kN = TGS_RASTER_N;  // splats per chunk (MMA N): 16 or 32
+#ifndef TGS_RASTER_SS
+#define TGS_RASTER_SS 4
+#endif
+constexpr int kSS = TGS_RASTER_SS;  // smem stages
+#ifndef TGS_RASTER_TS
+#define TGS_RASTER_TS 2
+#endif
+constexpr int kTS = TGS_RASTER_TS;  // TMEM accumulator stages
+#ifndef TGS_RASTER_SPW
+#define TGS_RASTER_SPW 4
+#endif
+#ifndef TGS_RASTER_PF
+#define TGS_RASTER_PF 1
+#endif
+constexpr int kPF = TGS_RASTER_PF;  // producer record batches in flight
+#ifndef TGS_RASTER_DI
+#define TGS_RASTER_DI 2
+#endif
+constexpr int kDI = TGS_RASTER_DI;  // producer list-index batches in flight beyond the records
+#ifndef TGS_RASTER_PROF
+#define TGS_RASTER_PROF 0
+#endif
+#if TGS_RASTER_PROF
+// role timing (debug builds only): [0] producer total [1] producer stage waits [2] producer
+// batches [3] chunks; [4] MMA total [5] MMA full waits [6] MMA TMEM-release waits; [8] epilogue
+// total (sum over warps) [9] epilogue tfull waits [10] active splat blocks [11] splat blocks
+__device__ unsigned long long g_rprof[16];
+__device__ unsigned int g_rprof_done;
+__device__ unsigned int g_ucyc[65536];  // per-unit cycles (unit index) and start order
+__device__ unsigned int g_uch[65536];
+__device__ unsigned int g_uent[65536];
+__device__ unsigned int g_uwait[65536];  // producer stage-wait cycles within the unit
+__device__ unsigned int g_usec[65536][3];  // producer cycles: retire check, row build, placement
+#endif
+#ifndef TGS_RASTER_COMPACT
+#define TGS_RASTER_COMPACT 1
+#endif
 
 struct ChunkHeader {
     int seq;      // per-CTA unit sequence number, -1 = end of stream
@@ -70,10 +109,11 @@ struct ChunkHeader {
 template <int SLOTS>
 struct Roles {
     static constexpr int kMT = 2 * SLOTS;
-    static constexpr int kSPW = SLOTS == 1 ? 1 : 2;            // slots (member tiles) per warp
+    static constexpr int kSPW = SLOTS == 1 ? 1 : TGS_RASTER_SPW;  // slots (member tiles) per warp
     static constexpr int kEpiWarps = 8 * SLOTS / kSPW;         // 16 (G>=2) or 8 (G=1)
     static constexpr int kThreads = (kEpiWarps + 2) * 32;
     static constexpr int kProd = kEpiWarps, kMma = kEpiWarps + 1;
+    static constexpr bool kCompact = SLOTS == 4 && kSPW == 4 && TGS_RASTER_COMPACT;
 };
 
 template <int SLOTS>
@@ -82,6 +122,7 @@ struct Smem {
     alignas(128) uint8_t a[kMT][128 * 32];   // pixel monomial rows (K-major, no swizzle)
     alignas(128) uint8_t b[kSS][kN * 32];    // splat coefficient rows
     float4 epi[kSS][kN];                     // r, g, b, min(alpha_clamp, opacity)
+    alignas(16) float cj[kSS][kN];           // min(alpha_clamp, opacity) again, packed for preload
     ChunkHeader hdr[kSS];
     alignas(16) int wdone[16];               // chunks each epilogue warp has completed
     alignas(16) int dead[16];                // (seq << 4) | retired member tiles, per warp
@@ -108,6 +149,18 @@ __device__ __forceinline__ void lane_pixel(int m, int l, int& x, int& y) {
     const int q = l >> 5, i = l & 31;
     x = (slot & 1) * 16 + (q & 1) * 8 + (i & 7);
     y = (slot >> 1) * 16 + half * 8 + (q >> 1) * 4 + (i >> 3);
+}
+
+// Compact mapping (G >= 2 with 4 slots per warp): epilogue warp w owns half-tile w of the unit
+// (tile w >> 1, rows (w & 1) * 8 ..), its slot k is the 8x4 block k of that half-tile.  Warp w may
+// only read TMEM lane quadrant w % 4, so its slots live in M-tiles 4 * (w >> 2) + k at quadrant
+// w % 4.  A splat footprint then activates the few warps whose half-tiles it overlaps, and all four
+// slots of an active warp are spatially adjacent.
+__device__ __forceinline__ void lane_pixel_compact(int m, int l, int& x, int& y) {
+    const int w = 4 * (m >> 2) + (l >> 5), k = m & 3, i = l & 31;
+    const int t = w >> 1;
+    x = (t & 1) * 16 + (k & 1) * 8 + (i & 7);
+    y = (t >> 1) * 16 + (w & 1) * 8 + (k >> 1) * 4 + (i >> 3);
 }
 
 // byte offset of (row, k-half) in a K-major no-swizzle operand: 8x16B core matrices
@@ -222,11 +275,12 @@ __device__ __forceinline__ UnitGeom unit_geom(const GroupGeom& gg, int unit) {
     return u;
 }
 
-template <int SLOTS>
+template <int SLOTS, int P2>
 __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kernel(RasterArgs a) {
     using R = Roles<SLOTS>;
     constexpr int kMT = R::kMT, SPW = R::kSPW, kEpiWarps = R::kEpiWarps;
     constexpr int kProd = R::kProd, kMma = R::kMma;
+    constexpr bool kCompact = R::kCompact;
     constexpr int kColsPerStage = kMT * kN;
     constexpr uint32_t kTmemCols = tmem_cols<SLOTS>();
     // No-swizzle K-major operands only need 16-byte alignment (descriptor addresses are >> 4).
@@ -241,10 +295,13 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
     for (int p = threadIdx.x; p < kMT * 128; p += blockDim.x) {
         const int m = p >> 7, l = p & 127;
         int x, y;
-        lane_pixel(m, l, x, y);
+        if (kCompact)
+            lane_pixel_compact(m, l, x, y);
+        else
+            lane_pixel(m, l, x, y);
         const float ux = (float)x + 0.5f - centre, uy = (float)y + 0.5f - centre;
         const float phi[6] = {ux * ux, ux * uy, uy * uy, ux, uy, 1.0f};
-        const int t = m >> 1;
+        const int t = kCompact ? 2 * (m >> 2) + (l >> 6) : m >> 1;
         uint4 lo, hi;
         lo.x = pack_half2(phi[0], phi[1]);
         lo.y = pack_half2(phi[2], phi[3]);
@@ -275,6 +332,8 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
+    [[maybe_unused]] unsigned long long pf[4] = {0, 0, 0, 0};
+    [[maybe_unused]] const long long pf_start = clock64();
 
     if (warp == kProd) {
         // ================================ producer ===========================================
@@ -293,6 +352,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
                         __nanosleep(32);
                         if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producer/done", (int)cc, s);
                     }
+                    if (TGS_RASTER_PROF) pf[1] += clock64() - t0;
                 }
             }
             __syncwarp();
@@ -318,6 +378,10 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
             if (t >= n_units) break;
             const int unit = a.order ? a.order[t] : t;
             const UnitGeom ug = unit_geom<SLOTS>(gg, unit);
+            [[maybe_unused]] const long long unit_t0 = clock64();
+            [[maybe_unused]] const uint32_t unit_c0 = c;
+            [[maybe_unused]] const unsigned long long unit_w0 = pf[1];
+            [[maybe_unused]] unsigned long long sec[3] = {0, 0, 0};
             const uint32_t begin = a.offsets[ug.gid], end = a.offsets[ug.gid + 1];
             const float ox = (float)(ug.tx0 * kTile) + centre, oy = (float)(ug.ty0 * kTile) + centre;
             int fill = 0;          // rows placed in the open chunk
@@ -347,13 +411,26 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
                 }
                 return r;
             };
-            uint32_t idx_next2 = ld_idx(1);
-            Rec nxt = ld_rec(ld_idx(0));
+            // records of batches bi+1 .. bi+kPF in flight, list indices of the kDI batches after
+            // those (an index load has kDI iterations to land before its record gather is issued)
+            Rec q[kPF];
+#pragma unroll
+            for (int k = 0; k < kPF; ++k) q[k] = ld_rec(ld_idx((uint32_t)k));
+            uint32_t iq[kDI];
+#pragma unroll
+            for (int k = 0; k < kDI; ++k) iq[k] = ld_idx((uint32_t)(kPF + k));
 
+            uint32_t n_batches = 0;
             for (uint32_t bi = 0; bi < nb; ++bi) {
-                const Rec cur = nxt;
-                nxt = ld_rec(idx_next2);
-                idx_next2 = ld_idx(bi + 2);
+                ++n_batches;
+                [[maybe_unused]] const long long tb0 = TGS_RASTER_PROF ? clock64() : 0;
+                const Rec cur = q[0];
+#pragma unroll
+                for (int k = 0; k + 1 < kPF; ++k) q[k] = q[k + 1];
+                q[kPF - 1] = ld_rec(iq[0]);
+#pragma unroll
+                for (int k = 0; k + 1 < kDI; ++k) iq[k] = iq[k + 1];
+                iq[kDI - 1] = ld_idx(bi + kPF + kDI);
                 if (emitted) {  // drop member tiles whose pixels all terminated (all owner warps)
                     uint32_t retired = 0xfu;
 #pragma unroll
@@ -363,7 +440,8 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
                             const int w = w4 + j;
-                            const uint32_t owned = ((1u << SPW) - 1u) << ((w >> 3) * SPW);
+                            const uint32_t owned =
+                                kCompact ? 1u << (w >> 1) : ((1u << SPW) - 1u) << ((w >> 3) * SPW);
                             retired &= ((dd[j] >> 4) == seq ? (uint32_t)(dd[j] & 15) : 0u) | (0xfu & ~owned);
                         }
                     }
@@ -373,6 +451,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
                     live &= ~retired;
                     if (live == 0u) break;
                 }
+                [[maybe_unused]] const long long tb1 = TGS_RASTER_PROF ? clock64() : 0;
                 bool keep = false;
                 uint4 r0, r1;
                 float4 epi_v = make_float4(0, 0, 0, 0);
@@ -395,6 +474,12 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
                     }
                 }
                 const uint32_t km = __ballot_sync(0xffffffffu, keep);
+                [[maybe_unused]] const long long tb2 = TGS_RASTER_PROF ? clock64() : 0;
+                if (TGS_RASTER_PROF) {
+                    pf[2] += 1;
+                    sec[0] += tb1 - tb0;
+                    sec[1] += tb2 - tb1;
+                }
                 if (km == 0u) continue;
 
                 const int nk = __popc(km);
@@ -404,25 +489,29 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
                     open = true;
                     fill = 0;
                 }
-                // place the kept ranks (nk <= 32 = kN, so a batch spills into at most one new chunk)
-                const int room = kN - fill;
-                if (keep && rank < room) {
-                    write_row(sm, s, fill + rank, r0, r1);
-                    sm.epi[s][fill + rank] = epi_v;
-                }
-                if (nk >= room) {  // chunk full: publish it, open the next for the remaining ranks
+                // place the kept ranks in order; a full chunk is published and the next one opened
+                // (a 32-lane batch spans at most 32 / kN + 1 chunks)
+                int placed = 0;
+                for (;;) {
+                    const int room = kN - fill;
+                    if (keep && rank >= placed && rank - placed < room) {
+                        write_row(sm, s, fill + rank - placed, r0, r1);
+                        sm.epi[s][fill + rank - placed] = epi_v;
+                        sm.cj[s][fill + rank - placed] = epi_v.w;
+                    }
+                    if (nk - placed < room) {
+                        fill += nk - placed;
+                        break;
+                    }
                     publish(s, seq, unit, kN, live);
                     ++c;
                     emitted = true;
                     s = open_stage(c);
-                    if (keep && rank >= room) {
-                        write_row(sm, s, rank - room, r0, r1);
-                        sm.epi[s][rank - room] = epi_v;
-                    }
-                    fill = nk - room;
-                } else {
-                    fill += nk;
+                    fill = 0;
+                    placed += room;
+                    if (placed == nk) break;
                 }
+                if (TGS_RASTER_PROF) sec[2] += clock64() - tb2;
             }
             // close the unit: pad and publish the partial chunk (or an empty one so the
             // epilogue still writes the unit's pixels)
@@ -439,6 +528,21 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
                 publish(s, seq, unit, 0, live);
                 ++c;
             }
+            // schedule feedback: list entries this unit walked (batches) plus rows it staged
+            if (a.unit_cost && lane == 0) a.unit_cost[unit] = 32u * n_batches + (uint32_t)kN * (c - unit_c0);
+#if TGS_RASTER_PROF
+            if (lane == 0) {
+                atomicMax(&g_rprof[13], (unsigned long long)(clock64() - unit_t0));
+                atomicMax(&g_rprof[14], (unsigned long long)(c - unit_c0));
+                if (unit < 65536) {
+                    g_ucyc[unit] = (unsigned int)(clock64() - unit_t0);
+                    g_uch[unit] = c - unit_c0;
+                    g_uent[unit] = (unsigned)t;
+                    g_uwait[unit] = (unsigned)(pf[1] - unit_w0);
+                    for (int k = 0; k < 3; ++k) g_usec[unit][k] = (unsigned)sec[k];
+                }
+            }
+#endif
         }
         const int s = open_stage(c);  // end of stream
         publish(s, -1, -1, 0, 0u);
@@ -448,13 +552,15 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
         const uint32_t a_base = ptx::smem_u32(&sm.a[0][0]);
         for (uint32_t c = 0;; ++c) {
             const int s = (int)(c % kSS), ts = (int)(c % kTS);
+            [[maybe_unused]] const long long tw0 = clock64();
             ptx::mbar_wait_wd(&sm.full[s], (c / kSS) & 1, "mma/full", (int)c, s);
+            if (TGS_RASTER_PROF) pf[1] += clock64() - tw0;
             if (c >= (uint32_t)kTS && lane == 0) {  // every epilogue warp finished chunk c - kTS
                 const int need = (int)(c - kTS + 1);
                 auto released = [&]() {
                     int mn = 0x7fffffff;
 #pragma unroll
-                    for (int w4 = 0; w4 < 16; w4 += 4) {
+                    for (int w4 = 0; w4 < kEpiWarps; w4 += 4) {
                         const int4 d = ld_volatile_v4(&sm.wdone[w4]);
                         mn = min(mn, min(min(d.x, d.y), min(d.z, d.w)));
                     }
@@ -466,6 +572,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
                         __nanosleep(32);
                         if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("mma/tempty", (int)c, 0);
                     }
+                    if (TGS_RASTER_PROF) pf[2] += clock64() - t0;
                 }
             }
             __syncwarp();
@@ -484,7 +591,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
                 const uint32_t dcol = tmem + (uint32_t)(ts * kColsPerStage);
 #pragma unroll
                 for (int m = 0; m < kMT; ++m)
-                    if ((hlive >> (m >> 1)) & 1u)
+                    if (kCompact ? ((hlive >> (2 * (m >> 2))) & 3u) : ((hlive >> (m >> 1)) & 1u))
                         ptx::mma_f16_ss_elect(dcol + (uint32_t)(m * kN),
                                               ptx::smem_desc(a_base + (uint32_t)(m * 128 * 32), 128, 256), bd, idesc, 0u);
                 ptx::mma_commit_elect(&sm.tfull[ts]);
@@ -499,9 +606,16 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
         // warp -> (lane quadrant q, tile half, slots k0 .. k0+SPW-1); slot i of a thread is a
         // pixel of member tile k0 + i
         const int q = warp & 3, half = (warp >> 2) & 1, k0 = (warp >> 3) * SPW;
+        // M-tile holding slot k of this warp
+        auto mtile = [&](int k) { return kCompact ? 4 * (warp >> 2) + k : 2 * (k0 + k) + half; };
         int relx[SPW], rely[SPW];
 #pragma unroll
-        for (int k = 0; k < SPW; ++k) lane_pixel(2 * (k0 + k) + half, q * 32 + lane, relx[k], rely[k]);
+        for (int k = 0; k < SPW; ++k) {
+            if (kCompact)
+                lane_pixel_compact(mtile(k), q * 32 + lane, relx[k], rely[k]);
+            else
+                lane_pixel(mtile(k), q * 32 + lane, relx[k], rely[k]);
+        }
         float T[SPW], cr[SPW], cg[SPW], cb[SPW], thr[SPW];
         int px[SPW], py[SPW];
         const float L = log2f(a.alpha_skip);
@@ -520,7 +634,9 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
         for (uint32_t c = 0;; ++c) {
             const int s = (int)(c % kSS), ts = (int)(c % kTS);
             // this warp consumed the phase of chunk c - kTS itself, so the parity is unambiguous
+            [[maybe_unused]] const long long tw0 = clock64();
             ptx::mbar_wait_wd(&sm.tfull[ts], (c / kTS) & 1, "epilogue/tfull", (int)c, warp);
+            if (TGS_RASTER_PROF) pf[1] += clock64() - tw0;
             ptx::tc_fence_after();
             const ChunkHeader h = sm.hdr[s];
             if (h.chunk != (int)c) {
@@ -566,8 +682,17 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
 #pragma unroll
                     for (int k = 0; k < SPW; ++k)
                         if (alive & (1u << k))
-                            ptx::tmem_ld16(lane_base + stage_col + (uint32_t)((2 * (k0 + k) + half) * kN + j0), d[k]);
+                            ptx::tmem_ld16(lane_base + stage_col + (uint32_t)(mtile(k) * kN + j0), d[k]);
                     ptx::tmem_wait_ld();
+#ifdef TGS_RASTER_TMEM2  // experiment: double the TMEM read traffic
+#pragma unroll
+                    for (int k = 0; k < SPW; ++k) ptx::reg_fence16(d[k]);
+#pragma unroll
+                    for (int k = 0; k < SPW; ++k)
+                        if (alive & (1u << k))
+                            ptx::tmem_ld16(lane_base + stage_col + (uint32_t)(mtile(k) * kN + j0), d[k]);
+                    ptx::tmem_wait_ld();
+#endif
 #pragma unroll
                     for (int k = 0; k < SPW; ++k) ptx::reg_fence16(d[k]);
                     // Phase 1 (branch-free, 16 independent chains): which of the 16 splats reach
@@ -581,11 +706,16 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
                         mk |= p & (1u << jj);
                     }
                     const uint32_t M = __reduce_or_sync(0xffffffffu, mk);
+                    if (TGS_RASTER_PROF) {
+                        pf[2] += __popc(M);
+                        pf[3] += 16;
+                    }
                     // Phase 2: ordered blend of the active splats (uniform branches).  A pixel blends
                     // splat j iff D >= log2(alpha_skip) and it had not terminated before j
                     // (T >= t_terminate): exactly alpha_of/blend/done (raster_scalar.hpp:40-55,
                     // raster_scalar.cpp:36-41) — the splat that drives T below t_terminate is
                     // blended, nothing after it.
+                    if constexpr (P2 == 0) {
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj) {
                         if (M & (1u << jj)) {
@@ -593,6 +723,128 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
 #pragma unroll
                             for (int k = 0; k < SPW; ++k) {
                                 const float dv = __uint_as_float(d[k][jj]);
+                                const float e2 = fminf(ej.w, ex2_approx(dv));
+                                const float al = (dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f;
+                                const float wt = T[k] * al;
+                                cr[k] = fmaf(wt, ej.x, cr[k]);
+                                cg[k] = fmaf(wt, ej.y, cg[k]);
+                                cb[k] = fmaf(wt, ej.z, cb[k]);
+                                T[k] -= wt;
+                            }
+                        }
+                    }
+                    } else if constexpr (P2 == 2 || P2 == 3) {
+                        // alpha caps of the 16 splats preloaded (4 x LDS.128), so an active splat's
+                        // critical path starts at its D (already in registers); colours are loaded
+                        // inside the block and only needed at its end
+                        float cjv[16];
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            const float4 t4 = *reinterpret_cast<const float4*>(&sm.cj[s][j0 + 4 * v]);
+                            cjv[4 * v] = t4.x;
+                            cjv[4 * v + 1] = t4.y;
+                            cjv[4 * v + 2] = t4.z;
+                            cjv[4 * v + 3] = t4.w;
+                        }
+                        auto blend = [&](int jj) {
+                            const float4 ej = sm.epi[s][j0 + jj];
+#pragma unroll
+                            for (int k = 0; k < SPW; ++k) {
+                                const float dv = __uint_as_float(d[k][jj]);
+                                const float e2 = fminf(cjv[jj], ex2_approx(dv));
+                                const float al = (dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f;
+                                const float wt = T[k] * al;
+                                cr[k] = fmaf(wt, ej.x, cr[k]);
+                                cg[k] = fmaf(wt, ej.y, cg[k]);
+                                cb[k] = fmaf(wt, ej.z, cb[k]);
+                                T[k] -= wt;
+                            }
+                        };
+                        if constexpr (P2 == 2) {
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj)
+                                if (M & (1u << jj)) blend(jj);
+                        } else {
+                            uint32_t Mr = M;
+#pragma unroll 1
+                            while (Mr) {
+                                const int jj = __ffs(Mr) - 1;
+                                Mr &= Mr - 1u;
+                                switch (jj) {
+#define TGS_CASE(n) case n: blend(n); break;
+                                    TGS_CASE(0) TGS_CASE(1) TGS_CASE(2) TGS_CASE(3) TGS_CASE(4) TGS_CASE(5)
+                                    TGS_CASE(6) TGS_CASE(7) TGS_CASE(8) TGS_CASE(9) TGS_CASE(10) TGS_CASE(11)
+                                    TGS_CASE(12) TGS_CASE(13) TGS_CASE(14) TGS_CASE(15)
+#undef TGS_CASE
+                                    default: break;
+                                }
+                            }
+                        }
+                    } else if constexpr (P2 == 4) {
+                        // loop over the active splats only, re-reading each one's D column from TMEM
+                        // (tcgen05.ld 32x32b.x1 per slot, next splat prefetched while this one blends)
+                        uint32_t Mr = M;
+                        if (Mr) {
+                            int jj = __ffs(Mr) - 1;
+                            Mr &= Mr - 1u;
+                            const uint32_t cbase = lane_base + stage_col + (uint32_t)j0;
+                            uint32_t dc[SPW];
+#pragma unroll
+                            for (int k = 0; k < SPW; ++k) ptx::tmem_ld1(cbase + (uint32_t)(mtile(k) * kN + jj), dc[k]);
+                            ptx::tmem_wait_ld();
+#pragma unroll
+                            for (int k = 0; k < SPW; ++k) ptx::reg_fence1(dc[k]);
+#pragma unroll 1
+                            for (;;) {
+                                const bool more = Mr != 0u;
+                                int jn = jj;
+                                uint32_t dn[SPW];
+                                if (more) {
+                                    jn = __ffs(Mr) - 1;
+                                    Mr &= Mr - 1u;
+#pragma unroll
+                                    for (int k = 0; k < SPW; ++k)
+                                        ptx::tmem_ld1(cbase + (uint32_t)(mtile(k) * kN + jn), dn[k]);
+                                }
+                                const float4 ej = sm.epi[s][j0 + jj];
+#pragma unroll
+                                for (int k = 0; k < SPW; ++k) {
+                                    const float dv = __uint_as_float(dc[k]);
+                                    const float e2 = fminf(ej.w, ex2_approx(dv));
+                                    const float al = (dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f;
+                                    const float wt = T[k] * al;
+                                    cr[k] = fmaf(wt, ej.x, cr[k]);
+                                    cg[k] = fmaf(wt, ej.y, cg[k]);
+                                    cb[k] = fmaf(wt, ej.z, cb[k]);
+                                    T[k] -= wt;
+                                }
+                                if (!more) break;
+                                ptx::tmem_wait_ld();
+#pragma unroll
+                                for (int k = 0; k < SPW; ++k) {
+                                    ptx::reg_fence1(dn[k]);
+                                    dc[k] = dn[k];
+                                }
+                                jj = jn;
+                            }
+                        }
+                    } else {
+                        // loop over the active splats only; D comes from a thread-local copy
+                        // (one LDL per slot) instead of 16 unrolled uniform branches
+                        uint32_t dl[SPW][16];
+#pragma unroll
+                        for (int k = 0; k < SPW; ++k)
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) dl[k][j] = d[k][j];
+                        uint32_t Mr = M;
+#pragma unroll 1
+                        while (Mr) {
+                            const int jj = __ffs(Mr) - 1;
+                            Mr &= Mr - 1u;
+                            const float4 ej = sm.epi[s][j0 + jj];
+#pragma unroll
+                            for (int k = 0; k < SPW; ++k) {
+                                const float dv = __uint_as_float(dl[k][jj]);
                                 const float e2 = fminf(ej.w, ex2_approx(dv));
                                 const float al = (dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f;
                                 const float wt = T[k] * al;
@@ -618,7 +870,9 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if (dead != reported) ((volatile int*)sm.dead)[warp] = (cur << 4) | (int)(dead << k0);
+                // published in member-tile bits (compact: the warp's half of tile warp >> 1)
+                const uint32_t dtiles = kCompact ? (dead == (1u << SPW) - 1u ? 1u << (warp >> 1) : 0u) : dead << k0;
+                if (dead != reported) ((volatile int*)sm.dead)[warp] = (cur << 4) | (int)dtiles;
                 __threadfence_block();
                 ((volatile int*)sm.wdone)[warp] = (int)c + 1;
                 atomicAdd(&sm.done_cnt[s], 1u);
@@ -627,29 +881,71 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
         }
     }
 
+#if TGS_RASTER_PROF
+    if (lane == 0) {
+        const int base = warp == kProd ? 0 : warp == kMma ? 4 : 8;
+        atomicAdd(&g_rprof[base], (unsigned long long)(clock64() - pf_start));
+        if (warp == kProd) atomicMax(&g_rprof[12], (unsigned long long)(clock64() - pf_start));
+        for (int i = 1; i < 4; ++i) atomicAdd(&g_rprof[base + i], pf[i]);
+        if (warp == kProd) atomicAdd(&g_rprof[3], (unsigned long long)0);
+    }
+#endif
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     if (warp == kMma) ptx::tmem_dealloc<kTmemCols>(tmem);
+#if TGS_RASTER_PROF
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&g_rprof_done, 1u) == gridDim.x - 1) {
+            unsigned long long v[16];
+            for (int i = 0; i < 16; ++i) v[i] = atomicExch(&g_rprof[i], 0ull);
+            g_rprof_done = 0;
+            // the 12 most expensive units: cycles, chunks, list length, position in the start order
+            for (int r = 0; r < 12; ++r) {
+                unsigned int best = 0;
+                int bu = -1;
+                for (int u = 0; u < n_units && u < 65536; ++u)
+                    if (g_ucyc[u] > best) { best = g_ucyc[u]; bu = u; }
+                if (bu < 0) break;
+                const int gid = SLOTS == 1 || gg.g == 2 ? bu : bu / 4;
+                printf("RUNIT %d cycles %u chunks %u list %u started #%u | producer wait %u retire %u row %u place %u\n",
+                       bu, best, g_uch[bu], a.offsets[gid + 1] - a.offsets[gid], g_uent[bu], g_uwait[bu],
+                       g_usec[bu][0], g_usec[bu][1], g_usec[bu][2]);
+                g_ucyc[bu] = 0;
+            }
+            const double n = (double)gridDim.x;
+            printf("RPROF ctas %d | producer total %.0f wait %.0f batches %.0f | mma total %.0f wfull %.0f wtmem %.0f | "
+                   "epi/warp total %.0f wtfull %.0f | active blocks %.3f of %.0f | cta max %llu unit max %llu "
+                   "chunks max %llu\n", gridDim.x, v[0] / n, v[1] / n,
+                   v[2] / n, v[4] / n, v[5] / n, v[6] / n, v[8] / n / kEpiWarps, v[9] / n / kEpiWarps,
+                   (double)v[10] / (double)(v[11] ? v[11] : 1), v[11] / n / kEpiWarps, v[12], v[13], v[14]);
+        }
+    }
+#endif
 }
 
-template <int SLOTS>
+template <int SLOTS, int P2>
 void launch_t(const RasterArgs& a, int num_sms, cudaStream_t st) {
     const size_t smem = sizeof(Smem<SLOTS>);
-    cudaFuncSetAttribute(raster_tensor_kernel<SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(raster_tensor_kernel<SLOTS, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int n_units = (SLOTS == 1 || a.gg.g == 2) ? a.gg.n_groups_band : a.gg.n_groups_band * 4;
     int grid = num_sms;
     if (grid > n_units) grid = n_units;
-    if (grid > 0) raster_tensor_kernel<SLOTS><<<grid, Roles<SLOTS>::kThreads, smem, st>>>(a);
+    if (grid > 0) raster_tensor_kernel<SLOTS, P2><<<grid, Roles<SLOTS>::kThreads, smem, st>>>(a);
 }
 
 }  // namespace
 
 void launch_raster_tensor(const RasterArgs& a, int num_sms, cudaStream_t st) {
+    static const int variant = [] {
+        const char* e = getenv("TGS_RASTER_VARIANT");  // A/B aid for epilogue experiments
+        return e ? atoi(e) : 0;
+    }();
     if (a.gg.g == 1)
-        launch_t<1>(a, num_sms, st);
+        variant == 4 ? launch_t<1, 4>(a, num_sms, st) : launch_t<1, 0>(a, num_sms, st);
     else
-        launch_t<4>(a, num_sms, st);
+        variant == 4 ? launch_t<4, 4>(a, num_sms, st) : launch_t<4, 0>(a, num_sms, st);
 }
 
 }  // namespace tgs

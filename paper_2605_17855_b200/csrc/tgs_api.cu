@@ -102,7 +102,8 @@ struct tgs_ctx {
     DBuf proj;          // mc | co | col (capacity n)
     DBuf pre_keys[2], pre_vals[2];
     DBuf rect, rrect;   // tile rect per compacted splat / per rank
-    DBuf list;          // sorted group lists (compacted indices)
+    DBuf list;          // sorted group lists (splat indices)
+    DBuf rowlist;       // group-row lists (binning level 1)
     DBuf hist, bsum;    // counting-sort [group][chunk] matrix and its scan block sums
     DBuf ghist, offsets, order;
     DBuf ucost;         // per unit, list entries the last frame walked (schedule feedback)
@@ -219,8 +220,11 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     TGS_CUDA_OK(ctx->rrect.ensure((size_t)n_alloc * sizeof(uint2)));
     const uint32_t cap = std::max<uint32_t>(ctx->capacity, 1u);
     TGS_CUDA_OK(ctx->list.ensure((size_t)cap * 4));
-    TGS_CUDA_OK(ctx->hist.ensure(bin_hist_elems(n_groups) * 4));
-    TGS_CUDA_OK(ctx->bsum.ensure(std::max(bin_bsum_elems(n_groups), scan_tmp_elems((size_t)256 * kSortBlocks)) * 4));
+    const size_t h1 = bin_hist1_elems(gg), h2 = bin_hist2_elems(gg, cap), hm = bin_meta_elems(gg);
+    TGS_CUDA_OK(ctx->hist.ensure((h1 + h2 + hm) * 4));
+    TGS_CUDA_OK(ctx->rowlist.ensure((size_t)cap * sizeof(uint2)));
+    TGS_CUDA_OK(ctx->bsum.ensure(
+        std::max({scan_tmp_elems(h1), scan_tmp_elems(h2), scan_tmp_elems((size_t)256 * kSortBlocks)}) * 4));
     TGS_CUDA_OK(ctx->ghist.ensure((size_t)256 * kSortBlocks * 4));
     TGS_CUDA_OK(ctx->offsets.ensure((size_t)(n_groups + 1) * 4));
     TGS_CUDA_OK(ctx->order.ensure((size_t)gg.tiles_x * gg.tiles_y * 4));
@@ -270,13 +274,15 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     ba.rect = ctx->rect.as<uint2>();
     ba.rrect = ctx->rrect.as<uint2>();
     ba.gg = gg;
-    ba.hist = ctx->hist.as<uint32_t>();
+    ba.hist1 = ctx->hist.as<uint32_t>();
+    ba.hist2 = ba.hist1 + h1;
+    ba.meta = ba.hist2 + h2;
+    ba.rowlist = ctx->rowlist.as<uint2>();
     ba.bsum = ctx->bsum.as<uint32_t>();
     ba.offsets = ctx->offsets.as<uint32_t>();
     ba.list = ctx->list.as<uint32_t>();
     ba.fc = fc;
     ba.capacity = ctx->capacity;
-    ba.n_chunks = bin_chunks(n_groups);
     launch_binning(ba, n_alloc, s);
     {
         const int per = gg.g == 4 ? 4 : 1;  // G=4 groups are rasterised as 2x2-tile quarters
@@ -466,7 +472,7 @@ void tgs_ctx_destroy(tgs_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->scratch_scene) tgs_scene_free(c->scratch_scene);
     DBuf* bufs[] = {&c->fc, &c->proj, &c->pre_keys[0], &c->pre_keys[1], &c->pre_vals[0],
-                    &c->pre_vals[1], &c->rect, &c->rrect, &c->list, &c->hist, &c->bsum, &c->ghist,
+                    &c->pre_vals[1], &c->rect, &c->rrect, &c->list, &c->rowlist, &c->hist, &c->bsum, &c->ghist,
                     &c->offsets, &c->order, &c->ucost, &c->image, &c->scratch_records};
     for (DBuf* b : bufs) b->release();
     for (auto& e : c->ev)

@@ -1,22 +1,25 @@
-// Tile/group binning + sort (north_star 2): a stable counting sort of (group, rank) entries.
+// Tile/group binning + sort (north_star 2): a stable partition of (group, rank) entries.
 // Reference: proj/src/binning.cpp:32-100 (tiles_overlapped, build_group_entries, sort_entries),
 // render.cpp:17-21.
 //
 // The reference emits one 16-byte entry per (splat, overlapped group) and std::stable_sorts them
 // on (group_id << 32) | f32_bits(depth) (ties: emission order = splat index).  Here the splats are
-// first radix-sorted by depth bits (tgs_sort.cu, values = compacted index, so ties keep index
-// order) — their "rank" order.  Every group's list is then the rank-ordered subsequence of splats
-// overlapping it, which a counting sort produces directly, writing each 4-byte entry once:
-//   gather  : rank-ordered tile rectangles (8 B per splat);
-//   count   : every warp owns a contiguous rank range (a "chunk") and builds its per-group entry
-//             counts with a 2D difference array in shared memory (4 atomics per splat, then row and
-//             column prefix sums) -> hist[group][chunk];
-//   scan    : exclusive scan of hist in group-major order -> the start of every (group, chunk) run;
-//   scatter : each warp replays its splats in rank order and writes entry slots from per-warp
-//             shared-memory cursors (a splat has at most one entry per group, so the lanes writing
-//             one splat's entries never collide).
-// Entries carry only the splat index; the member-tile mask (binning.cpp:56-65) is a pure function of
-// the splat's tile rectangle and the group, so consumers recompute it.
+// first radix-sorted by depth bits (tgs_sort.cu, values = splat index, so ties keep index order) —
+// their "rank" order.  Every group's list is then the rank-ordered subsequence of splats
+// overlapping it, built by two stable partitions that write each entry once:
+//   gather : rank-ordered tile rectangles (8 B per splat);
+//   level 1: splats -> group-row lists.  Each warp owns a contiguous rank range (chunk); per-row
+//            counts (1D difference array) -> scan over (row, chunk) -> every lane owns some rows
+//            and appends the chunk's splats to them in rank order (8-byte row entries: splat
+//            index, column range);
+//   level 2: group-row lists -> group lists.  Each warp owns a segment of one row list; per-column
+//            counts -> scan over (row, column, segment) = group-major -> every lane owns some
+//            columns and appends the segment's splats to them in order.
+// The lane that owns a row / column appends sequentially, so order is stable by construction —
+// no atomics or match on the placement path, and every (row, chunk) / (group, segment) run is a
+// contiguous burst.  Entries carry only the splat index; the member-tile mask
+// (binning.cpp:56-65) is a pure function of the splat's tile rectangle and the group, so
+// consumers recompute it.
 #include "tgs_common.cuh"
 #include "tgs_kernels.cuh"
 
@@ -26,7 +29,9 @@ namespace tgs {
 
 namespace {
 
-constexpr int kMaxBinWarps = 8;       // warps per count/scatter block (fewer for huge grids)
+constexpr int kBinWarps = 8;          // warps per binning block (one chunk / segment per warp)
+constexpr int kRowChunks = 148 * 32;  // level-1 chunks (contiguous rank ranges, one warp each)
+constexpr uint32_t kSegLen = 2048;    // level-2 segment: row-list entries per warp
 constexpr int kScanItems = 16;        // per thread in the hist scan
 constexpr int kScanBlock = 256;
 constexpr int kScanTile = kScanItems * kScanBlock;
@@ -63,71 +68,256 @@ __global__ void __launch_bounds__(256) rank_gather_kernel(BinArgs a) {
         a.rrect[r] = __ldg(&a.rect[__ldg(&a.sval[r])]);
 }
 
-// Per-warp group counts of the rank range [r0, r1): 2D difference array in shared memory (4
-// atomics per splat), then prefix sums along x and y.  Afterwards D[gy * pitch + gx] = entries of
-// the range in band-local group (gx, gy).
-__device__ __forceinline__ void warp_group_counts(const BinArgs& a, int* D, uint32_t r0, uint32_t r1, int lane) {
-    const GroupGeom& gg = a.gg;
-    const int gx = gg.groups_x, gyb = gg.band_gy1 - gg.band_gy0;
-    const int pitch = gx + 1, area = (gyb + 1) * pitch;
-    for (int i = lane; i < area; i += 32) D[i] = 0;
+// ---- level 1: splats -> group-row lists -----------------------------------------------------
+// A "chunk" is one warp's contiguous rank range.  Row entries are (splat index, gx0 | gx1 << 16)
+// and row y's list is the concatenation over chunks of the chunk's splats overlapping row y.
+
+// hist1[y * kRowChunks + chunk] = splats of the chunk overlapping group row y; fc->n_entries +=
+// the chunk's (splat, group) entries (the capacity check needs the total before any placement).
+__global__ void __launch_bounds__(kBinWarps * 32) rows_count_kernel(BinArgs a) {
+    extern __shared__ int sdiff[];
+    const int rows = a.gg.band_gy1 - a.gg.band_gy0;
+    const int lane = threadIdx.x & 31, chunk = blockIdx.x * kBinWarps + (threadIdx.x >> 5);
+    int* D = sdiff + (threadIdx.x >> 5) * (rows + 1);
+    for (int i = lane; i <= rows; i += 32) D[i] = 0;
     __syncwarp();
+    uint32_t r0, r1;
+    chunk_range(*a.visible, kRowChunks, chunk, r0, r1);
+    uint32_t ent = 0;
     for (uint32_t r = r0 + lane; r < r1; r += 32) {
         int gx0, gx1, gy0, gy1;
-        if (!band_groups(gg, __ldg(&a.rrect[r]), gx0, gx1, gy0, gy1)) continue;
-        atomicAdd(&D[gy0 * pitch + gx0], 1);
-        atomicAdd(&D[gy0 * pitch + gx1 + 1], -1);
-        atomicAdd(&D[(gy1 + 1) * pitch + gx0], -1);
-        atomicAdd(&D[(gy1 + 1) * pitch + gx1 + 1], 1);
+        if (!band_groups(a.gg, __ldg(&a.rrect[r]), gx0, gx1, gy0, gy1)) continue;
+        atomicAdd(&D[gy0], 1);
+        atomicAdd(&D[gy1 + 1], -1);
+        ent += (uint32_t)((gx1 - gx0 + 1) * (gy1 - gy0 + 1));
     }
     __syncwarp();
-    for (int y = lane; y < gyb; y += 32) {  // prefix along x (one row per lane)
-        int run = 0;
-        for (int x = 0; x < gx; ++x) {
-            run += D[y * pitch + x];
-            D[y * pitch + x] = run;
+    int carry = 0;
+    for (int base = 0; base < rows; base += 32) {
+        const int y = base + lane;
+        int incl = y < rows ? D[y] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
         }
+        if (y < rows) a.hist1[(size_t)y * kRowChunks + chunk] = (uint32_t)(carry + incl);
+        carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    __syncwarp();
-    for (int x = lane; x < gx; x += 32) {  // prefix along y (one column per lane)
-        int run = 0;
-        for (int y = 0; y < gyb; ++y) {
-            run += D[y * pitch + x];
-            D[y * pitch + x] = run;
-        }
-    }
-    __syncwarp();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ent += __shfl_xor_sync(0xffffffffu, ent, o);
+    if (lane == 0 && ent) atomicAdd(&a.fc->n_entries, ent);
 }
 
-// Chunk = one block: the block's rank range, split evenly over its warps.
-__device__ __forceinline__ void block_warp_range(const BinArgs& a, int wib, int wpb, uint32_t& r0, uint32_t& r1) {
-    uint32_t b0, b1;
-    chunk_range(*a.visible, a.n_chunks, blockIdx.x, b0, b1);
-    uint32_t w0, w1;
-    chunk_range(b1 - b0, wpb, wib, w0, w1);
-    r0 = b0 + w0;
-    r1 = b0 + w1;
+// One warp: capacity check, row starts, per-row segment counts and the level-2 histogram layout.
+//   meta[0 .. rows]            row list starts (meta[rows] = row entries)
+//   meta[M1 .. M1 + rows]      prefix of segments per row (M1 = rows + 1; last = segments)
+//   meta[M2 .. M2 + rows]      prefix of gx * segments per row: hist2 block of row y (M2 = 2 rows + 2)
+__global__ void rows_meta_kernel(BinArgs a, const uint32_t* __restrict__ scan1_total) {
+    const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x, lane = threadIdx.x;
+    uint32_t* rowstart = a.meta;
+    uint32_t* nsegp = a.meta + rows + 1;
+    uint32_t* rowbase2 = a.meta + 2 * rows + 2;
+    const uint32_t total = a.fc->n_entries;
+    const bool over = total > a.capacity;  // lists do not fit: nothing is placed, host grows + re-renders
+    if (lane == 0) {
+        if (over)
+            a.fc->overflow = 1u;
+        else
+            a.fc->n_sort = total;
+    }
+    uint32_t cs = 0, cb = 0;
+    for (int base = 0; base <= rows; base += 32) {
+        const int y = base + lane;
+        uint32_t start = 0, nseg = 0;
+        if (y < rows) {
+            start = a.hist1[(size_t)y * kRowChunks];
+            const uint32_t next = y + 1 < rows ? a.hist1[(size_t)(y + 1) * kRowChunks] : *scan1_total;
+            nseg = over ? 0u : (next - start + kSegLen - 1u) / kSegLen;
+        } else if (y == rows) {
+            start = *scan1_total;
+        }
+        uint32_t inc_s = nseg;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc_s, o);
+            if (lane >= o) inc_s += t;
+        }
+        if (y <= rows) {
+            rowstart[y] = start;
+            nsegp[y] = cs + inc_s - nseg;
+            rowbase2[y] = (cs + inc_s - nseg) * (uint32_t)gx;
+        }
+        cs += __shfl_sync(0xffffffffu, inc_s, 31);
+        (void)cb;
+    }
 }
 
-// hist[g * n_chunks + chunk] = entries the chunk (one block) contributes to group g.
-__global__ void __launch_bounds__(kMaxBinWarps * 32) group_count_kernel(BinArgs a) {
-    extern __shared__ int sdiff[];
-    const GroupGeom& gg = a.gg;
-    const int gx = gg.groups_x, gyb = gg.band_gy1 - gg.band_gy0;
-    const int pitch = gx + 1, area = (gyb + 1) * pitch, ng = gx * gyb;
-    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+// Row placement: lane l owns group rows l, l + 32, ... (KR per lane) with register cursors; the
+// warp walks its chunk 32 splats at a time and, splat by splat (broadcast), every owning lane
+// appends the splat to its row.  Rank order within a row follows from the walk order.
+template <int KR>
+__global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
+    if (a.fc->overflow) return;
+    const int rows = a.gg.band_gy1 - a.gg.band_gy0;
+    const int lane = threadIdx.x & 31, chunk = blockIdx.x * kBinWarps + (threadIdx.x >> 5);
     uint32_t r0, r1;
-    block_warp_range(a, wib, wpb, r0, r1);
-    warp_group_counts(a, sdiff + wib * area, r0, r1, lane);
-    __syncthreads();
-    for (int g = threadIdx.x; g < ng; g += blockDim.x) {
-        const int y = g / gx, di = y * pitch + (g - y * gx);
-        uint32_t t = 0;
-        for (int w = 0; w < wpb; ++w) t += (uint32_t)sdiff[w * area + di];
-        a.hist[(size_t)g * a.n_chunks + blockIdx.x] = t;
+    chunk_range(*a.visible, kRowChunks, chunk, r0, r1);
+    uint32_t cur[KR];
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+        const int y = lane + 32 * k;
+        cur[k] = y < rows ? a.hist1[(size_t)y * kRowChunks + chunk] : 0u;
+    }
+    for (uint32_t rb = r0; rb < r1; rb += 32) {
+        const uint32_t r = rb + lane;
+        uint32_t yp = 0xffffu, xp = 0u, idx = 0u;  // yp: gy0 | gy1 << 16 (empty: lo > hi)
+        if (r < r1) {
+            int gx0, gx1, gy0, gy1;
+            if (band_groups(a.gg, __ldg(&a.rrect[r]), gx0, gx1, gy0, gy1)) {
+                yp = (uint32_t)gy0 | ((uint32_t)gy1 << 16);
+                xp = (uint32_t)gx0 | ((uint32_t)gx1 << 16);
+            }
+            idx = __ldg(&a.sval[r]);
+        }
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t yj = __shfl_sync(0xffffffffu, yp, j);
+            const uint32_t xj = __shfl_sync(0xffffffffu, xp, j);
+            const uint32_t ij = __shfl_sync(0xffffffffu, idx, j);
+            const int lo = (int)(yj & 0xffffu), hi = (int)(yj >> 16);
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+                const int y = lane + 32 * k;
+                if (y >= lo && y <= hi) a.rowlist[cur[k]++] = make_uint2(ij, xj);
+            }
+        }
     }
 }
 
+// ---- level 2: group-row lists -> group lists ----------------------------------------------------
+// Row y's list is cut into segments of kSegLen entries (one warp each).  hist2 holds, per row, a
+// [column][segment] block, so the exclusive scan of hist2 (rows in order) is directly the global
+// start of every (group, segment) run and group g = (y, x) starts at its segment-0 slot.
+
+__device__ __forceinline__ void seg_locate(const uint32_t* nsegp, int rows, uint32_t q, int& y, uint32_t& s) {
+    int lo = 0, hi = rows - 1;  // last row with nsegp[y] <= q
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (nsegp[mid] <= q)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    y = lo;
+    s = q - nsegp[lo];
+}
+
+__global__ void __launch_bounds__(kBinWarps * 32) cols_count_kernel(BinArgs a) {
+    extern __shared__ int sdiff[];
+    if (a.fc->overflow) return;
+    const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x;
+    const int lane = threadIdx.x & 31;
+    const uint32_t* rowstart = a.meta;
+    const uint32_t* nsegp = a.meta + rows + 1;
+    const uint32_t* rowbase2 = a.meta + 2 * rows + 2;
+    const uint32_t nq = nsegp[rows];
+    int* D = sdiff + (threadIdx.x >> 5) * (gx + 1);
+    for (uint32_t q = blockIdx.x * kBinWarps + (threadIdx.x >> 5); q < nq; q += gridDim.x * kBinWarps) {
+        int y;
+        uint32_t s;
+        seg_locate(nsegp, rows, q, y, s);
+        const uint32_t nseg = nsegp[y + 1] - nsegp[y];
+        const uint32_t e0 = rowstart[y] + s * kSegLen, e1 = min(rowstart[y + 1], e0 + kSegLen);
+        for (int i = lane; i <= gx; i += 32) D[i] = 0;
+        __syncwarp();
+        for (uint32_t e = e0 + lane; e < e1; e += 32) {
+            const uint32_t xp = __ldg(&a.rowlist[e].y);
+            atomicAdd(&D[xp & 0xffffu], 1);
+            atomicAdd(&D[(xp >> 16) + 1], -1);
+        }
+        __syncwarp();
+        int carry = 0;
+        for (int base = 0; base < gx; base += 32) {
+            const int x = base + lane;
+            int incl = x < gx ? D[x] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (x < gx) a.hist2[rowbase2[y] + (uint32_t)x * nseg + s] = (uint32_t)(carry + incl);
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
+    }
+}
+
+// offsets[g] = global start of group g = its segment-0 slot of the scanned hist2 (an empty row has
+// a zero-size block: the slot holds the running total, which is its groups' start); offsets[ng] =
+// total.  Overflow: every list empty.
+__global__ void offsets_kernel(BinArgs a, size_t hist2_len) {
+    const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x, ng = a.gg.n_groups_band;
+    const uint32_t* nsegp = a.meta + rows + 1;
+    const uint32_t* rowbase2 = a.meta + 2 * rows + 2;
+    const bool over = a.fc->overflow != 0u;
+    const uint32_t total = a.fc->n_entries;
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g <= ng; g += gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        if (!over) {
+            if (g == ng) {
+                v = total;
+            } else {
+                const int y = g / gx, x = g - y * gx;
+                const size_t i = (size_t)rowbase2[y] + (size_t)x * (nsegp[y + 1] - nsegp[y]);
+                v = i < hist2_len ? a.hist2[i] : total;
+            }
+        }
+        a.offsets[g] = v;
+    }
+}
+
+// Group placement: lane l owns columns l, l + 32, ... (KC per lane) of the segment's row with
+// register cursors; entries are broadcast one by one and every owning column appends the splat.
+template <int KC>
+__global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
+    if (a.fc->overflow) return;
+    const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x;
+    const int lane = threadIdx.x & 31;
+    const uint32_t* rowstart = a.meta;
+    const uint32_t* nsegp = a.meta + rows + 1;
+    const uint32_t* rowbase2 = a.meta + 2 * rows + 2;
+    const uint32_t nq = nsegp[rows];
+    for (uint32_t q = blockIdx.x * kBinWarps + (threadIdx.x >> 5); q < nq; q += gridDim.x * kBinWarps) {
+        int y;
+        uint32_t s;
+        seg_locate(nsegp, rows, q, y, s);
+        const uint32_t nseg = nsegp[y + 1] - nsegp[y];
+        const uint32_t e0 = rowstart[y] + s * kSegLen, e1 = min(rowstart[y + 1], e0 + kSegLen);
+        uint32_t cur[KC];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            const int x = lane + 32 * k;
+            cur[k] = x < gx ? a.hist2[rowbase2[y] + (uint32_t)x * nseg + s] : 0u;
+        }
+        for (uint32_t eb = e0; eb < e1; eb += 32) {
+            const uint32_t e = eb + lane;
+            uint2 v = make_uint2(0u, 0xffffu);  // empty column range (lo > hi)
+            if (e < e1) v = __ldg(&a.rowlist[e]);
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t ij = __shfl_sync(0xffffffffu, v.x, j);
+                const uint32_t xj = __shfl_sync(0xffffffffu, v.y, j);
+                const int lo = (int)(xj & 0xffffu), hi = (int)(xj >> 16);
+#pragma unroll
+                for (int k = 0; k < KC; ++k) {
+                    const int x = lane + 32 * k;
+                    if (x >= lo && x <= hi) a.list[cur[k]++] = ij;
+                }
+            }
+        }
+    }
+}
 // ---- exclusive scan of hist (block sums -> single-block scan of the sums -> apply) ----------
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& total) {
     __shared__ uint32_t wsum[kScanBlock / 32];
@@ -241,151 +431,6 @@ __global__ void __launch_bounds__(kScanBlock) scan_apply_kernel(uint32_t* __rest
     }
 }
 
-// offsets[g] = start of group g's list; offsets[ng] = total; capacity check -> fc flags.
-__global__ void offsets_kernel(BinArgs a, int n_scan_blocks) {
-    const int ng = a.gg.n_groups_band;
-    const uint32_t total = a.bsum[n_scan_blocks];
-    const bool over = total > a.capacity;  // lists do not fit: every list empty, host grows + re-renders
-    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g <= ng; g += gridDim.x * blockDim.x)
-        a.offsets[g] = over ? 0u : (g < ng ? a.hist[(size_t)g * a.n_chunks] : total);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.fc->n_entries = total;
-        if (total > a.capacity)
-            a.fc->overflow = 1u;
-        else
-            a.fc->n_sort = total;
-    }
-}
-
-// The block's chunk, sorted locally: per-warp group counts -> per-(warp, group) start inside the
-// chunk -> entries placed in shared memory in (group, rank) order -> flushed so that every
-// (group, chunk) run lands as one contiguous burst.  Chunks too large for the shared buffer write
-// each entry straight to its global slot instead (same slots, scattered writes).
-//
-// Placement expands the warp's splats 32 entries per step (rank-major, entries of a splat in
-// row-major group order, like build_group_entries binning.cpp:50-72); entries of one step that
-// hit the same group come from different splats and are ranked by lane (= rank order) with
-// match_any, the highest such lane advancing the group's cursor.
-__global__ void __launch_bounds__(kMaxBinWarps * 32) group_scatter_kernel(BinArgs a, int buf_cap) {
-    extern __shared__ int smem[];
-    const GroupGeom& gg = a.gg;
-    const int gx = gg.groups_x, gyb = gg.band_gy1 - gg.band_gy0;
-    const int pitch = gx + 1, area = (gyb + 1) * pitch, ng = gx * gyb;
-    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-    int* D = smem;                                                 // wpb x area: counts, then cursors
-    uint32_t* T = reinterpret_cast<uint32_t*>(smem + wpb * area);  // [ng + 1] local run starts
-    uint32_t* G0 = T + ng + 1;                                     // [ng] global run starts
-    uint32_t* buf = G0 + ng;                                       // [buf_cap] sorted entries
-    uint16_t* gbuf = reinterpret_cast<uint16_t*>(buf + buf_cap);   // [buf_cap] their groups
-    __shared__ uint32_t s_total;
-    if (a.fc->overflow) return;
-    uint32_t r0, r1;
-    block_warp_range(a, wib, wpb, r0, r1);
-    int* Dw = D + wib * area;
-    warp_group_counts(a, Dw, r0, r1, lane);
-    __syncthreads();
-    // per-(warp, group) exclusive prefix over the warps; T = block totals; G0 = global run starts
-    for (int g = threadIdx.x; g < ng; g += blockDim.x) {
-        const int y = g / gx, di = y * pitch + (g - y * gx);
-        uint32_t run = 0;
-        for (int w = 0; w < wpb; ++w) {
-            const uint32_t c = (uint32_t)D[w * area + di];
-            D[w * area + di] = (int)run;
-            run += c;
-        }
-        T[g] = run;
-        G0[g] = a.hist[(size_t)g * a.n_chunks + blockIdx.x];
-    }
-    __syncthreads();
-    // exclusive scan of T over the groups (one warp; ng is a few thousand at most)
-    if (wib == 0) {
-        uint32_t carry = 0;
-        for (int base = 0; base < ng; base += 32) {
-            const int g = base + lane;
-            const uint32_t v = g < ng ? T[g] : 0u;
-            uint32_t incl = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            if (g < ng) T[g] = carry + incl - v;
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        if (lane == 0) {
-            T[ng] = carry;
-            s_total = carry;
-        }
-    }
-    __syncthreads();
-    const bool local = s_total <= (uint32_t)buf_cap;
-    const uint32_t lt = (1u << lane) - 1u;
-    for (uint32_t rb = r0; rb < r1; rb += 32) {  // this warp's splats in rank order, 32 at a time
-        const uint32_t r = rb + lane;
-        int gx0 = 0, gy0 = 0, gw = 1, cnt = 0;
-        uint32_t idx = 0;
-        if (r < r1) {
-            int gx1, gy1;
-            if (band_groups(gg, __ldg(&a.rrect[r]), gx0, gx1, gy0, gy1)) {
-                gw = gx1 - gx0 + 1;
-                cnt = gw * (gy1 - gy0 + 1);
-            }
-            idx = __ldg(&a.sval[r]);
-        }
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        const int excl = incl - cnt;
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        for (int e0 = 0; e0 < total; e0 += 32) {
-            const int e = e0 + lane;
-            // owning splat of entry e: the last lane whose exclusive offset is <= e
-            int pos = 0;
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const int t = __shfl_sync(0xffffffffu, excl, (pos + step) & 31);
-                if (pos + step < 32 && t <= e) pos += step;
-            }
-            const int o_excl = __shfl_sync(0xffffffffu, excl, pos);
-            const int o_gx0 = __shfl_sync(0xffffffffu, gx0, pos);
-            const int o_gy0 = __shfl_sync(0xffffffffu, gy0, pos);
-            const int o_gw = __shfl_sync(0xffffffffu, gw, pos);
-            const uint32_t o_idx = __shfl_sync(0xffffffffu, idx, pos);
-            const bool valid = e < total;
-            const int k = e - o_excl;
-            const int dy = __float2int_rz(((float)k + 0.5f) * __frcp_rn((float)o_gw)), dx = k - dy * o_gw;
-            const int yy = o_gy0 + dy, xx = o_gx0 + dx;
-            const int g = valid ? yy * gx + xx : -1 - lane;  // invalid lanes match nobody
-            const uint32_t peers = __match_any_sync(0xffffffffu, g);
-            if (valid) {
-                const int di = yy * pitch + xx;
-                const uint32_t before = (uint32_t)Dw[di];
-                const uint32_t kk = before + (uint32_t)__popc(peers & lt);
-                if ((31 - __clz(peers)) == lane) Dw[di] = (int)(before + (uint32_t)__popc(peers));
-                if (local) {
-                    const uint32_t p = T[g] + kk;
-                    buf[p] = o_idx;
-                    gbuf[p] = (uint16_t)g;
-                } else {
-                    a.list[G0[g] + kk] = o_idx;
-                }
-            }
-            __syncwarp();  // cursor updates visible to the next step
-        }
-    }
-    if (!local) return;
-    __syncthreads();
-    // flush: entry i of the sorted buffer belongs to group gbuf[i]; runs land contiguously
-    const uint32_t tot = s_total;
-    for (uint32_t i = threadIdx.x; i < tot; i += blockDim.x) {
-        const uint32_t g = gbuf[i];
-        a.list[G0[g] + (i - T[g])] = buf[i];
-    }
-}
-
 __global__ void lists_readback_kernel(const uint32_t* __restrict__ sorted_idx,
                                       const uint32_t* __restrict__ offsets, int n_groups,
                                       DevProjected proj, GroupGeom gg, tgs_group_entry* out) {
@@ -457,24 +502,13 @@ void launch_unit_order(const uint32_t* offsets, const uint32_t* feedback, int n_
     if (n_units > 0) unit_order_kernel<<<1, 1024, 0, st>>>(offsets, feedback, n_units, per_group, order);
 }
 
-// Warps per count/scatter block: one difference array ((rows+1) x (cols+1) ints) per warp in
-// shared memory, plus (scatter) three per-group arrays and the local entry buffer.
-static int bin_warps_per_block(const GroupGeom& gg) {
-    const size_t per_warp = (size_t)(gg.band_gy1 - gg.band_gy0 + 1) * (gg.groups_x + 1) * 4;
-    int w = kMaxBinWarps;
-    while (w > 1 && per_warp * w > 96u * 1024u) w >>= 1;
-    return w;
+int bin_chunks(int) { return kRowChunks; }
+size_t bin_hist1_elems(const GroupGeom& gg) { return (size_t)std::max(1, gg.band_gy1 - gg.band_gy0) * kRowChunks; }
+size_t bin_hist2_elems(const GroupGeom& gg, uint32_t capacity) {
+    const size_t rows = (size_t)std::max(1, gg.band_gy1 - gg.band_gy0);
+    return (size_t)gg.groups_x * (rows + capacity / kSegLen + 1);
 }
-
-int bin_chunks(int n_groups) {
-    // chunks (= blocks) so that a chunk's entries usually fit the scatter's shared buffer, with
-    // the [group][chunk] matrix kept within ~16M entries
-    long c = 148L * 24;
-    while (c > 148 && (long)n_groups * c > (16L << 20)) c /= 2;
-    return (int)c;
-}
-size_t bin_hist_elems(int n_groups) { return (size_t)std::max(1, n_groups) * bin_chunks(n_groups); }
-size_t bin_bsum_elems(int n_groups) { return (bin_hist_elems(n_groups) + kScanTile - 1) / kScanTile + 1; }
+size_t bin_meta_elems(const GroupGeom& gg) { return 3 * (size_t)(gg.band_gy1 - gg.band_gy0 + 1) + 1; }
 
 size_t scan_tmp_elems(size_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
 
@@ -489,24 +523,46 @@ void launch_exclusive_scan(uint32_t* x, size_t n, uint32_t* tmp, cudaStream_t st
 
 void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     const GroupGeom& gg = a.gg;
-    const int wpb = bin_warps_per_block(gg);
-    const int ng = gg.n_groups_band;
-    const size_t diff_smem = (size_t)wpb * (gg.band_gy1 - gg.band_gy0 + 1) * (gg.groups_x + 1) * sizeof(int);
-    const size_t arrays = (size_t)(3 * ng + 1) * sizeof(uint32_t);
-    const size_t max_smem = 220u * 1024u;
-    // local buffer: u32 entry + u16 group per slot
-    const int buf_cap = (int)std::max<long>(0, ((long)max_smem - (long)(diff_smem + arrays)) / 6) & ~1;
-    const size_t scatter_smem = diff_smem + arrays + (size_t)buf_cap * 6;
-    const size_t n = (size_t)ng * a.n_chunks;
-    const int scan_blocks = (int)((n + kScanTile - 1) / kScanTile);
+    const int rows = gg.band_gy1 - gg.band_gy0, gx = gg.groups_x;
     const int gblocks = std::max(1, std::min(148 * 8, (max_visible + 255) / 256));
     rank_gather_kernel<<<gblocks, 256, 0, st>>>(a);
-    cudaFuncSetAttribute(group_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diff_smem);
-    group_count_kernel<<<a.n_chunks, wpb * 32, diff_smem, st>>>(a);
-    launch_exclusive_scan(a.hist, n, a.bsum, st);
-    offsets_kernel<<<(ng + 256) / 256, 256, 0, st>>>(a, scan_blocks);
-    cudaFuncSetAttribute(group_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scatter_smem);
-    group_scatter_kernel<<<a.n_chunks, wpb * 32, scatter_smem, st>>>(a, buf_cap);
+    // level 1
+    const size_t n1 = bin_hist1_elems(gg);
+    rows_count_kernel<<<kRowChunks / kBinWarps, kBinWarps * 32, kBinWarps * (rows + 1) * sizeof(int), st>>>(a);
+    uint32_t* tmp = a.bsum;
+    launch_exclusive_scan(a.hist1, n1, tmp, st);
+    const uint32_t* scan1_total = tmp + (n1 + kScanTile - 1) / kScanTile;
+    rows_meta_kernel<<<1, 32, 0, st>>>(a, scan1_total);
+    const int kr = (rows + 31) / 32, b1 = kRowChunks / kBinWarps, t1 = kBinWarps * 32;
+    if (kr <= 1)
+        rows_place_kernel<1><<<b1, t1, 0, st>>>(a);
+    else if (kr <= 2)
+        rows_place_kernel<2><<<b1, t1, 0, st>>>(a);
+    else if (kr <= 4)
+        rows_place_kernel<4><<<b1, t1, 0, st>>>(a);
+    else if (kr <= 8)
+        rows_place_kernel<8><<<b1, t1, 0, st>>>(a);
+    else
+        rows_place_kernel<16><<<b1, t1, 0, st>>>(a);
+    // level 2
+    const size_t n2 = bin_hist2_elems(gg, a.capacity);
+    cudaMemsetAsync(a.hist2, 0, n2 * sizeof(uint32_t), st);
+    const size_t max_seg = (size_t)rows + a.capacity / kSegLen + 1;
+    const int qblocks = (int)std::max<size_t>(1, std::min<size_t>(148 * 8, (max_seg + kBinWarps - 1) / kBinWarps));
+    cols_count_kernel<<<qblocks, kBinWarps * 32, kBinWarps * (gx + 1) * sizeof(int), st>>>(a);
+    launch_exclusive_scan(a.hist2, n2, tmp, st);
+    offsets_kernel<<<(gg.n_groups_band + 256) / 256, 256, 0, st>>>(a, n2);
+    const int kc = (gx + 31) / 32, t2 = kBinWarps * 32;
+    if (kc <= 1)
+        cols_place_kernel<1><<<qblocks, t2, 0, st>>>(a);
+    else if (kc <= 2)
+        cols_place_kernel<2><<<qblocks, t2, 0, st>>>(a);
+    else if (kc <= 4)
+        cols_place_kernel<4><<<qblocks, t2, 0, st>>>(a);
+    else if (kc <= 8)
+        cols_place_kernel<8><<<qblocks, t2, 0, st>>>(a);
+    else
+        cols_place_kernel<16><<<qblocks, t2, 0, st>>>(a);
 }
 
 void launch_lists_readback(const uint32_t* sorted_idx, const uint32_t* offsets, int n_groups,

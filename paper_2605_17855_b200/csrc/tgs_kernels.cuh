@@ -41,22 +41,24 @@ int radix_sort(SortBuffers& b, const uint32_t* count_first, const uint32_t* coun
 // of the reference (binning.cpp:86-91) entry for entry.
 struct BinArgs {
     const uint32_t* visible;     // &fc->visible (device-side count)
-    const uint32_t* sval;        // rank -> compacted index
-    const uint2* rect;           // compacted index -> tile rect
+    const uint32_t* sval;        // rank -> splat index
+    const uint2* rect;           // splat index -> tile rect
     uint2* rrect;                // rank -> tile rect
     GroupGeom gg;
-    uint32_t* hist;              // [n_groups_band * n_chunks], scanned in place
+    uint32_t* hist1;             // [rows * bin_chunks] level-1 counts, scanned in place
+    uint32_t* hist2;             // [bin_hist2_elems] level-2 counts, scanned in place
+    uint32_t* meta;              // [bin_meta_elems] row starts / segment layout
     uint32_t* bsum;              // scan block sums (+1)
+    uint2* rowlist;              // [capacity] group-row entries (splat index, gx0 | gx1 << 16)
     uint32_t* offsets;           // [n_groups_band + 1]
-    uint32_t* list;              // [capacity] output entries (compacted indices)
+    uint32_t* list;              // [capacity] output entries (splat indices)
     FrameCounters* fc;
     uint32_t capacity;
-    int n_chunks;
 };
-// chunk count for a band of n_groups groups (bounds the histogram matrix)
-int bin_chunks(int n_groups);
-size_t bin_hist_elems(int n_groups);   // hist length
-size_t bin_bsum_elems(int n_groups);   // bsum length
+int bin_chunks(int n_groups);                                      // level-1 chunks
+size_t bin_hist1_elems(const GroupGeom& gg);
+size_t bin_hist2_elems(const GroupGeom& gg, uint32_t capacity);
+size_t bin_meta_elems(const GroupGeom& gg);
 void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st);
 // In-place exclusive scan of n u32 (multi-block: block sums, one-block scan of the sums, apply);
 // tmp holds scan_tmp_elems(n) u32 and ends with the total.

@@ -31,7 +31,8 @@ namespace {
 
 constexpr int kBinWarps = 8;          // warps per binning block (one chunk / segment per warp)
 constexpr int kRowChunks = 148 * 32;  // level-1 chunks (contiguous rank ranges, one warp each)
-constexpr uint32_t kSegLen = 2048;    // level-2 segment: row-list entries per warp
+constexpr uint32_t kSegLen = 256;     // level-2 segment: row-list entries per warp
+constexpr int kStage2 = 2048;         // level-2 per-warp output staging (entries)
 constexpr int kScanItems = 16;        // per thread in the hist scan
 constexpr int kScanBlock = 256;
 constexpr int kScanTile = kScanItems * kScanBlock;
@@ -66,6 +67,10 @@ __global__ void __launch_bounds__(256) rank_gather_kernel(BinArgs a) {
     const uint32_t n = *a.visible;
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
         a.rrect[r] = __ldg(&a.rect[__ldg(&a.sval[r])]);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
 }
 
 // ---- level 1: splats -> group-row lists -----------------------------------------------------
@@ -153,14 +158,24 @@ __global__ void rows_meta_kernel(BinArgs a, const uint32_t* __restrict__ scan1_t
     }
 }
 
+// Bits [lo, hi] of the 32-row/column block k (bit i = row/column 32k + i); 0 if disjoint.
+__device__ __forceinline__ uint32_t range_mask(int lo, int hi, int k) {
+    const int a = max(lo - 32 * k, 0), b = min(hi - 32 * k, 31);
+    return a > b ? 0u : (0xffffffffu >> (31 - b)) & (0xffffffffu << a);
+}
+
 // Row placement: lane l owns group rows l, l + 32, ... (KR per lane) with register cursors; the
-// warp walks its chunk 32 splats at a time and, splat by splat (broadcast), every owning lane
-// appends the splat to its row.  Rank order within a row follows from the walk order.
+// warp walks its chunk 32 splats at a time, each lane staging its splat (index, column range, row
+// masks) in shared memory, then splat by splat (broadcast read) every owning lane appends the splat
+// to its row.  Rank order within a row follows from the walk order.
 template <int KR>
 __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
+    constexpr int NW = (KR + 2 + 3) / 4;  // uint4 words per staged splat: idx, xp, KR masks
+    __shared__ uint4 stage[kBinWarps][32][NW];
     if (a.fc->overflow) return;
     const int rows = a.gg.band_gy1 - a.gg.band_gy0;
-    const int lane = threadIdx.x & 31, chunk = blockIdx.x * kBinWarps + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, chunk = blockIdx.x * kBinWarps + wib;
+    const uint32_t lanebit = 1u << lane;
     uint32_t r0, r1;
     chunk_range(*a.visible, kRowChunks, chunk, r0, r1);
     uint32_t cur[KR];
@@ -169,28 +184,41 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
         const int y = lane + 32 * k;
         cur[k] = y < rows ? a.hist1[(size_t)y * kRowChunks + chunk] : 0u;
     }
+    uint32_t* my = reinterpret_cast<uint32_t*>(&stage[wib][lane][0]);
     for (uint32_t rb = r0; rb < r1; rb += 32) {
         const uint32_t r = rb + lane;
-        uint32_t yp = 0xffffu, xp = 0u, idx = 0u;  // yp: gy0 | gy1 << 16 (empty: lo > hi)
+        uint32_t w[4 * NW];
+#pragma unroll
+        for (int i = 0; i < 4 * NW; ++i) w[i] = 0u;
         if (r < r1) {
             int gx0, gx1, gy0, gy1;
+            w[0] = __ldg(&a.sval[r]);
             if (band_groups(a.gg, __ldg(&a.rrect[r]), gx0, gx1, gy0, gy1)) {
-                yp = (uint32_t)gy0 | ((uint32_t)gy1 << 16);
-                xp = (uint32_t)gx0 | ((uint32_t)gx1 << 16);
-            }
-            idx = __ldg(&a.sval[r]);
-        }
-#pragma unroll 8
-        for (int j = 0; j < 32; ++j) {
-            const uint32_t yj = __shfl_sync(0xffffffffu, yp, j);
-            const uint32_t xj = __shfl_sync(0xffffffffu, xp, j);
-            const uint32_t ij = __shfl_sync(0xffffffffu, idx, j);
-            const int lo = (int)(yj & 0xffffu), hi = (int)(yj >> 16);
+                w[1] = (uint32_t)gx0 | ((uint32_t)gx1 << 16);
 #pragma unroll
-            for (int k = 0; k < KR; ++k) {
-                const int y = lane + 32 * k;
-                if (y >= lo && y <= hi) a.rowlist[cur[k]++] = make_uint2(ij, xj);
+                for (int k = 0; k < KR; ++k) w[2 + k] = range_mask(gy0, gy1, k);
             }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < NW; ++i)
+            reinterpret_cast<uint4*>(my)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+        __syncwarp();
+        const int n = (int)min(32u, r1 - rb);
+#pragma unroll 4
+        for (int j = 0; j < n; ++j) {
+            uint32_t v[4 * NW];
+#pragma unroll
+            for (int i = 0; i < NW; ++i) {
+                const uint4 q = stage[wib][j][i];
+                v[4 * i] = q.x;
+                v[4 * i + 1] = q.y;
+                v[4 * i + 2] = q.z;
+                v[4 * i + 3] = q.w;
+            }
+#pragma unroll
+            for (int k = 0; k < KR; ++k)
+                if (v[2 + k] & lanebit) a.rowlist[cur[k]++] = make_uint2(v[0], v[1]);
         }
     }
 }
@@ -256,12 +284,13 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_count_kernel(BinArgs a) {
 // offsets[g] = global start of group g = its segment-0 slot of the scanned hist2 (an empty row has
 // a zero-size block: the slot holds the running total, which is its groups' start); offsets[ng] =
 // total.  Overflow: every list empty.
-__global__ void offsets_kernel(BinArgs a, size_t hist2_len) {
+__global__ void offsets_kernel(BinArgs a) {
     const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x, ng = a.gg.n_groups_band;
     const uint32_t* nsegp = a.meta + rows + 1;
     const uint32_t* rowbase2 = a.meta + 2 * rows + 2;
     const bool over = a.fc->overflow != 0u;
     const uint32_t total = a.fc->n_entries;
+    const size_t hist2_len = rowbase2[rows];
     for (int g = blockIdx.x * blockDim.x + threadIdx.x; g <= ng; g += gridDim.x * blockDim.x) {
         uint32_t v = 0;
         if (!over) {
@@ -278,46 +307,135 @@ __global__ void offsets_kernel(BinArgs a, size_t hist2_len) {
 }
 
 // Group placement: lane l owns columns l, l + 32, ... (KC per lane) of the segment's row with
-// register cursors; entries are broadcast one by one and every owning column appends the splat.
+// cursors; each lane stages one row entry (splat index + its column masks) in shared memory, then
+// entries are read back one by one (broadcast) and every owning column appends the splat.  The
+// segment's (column, segment) runs are assembled in a per-warp shared buffer (column-major, i.e.
+// the order of their global slots) and flushed run by run with coalesced stores; a segment whose
+// output exceeds the buffer appends straight to global memory.
 template <int KC>
 __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
+    constexpr int NW = (KC + 1 + 3) / 4;  // uint4 words per staged entry: idx, KC masks
+    __shared__ uint4 stage[kBinWarps][32][NW];
+    extern __shared__ uint32_t sout[];    // [kBinWarps][kStage2]
     if (a.fc->overflow) return;
     const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint32_t lanebit = 1u << lane;
     const uint32_t* rowstart = a.meta;
     const uint32_t* nsegp = a.meta + rows + 1;
     const uint32_t* rowbase2 = a.meta + 2 * rows + 2;
-    const uint32_t nq = nsegp[rows];
-    for (uint32_t q = blockIdx.x * kBinWarps + (threadIdx.x >> 5); q < nq; q += gridDim.x * kBinWarps) {
+    const uint32_t nq = nsegp[rows], h2 = rowbase2[rows], total = a.fc->n_entries;
+    uint32_t* my = reinterpret_cast<uint32_t*>(&stage[wib][lane][0]);
+    uint32_t* out = sout + wib * kStage2;
+    uint32_t* list = a.list;
+    for (uint32_t q = blockIdx.x * kBinWarps + wib; q < nq; q += gridDim.x * kBinWarps) {
         int y;
         uint32_t s;
         seg_locate(nsegp, rows, q, y, s);
         const uint32_t nseg = nsegp[y + 1] - nsegp[y];
         const uint32_t e0 = rowstart[y] + s * kSegLen, e1 = min(rowstart[y + 1], e0 + kSegLen);
-        uint32_t cur[KC];
+        uint32_t gpos[KC], cnt[KC], pos[KC];
+        uint32_t carry = 0;
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
             const int x = lane + 32 * k;
-            cur[k] = x < gx ? a.hist2[rowbase2[y] + (uint32_t)x * nseg + s] : 0u;
+            const uint32_t i = rowbase2[y] + (uint32_t)x * nseg + s;
+            gpos[k] = x < gx ? a.hist2[i] : 0u;
+            cnt[k] = x < gx ? (i + 1 < h2 ? a.hist2[i + 1] : total) - gpos[k] : 0u;
+            uint32_t incl = cnt[k];  // local run starts: exclusive prefix over columns
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            pos[k] = carry + incl - cnt[k];
+            carry += __shfl_sync(0xffffffffu, incl, 31);
         }
+        const bool staged = carry <= (uint32_t)kStage2;
+#pragma unroll
+        for (int k = 0; k < KC; ++k)
+            if (!staged) pos[k] = gpos[k];
+        // placement: shared-memory byte addresses when staged, global slots otherwise (two loops,
+        // so the staged one is plain STS with 32-bit addresses)
+        uint32_t sa[KC];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) sa[k] = smem_u32(out + pos[k]);
         for (uint32_t eb = e0; eb < e1; eb += 32) {
             const uint32_t e = eb + lane;
-            uint2 v = make_uint2(0u, 0xffffu);  // empty column range (lo > hi)
-            if (e < e1) v = __ldg(&a.rowlist[e]);
-#pragma unroll 8
-            for (int j = 0; j < 32; ++j) {
-                const uint32_t ij = __shfl_sync(0xffffffffu, v.x, j);
-                const uint32_t xj = __shfl_sync(0xffffffffu, v.y, j);
-                const int lo = (int)(xj & 0xffffu), hi = (int)(xj >> 16);
+            uint32_t w[4 * NW];
 #pragma unroll
-                for (int k = 0; k < KC; ++k) {
-                    const int x = lane + 32 * k;
-                    if (x >= lo && x <= hi) a.list[cur[k]++] = ij;
+            for (int i = 0; i < 4 * NW; ++i) w[i] = 0u;
+            if (e < e1) {
+                const uint2 v = __ldg(&a.rowlist[e]);
+                w[0] = v.x;
+#pragma unroll
+                for (int k = 0; k < KC; ++k) w[1 + k] = range_mask((int)(v.y & 0xffffu), (int)(v.y >> 16), k);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < NW; ++i)
+                reinterpret_cast<uint4*>(my)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+            __syncwarp();
+            const int n = (int)min(32u, e1 - eb);
+            if (staged) {
+#pragma unroll 4
+                for (int j = 0; j < n; ++j) {
+                    uint32_t v[4 * NW];
+#pragma unroll
+                    for (int i = 0; i < NW; ++i) {
+                        const uint4 qv = stage[wib][j][i];
+                        v[4 * i] = qv.x;
+                        v[4 * i + 1] = qv.y;
+                        v[4 * i + 2] = qv.z;
+                        v[4 * i + 3] = qv.w;
+                    }
+#pragma unroll
+                    for (int k = 0; k < KC; ++k)
+                        if (v[1 + k] & lanebit) {
+                            asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa[k]), "r"(v[0]) : "memory");
+                            sa[k] += 4u;
+                        }
+                }
+            } else {
+#pragma unroll 4
+                for (int j = 0; j < n; ++j) {
+                    uint32_t v[4 * NW];
+#pragma unroll
+                    for (int i = 0; i < NW; ++i) {
+                        const uint4 qv = stage[wib][j][i];
+                        v[4 * i] = qv.x;
+                        v[4 * i + 1] = qv.y;
+                        v[4 * i + 2] = qv.z;
+                        v[4 * i + 3] = qv.w;
+                    }
+#pragma unroll
+                    for (int k = 0; k < KC; ++k)
+                        if (v[1 + k] & lanebit) list[pos[k]++] = v[0];
                 }
             }
         }
+#pragma unroll
+        for (int k = 0; k < KC; ++k)
+            if (staged) pos[k] = (sa[k] - smem_u32(out)) >> 2;
+        if (staged) {
+            __syncwarp();
+            // flush: run of column x = out[pos0_x, +cnt_x) -> list[gpos_x, ...), coalesced
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                const uint32_t p0 = pos[k] - cnt[k];
+                for (int l = 0; l < 32; ++l) {
+                    const uint32_t c = __shfl_sync(0xffffffffu, cnt[k], l);
+                    if (c == 0u) continue;
+                    const uint32_t src = __shfl_sync(0xffffffffu, p0, l);
+                    const uint32_t g0 = __shfl_sync(0xffffffffu, gpos[k], l);
+                    for (uint32_t i = lane; i < c; i += 32) list[g0 + i] = out[src + i];
+                }
+            }
+            __syncwarp();
+        }
     }
 }
+
 // ---- exclusive scan of hist (block sums -> single-block scan of the sums -> apply) ----------
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& total) {
     __shared__ uint32_t wsum[kScanBlock / 32];
@@ -351,7 +469,13 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& t
 }
 
 __global__ void __launch_bounds__(kScanBlock) scan_reduce_kernel(const uint32_t* __restrict__ x, size_t n,
+                                                                 const uint32_t* __restrict__ n_dev,
                                                                  uint32_t* __restrict__ bsum) {
+    if (n_dev) n = min(n, (size_t)*n_dev);
+    if ((size_t)blockIdx.x * kScanTile >= n) {  // past the device-side length: empty block
+        if (threadIdx.x == 0) bsum[blockIdx.x] = 0u;
+        return;
+    }
     const size_t base = (size_t)blockIdx.x * kScanTile + (size_t)threadIdx.x * kScanItems;
     uint32_t s = 0;
 #pragma unroll
@@ -412,7 +536,10 @@ __global__ void __launch_bounds__(1024) scan_small_kernel(uint32_t* data, int n)
 }
 
 __global__ void __launch_bounds__(kScanBlock) scan_apply_kernel(uint32_t* __restrict__ x, size_t n,
+                                                                const uint32_t* __restrict__ n_dev,
                                                                 const uint32_t* __restrict__ bsum) {
+    if (n_dev) n = min(n, (size_t)*n_dev);
+    if ((size_t)blockIdx.x * kScanTile >= n) return;
     const size_t base = (size_t)blockIdx.x * kScanTile + (size_t)threadIdx.x * kScanItems;
     uint32_t v[kScanItems], s = 0;
 #pragma unroll
@@ -512,13 +639,13 @@ size_t bin_meta_elems(const GroupGeom& gg) { return 3 * (size_t)(gg.band_gy1 - g
 
 size_t scan_tmp_elems(size_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
 
-void launch_exclusive_scan(uint32_t* x, size_t n, uint32_t* tmp, cudaStream_t st) {
+void launch_exclusive_scan(uint32_t* x, size_t n, uint32_t* tmp, cudaStream_t st, const uint32_t* n_dev) {
     const int blocks = (int)((n + kScanTile - 1) / kScanTile);
     if (blocks == 0) return;
-    scan_reduce_kernel<<<blocks, kScanBlock, 0, st>>>(x, n, tmp);
+    scan_reduce_kernel<<<blocks, kScanBlock, 0, st>>>(x, n, n_dev, tmp);
     cudaMemsetAsync(tmp + blocks, 0, sizeof(uint32_t), st);
     scan_small_kernel<<<1, 1024, 0, st>>>(tmp, blocks + 1);
-    scan_apply_kernel<<<blocks, kScanBlock, 0, st>>>(x, n, tmp);
+    scan_apply_kernel<<<blocks, kScanBlock, 0, st>>>(x, n, n_dev, tmp);
 }
 
 void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
@@ -530,7 +657,7 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     const size_t n1 = bin_hist1_elems(gg);
     rows_count_kernel<<<kRowChunks / kBinWarps, kBinWarps * 32, kBinWarps * (rows + 1) * sizeof(int), st>>>(a);
     uint32_t* tmp = a.bsum;
-    launch_exclusive_scan(a.hist1, n1, tmp, st);
+    launch_exclusive_scan(a.hist1, n1, tmp, st, nullptr);
     const uint32_t* scan1_total = tmp + (n1 + kScanTile - 1) / kScanTile;
     rows_meta_kernel<<<1, 32, 0, st>>>(a, scan1_total);
     const int kr = (rows + 31) / 32, b1 = kRowChunks / kBinWarps, t1 = kBinWarps * 32;
@@ -546,23 +673,28 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
         rows_place_kernel<16><<<b1, t1, 0, st>>>(a);
     // level 2
     const size_t n2 = bin_hist2_elems(gg, a.capacity);
-    cudaMemsetAsync(a.hist2, 0, n2 * sizeof(uint32_t), st);
+    const uint32_t* h2_len = a.meta + 3 * rows + 2;  // rowbase2[rows]: device-side hist2 length
     const size_t max_seg = (size_t)rows + a.capacity / kSegLen + 1;
     const int qblocks = (int)std::max<size_t>(1, std::min<size_t>(148 * 8, (max_seg + kBinWarps - 1) / kBinWarps));
     cols_count_kernel<<<qblocks, kBinWarps * 32, kBinWarps * (gx + 1) * sizeof(int), st>>>(a);
-    launch_exclusive_scan(a.hist2, n2, tmp, st);
-    offsets_kernel<<<(gg.n_groups_band + 256) / 256, 256, 0, st>>>(a, n2);
+    launch_exclusive_scan(a.hist2, n2, tmp, st, h2_len);
+    offsets_kernel<<<(gg.n_groups_band + 256) / 256, 256, 0, st>>>(a);
     const int kc = (gx + 31) / 32, t2 = kBinWarps * 32;
+    const size_t so = (size_t)kBinWarps * kStage2 * sizeof(uint32_t);
+    auto launch = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)so);
+        kern<<<qblocks, t2, so, st>>>(a);
+    };
     if (kc <= 1)
-        cols_place_kernel<1><<<qblocks, t2, 0, st>>>(a);
+        launch(cols_place_kernel<1>);
     else if (kc <= 2)
-        cols_place_kernel<2><<<qblocks, t2, 0, st>>>(a);
+        launch(cols_place_kernel<2>);
     else if (kc <= 4)
-        cols_place_kernel<4><<<qblocks, t2, 0, st>>>(a);
+        launch(cols_place_kernel<4>);
     else if (kc <= 8)
-        cols_place_kernel<8><<<qblocks, t2, 0, st>>>(a);
+        launch(cols_place_kernel<8>);
     else
-        cols_place_kernel<16><<<qblocks, t2, 0, st>>>(a);
+        launch(cols_place_kernel<16>);
 }
 
 void launch_lists_readback(const uint32_t* sorted_idx, const uint32_t* offsets, int n_groups,

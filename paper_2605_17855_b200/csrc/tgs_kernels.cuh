@@ -63,7 +63,8 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st);
 // In-place exclusive scan of n u32 (multi-block: block sums, one-block scan of the sums, apply);
 // tmp holds scan_tmp_elems(n) u32 and ends with the total.
 size_t scan_tmp_elems(size_t n);
-void launch_exclusive_scan(uint32_t* x, size_t n, uint32_t* tmp, cudaStream_t st);
+// n_dev (optional): device-side length <= n; elements past it are left untouched.
+void launch_exclusive_scan(uint32_t* x, size_t n, uint32_t* tmp, cudaStream_t st, const uint32_t* n_dev = nullptr);
 
 // Sorted lists -> GroupEntry array (for readback).
 void launch_lists_readback(const uint32_t* sorted_idx, const uint32_t* offsets, int n_groups,

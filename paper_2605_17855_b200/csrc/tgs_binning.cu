@@ -32,7 +32,8 @@ namespace {
 constexpr int kBinWarps = 8;          // warps per binning block (one chunk / segment per warp)
 constexpr int kRowChunks = 148 * 32;  // level-1 chunks (contiguous rank ranges, one warp each)
 constexpr uint32_t kSegLen = 256;     // level-2 segment: row-list entries per warp
-constexpr int kStage2 = 2048;         // level-2 per-warp output staging (entries)
+constexpr uint32_t kSegGroup = kBinWarps;  // level-2 block: consecutive segments of one row
+constexpr int kStage2 = 16384;        // level-2 per-block output staging (entries)
 constexpr int kScanItems = 16;        // per thread in the hist scan
 constexpr int kScanBlock = 256;
 constexpr int kScanTile = kScanItems * kScanBlock;
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_count_kernel(BinArgs a) {
 //   meta[0 .. rows]            row list starts (meta[rows] = row entries)
 //   meta[M1 .. M1 + rows]      prefix of segments per row (M1 = rows + 1; last = segments)
 //   meta[M2 .. M2 + rows]      prefix of gx * segments per row: hist2 block of row y (M2 = 2 rows + 2)
+//   meta[M3 .. M3 + rows]      prefix of segment groups (kSegGroup segments) per row (M3 = 3 rows + 3)
 __global__ void rows_meta_kernel(BinArgs a, const uint32_t* __restrict__ scan1_total) {
     const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x, lane = threadIdx.x;
     uint32_t* rowstart = a.meta;
@@ -131,6 +133,7 @@ __global__ void rows_meta_kernel(BinArgs a, const uint32_t* __restrict__ scan1_t
         else
             a.fc->n_sort = total;
     }
+    uint32_t* ngrp = a.meta + 3 * rows + 3;
     uint32_t cs = 0, cb = 0;
     for (int base = 0; base <= rows; base += 32) {
         const int y = base + lane;
@@ -142,19 +145,25 @@ __global__ void rows_meta_kernel(BinArgs a, const uint32_t* __restrict__ scan1_t
         } else if (y == rows) {
             start = *scan1_total;
         }
-        uint32_t inc_s = nseg;
+        const uint32_t ng = (nseg + kSegGroup - 1u) / kSegGroup;
+        uint32_t inc_s = nseg, inc_g = ng;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t t = __shfl_up_sync(0xffffffffu, inc_s, o);
-            if (lane >= o) inc_s += t;
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc_g, o);
+            if (lane >= o) {
+                inc_s += t;
+                inc_g += u;
+            }
         }
         if (y <= rows) {
             rowstart[y] = start;
             nsegp[y] = cs + inc_s - nseg;
             rowbase2[y] = (cs + inc_s - nseg) * (uint32_t)gx;
+            ngrp[y] = cb + inc_g - ng;
         }
         cs += __shfl_sync(0xffffffffu, inc_s, 31);
-        (void)cb;
+        cb += __shfl_sync(0xffffffffu, inc_g, 31);
     }
 }
 
@@ -306,17 +315,18 @@ __global__ void offsets_kernel(BinArgs a) {
     }
 }
 
-// Group placement: lane l owns columns l, l + 32, ... (KC per lane) of the segment's row with
-// cursors; each lane stages one row entry (splat index + its column masks) in shared memory, then
-// entries are read back one by one (broadcast) and every owning column appends the splat.  The
-// segment's (column, segment) runs are assembled in a per-warp shared buffer (column-major, i.e.
-// the order of their global slots) and flushed run by run with coalesced stores; a segment whose
-// output exceeds the buffer appends straight to global memory.
+// Group placement.  A block takes kSegGroup consecutive segments of one row (one per warp); in the
+// [row][column][segment] layout the block's runs of column x are consecutive, i.e. one contiguous
+// global range.  Lane l of every warp owns columns l, l + 32, ... (KC per lane); each lane stages
+// one row entry (splat index + column masks) in shared memory, then entries are read back one by
+// one (broadcast) and every owning column appends the splat — into the block's shared output
+// buffer at (column run start + the warp's offset in it), so that every column run is then
+// flushed with coalesced stores.  A block whose output exceeds the buffer writes to global slots.
 template <int KC>
 __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
     constexpr int NW = (KC + 1 + 3) / 4;  // uint4 words per staged entry: idx, KC masks
     __shared__ uint4 stage[kBinWarps][32][NW];
-    extern __shared__ uint32_t sout[];    // [kBinWarps][kStage2]
+    extern __shared__ uint32_t sout[];    // [kStage2]
     if (a.fc->overflow) return;
     const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -324,115 +334,113 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
     const uint32_t* rowstart = a.meta;
     const uint32_t* nsegp = a.meta + rows + 1;
     const uint32_t* rowbase2 = a.meta + 2 * rows + 2;
-    const uint32_t nq = nsegp[rows], h2 = rowbase2[rows], total = a.fc->n_entries;
+    const uint32_t* ngrp = a.meta + 3 * rows + 3;
+    const uint32_t nu = ngrp[rows], h2 = rowbase2[rows], total = a.fc->n_entries;
     uint32_t* my = reinterpret_cast<uint32_t*>(&stage[wib][lane][0]);
-    uint32_t* out = sout + wib * kStage2;
     uint32_t* list = a.list;
-    for (uint32_t q = blockIdx.x * kBinWarps + wib; q < nq; q += gridDim.x * kBinWarps) {
+    const uint32_t out0 = smem_u32(sout);
+    auto h2at = [&](uint32_t i) { return i < h2 ? a.hist2[i] : total; };
+    for (uint32_t u = blockIdx.x; u < nu; u += gridDim.x) {
         int y;
-        uint32_t s;
-        seg_locate(nsegp, rows, q, y, s);
+        uint32_t sg;
+        seg_locate(ngrp, rows, u, y, sg);
         const uint32_t nseg = nsegp[y + 1] - nsegp[y];
-        const uint32_t e0 = rowstart[y] + s * kSegLen, e1 = min(rowstart[y + 1], e0 + kSegLen);
-        uint32_t gpos[KC], cnt[KC], pos[KC];
+        const uint32_t s0 = sg * kSegGroup, s1 = min(nseg, s0 + kSegGroup), s = s0 + (uint32_t)wib;
+        const bool active = s < s1;
+        // per column: block run [base, end) globally, local start P (prefix over columns)
+        uint32_t base[KC], len[KC], P[KC], pos[KC];
         uint32_t carry = 0;
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
             const int x = lane + 32 * k;
-            const uint32_t i = rowbase2[y] + (uint32_t)x * nseg + s;
-            gpos[k] = x < gx ? a.hist2[i] : 0u;
-            cnt[k] = x < gx ? (i + 1 < h2 ? a.hist2[i + 1] : total) - gpos[k] : 0u;
-            uint32_t incl = cnt[k];  // local run starts: exclusive prefix over columns
+            const uint32_t i0 = rowbase2[y] + (uint32_t)x * nseg;
+            base[k] = x < gx ? h2at(i0 + s0) : 0u;
+            len[k] = x < gx ? h2at(i0 + s1) - base[k] : 0u;
+            pos[k] = (x < gx && active) ? h2at(i0 + s) : 0u;  // global slot of this warp's run
+            uint32_t incl = len[k];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += t;
             }
-            pos[k] = carry + incl - cnt[k];
+            P[k] = carry + incl - len[k];
             carry += __shfl_sync(0xffffffffu, incl, 31);
         }
-        const bool staged = carry <= (uint32_t)kStage2;
-#pragma unroll
-        for (int k = 0; k < KC; ++k)
-            if (!staged) pos[k] = gpos[k];
-        // placement: shared-memory byte addresses when staged, global slots otherwise (two loops,
-        // so the staged one is plain STS with 32-bit addresses)
+        const bool staged = carry <= (uint32_t)kStage2;  // block-uniform
         uint32_t sa[KC];
 #pragma unroll
-        for (int k = 0; k < KC; ++k) sa[k] = smem_u32(out + pos[k]);
-        for (uint32_t eb = e0; eb < e1; eb += 32) {
-            const uint32_t e = eb + lane;
-            uint32_t w[4 * NW];
+        for (int k = 0; k < KC; ++k) sa[k] = out0 + 4u * (P[k] + (pos[k] - base[k]));
+        if (active) {
+            const uint32_t e0 = rowstart[y] + s * kSegLen, e1 = min(rowstart[y + 1], e0 + kSegLen);
+            for (uint32_t eb = e0; eb < e1; eb += 32) {
+                const uint32_t e = eb + lane;
+                uint32_t w[4 * NW];
 #pragma unroll
-            for (int i = 0; i < 4 * NW; ++i) w[i] = 0u;
-            if (e < e1) {
-                const uint2 v = __ldg(&a.rowlist[e]);
-                w[0] = v.x;
-#pragma unroll
-                for (int k = 0; k < KC; ++k) w[1 + k] = range_mask((int)(v.y & 0xffffu), (int)(v.y >> 16), k);
-            }
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < NW; ++i)
-                reinterpret_cast<uint4*>(my)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
-            __syncwarp();
-            const int n = (int)min(32u, e1 - eb);
-            if (staged) {
-#pragma unroll 4
-                for (int j = 0; j < n; ++j) {
-                    uint32_t v[4 * NW];
-#pragma unroll
-                    for (int i = 0; i < NW; ++i) {
-                        const uint4 qv = stage[wib][j][i];
-                        v[4 * i] = qv.x;
-                        v[4 * i + 1] = qv.y;
-                        v[4 * i + 2] = qv.z;
-                        v[4 * i + 3] = qv.w;
-                    }
+                for (int i = 0; i < 4 * NW; ++i) w[i] = 0u;
+                if (e < e1) {
+                    const uint2 v = __ldg(&a.rowlist[e]);
+                    w[0] = v.x;
 #pragma unroll
                     for (int k = 0; k < KC; ++k)
-                        if (v[1 + k] & lanebit) {
-                            asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa[k]), "r"(v[0]) : "memory");
-                            sa[k] += 4u;
+                        w[1 + k] = range_mask((int)(v.y & 0xffffu), (int)(v.y >> 16), k);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < NW; ++i)
+                    reinterpret_cast<uint4*>(my)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+                __syncwarp();
+                const int n = (int)min(32u, e1 - eb);
+                if (staged) {
+#pragma unroll 4
+                    for (int j = 0; j < n; ++j) {
+                        uint32_t v[4 * NW];
+#pragma unroll
+                        for (int i = 0; i < NW; ++i) {
+                            const uint4 qv = stage[wib][j][i];
+                            v[4 * i] = qv.x;
+                            v[4 * i + 1] = qv.y;
+                            v[4 * i + 2] = qv.z;
+                            v[4 * i + 3] = qv.w;
                         }
-                }
-            } else {
-#pragma unroll 4
-                for (int j = 0; j < n; ++j) {
-                    uint32_t v[4 * NW];
 #pragma unroll
-                    for (int i = 0; i < NW; ++i) {
-                        const uint4 qv = stage[wib][j][i];
-                        v[4 * i] = qv.x;
-                        v[4 * i + 1] = qv.y;
-                        v[4 * i + 2] = qv.z;
-                        v[4 * i + 3] = qv.w;
+                        for (int k = 0; k < KC; ++k)
+                            if (v[1 + k] & lanebit) {
+                                asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa[k]), "r"(v[0]) : "memory");
+                                sa[k] += 4u;
+                            }
                     }
+                } else {
+#pragma unroll 4
+                    for (int j = 0; j < n; ++j) {
+                        uint32_t v[4 * NW];
 #pragma unroll
-                    for (int k = 0; k < KC; ++k)
-                        if (v[1 + k] & lanebit) list[pos[k]++] = v[0];
+                        for (int i = 0; i < NW; ++i) {
+                            const uint4 qv = stage[wib][j][i];
+                            v[4 * i] = qv.x;
+                            v[4 * i + 1] = qv.y;
+                            v[4 * i + 2] = qv.z;
+                            v[4 * i + 3] = qv.w;
+                        }
+#pragma unroll
+                        for (int k = 0; k < KC; ++k)
+                            if (v[1 + k] & lanebit) list[pos[k]++] = v[0];
+                    }
                 }
             }
         }
-#pragma unroll
-        for (int k = 0; k < KC; ++k)
-            if (staged) pos[k] = (sa[k] - smem_u32(out)) >> 2;
         if (staged) {
-            __syncwarp();
-            // flush: run of column x = out[pos0_x, +cnt_x) -> list[gpos_x, ...), coalesced
+            __syncthreads();
+            // flush: warp w copies the block runs of columns w, w + 8, ... (coalesced)
 #pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                const uint32_t p0 = pos[k] - cnt[k];
-                for (int l = 0; l < 32; ++l) {
-                    const uint32_t c = __shfl_sync(0xffffffffu, cnt[k], l);
-                    if (c == 0u) continue;
-                    const uint32_t src = __shfl_sync(0xffffffffu, p0, l);
-                    const uint32_t g0 = __shfl_sync(0xffffffffu, gpos[k], l);
-                    for (uint32_t i = lane; i < c; i += 32) list[g0 + i] = out[src + i];
+            for (int k = 0; k < KC; ++k)
+                for (int l = wib; l < 32; l += kBinWarps) {
+                    const uint32_t c = __shfl_sync(0xffffffffu, len[k], l);
+                    const uint32_t src = __shfl_sync(0xffffffffu, P[k], l);
+                    const uint32_t dst = __shfl_sync(0xffffffffu, base[k], l);
+                    for (uint32_t i = lane; i < c; i += 32) list[dst + i] = sout[src + i];
                 }
-            }
-            __syncwarp();
         }
+        __syncthreads();
     }
 }
 
@@ -635,7 +643,7 @@ size_t bin_hist2_elems(const GroupGeom& gg, uint32_t capacity) {
     const size_t rows = (size_t)std::max(1, gg.band_gy1 - gg.band_gy0);
     return (size_t)gg.groups_x * (rows + capacity / kSegLen + 1);
 }
-size_t bin_meta_elems(const GroupGeom& gg) { return 3 * (size_t)(gg.band_gy1 - gg.band_gy0 + 1) + 1; }
+size_t bin_meta_elems(const GroupGeom& gg) { return 4 * (size_t)(gg.band_gy1 - gg.band_gy0 + 1) + 1; }
 
 size_t scan_tmp_elems(size_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
 
@@ -680,7 +688,7 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     launch_exclusive_scan(a.hist2, n2, tmp, st, h2_len);
     offsets_kernel<<<(gg.n_groups_band + 256) / 256, 256, 0, st>>>(a);
     const int kc = (gx + 31) / 32, t2 = kBinWarps * 32;
-    const size_t so = (size_t)kBinWarps * kStage2 * sizeof(uint32_t);
+    const size_t so = (size_t)kStage2 * sizeof(uint32_t);
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)so);
         kern<<<qblocks, t2, so, st>>>(a);

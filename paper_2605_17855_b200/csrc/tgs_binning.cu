@@ -30,7 +30,8 @@ namespace tgs {
 namespace {
 
 constexpr int kBinWarps = 8;          // warps per binning block (one chunk / segment per warp)
-constexpr int kRowChunks = 148 * 32;  // level-1 chunks (contiguous rank ranges, one warp each)
+constexpr int kRowChunks = 148 * 128;  // level-1 chunks (contiguous rank ranges, one warp each)
+constexpr int kStage1 = 8192;          // level-1 per-block output staging (row entries)
 constexpr uint32_t kSegLen = 256;     // level-2 segment: row-list entries per warp
 constexpr uint32_t kSegGroup = kBinWarps;  // level-2 block: consecutive segments of one row
 constexpr int kStage2 = 16384;        // level-2 per-block output staging (entries)
@@ -173,26 +174,51 @@ __device__ __forceinline__ uint32_t range_mask(int lo, int hi, int k) {
     return a > b ? 0u : (0xffffffffu >> (31 - b)) & (0xffffffffu << a);
 }
 
-// Row placement: lane l owns group rows l, l + 32, ... (KR per lane) with register cursors; the
-// warp walks its chunk 32 splats at a time, each lane staging its splat (index, column range, row
-// masks) in shared memory, then splat by splat (broadcast read) every owning lane appends the splat
-// to its row.  Rank order within a row follows from the walk order.
+// Row placement.  A block takes kBinWarps consecutive chunks (one per warp); in the [row][chunk]
+// layout the block's runs of row y are consecutive, i.e. one contiguous global range.  Lane l of
+// every warp owns rows l, l + 32, ... (KR per lane); the warp walks its chunk 32 splats at a time,
+// each lane staging its splat (index, column range, row masks) in shared memory, then splat by
+// splat (broadcast read) every owning lane appends the splat to its row — into the block's shared
+// output buffer at (row run start + the warp's offset in it); every row run is then flushed with
+// coalesced stores.  A block whose output exceeds the buffer writes to global slots directly.
 template <int KR>
 __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
     constexpr int NW = (KR + 2 + 3) / 4;  // uint4 words per staged splat: idx, xp, KR masks
     __shared__ uint4 stage[kBinWarps][32][NW];
+    extern __shared__ uint2 sout1[];      // [kStage1]
     if (a.fc->overflow) return;
     const int rows = a.gg.band_gy1 - a.gg.band_gy0;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, chunk = blockIdx.x * kBinWarps + wib;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int c0 = blockIdx.x * kBinWarps, chunk = c0 + wib;
     const uint32_t lanebit = 1u << lane;
+    const uint32_t total = a.meta[rows];  // row entries
+    auto h1at = [&](int y, int c) {       // scanned hist1 at (row y, chunk c); c may be kRowChunks
+        const size_t i = (size_t)y * kRowChunks + c;
+        return i < (size_t)rows * kRowChunks ? a.hist1[i] : total;
+    };
     uint32_t r0, r1;
     chunk_range(*a.visible, kRowChunks, chunk, r0, r1);
-    uint32_t cur[KR];
+    uint32_t base[KR], len[KR], P[KR], pos[KR], carry = 0;
 #pragma unroll
     for (int k = 0; k < KR; ++k) {
         const int y = lane + 32 * k;
-        cur[k] = y < rows ? a.hist1[(size_t)y * kRowChunks + chunk] : 0u;
+        base[k] = y < rows ? h1at(y, c0) : 0u;
+        len[k] = y < rows ? h1at(y, c0 + kBinWarps) - base[k] : 0u;
+        pos[k] = y < rows ? h1at(y, chunk) : 0u;
+        uint32_t incl = len[k];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        P[k] = carry + incl - len[k];
+        carry += __shfl_sync(0xffffffffu, incl, 31);
     }
+    const bool staged = carry <= (uint32_t)kStage1;  // block-uniform
+    const uint32_t out0 = smem_u32(sout1);
+    uint32_t sa[KR];
+#pragma unroll
+    for (int k = 0; k < KR; ++k) sa[k] = out0 + 8u * (P[k] + (pos[k] - base[k]));
     uint32_t* my = reinterpret_cast<uint32_t*>(&stage[wib][lane][0]);
     for (uint32_t rb = r0; rb < r1; rb += 32) {
         const uint32_t r = rb + lane;
@@ -214,21 +240,54 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
             reinterpret_cast<uint4*>(my)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         __syncwarp();
         const int n = (int)min(32u, r1 - rb);
+        if (staged) {
 #pragma unroll 4
-        for (int j = 0; j < n; ++j) {
-            uint32_t v[4 * NW];
+            for (int j = 0; j < n; ++j) {
+                uint32_t v[4 * NW];
 #pragma unroll
-            for (int i = 0; i < NW; ++i) {
-                const uint4 q = stage[wib][j][i];
-                v[4 * i] = q.x;
-                v[4 * i + 1] = q.y;
-                v[4 * i + 2] = q.z;
-                v[4 * i + 3] = q.w;
+                for (int i = 0; i < NW; ++i) {
+                    const uint4 q = stage[wib][j][i];
+                    v[4 * i] = q.x;
+                    v[4 * i + 1] = q.y;
+                    v[4 * i + 2] = q.z;
+                    v[4 * i + 3] = q.w;
+                }
+#pragma unroll
+                for (int k = 0; k < KR; ++k)
+                    if (v[2 + k] & lanebit) {
+                        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(sa[k]), "r"(v[0]), "r"(v[1]) : "memory");
+                        sa[k] += 8u;
+                    }
             }
+        } else {
+#pragma unroll 4
+            for (int j = 0; j < n; ++j) {
+                uint32_t v[4 * NW];
 #pragma unroll
-            for (int k = 0; k < KR; ++k)
-                if (v[2 + k] & lanebit) a.rowlist[cur[k]++] = make_uint2(v[0], v[1]);
+                for (int i = 0; i < NW; ++i) {
+                    const uint4 q = stage[wib][j][i];
+                    v[4 * i] = q.x;
+                    v[4 * i + 1] = q.y;
+                    v[4 * i + 2] = q.z;
+                    v[4 * i + 3] = q.w;
+                }
+#pragma unroll
+                for (int k = 0; k < KR; ++k)
+                    if (v[2 + k] & lanebit) a.rowlist[pos[k]++] = make_uint2(v[0], v[1]);
+            }
         }
+    }
+    if (staged) {
+        __syncthreads();
+        // flush: warp w copies the block runs of rows w, w + 8, ... (coalesced)
+#pragma unroll
+        for (int k = 0; k < KR; ++k)
+            for (int l = wib; l < 32; l += kBinWarps) {
+                const uint32_t c = __shfl_sync(0xffffffffu, len[k], l);
+                const uint32_t src = __shfl_sync(0xffffffffu, P[k], l);
+                const uint32_t dst = __shfl_sync(0xffffffffu, base[k], l);
+                for (uint32_t i = lane; i < c; i += 32) a.rowlist[dst + i] = sout1[src + i];
+            }
     }
 }
 
@@ -669,16 +728,21 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     const uint32_t* scan1_total = tmp + (n1 + kScanTile - 1) / kScanTile;
     rows_meta_kernel<<<1, 32, 0, st>>>(a, scan1_total);
     const int kr = (rows + 31) / 32, b1 = kRowChunks / kBinWarps, t1 = kBinWarps * 32;
+    const size_t so1 = (size_t)kStage1 * sizeof(uint2);
+    auto launch1 = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)so1);
+        kern<<<b1, t1, so1, st>>>(a);
+    };
     if (kr <= 1)
-        rows_place_kernel<1><<<b1, t1, 0, st>>>(a);
+        launch1(rows_place_kernel<1>);
     else if (kr <= 2)
-        rows_place_kernel<2><<<b1, t1, 0, st>>>(a);
+        launch1(rows_place_kernel<2>);
     else if (kr <= 4)
-        rows_place_kernel<4><<<b1, t1, 0, st>>>(a);
+        launch1(rows_place_kernel<4>);
     else if (kr <= 8)
-        rows_place_kernel<8><<<b1, t1, 0, st>>>(a);
+        launch1(rows_place_kernel<8>);
     else
-        rows_place_kernel<16><<<b1, t1, 0, st>>>(a);
+        launch1(rows_place_kernel<16>);
     // level 2
     const size_t n2 = bin_hist2_elems(gg, a.capacity);
     const uint32_t* h2_len = a.meta + 3 * rows + 2;  // rowbase2[rows]: device-side hist2 length

@@ -32,9 +32,9 @@ namespace {
 constexpr int kBinWarps = 8;          // warps per binning block (one chunk / segment per warp)
 constexpr int kRowChunks = 148 * 128;  // level-1 chunks (contiguous rank ranges, one warp each)
 constexpr int kStage1 = 8192;          // level-1 per-block output staging (row entries)
-constexpr uint32_t kSegLen = 256;     // level-2 segment: row-list entries per warp
-constexpr uint32_t kSegGroup = kBinWarps;  // level-2 block: consecutive segments of one row
-constexpr int kStage2 = 16384;        // level-2 per-block output staging (entries)
+constexpr uint32_t kSliceLen = 128;   // level-2 placement: row-list entries per warp
+constexpr uint32_t kSegLen = kSliceLen * kBinWarps;  // level-2 segment: one count warp / one placement block
+constexpr int kStage2 = 8192;         // level-2 per-block output staging (entries)
 constexpr int kScanItems = 16;        // per thread in the hist scan
 constexpr int kScanBlock = 256;
 constexpr int kScanTile = kScanItems * kScanBlock;
@@ -120,7 +120,6 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_count_kernel(BinArgs a) {
 //   meta[0 .. rows]            row list starts (meta[rows] = row entries)
 //   meta[M1 .. M1 + rows]      prefix of segments per row (M1 = rows + 1; last = segments)
 //   meta[M2 .. M2 + rows]      prefix of gx * segments per row: hist2 block of row y (M2 = 2 rows + 2)
-//   meta[M3 .. M3 + rows]      prefix of segment groups (kSegGroup segments) per row (M3 = 3 rows + 3)
 __global__ void rows_meta_kernel(BinArgs a, const uint32_t* __restrict__ scan1_total) {
     const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x, lane = threadIdx.x;
     uint32_t* rowstart = a.meta;
@@ -134,8 +133,7 @@ __global__ void rows_meta_kernel(BinArgs a, const uint32_t* __restrict__ scan1_t
         else
             a.fc->n_sort = total;
     }
-    uint32_t* ngrp = a.meta + 3 * rows + 3;
-    uint32_t cs = 0, cb = 0;
+    uint32_t cs = 0;
     for (int base = 0; base <= rows; base += 32) {
         const int y = base + lane;
         uint32_t start = 0, nseg = 0;
@@ -146,25 +144,18 @@ __global__ void rows_meta_kernel(BinArgs a, const uint32_t* __restrict__ scan1_t
         } else if (y == rows) {
             start = *scan1_total;
         }
-        const uint32_t ng = (nseg + kSegGroup - 1u) / kSegGroup;
-        uint32_t inc_s = nseg, inc_g = ng;
+        uint32_t inc_s = nseg;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t t = __shfl_up_sync(0xffffffffu, inc_s, o);
-            const uint32_t u = __shfl_up_sync(0xffffffffu, inc_g, o);
-            if (lane >= o) {
-                inc_s += t;
-                inc_g += u;
-            }
+            if (lane >= o) inc_s += t;
         }
         if (y <= rows) {
             rowstart[y] = start;
             nsegp[y] = cs + inc_s - nseg;
             rowbase2[y] = (cs + inc_s - nseg) * (uint32_t)gx;
-            ngrp[y] = cb + inc_g - ng;
         }
         cs += __shfl_sync(0xffffffffu, inc_s, 31);
-        cb += __shfl_sync(0xffffffffu, inc_g, 31);
     }
 }
 
@@ -374,18 +365,19 @@ __global__ void offsets_kernel(BinArgs a) {
     }
 }
 
-// Group placement.  A block takes kSegGroup consecutive segments of one row (one per warp); in the
-// [row][column][segment] layout the block's runs of column x are consecutive, i.e. one contiguous
-// global range.  Lane l of every warp owns columns l, l + 32, ... (KC per lane); each lane stages
-// one row entry (splat index + column masks) in shared memory, then entries are read back one by
-// one (broadcast) and every owning column appends the splat — into the block's shared output
-// buffer at (column run start + the warp's offset in it), so that every column run is then
-// flushed with coalesced stores.  A block whose output exceeds the buffer writes to global slots.
+// Group placement.  A block takes one segment (kBinWarps slices of kSliceLen row entries, one per
+// warp); the segment's run of column x is one contiguous global range [base_x, base_x + len_x),
+// inside which warp w's part starts after the parts of warps < w (per-slice column counts, made
+// here in shared memory).  Lane l of every warp owns columns l, l + 32, ... (KC per lane); each
+// lane stages one row entry (splat index + column masks) in shared memory, then entries are read
+// back in batches (broadcast) and every owning column appends the splat — into the block's shared
+// output buffer, so that every column run is flushed with coalesced stores.  A block whose output
+// exceeds the buffer writes to global slots instead.
 template <int KC>
 __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
     constexpr int NW = (KC + 1 + 3) / 4;  // uint4 words per staged entry: idx, KC masks
     __shared__ uint4 stage[kBinWarps][32][NW];
-    extern __shared__ uint32_t sout[];    // [kStage2]
+    extern __shared__ uint32_t sout[];    // [kStage2] output, then [kBinWarps][gx + 1] slice counts
     if (a.fc->overflow) return;
     const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -393,29 +385,55 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
     const uint32_t* rowstart = a.meta;
     const uint32_t* nsegp = a.meta + rows + 1;
     const uint32_t* rowbase2 = a.meta + 2 * rows + 2;
-    const uint32_t* ngrp = a.meta + 3 * rows + 3;
-    const uint32_t nu = ngrp[rows], h2 = rowbase2[rows], total = a.fc->n_entries;
+    const uint32_t nq = nsegp[rows], h2 = rowbase2[rows], total = a.fc->n_entries;
+    int* cntw = reinterpret_cast<int*>(sout + kStage2);
+    int* D = cntw + wib * (gx + 1);
     uint32_t* my = reinterpret_cast<uint32_t*>(&stage[wib][lane][0]);
     uint32_t* list = a.list;
     const uint32_t out0 = smem_u32(sout);
     auto h2at = [&](uint32_t i) { return i < h2 ? a.hist2[i] : total; };
-    for (uint32_t u = blockIdx.x; u < nu; u += gridDim.x) {
+    for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
         int y;
-        uint32_t sg;
-        seg_locate(ngrp, rows, u, y, sg);
+        uint32_t s;
+        seg_locate(nsegp, rows, q, y, s);
         const uint32_t nseg = nsegp[y + 1] - nsegp[y];
-        const uint32_t s0 = sg * kSegGroup, s1 = min(nseg, s0 + kSegGroup), s = s0 + (uint32_t)wib;
-        const bool active = s < s1;
-        // per column: block run [base, end) globally, local start P (prefix over columns)
-        uint32_t base[KC], len[KC], P[KC], pos[KC];
-        uint32_t carry = 0;
+        const uint32_t se0 = rowstart[y] + s * kSegLen, se1 = min(rowstart[y + 1], se0 + kSegLen);
+        const uint32_t e0 = min(se1, se0 + (uint32_t)wib * kSliceLen), e1 = min(se1, e0 + kSliceLen);
+        // this warp's slice: per-column counts (difference array -> prefix)
+        for (int i = lane; i <= gx; i += 32) D[i] = 0;
+        __syncwarp();
+        for (uint32_t e = e0 + lane; e < e1; e += 32) {
+            const uint32_t xp = __ldg(&a.rowlist[e].y);
+            atomicAdd(&D[xp & 0xffffu], 1);
+            atomicAdd(&D[(xp >> 16) + 1], -1);
+        }
+        __syncwarp();
+        {
+            int run = 0;
+            for (int b0 = 0; b0 < gx; b0 += 32) {
+                const int x = b0 + lane;
+                int incl = x < gx ? D[x] : 0;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                if (x < gx) D[x] = run + incl;
+                run += __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+        __syncthreads();
+        // column runs of the segment: [base, base + len) globally, local start P; this warp's part
+        uint32_t base[KC], len[KC], P[KC], off[KC], carry = 0;
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
             const int x = lane + 32 * k;
-            const uint32_t i0 = rowbase2[y] + (uint32_t)x * nseg;
-            base[k] = x < gx ? h2at(i0 + s0) : 0u;
-            len[k] = x < gx ? h2at(i0 + s1) - base[k] : 0u;
-            pos[k] = (x < gx && active) ? h2at(i0 + s) : 0u;  // global slot of this warp's run
+            const uint32_t i0 = rowbase2[y] + (uint32_t)x * nseg + s;
+            base[k] = x < gx ? h2at(i0) : 0u;
+            len[k] = x < gx ? h2at(i0 + 1) - base[k] : 0u;
+            off[k] = 0u;
+            if (x < gx)
+                for (int w = 0; w < wib; ++w) off[k] += (uint32_t)cntw[w * (gx + 1) + x];
             uint32_t incl = len[k];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -426,70 +444,73 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
             carry += __shfl_sync(0xffffffffu, incl, 31);
         }
         const bool staged = carry <= (uint32_t)kStage2;  // block-uniform
-        uint32_t sa[KC];
+        uint32_t sa[KC], pos[KC];
 #pragma unroll
-        for (int k = 0; k < KC; ++k) sa[k] = out0 + 4u * (P[k] + (pos[k] - base[k]));
-        if (active) {
-            const uint32_t e0 = rowstart[y] + s * kSegLen, e1 = min(rowstart[y + 1], e0 + kSegLen);
-            for (uint32_t eb = e0; eb < e1; eb += 32) {
-                const uint32_t e = eb + lane;
-                uint32_t w[4 * NW];
+        for (int k = 0; k < KC; ++k) {
+            sa[k] = out0 + 4u * (P[k] + off[k]);
+            pos[k] = base[k] + off[k];
+        }
+        for (uint32_t eb = e0; eb < e1; eb += 32) {
+            const uint32_t e = eb + lane;
+            uint32_t w[4 * NW];
 #pragma unroll
-                for (int i = 0; i < 4 * NW; ++i) w[i] = 0u;
-                if (e < e1) {
-                    const uint2 v = __ldg(&a.rowlist[e]);
-                    w[0] = v.x;
+            for (int i = 0; i < 4 * NW; ++i) w[i] = 0u;
+            if (e < e1) {
+                const uint2 v = __ldg(&a.rowlist[e]);
+                w[0] = v.x;
 #pragma unroll
-                    for (int k = 0; k < KC; ++k)
-                        w[1 + k] = range_mask((int)(v.y & 0xffffu), (int)(v.y >> 16), k);
-                }
-                __syncwarp();
+                for (int k = 0; k < KC; ++k) w[1 + k] = range_mask((int)(v.y & 0xffffu), (int)(v.y >> 16), k);
+            }
+            __syncwarp();
 #pragma unroll
-                for (int i = 0; i < NW; ++i)
-                    reinterpret_cast<uint4*>(my)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
-                __syncwarp();
-                const int n = (int)min(32u, e1 - eb);
-                if (staged) {
-#pragma unroll 4
-                    for (int j = 0; j < n; ++j) {
-                        uint32_t v[4 * NW];
+            for (int i = 0; i < NW; ++i)
+                reinterpret_cast<uint4*>(my)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+            __syncwarp();
+            const int n = (int)min(32u, e1 - eb);
+            if (staged) {
+                // batches of 4 entries: all broadcast loads first, then the appends
+                for (int j0 = 0; j0 < n; j0 += 4) {
+                    uint32_t v[4][4 * NW];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
 #pragma unroll
                         for (int i = 0; i < NW; ++i) {
-                            const uint4 qv = stage[wib][j][i];
-                            v[4 * i] = qv.x;
-                            v[4 * i + 1] = qv.y;
-                            v[4 * i + 2] = qv.z;
-                            v[4 * i + 3] = qv.w;
+                            const uint4 qv = stage[wib][(j0 + t) & 31][i];
+                            v[t][4 * i] = qv.x;
+                            v[t][4 * i + 1] = qv.y;
+                            v[t][4 * i + 2] = qv.z;
+                            v[t][4 * i + 3] = qv.w;
                         }
 #pragma unroll
+                    for (int t = 0; t < 4; ++t)
+#pragma unroll
                         for (int k = 0; k < KC; ++k)
-                            if (v[1 + k] & lanebit) {
-                                asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa[k]), "r"(v[0]) : "memory");
+                            if ((v[t][1 + k] & lanebit) && j0 + t < n) {
+                                asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa[k]), "r"(v[t][0]) : "memory");
                                 sa[k] += 4u;
                             }
-                    }
-                } else {
+                }
+            } else {
 #pragma unroll 4
-                    for (int j = 0; j < n; ++j) {
-                        uint32_t v[4 * NW];
+                for (int j = 0; j < n; ++j) {
+                    uint32_t v[4 * NW];
 #pragma unroll
-                        for (int i = 0; i < NW; ++i) {
-                            const uint4 qv = stage[wib][j][i];
-                            v[4 * i] = qv.x;
-                            v[4 * i + 1] = qv.y;
-                            v[4 * i + 2] = qv.z;
-                            v[4 * i + 3] = qv.w;
-                        }
-#pragma unroll
-                        for (int k = 0; k < KC; ++k)
-                            if (v[1 + k] & lanebit) list[pos[k]++] = v[0];
+                    for (int i = 0; i < NW; ++i) {
+                        const uint4 qv = stage[wib][j][i];
+                        v[4 * i] = qv.x;
+                        v[4 * i + 1] = qv.y;
+                        v[4 * i + 2] = qv.z;
+                        v[4 * i + 3] = qv.w;
                     }
+#pragma unroll
+                    for (int k = 0; k < KC; ++k)
+                        if (v[1 + k] & lanebit) list[pos[k]++] = v[0];
                 }
             }
         }
+        __syncthreads();
         if (staged) {
-            __syncthreads();
-            // flush: warp w copies the block runs of columns w, w + 8, ... (coalesced)
+            // flush: warp w copies the runs of columns w, w + 8, ... (coalesced)
 #pragma unroll
             for (int k = 0; k < KC; ++k)
                 for (int l = wib; l < 32; l += kBinWarps) {
@@ -498,8 +519,8 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
                     const uint32_t dst = __shfl_sync(0xffffffffu, base[k], l);
                     for (uint32_t i = lane; i < c; i += 32) list[dst + i] = sout[src + i];
                 }
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
 
@@ -752,7 +773,7 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     launch_exclusive_scan(a.hist2, n2, tmp, st, h2_len);
     offsets_kernel<<<(gg.n_groups_band + 256) / 256, 256, 0, st>>>(a);
     const int kc = (gx + 31) / 32, t2 = kBinWarps * 32;
-    const size_t so = (size_t)kStage2 * sizeof(uint32_t);
+    const size_t so = (size_t)kStage2 * sizeof(uint32_t) + (size_t)kBinWarps * (gx + 1) * sizeof(int);
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)so);
         kern<<<qblocks, t2, so, st>>>(a);

@@ -76,6 +76,14 @@ constexpr int kPF = TGS_RASTER_PF;  // producer record batches in flight
 #define TGS_RASTER_DI 2
 #endif
 constexpr int kDI = TGS_RASTER_DI;  // producer list-index batches in flight beyond the records
+#ifndef TGS_RASTER_CTAS
+#define TGS_RASTER_CTAS 1
+#endif
+constexpr int kCtasPerSm = TGS_RASTER_CTAS;  // resident CTAs per SM (TMEM columns must fit)
+#ifndef TGS_RASTER_JB
+#define TGS_RASTER_JB 16
+#endif
+constexpr int kJB = TGS_RASTER_JB;  // accumulator columns (splats) per epilogue batch: 16 or 8
 #ifndef TGS_RASTER_PROF
 #define TGS_RASTER_PROF 0
 #endif
@@ -122,7 +130,6 @@ struct Smem {
     alignas(128) uint8_t a[kMT][128 * 32];   // pixel monomial rows (K-major, no swizzle)
     alignas(128) uint8_t b[kSS][kN * 32];    // splat coefficient rows
     float4 epi[kSS][kN];                     // r, g, b, min(alpha_clamp, opacity)
-    alignas(16) float cj[kSS][kN];           // min(alpha_clamp, opacity) again, packed for preload
     ChunkHeader hdr[kSS];
     alignas(16) int wdone[16];               // chunks each epilogue warp has completed
     alignas(16) int dead[16];                // (seq << 4) | retired member tiles, per warp
@@ -276,7 +283,7 @@ __device__ __forceinline__ UnitGeom unit_geom(const GroupGeom& gg, int unit) {
 }
 
 template <int SLOTS, int P2>
-__global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kernel(RasterArgs a) {
+__global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_tensor_kernel(RasterArgs a) {
     using R = Roles<SLOTS>;
     constexpr int kMT = R::kMT, SPW = R::kSPW, kEpiWarps = R::kEpiWarps;
     constexpr int kProd = R::kProd, kMma = R::kMma;
@@ -497,7 +504,6 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
                     if (keep && rank >= placed && rank - placed < room) {
                         write_row(sm, s, fill + rank - placed, r0, r1);
                         sm.epi[s][fill + rank - placed] = epi_v;
-                        sm.cj[s][fill + rank - placed] = epi_v.w;
                     }
                     if (nk - placed < room) {
                         fill += nk - placed;
@@ -626,11 +632,11 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
         // Accumulator registers.  A retired slot skips its tcgen05.ld and keeps stale finite
         // values, which never pass the D >= thr test because its thr is +inf.
-        uint32_t d[SPW][16];
+        uint32_t d[SPW][kJB];
 #pragma unroll
         for (int k = 0; k < SPW; ++k)
 #pragma unroll
-            for (int j = 0; j < 16; ++j) d[k][j] = 0u;
+            for (int j = 0; j < kJB; ++j) d[k][j] = 0u;
         for (uint32_t c = 0;; ++c) {
             const int s = (int)(c % kSS), ts = (int)(c % kTS);
             // this warp consumed the phase of chunk c - kTS itself, so the parity is unambiguous
@@ -678,28 +684,29 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
             const uint32_t stage_col = (uint32_t)(ts * kColsPerStage);
             if (nv > 0 && alive != 0u) {
 #pragma unroll 1
-                for (int j0 = 0; j0 < nv; j0 += 16) {
+                for (int j0 = 0; j0 < nv; j0 += kJB) {
 #pragma unroll
                     for (int k = 0; k < SPW; ++k)
-                        if (alive & (1u << k))
-                            ptx::tmem_ld16(lane_base + stage_col + (uint32_t)(mtile(k) * kN + j0), d[k]);
+                        if (alive & (1u << k)) {
+                            const uint32_t ta = lane_base + stage_col + (uint32_t)(mtile(k) * kN + j0);
+                            if constexpr (kJB == 16)
+                                ptx::tmem_ld16(ta, d[k]);
+                            else
+                                ptx::tmem_ld8(ta, d[k]);
+                        }
                     ptx::tmem_wait_ld();
-#ifdef TGS_RASTER_TMEM2  // experiment: double the TMEM read traffic
 #pragma unroll
-                    for (int k = 0; k < SPW; ++k) ptx::reg_fence16(d[k]);
-#pragma unroll
-                    for (int k = 0; k < SPW; ++k)
-                        if (alive & (1u << k))
-                            ptx::tmem_ld16(lane_base + stage_col + (uint32_t)(mtile(k) * kN + j0), d[k]);
-                    ptx::tmem_wait_ld();
-#endif
-#pragma unroll
-                    for (int k = 0; k < SPW; ++k) ptx::reg_fence16(d[k]);
-                    // Phase 1 (branch-free, 16 independent chains): which of the 16 splats reach
-                    // alpha_skip at any of this warp's pixels -> warp-uniform mask.
+                    for (int k = 0; k < SPW; ++k) {
+                        if constexpr (kJB == 16)
+                            ptx::reg_fence16(d[k]);
+                        else
+                            ptx::reg_fence8(d[k]);
+                    }
+                    // Phase 1 (branch-free, kJB independent chains): which of the batch's splats
+                    // reach alpha_skip at any of this warp's pixels -> warp-uniform mask.
                     uint32_t mk = 0;
 #pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) {
+                    for (int jj = 0; jj < kJB; ++jj) {
                         uint32_t p = 0;
 #pragma unroll
                         for (int k = 0; k < SPW; ++k) p |= fset_ge(__uint_as_float(d[k][jj]), thr[k]);
@@ -708,79 +715,37 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
                     const uint32_t M = __reduce_or_sync(0xffffffffu, mk);
                     if (TGS_RASTER_PROF) {
                         pf[2] += __popc(M);
-                        pf[3] += 16;
+                        pf[3] += kJB;
                     }
                     // Phase 2: ordered blend of the active splats (uniform branches).  A pixel blends
                     // splat j iff D >= log2(alpha_skip) and it had not terminated before j
                     // (T >= t_terminate): exactly alpha_of/blend/done (raster_scalar.hpp:40-55,
                     // raster_scalar.cpp:36-41) — the splat that drives T below t_terminate is
                     // blended, nothing after it.
+                    auto blend = [&](int jj, const uint32_t* dk) {
+                        const float4 ej = sm.epi[s][j0 + jj];
+#pragma unroll
+                        for (int k = 0; k < SPW; ++k) {
+                            const float dv = __uint_as_float(dk[k]);
+                            const float e2 = fminf(ej.w, ex2_approx(dv));
+                            const float al = (dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f;
+                            const float wt = T[k] * al;
+                            cr[k] = fmaf(wt, ej.x, cr[k]);
+                            cg[k] = fmaf(wt, ej.y, cg[k]);
+                            cb[k] = fmaf(wt, ej.z, cb[k]);
+                            T[k] -= wt;
+                        }
+                    };
                     if constexpr (P2 == 0) {
 #pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) {
-                        if (M & (1u << jj)) {
-                            const float4 ej = sm.epi[s][j0 + jj];
+                        for (int jj = 0; jj < kJB; ++jj)
+                            if (M & (1u << jj)) {
+                                uint32_t dk[SPW];
 #pragma unroll
-                            for (int k = 0; k < SPW; ++k) {
-                                const float dv = __uint_as_float(d[k][jj]);
-                                const float e2 = fminf(ej.w, ex2_approx(dv));
-                                const float al = (dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f;
-                                const float wt = T[k] * al;
-                                cr[k] = fmaf(wt, ej.x, cr[k]);
-                                cg[k] = fmaf(wt, ej.y, cg[k]);
-                                cb[k] = fmaf(wt, ej.z, cb[k]);
-                                T[k] -= wt;
+                                for (int k = 0; k < SPW; ++k) dk[k] = d[k][jj];
+                                blend(jj, dk);
                             }
-                        }
-                    }
-                    } else if constexpr (P2 == 2 || P2 == 3) {
-                        // alpha caps of the 16 splats preloaded (4 x LDS.128), so an active splat's
-                        // critical path starts at its D (already in registers); colours are loaded
-                        // inside the block and only needed at its end
-                        float cjv[16];
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) {
-                            const float4 t4 = *reinterpret_cast<const float4*>(&sm.cj[s][j0 + 4 * v]);
-                            cjv[4 * v] = t4.x;
-                            cjv[4 * v + 1] = t4.y;
-                            cjv[4 * v + 2] = t4.z;
-                            cjv[4 * v + 3] = t4.w;
-                        }
-                        auto blend = [&](int jj) {
-                            const float4 ej = sm.epi[s][j0 + jj];
-#pragma unroll
-                            for (int k = 0; k < SPW; ++k) {
-                                const float dv = __uint_as_float(d[k][jj]);
-                                const float e2 = fminf(cjv[jj], ex2_approx(dv));
-                                const float al = (dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f;
-                                const float wt = T[k] * al;
-                                cr[k] = fmaf(wt, ej.x, cr[k]);
-                                cg[k] = fmaf(wt, ej.y, cg[k]);
-                                cb[k] = fmaf(wt, ej.z, cb[k]);
-                                T[k] -= wt;
-                            }
-                        };
-                        if constexpr (P2 == 2) {
-#pragma unroll
-                            for (int jj = 0; jj < 16; ++jj)
-                                if (M & (1u << jj)) blend(jj);
-                        } else {
-                            uint32_t Mr = M;
-#pragma unroll 1
-                            while (Mr) {
-                                const int jj = __ffs(Mr) - 1;
-                                Mr &= Mr - 1u;
-                                switch (jj) {
-#define TGS_CASE(n) case n: blend(n); break;
-                                    TGS_CASE(0) TGS_CASE(1) TGS_CASE(2) TGS_CASE(3) TGS_CASE(4) TGS_CASE(5)
-                                    TGS_CASE(6) TGS_CASE(7) TGS_CASE(8) TGS_CASE(9) TGS_CASE(10) TGS_CASE(11)
-                                    TGS_CASE(12) TGS_CASE(13) TGS_CASE(14) TGS_CASE(15)
-#undef TGS_CASE
-                                    default: break;
-                                }
-                            }
-                        }
-                    } else if constexpr (P2 == 4) {
+                    } else {
                         // loop over the active splats only, re-reading each one's D column from TMEM
                         // (tcgen05.ld 32x32b.x1 per slot, next splat prefetched while this one blends)
                         uint32_t Mr = M;
@@ -806,18 +771,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
                                     for (int k = 0; k < SPW; ++k)
                                         ptx::tmem_ld1(cbase + (uint32_t)(mtile(k) * kN + jn), dn[k]);
                                 }
-                                const float4 ej = sm.epi[s][j0 + jj];
-#pragma unroll
-                                for (int k = 0; k < SPW; ++k) {
-                                    const float dv = __uint_as_float(dc[k]);
-                                    const float e2 = fminf(ej.w, ex2_approx(dv));
-                                    const float al = (dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f;
-                                    const float wt = T[k] * al;
-                                    cr[k] = fmaf(wt, ej.x, cr[k]);
-                                    cg[k] = fmaf(wt, ej.y, cg[k]);
-                                    cb[k] = fmaf(wt, ej.z, cb[k]);
-                                    T[k] -= wt;
-                                }
+                                blend(jj, dc);
                                 if (!more) break;
                                 ptx::tmem_wait_ld();
 #pragma unroll
@@ -826,32 +780,6 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, 1) raster_tensor_kerne
                                     dc[k] = dn[k];
                                 }
                                 jj = jn;
-                            }
-                        }
-                    } else {
-                        // loop over the active splats only; D comes from a thread-local copy
-                        // (one LDL per slot) instead of 16 unrolled uniform branches
-                        uint32_t dl[SPW][16];
-#pragma unroll
-                        for (int k = 0; k < SPW; ++k)
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) dl[k][j] = d[k][j];
-                        uint32_t Mr = M;
-#pragma unroll 1
-                        while (Mr) {
-                            const int jj = __ffs(Mr) - 1;
-                            Mr &= Mr - 1u;
-                            const float4 ej = sm.epi[s][j0 + jj];
-#pragma unroll
-                            for (int k = 0; k < SPW; ++k) {
-                                const float dv = __uint_as_float(dl[k][jj]);
-                                const float e2 = fminf(ej.w, ex2_approx(dv));
-                                const float al = (dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f;
-                                const float wt = T[k] * al;
-                                cr[k] = fmaf(wt, ej.x, cr[k]);
-                                cg[k] = fmaf(wt, ej.y, cg[k]);
-                                cb[k] = fmaf(wt, ej.z, cb[k]);
-                                T[k] -= wt;
                             }
                         }
                     }
@@ -930,7 +858,7 @@ void launch_t(const RasterArgs& a, int num_sms, cudaStream_t st) {
     const size_t smem = sizeof(Smem<SLOTS>);
     cudaFuncSetAttribute(raster_tensor_kernel<SLOTS, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int n_units = (SLOTS == 1 || a.gg.g == 2) ? a.gg.n_groups_band : a.gg.n_groups_band * 4;
-    int grid = num_sms;
+    int grid = num_sms * kCtasPerSm;
     if (grid > n_units) grid = n_units;
     if (grid > 0) raster_tensor_kernel<SLOTS, P2><<<grid, Roles<SLOTS>::kThreads, smem, st>>>(a);
 }

@@ -12,8 +12,9 @@ import sys
 
 STAGE = {"preprocess_kernel": "preprocess", "hist_kernel": "sort", "scatter_kernel": "sort",
          "scan_reduce_kernel": None, "scan_small_kernel": None, "scan_apply_kernel": None,
-         "rank_gather_kernel": "binning", "group_count_kernel": "binning", "offsets_kernel": "binning",
-         "group_scatter_kernel": "binning", "unit_order_kernel": "binning",
+         "rank_gather_kernel": "binning", "rows_count_kernel": "binning", "rows_meta_kernel": "binning",
+         "rows_place_kernel": "binning", "cols_count_kernel": "binning", "offsets_kernel": "binning",
+         "cols_place_kernel": "binning", "unit_order_kernel": "binning",
          "raster_tensor_kernel": "raster", "raster_scalar_kernel": "raster"}
 
 

@@ -224,8 +224,8 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     TGS_CUDA_OK(ctx->hist.ensure((h1 + h2 + hm) * 4));
     TGS_CUDA_OK(ctx->rowlist.ensure((size_t)cap * sizeof(uint2)));
     TGS_CUDA_OK(ctx->bsum.ensure(
-        std::max({scan_tmp_elems(h1), scan_tmp_elems(h2), scan_tmp_elems((size_t)256 * kSortBlocks)}) * 4));
-    TGS_CUDA_OK(ctx->ghist.ensure((size_t)256 * kSortBlocks * 4));
+        std::max({scan_tmp_elems(h1), scan_tmp_elems(h2), scan_tmp_elems(sort_scratch_elems((size_t)n_alloc))}) * 4));
+    TGS_CUDA_OK(ctx->ghist.ensure(sort_scratch_elems((size_t)n_alloc) * 4));
     TGS_CUDA_OK(ctx->offsets.ensure((size_t)(n_groups + 1) * 4));
     TGS_CUDA_OK(ctx->order.ensure((size_t)gg.tiles_x * gg.tiles_y * 4));
     TGS_CUDA_OK(ctx->ucost.ensure((size_t)gg.tiles_x * gg.tiles_y * 4));
@@ -262,7 +262,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     pb.ghist = ctx->ghist.as<uint32_t>();
     pb.scan_tmp = ctx->bsum.as<uint32_t>();
     // pass 1 covers all n splats and drops the culled ones (key kCulledKey); later passes the kept
-    const int pr = radix_sort(pb, &fc->n_input, &fc->visible, 32, true, false, s);
+    const int pr = radix_sort(pb, &fc->n_input, &fc->visible, 32, true, false, (size_t)n_alloc, s);
     TGS_CUDA_OK(cudaGetLastError());
 
     TGS_CUDA_OK(cudaEventRecord(ctx->ev[2], s));

@@ -22,16 +22,17 @@ void launch_preprocess(const PreprocessArgs& a, cudaStream_t st);
 struct SortBuffers {
     uint32_t* keys[2];
     uint32_t* vals[2];
-    uint32_t* ghist;      // [256 * kSortBlocks]
-    uint32_t* scan_tmp;   // scan_tmp_elems(256 * kSortBlocks) u32
+    uint32_t* ghist;      // sort_scratch_elems(max_items): [digit][tile] counts, scanned in place
+    uint32_t* scan_tmp;   // scan_tmp_elems(sort_scratch_elems(max_items))
 };
-constexpr int kSortBlocks = 592;  // 4 x 148 SMs
-// Sorts keys[0]/vals[0] by bits [0, nbits); the first pass covers *count_first items and, with
-// drop_first, drops keys equal to kCulledKey; later passes cover *count_rest items (device-side
-// counts).  Result in keys[r]/vals[r], r returned.  want_keys_last == false skips writing keys
-// in the last pass (only values are needed downstream).
+constexpr int kSortBlocks = 592;  // 4 x 148 SMs (grid of the binning/scan helpers)
+size_t sort_scratch_elems(size_t max_items);
+// Sorts keys[0]/vals[0] by bits [0, nbits) in 8-bit passes; the first pass covers
+// *count_first items and, with drop_first, drops keys equal to kCulledKey; later passes cover
+// *count_rest items (device-side counts, <= max_items).  Result in keys[r]/vals[r], r returned.
+// want_keys_last == false skips writing keys in the last pass (only values are needed downstream).
 int radix_sort(SortBuffers& b, const uint32_t* count_first, const uint32_t* count_rest, int nbits,
-               bool drop_first, bool want_keys_last, cudaStream_t st);
+               bool drop_first, bool want_keys_last, size_t max_items, cudaStream_t st);
 
 // ---- binning: stable counting sort of (group, rank) entries ---------------------------------
 // The splats are presorted by (depth, index) (rank order); every warp of the count/scatter grids

@@ -373,7 +373,9 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                 sm.hdr[s].live = (int)live;
                 sm.hdr[s].chunk = (int)c;
             }
+#ifndef TGS_RASTER_NOFENCE  // experiment only: timing without the proxy fence (unsafe)
             ptx::fence_proxy_async_smem();
+#endif
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&sm.full[s]);
             __syncwarp();
@@ -418,106 +420,106 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                 }
                 return r;
             };
-            // records of batches bi+1 .. bi+kPF in flight, list indices of the kDI batches after
-            // those (an index load has kDI iterations to land before its record gather is issued)
-            Rec q[kPF];
-#pragma unroll
-            for (int k = 0; k < kPF; ++k) q[k] = ld_rec(ld_idx((uint32_t)k));
-            uint32_t iq[kDI];
-#pragma unroll
-            for (int k = 0; k < kDI; ++k) iq[k] = ld_idx((uint32_t)(kPF + k));
-
+            // Software-pipelined gather without register moves of in-flight loads (a move would
+            // wait on the load's scoreboard): two record slots consumed in turn, each refilled two
+            // batches ahead right after use; list indices four batches ahead.
             uint32_t n_batches = 0;
-            for (uint32_t bi = 0; bi < nb; ++bi) {
+            // one batch: retire check, row build, ordered placement; true = unit finished
+            auto batch = [&](const Rec& cur) -> bool {
                 ++n_batches;
                 [[maybe_unused]] const long long tb0 = TGS_RASTER_PROF ? clock64() : 0;
-                const Rec cur = q[0];
+                    if (emitted) {  // drop member tiles whose pixels all terminated (all owner warps)
+                        uint32_t retired = 0xfu;
 #pragma unroll
-                for (int k = 0; k + 1 < kPF; ++k) q[k] = q[k + 1];
-                q[kPF - 1] = ld_rec(iq[0]);
+                        for (int w4 = 0; w4 < kEpiWarps; w4 += 4) {
+                            const int4 d = ld_volatile_v4(&sm.dead[w4]);
+                            const int dd[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
-                for (int k = 0; k + 1 < kDI; ++k) iq[k] = iq[k + 1];
-                iq[kDI - 1] = ld_idx(bi + kPF + kDI);
-                if (emitted) {  // drop member tiles whose pixels all terminated (all owner warps)
-                    uint32_t retired = 0xfu;
+                            for (int j = 0; j < 4; ++j) {
+                                const int w = w4 + j;
+                                const uint32_t owned =
+                                    kCompact ? 1u << (w >> 1) : ((1u << SPW) - 1u) << ((w >> 3) * SPW);
+                                retired &= ((dd[j] >> 4) == seq ? (uint32_t)(dd[j] & 15) : 0u) | (0xfu & ~owned);
+                            }
+                        }
+                        // sm.dead is written concurrently by the epilogue warps: take lane 0's view so
+                        // the whole warp makes the same decision (lanes may read it at different times)
+                        retired = __shfl_sync(0xffffffffu, retired, 0);
+                        live &= ~retired;
+                        if (live == 0u) return true;
+                    }
+                    [[maybe_unused]] const long long tb1 = TGS_RASTER_PROF ? clock64() : 0;
+                    bool keep = false;
+                    uint4 r0, r1;
+                    float4 epi_v = make_float4(0, 0, 0, 0);
+                    if (cur.idx != 0xffffffffu) {
+                        int x0, y0, x1, y1;
+                        tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1,
+                                  y1);
+                        uint32_t cover = 0;
 #pragma unroll
-                    for (int w4 = 0; w4 < kEpiWarps; w4 += 4) {
-                        const int4 d = ld_volatile_v4(&sm.dead[w4]);
-                        const int dd[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int w = w4 + j;
-                            const uint32_t owned =
-                                kCompact ? 1u << (w >> 1) : ((1u << SPW) - 1u) << ((w >> 3) * SPW);
-                            retired &= ((dd[j] >> 4) == seq ? (uint32_t)(dd[j] & 15) : 0u) | (0xfu & ~owned);
+                        for (int k = 0; k < SLOTS; ++k) {
+                            const int tx = ug.tx0 + (k & 1), ty = ug.ty0 + (k >> 1);
+                            if (tx >= x0 && tx <= x1 && ty >= y0 && ty <= y1) cover |= 1u << k;
+                        }
+                        cover &= live;
+                        const float cj = fminf(clampv, cur.co.y);
+                        if (cover != 0u && !(cj < skip)) {
+                            keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox,
+                                            oy, cover, r0, r1);
+                            epi_v = make_float4(cur.col.x, cur.col.y, cur.col.z, cj);
                         }
                     }
-                    // sm.dead is written concurrently by the epilogue warps: take lane 0's view so
-                    // the whole warp makes the same decision (lanes may read it at different times)
-                    retired = __shfl_sync(0xffffffffu, retired, 0);
-                    live &= ~retired;
-                    if (live == 0u) break;
-                }
-                [[maybe_unused]] const long long tb1 = TGS_RASTER_PROF ? clock64() : 0;
-                bool keep = false;
-                uint4 r0, r1;
-                float4 epi_v = make_float4(0, 0, 0, 0);
-                if (cur.idx != 0xffffffffu) {
-                    int x0, y0, x1, y1;
-                    tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1,
-                              y1);
-                    uint32_t cover = 0;
-#pragma unroll
-                    for (int k = 0; k < SLOTS; ++k) {
-                        const int tx = ug.tx0 + (k & 1), ty = ug.ty0 + (k >> 1);
-                        if (tx >= x0 && tx <= x1 && ty >= y0 && ty <= y1) cover |= 1u << k;
+                    const uint32_t km = __ballot_sync(0xffffffffu, keep);
+                    [[maybe_unused]] const long long tb2 = TGS_RASTER_PROF ? clock64() : 0;
+                    if (TGS_RASTER_PROF) {
+                        pf[2] += 1;
+                        sec[0] += tb1 - tb0;
+                        sec[1] += tb2 - tb1;
                     }
-                    cover &= live;
-                    const float cj = fminf(clampv, cur.co.y);
-                    if (cover != 0u && !(cj < skip)) {
-                        keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox,
-                                        oy, cover, r0, r1);
-                        epi_v = make_float4(cur.col.x, cur.col.y, cur.col.z, cj);
-                    }
-                }
-                const uint32_t km = __ballot_sync(0xffffffffu, keep);
-                [[maybe_unused]] const long long tb2 = TGS_RASTER_PROF ? clock64() : 0;
-                if (TGS_RASTER_PROF) {
-                    pf[2] += 1;
-                    sec[0] += tb1 - tb0;
-                    sec[1] += tb2 - tb1;
-                }
-                if (km == 0u) continue;
+                    if (km == 0u) return false;
 
-                const int nk = __popc(km);
-                const int rank = __popc(km & lt);
-                if (!open) {
-                    s = open_stage(c);
-                    open = true;
-                    fill = 0;
-                }
-                // place the kept ranks in order; a full chunk is published and the next one opened
-                // (a 32-lane batch spans at most 32 / kN + 1 chunks)
-                int placed = 0;
-                for (;;) {
-                    const int room = kN - fill;
-                    if (keep && rank >= placed && rank - placed < room) {
-                        write_row(sm, s, fill + rank - placed, r0, r1);
-                        sm.epi[s][fill + rank - placed] = epi_v;
+                    const int nk = __popc(km);
+                    const int rank = __popc(km & lt);
+                    if (!open) {
+                        s = open_stage(c);
+                        open = true;
+                        fill = 0;
                     }
-                    if (nk - placed < room) {
-                        fill += nk - placed;
-                        break;
+                    // place the kept ranks in order; a full chunk is published and the next one opened
+                    // (a 32-lane batch spans at most 32 / kN + 1 chunks)
+                    int placed = 0;
+                    for (;;) {
+                        const int room = kN - fill;
+                        if (keep && rank >= placed && rank - placed < room) {
+                            write_row(sm, s, fill + rank - placed, r0, r1);
+                            sm.epi[s][fill + rank - placed] = epi_v;
+                        }
+                        if (nk - placed < room) {
+                            fill += nk - placed;
+                            break;
+                        }
+                        publish(s, seq, unit, kN, live);
+                        ++c;
+                        emitted = true;
+                        s = open_stage(c);
+                        fill = 0;
+                        placed += room;
+                        if (placed == nk) break;
                     }
-                    publish(s, seq, unit, kN, live);
-                    ++c;
-                    emitted = true;
-                    s = open_stage(c);
-                    fill = 0;
-                    placed += room;
-                    if (placed == nk) break;
-                }
-                if (TGS_RASTER_PROF) sec[2] += clock64() - tb2;
+                    if (TGS_RASTER_PROF) sec[2] += clock64() - tb2;
+                    return false;
+            };
+            Rec qa = ld_rec(ld_idx(0)), qb = ld_rec(ld_idx(1));
+            uint32_t ia = ld_idx(2), ib = ld_idx(3);
+            for (uint32_t bi = 0; bi < nb; bi += 2) {
+                if (batch(qa)) break;
+                qa = ld_rec(ia);
+                ia = ld_idx(bi + 4);
+                if (bi + 1 >= nb) break;
+                if (batch(qb)) break;
+                qb = ld_rec(ib);
+                ib = ld_idx(bi + 5);
             }
             // close the unit: pad and publish the partial chunk (or an empty one so the
             // epilogue still writes the unit's pixels)
@@ -592,6 +594,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                 if (lane == 0) printf("MMA header mismatch: expected chunk %d found %d (seq %d)\n", (int)c, hch, hseq);
                 __trap();
             }
+            [[maybe_unused]] const long long ti0 = TGS_RASTER_PROF ? clock64() : 0;
             if (hseq >= 0 && hnv > 0) {
                 const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[s][0]), 128, 256);
                 const uint32_t dcol = tmem + (uint32_t)(ts * kColsPerStage);
@@ -605,6 +608,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                 ptx::mbar_arrive(&sm.tfull[ts]);
             }
             __syncwarp();
+            if (TGS_RASTER_PROF) pf[3] += clock64() - ti0;
             if (hseq < 0) break;
         }
     } else {
@@ -705,6 +709,10 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                     // Phase 1 (branch-free, kJB independent chains): which of the batch's splats
                     // reach alpha_skip at any of this warp's pixels -> warp-uniform mask.
                     uint32_t mk = 0;
+#ifdef TGS_RASTER_NOEPI  // experiment: skip the epilogue's compute (wrong images)
+                    if (nv >= 0) {
+                    } else
+#endif
 #pragma unroll
                     for (int jj = 0; jj < kJB; ++jj) {
                         uint32_t p = 0;
@@ -844,9 +852,9 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
             }
             const double n = (double)gridDim.x;
             printf("RPROF ctas %d | producer total %.0f wait %.0f batches %.0f | mma total %.0f wfull %.0f wtmem %.0f | "
-                   "epi/warp total %.0f wtfull %.0f | active blocks %.3f of %.0f | cta max %llu unit max %llu "
+                   "mma issue %.0f | epi/warp total %.0f wtfull %.0f | active blocks %.3f of %.0f | cta max %llu unit max %llu "
                    "chunks max %llu\n", gridDim.x, v[0] / n, v[1] / n,
-                   v[2] / n, v[4] / n, v[5] / n, v[6] / n, v[8] / n / kEpiWarps, v[9] / n / kEpiWarps,
+                   v[2] / n, v[4] / n, v[5] / n, v[6] / n, v[7] / n, v[8] / n / kEpiWarps, v[9] / n / kEpiWarps,
                    (double)v[10] / (double)(v[11] ? v[11] : 1), v[11] / n / kEpiWarps, v[12], v[13], v[14]);
         }
     }

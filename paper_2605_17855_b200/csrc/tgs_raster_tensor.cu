@@ -24,11 +24,13 @@
 // D < log2(alpha_skip) — which also realises the positive-power clamp (raster_scalar.hpp:41).
 //
 // CTA (persistent, one per SM) = one unit of 2x2 tiles at a time (G=2: the group; G=4: a
-// quarter group; G=1: a single tile with SLOTS = 1), units in longest-list-first order:
-//   epilogue warps (16; 8 for G=1): warp w reads TMEM lane quadrant q = w%4 of the M-tiles
-//              2*(k0+i) + half (i < SPW = 2), so each thread owns one pixel in two member tiles;
-//              the ordered blend runs on CUDA cores + MUFU ex2; a retired tile drops out at once;
-//   producer warp: streams the unit's list in 32-entry batches (prefetched two ahead), gathers
+// quarter group; G=1: a single tile with SLOTS = 1), units in the order of the previous frame's
+// measured walks (unit_order_kernel):
+//   epilogue warps (8): compact mapping — warp w owns the 16x8 half-tile w and reads TMEM lane
+//              quadrant w%4 of M-tiles 4*(w/4)+k, k<4 (its four 8x4 pixel blocks), so each thread
+//              owns four pixels of one half-tile; the ordered blend runs on CUDA cores + MUFU ex2;
+//              a half-tile whose pixels all terminated drops out at once;
+//   producer warp: streams the unit's list in 32-entry batches (records two batches ahead), gathers
 //              each splat once per group, drops entries whose member tiles are all retired or
 //              that can never reach alpha_skip (ballot compaction keeps list order), and writes the
 //              unit-centred coefficient rows (+ mask lanes) and blend data into an smem stage;
@@ -68,14 +70,6 @@ constexpr int kTS = TGS_RASTER_TS;  // TMEM accumulator stages
 #ifndef TGS_RASTER_SPW
 #define TGS_RASTER_SPW 4
 #endif
-#ifndef TGS_RASTER_PF
-#define TGS_RASTER_PF 1
-#endif
-constexpr int kPF = TGS_RASTER_PF;  // producer record batches in flight
-#ifndef TGS_RASTER_DI
-#define TGS_RASTER_DI 2
-#endif
-constexpr int kDI = TGS_RASTER_DI;  // producer list-index batches in flight beyond the records
 #ifndef TGS_RASTER_CTAS
 #define TGS_RASTER_CTAS 1
 #endif
@@ -84,6 +78,10 @@ constexpr int kCtasPerSm = TGS_RASTER_CTAS;  // resident CTAs per SM (TMEM colum
 #define TGS_RASTER_JB 16
 #endif
 constexpr int kJB = TGS_RASTER_JB;  // accumulator columns (splats) per epilogue batch: 16 or 8
+#ifndef TGS_RASTER_ATMEM
+#define TGS_RASTER_ATMEM 0
+#endif
+constexpr bool kATmem = TGS_RASTER_ATMEM;  // pixel operand A held in TMEM (8 columns per M-tile)
 #ifndef TGS_RASTER_PROF
 #define TGS_RASTER_PROF 0
 #endif
@@ -144,7 +142,7 @@ struct Smem {
 
 template <int SLOTS>
 constexpr uint32_t tmem_cols() {
-    constexpr int c = kTS * 2 * SLOTS * kN;
+    constexpr int c = kTS * 2 * SLOTS * kN + (kATmem ? 8 * 2 * SLOTS : 0);
     return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
 }
 
@@ -339,6 +337,24 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
+    constexpr uint32_t kACol = (uint32_t)(kTS * kColsPerStage);  // A operand columns (kATmem)
+    if constexpr (kATmem) {
+        // warps 0..3 write the pixel operand rows of their lane quadrant into TMEM (row = lane,
+        // K pairs in 8 consecutive 32-bit columns)
+        if (warp < 4) {
+            for (int m = 0; m < kMT; ++m) {
+                const int l = warp * 32 + lane;
+                const uint4 lo = *reinterpret_cast<const uint4*>(&sm.a[m][core_off(l, 0)]);
+                const uint4 hi = *reinterpret_cast<const uint4*>(&sm.a[m][core_off(l, 1)]);
+                const uint32_t r[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+                ptx::tmem_st8(tmem + ((uint32_t)(warp * 32) << 16) + kACol + (uint32_t)(8 * m), r);
+            }
+            ptx::tmem_wait_st();
+        }
+        ptx::tc_fence_before();
+        __syncthreads();
+        ptx::tc_fence_after();
+    }
     [[maybe_unused]] unsigned long long pf[4] = {0, 0, 0, 0};
     [[maybe_unused]] const long long pf_start = clock64();
 
@@ -373,9 +389,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                 sm.hdr[s].live = (int)live;
                 sm.hdr[s].chunk = (int)c;
             }
-#ifndef TGS_RASTER_NOFENCE  // experiment only: timing without the proxy fence (unsafe)
             ptx::fence_proxy_async_smem();
-#endif
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&sm.full[s]);
             __syncwarp();
@@ -601,8 +615,14 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
 #pragma unroll
                 for (int m = 0; m < kMT; ++m)
                     if (kCompact ? ((hlive >> (2 * (m >> 2))) & 3u) : ((hlive >> (m >> 1)) & 1u))
-                        ptx::mma_f16_ss_elect(dcol + (uint32_t)(m * kN),
-                                              ptx::smem_desc(a_base + (uint32_t)(m * 128 * 32), 128, 256), bd, idesc, 0u);
+                    {
+                        if constexpr (kATmem)
+                            ptx::mma_f16_ts_elect(dcol + (uint32_t)(m * kN), tmem + kACol + (uint32_t)(8 * m), bd, idesc, 0u);
+                        else
+                            ptx::mma_f16_ss_elect(dcol + (uint32_t)(m * kN),
+                                                  ptx::smem_desc(a_base + (uint32_t)(m * 128 * 32), 128, 256), bd, idesc,
+                                                  0u);
+                    }
                 ptx::mma_commit_elect(&sm.tfull[ts]);
             } else if (lane == 0) {
                 ptx::mbar_arrive(&sm.tfull[ts]);
@@ -709,10 +729,6 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                     // Phase 1 (branch-free, kJB independent chains): which of the batch's splats
                     // reach alpha_skip at any of this warp's pixels -> warp-uniform mask.
                     uint32_t mk = 0;
-#ifdef TGS_RASTER_NOEPI  // experiment: skip the epilogue's compute (wrong images)
-                    if (nv >= 0) {
-                    } else
-#endif
 #pragma unroll
                     for (int jj = 0; jj < kJB; ++jj) {
                         uint32_t p = 0;

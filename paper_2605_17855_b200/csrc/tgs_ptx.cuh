@@ -47,6 +47,19 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
 
 // Bounded wait: a deadlock (a protocol bug) must become a reported kernel error, never a hung
 // GPU.  After ~4e9 cycles (~2 s) the waiter prints where it is stuck and traps.
+// non-blocking phase test
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
     // try_wait with a suspend-time hint: the thread sleeps in hardware until the phase completes
     // or ~20 us pass, so waiting warps do not steal issue slots from working ones

@@ -100,6 +100,12 @@ __device__ unsigned int g_usec[65536][3];  // producer cycles: retire check, row
 #ifndef TGS_RASTER_COMPACT
 #define TGS_RASTER_COMPACT 1
 #endif
+#ifndef TGS_RASTER_PREFETCH4
+#define TGS_RASTER_PREFETCH4 0
+#endif
+#ifndef TGS_RASTER_STREAMS
+#define TGS_RASTER_STREAMS 1
+#endif
 
 struct ChunkHeader {
     int seq;      // per-CTA unit sequence number, -1 = end of stream
@@ -120,23 +126,28 @@ struct Roles {
     static constexpr int kThreads = (kEpiWarps + 2) * 32;
     static constexpr int kProd = kEpiWarps, kMma = kEpiWarps + 1;
     static constexpr bool kCompact = SLOTS == 4 && kSPW == 4 && TGS_RASTER_COMPACT;
+    // chunk streams: with 2, the unit's top tile row (tiles 0,1: warps 0-3, M-tiles 0-3) and bottom
+    // row (tiles 2,3: warps 4-7, M-tiles 4-7) get their own chunk streams carrying only the splats
+    // that overlap them, and progress independently
+    static constexpr int kNS = (kCompact && TGS_RASTER_STREAMS == 2) ? 2 : 1;
 };
 
 template <int SLOTS>
 struct Smem {
     static constexpr int kMT = 2 * SLOTS;
+    static constexpr int kNS = Roles<SLOTS>::kNS;
     alignas(128) uint8_t a[kMT][128 * 32];   // pixel monomial rows (K-major, no swizzle)
-    alignas(128) uint8_t b[kSS][kN * 32];    // splat coefficient rows
-    float4 epi[kSS][kN];                     // r, g, b, min(alpha_clamp, opacity)
-    ChunkHeader hdr[kSS];
-    alignas(16) int wdone[16];               // chunks each epilogue warp has completed
+    alignas(128) uint8_t b[kNS][kSS][kN * 32];  // splat coefficient rows, per stream
+    float4 epi[kNS][kSS][kN];                // r, g, b, min(alpha_clamp, opacity)
+    ChunkHeader hdr[kNS][kSS];
+    alignas(16) int wdone[16];               // chunks (of its stream) each epilogue warp has completed
     alignas(16) int dead[16];                // (seq << 4) | retired member tiles, per warp
-    uint64_t full[kSS];                      // producer -> MMA
-    uint64_t tfull[kTS];                     // MMA -> epilogue (tcgen05.commit)
+    uint64_t full[kNS][kSS];                 // producer -> MMA
+    uint64_t tfull[kNS][kTS];                // MMA -> epilogue (tcgen05.commit)
     // Releases are monotonic counters compared with absolute targets (no mbarrier phase
     // aliasing): done_cnt[s] = warps that finished a chunk on smem stage s; a TMEM stage is free
     // once every epilogue warp's wdone passed the chunk that used it.
-    unsigned int done_cnt[kSS];
+    unsigned int done_cnt[kNS][kSS];
     uint32_t tmem_base;
 };
 
@@ -243,9 +254,9 @@ __device__ __forceinline__ void never_row(uint4& r0, uint4& r1) {
 }
 
 template <int SLOTS>
-__device__ __forceinline__ void write_row(Smem<SLOTS>& sm, int s, int slot, const uint4& r0, const uint4& r1) {
-    *reinterpret_cast<uint4*>(&sm.b[s][core_off(slot, 0)]) = r0;
-    *reinterpret_cast<uint4*>(&sm.b[s][core_off(slot, 1)]) = r1;
+__device__ __forceinline__ void write_row(Smem<SLOTS>& sm, int h, int s, int slot, const uint4& r0, const uint4& r1) {
+    *reinterpret_cast<uint4*>(&sm.b[h][s][core_off(slot, 0)]) = r0;
+    *reinterpret_cast<uint4*>(&sm.b[h][s][core_off(slot, 1)]) = r1;
 }
 
 // Unit geometry: the unit's top-left tile, the group whose list it walks, member-tile liveness.
@@ -286,6 +297,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
     constexpr int kMT = R::kMT, SPW = R::kSPW, kEpiWarps = R::kEpiWarps;
     constexpr int kProd = R::kProd, kMma = R::kMma;
     constexpr bool kCompact = R::kCompact;
+    constexpr int kNS = R::kNS, kWPS = kEpiWarps / kNS, kMPS = kMT / kNS;  // warps, M-tiles per stream
     constexpr int kColsPerStage = kMT * kN;
     constexpr uint32_t kTmemCols = tmem_cols<SLOTS>();
     // No-swizzle K-major operands only need 16-byte alignment (descriptor addresses are >> 4).
@@ -324,11 +336,13 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
         sm.dead[threadIdx.x] = -1;
     }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kSS; ++s) {
-            ptx::mbar_init(&sm.full[s], 1);
-            sm.done_cnt[s] = 0;
+        for (int h = 0; h < kNS; ++h) {
+            for (int s = 0; s < kSS; ++s) {
+                ptx::mbar_init(&sm.full[h][s], 1);
+                sm.done_cnt[h][s] = 0;
+            }
+            for (int s = 0; s < kTS; ++s) ptx::mbar_init(&sm.tfull[h][s], 1);
         }
-        for (int s = 0; s < kTS; ++s) ptx::mbar_init(&sm.tfull[s], 1);
         ptx::mbar_fence_init();
     }
     if (warp == kMma) ptx::tmem_alloc<kTmemCols>(&sm.tmem_base);
@@ -361,17 +375,19 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
     if (warp == kProd) {
         // ================================ producer ===========================================
         const float skip = a.alpha_skip, clampv = a.alpha_clamp;
-        uint32_t c = 0;  // chunks emitted so far
+        uint32_t c[kNS];  // chunks emitted so far, per stream
+#pragma unroll
+        for (int h = 0; h < kNS; ++h) c[h] = 0;
         const uint32_t lt = (1u << lane) - 1u;
-        auto open_stage = [&](uint32_t cc) {
-            // stage cc % kSS is free once every epilogue warp finished chunk cc - kSS (lane 0
-            // polls, the warp reconverges after)
+        auto open_stage = [&](int h, uint32_t cc) {
+            // stage cc % kSS of stream h is free once the stream's epilogue warps finished chunk
+            // cc - kSS (lane 0 polls, the warp reconverges after)
             const int s = (int)(cc % kSS);
             if (cc >= (uint32_t)kSS && lane == 0) {
-                const unsigned int need = (unsigned int)kEpiWarps * (cc / kSS);
-                if (ld_volatile_u32(&sm.done_cnt[s]) < need) {
+                const unsigned int need = (unsigned int)kWPS * (cc / kSS);
+                if (ld_volatile_u32(&sm.done_cnt[h][s]) < need) {
                     const long long t0 = clock64();
-                    while (ld_volatile_u32(&sm.done_cnt[s]) < need) {
+                    while (ld_volatile_u32(&sm.done_cnt[h][s]) < need) {
                         __nanosleep(32);
                         if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producer/done", (int)cc, s);
                     }
@@ -381,19 +397,21 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
             __syncwarp();
             return s;
         };
-        auto publish = [&](int s, int seq, int unit, int n_valid, uint32_t live) {
+        auto publish = [&](int h, int s, int seq, int unit, int n_valid, uint32_t live) {
             if (lane == 0) {
-                sm.hdr[s].seq = seq;
-                sm.hdr[s].unit = unit;
-                sm.hdr[s].n_valid = n_valid;
-                sm.hdr[s].live = (int)live;
-                sm.hdr[s].chunk = (int)c;
+                sm.hdr[h][s].seq = seq;
+                sm.hdr[h][s].unit = unit;
+                sm.hdr[h][s].n_valid = n_valid;
+                sm.hdr[h][s].live = (int)live;
+                sm.hdr[h][s].chunk = (int)c[h];
             }
             ptx::fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&sm.full[s]);
+            if (lane == 0) ptx::mbar_arrive(&sm.full[h][s]);
             __syncwarp();
         };
+        // member tiles of stream h
+        auto smask = [&](int h) -> uint32_t { return kNS == 1 ? 0xfu : (h == 0 ? 0x3u : 0xcu); };
         for (int seq = 0;; ++seq) {
             int t = 0;
             if (lane == 0) t = (int)atomicAdd(&a.fc->group_counter, 1u);
@@ -402,16 +420,25 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
             const int unit = a.order ? a.order[t] : t;
             const UnitGeom ug = unit_geom<SLOTS>(gg, unit);
             [[maybe_unused]] const long long unit_t0 = clock64();
-            [[maybe_unused]] const uint32_t unit_c0 = c;
+            [[maybe_unused]] uint32_t unit_c0 = 0;
+#pragma unroll
+            for (int h = 0; h < kNS; ++h) unit_c0 += c[h];
             [[maybe_unused]] const unsigned long long unit_w0 = pf[1];
             [[maybe_unused]] unsigned long long sec[3] = {0, 0, 0};
             const uint32_t begin = a.offsets[ug.gid], end = a.offsets[ug.gid + 1];
             const float ox = (float)(ug.tx0 * kTile) + centre, oy = (float)(ug.ty0 * kTile) + centre;
-            int fill = 0;          // rows placed in the open chunk
-            bool open = false;     // a stage is open for this unit
-            bool emitted = false;  // at least one chunk of this unit emitted
+            int fill[kNS], s[kNS];   // rows placed in the open chunk / its stage, per stream
+            bool open[kNS];          // a stage is open for this unit
+            bool emitted_h[kNS];     // at least one chunk of this unit emitted
+#pragma unroll
+            for (int h = 0; h < kNS; ++h) {
+                fill[h] = 0;
+                s[h] = 0;
+                open[h] = false;
+                emitted_h[h] = false;
+            }
+            bool emitted = false;    // any stream
             uint32_t live = ug.live;
-            int s = 0;
             // software-pipelined gather: list indices two batches ahead, records one ahead
             const uint32_t nb = (end - begin + 31u) / 32u;
             auto ld_idx = [&](uint32_t b) -> uint32_t {
@@ -464,6 +491,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                     }
                     [[maybe_unused]] const long long tb1 = TGS_RASTER_PROF ? clock64() : 0;
                     bool keep = false;
+                    uint32_t cover_kept = 0;
                     uint4 r0, r1;
                     float4 epi_v = make_float4(0, 0, 0, 0);
                     if (cur.idx != 0xffffffffu) {
@@ -481,49 +509,72 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                         if (cover != 0u && !(cj < skip)) {
                             keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox,
                                             oy, cover, r0, r1);
+                            cover_kept = cover;
                             epi_v = make_float4(cur.col.x, cur.col.y, cur.col.z, cj);
                         }
                     }
-                    const uint32_t km = __ballot_sync(0xffffffffu, keep);
                     [[maybe_unused]] const long long tb2 = TGS_RASTER_PROF ? clock64() : 0;
                     if (TGS_RASTER_PROF) {
                         pf[2] += 1;
                         sec[0] += tb1 - tb0;
                         sec[1] += tb2 - tb1;
                     }
-                    if (km == 0u) return false;
-
-                    const int nk = __popc(km);
-                    const int rank = __popc(km & lt);
-                    if (!open) {
-                        s = open_stage(c);
-                        open = true;
-                        fill = 0;
-                    }
-                    // place the kept ranks in order; a full chunk is published and the next one opened
-                    // (a 32-lane batch spans at most 32 / kN + 1 chunks)
-                    int placed = 0;
-                    for (;;) {
-                        const int room = kN - fill;
-                        if (keep && rank >= placed && rank - placed < room) {
-                            write_row(sm, s, fill + rank - placed, r0, r1);
-                            sm.epi[s][fill + rank - placed] = epi_v;
+#pragma unroll
+                    for (int h = 0; h < kNS; ++h) {
+                        const bool keep_h = keep && (cover_kept & smask(h)) != 0u;
+                        const uint32_t km = __ballot_sync(0xffffffffu, keep_h);
+                        if (km == 0u) continue;
+                        const int nk = __popc(km);
+                        const int rank = __popc(km & lt);
+                        if (!open[h]) {
+                            s[h] = open_stage(h, c[h]);
+                            open[h] = true;
+                            fill[h] = 0;
                         }
-                        if (nk - placed < room) {
-                            fill += nk - placed;
-                            break;
+                        // place the kept ranks in order; a full chunk is published and the next one
+                        // opened (a 32-lane batch spans at most 32 / kN + 1 chunks)
+                        int placed = 0;
+                        for (;;) {
+                            const int room = kN - fill[h];
+                            if (keep_h && rank >= placed && rank - placed < room) {
+                                write_row(sm, h, s[h], fill[h] + rank - placed, r0, r1);
+                                sm.epi[h][s[h]][fill[h] + rank - placed] = epi_v;
+                            }
+                            if (nk - placed < room) {
+                                fill[h] += nk - placed;
+                                break;
+                            }
+                            publish(h, s[h], seq, unit, kN, live & smask(h));
+                            ++c[h];
+                            emitted = true;
+                            emitted_h[h] = true;
+                            s[h] = open_stage(h, c[h]);
+                            fill[h] = 0;
+                            placed += room;
+                            if (placed == nk) break;
                         }
-                        publish(s, seq, unit, kN, live);
-                        ++c;
-                        emitted = true;
-                        s = open_stage(c);
-                        fill = 0;
-                        placed += room;
-                        if (placed == nk) break;
                     }
                     if (TGS_RASTER_PROF) sec[2] += clock64() - tb2;
                     return false;
             };
+#if TGS_RASTER_PREFETCH4
+            Rec q0 = ld_rec(ld_idx(0)), q1 = ld_rec(ld_idx(1)), q2 = ld_rec(ld_idx(2)), q3 = ld_rec(ld_idx(3));
+            uint32_t i0 = ld_idx(4), i1 = ld_idx(5), i2 = ld_idx(6), i3 = ld_idx(7);
+            for (uint32_t bi = 0; bi < nb; bi += 4) {
+                if (batch(q0)) break;
+                q0 = ld_rec(i0);
+                i0 = ld_idx(bi + 8);
+                if (bi + 1 >= nb || batch(q1)) break;
+                q1 = ld_rec(i1);
+                i1 = ld_idx(bi + 9);
+                if (bi + 2 >= nb || batch(q2)) break;
+                q2 = ld_rec(i2);
+                i2 = ld_idx(bi + 10);
+                if (bi + 3 >= nb || batch(q3)) break;
+                q3 = ld_rec(i3);
+                i3 = ld_idx(bi + 11);
+            }
+#else
             Rec qa = ld_rec(ld_idx(0)), qb = ld_rec(ld_idx(1));
             uint32_t ia = ld_idx(2), ib = ld_idx(3);
             for (uint32_t bi = 0; bi < nb; bi += 2) {
@@ -535,30 +586,37 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                 qb = ld_rec(ib);
                 ib = ld_idx(bi + 5);
             }
+#endif
             // close the unit: pad and publish the partial chunk (or an empty one so the
             // epilogue still writes the unit's pixels)
-            if (open && (fill > 0 || !emitted)) {
-                if (lane >= fill && lane < kN) {
-                    uint4 r0, r1;
-                    never_row(r0, r1);
-                    write_row(sm, s, lane, r0, r1);
+#pragma unroll
+            for (int h = 0; h < kNS; ++h) {
+                if (open[h] && (fill[h] > 0 || !emitted_h[h])) {
+                    if (lane >= fill[h] && lane < kN) {
+                        uint4 r0, r1;
+                        never_row(r0, r1);
+                        write_row(sm, h, s[h], lane, r0, r1);
+                    }
+                    publish(h, s[h], seq, unit, fill[h], live & smask(h));
+                    ++c[h];
+                } else if (!open[h]) {
+                    s[h] = open_stage(h, c[h]);
+                    publish(h, s[h], seq, unit, 0, live & smask(h));
+                    ++c[h];
                 }
-                publish(s, seq, unit, fill, live);
-                ++c;
-            } else if (!open) {
-                s = open_stage(c);
-                publish(s, seq, unit, 0, live);
-                ++c;
             }
+            uint32_t c_now = 0;
+#pragma unroll
+            for (int h = 0; h < kNS; ++h) c_now += c[h];
             // schedule feedback: list entries this unit walked (batches) plus rows it staged
-            if (a.unit_cost && lane == 0) a.unit_cost[unit] = 32u * n_batches + (uint32_t)kN * (c - unit_c0);
+            if (a.unit_cost && lane == 0) a.unit_cost[unit] = 32u * n_batches + (uint32_t)kN * (c_now - unit_c0);
 #if TGS_RASTER_PROF
             if (lane == 0) {
                 atomicMax(&g_rprof[13], (unsigned long long)(clock64() - unit_t0));
-                atomicMax(&g_rprof[14], (unsigned long long)(c - unit_c0));
+                atomicMax(&g_rprof[14], (unsigned long long)(c_now - unit_c0));
                 if (unit < 65536) {
                     g_ucyc[unit] = (unsigned int)(clock64() - unit_t0);
-                    g_uch[unit] = c - unit_c0;
+                    g_uch[unit] = c_now - unit_c0;
                     g_uent[unit] = (unsigned)t;
                     g_uwait[unit] = (unsigned)(pf[1] - unit_w0);
                     for (int k = 0; k < 3; ++k) g_usec[unit][k] = (unsigned)sec[k];
@@ -566,76 +624,102 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
             }
 #endif
         }
-        const int s = open_stage(c);  // end of stream
-        publish(s, -1, -1, 0, 0u);
+#pragma unroll
+        for (int h = 0; h < kNS; ++h) {  // end of stream
+            const int se = open_stage(h, c[h]);
+            publish(h, se, -1, -1, 0, 0u);
+        }
     } else if (warp == kMma) {
         // ================================ MMA issuer ==========================================
         constexpr uint32_t idesc = ptx::idesc_f16(128, kN);
         const uint32_t a_base = ptx::smem_u32(&sm.a[0][0]);
-        for (uint32_t c = 0;; ++c) {
-            const int s = (int)(c % kSS), ts = (int)(c % kTS);
-            [[maybe_unused]] const long long tw0 = clock64();
-            ptx::mbar_wait_wd(&sm.full[s], (c / kSS) & 1, "mma/full", (int)c, s);
-            if (TGS_RASTER_PROF) pf[1] += clock64() - tw0;
-            if (c >= (uint32_t)kTS && lane == 0) {  // every epilogue warp finished chunk c - kTS
-                const int need = (int)(c - kTS + 1);
-                auto released = [&]() {
-                    int mn = 0x7fffffff;
+        uint32_t cs[kNS];
+        bool ended[kNS];
 #pragma unroll
-                    for (int w4 = 0; w4 < kEpiWarps; w4 += 4) {
-                        const int4 d = ld_volatile_v4(&sm.wdone[w4]);
-                        mn = min(mn, min(min(d.x, d.y), min(d.z, d.w)));
-                    }
-                    return mn >= need;
-                };
-                if (!released()) {
-                    const long long t0 = clock64();
-                    while (!released()) {
-                        __nanosleep(32);
-                        if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("mma/tempty", (int)c, 0);
-                    }
-                    if (TGS_RASTER_PROF) pf[2] += clock64() - t0;
+        for (int h = 0; h < kNS; ++h) {
+            cs[h] = 0;
+            ended[h] = false;
+        }
+        int n_ended = 0;
+        long long idle0 = clock64();
+        // stream h's TMEM stage for chunk c is free once its warps finished chunk c - kTS
+        auto released = [&](int h, int need) {
+            int mn = 0x7fffffff;
+#pragma unroll
+            for (int w4 = 0; w4 < kWPS; w4 += 4) {
+                const int4 d = ld_volatile_v4(&sm.wdone[h * kWPS + w4]);
+                mn = min(mn, min(min(d.x, d.y), min(d.z, d.w)));
+            }
+            return mn >= need;
+        };
+        while (n_ended < kNS) {
+            bool did = false;
+#pragma unroll
+            for (int h = 0; h < kNS; ++h) {
+                if (ended[h]) continue;
+                const uint32_t c = cs[h];
+                const int s = (int)(c % kSS), ts = (int)(c % kTS);
+                int ready = 0;
+                if (lane == 0)
+                    ready = ptx::mbar_test(&sm.full[h][s], (c / kSS) & 1) &&
+                            (c < (uint32_t)kTS || released(h, (int)(c - kTS + 1)));
+                ready = __shfl_sync(0xffffffffu, ready, 0);
+                if (!ready) continue;
+                __syncwarp();
+                ptx::tc_fence_after();
+                // warp-uniform issue (operands stay uniform; one elected lane issues)
+                const int hseq = __shfl_sync(0xffffffffu, sm.hdr[h][s].seq, 0);
+                const int hnv = __shfl_sync(0xffffffffu, sm.hdr[h][s].n_valid, 0);
+                const uint32_t hlive = __shfl_sync(0xffffffffu, (uint32_t)sm.hdr[h][s].live, 0);
+                const int hch = __shfl_sync(0xffffffffu, sm.hdr[h][s].chunk, 0);
+                if (hch != (int)c) {
+                    if (lane == 0)
+                        printf("MMA header mismatch: stream %d expected chunk %d found %d (seq %d)\n", h, (int)c, hch, hseq);
+                    __trap();
                 }
-            }
-            __syncwarp();
-            ptx::tc_fence_after();
-            // warp-uniform issue (operands stay uniform; one elected lane issues)
-            const int hseq = __shfl_sync(0xffffffffu, sm.hdr[s].seq, 0);
-            const int hnv = __shfl_sync(0xffffffffu, sm.hdr[s].n_valid, 0);
-            const uint32_t hlive = __shfl_sync(0xffffffffu, (uint32_t)sm.hdr[s].live, 0);
-            const int hch = __shfl_sync(0xffffffffu, sm.hdr[s].chunk, 0);
-            if (hch != (int)c) {
-                if (lane == 0) printf("MMA header mismatch: expected chunk %d found %d (seq %d)\n", (int)c, hch, hseq);
-                __trap();
-            }
-            [[maybe_unused]] const long long ti0 = TGS_RASTER_PROF ? clock64() : 0;
-            if (hseq >= 0 && hnv > 0) {
-                const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[s][0]), 128, 256);
-                const uint32_t dcol = tmem + (uint32_t)(ts * kColsPerStage);
+                [[maybe_unused]] const long long ti0 = TGS_RASTER_PROF ? clock64() : 0;
+                if (hseq >= 0 && hnv > 0) {
+                    const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[h][s][0]), 128, 256);
+                    const uint32_t dcol = tmem + (uint32_t)(ts * kColsPerStage);
 #pragma unroll
-                for (int m = 0; m < kMT; ++m)
-                    if (kCompact ? ((hlive >> (2 * (m >> 2))) & 3u) : ((hlive >> (m >> 1)) & 1u))
-                    {
-                        if constexpr (kATmem)
-                            ptx::mma_f16_ts_elect(dcol + (uint32_t)(m * kN), tmem + kACol + (uint32_t)(8 * m), bd, idesc, 0u);
-                        else
-                            ptx::mma_f16_ss_elect(dcol + (uint32_t)(m * kN),
-                                                  ptx::smem_desc(a_base + (uint32_t)(m * 128 * 32), 128, 256), bd, idesc,
-                                                  0u);
+                    for (int mm = 0; mm < kMPS; ++mm) {
+                        const int m = h * kMPS + mm;
+                        if (kCompact ? ((hlive >> (2 * (m >> 2))) & 3u) : ((hlive >> (m >> 1)) & 1u)) {
+                            if constexpr (kATmem)
+                                ptx::mma_f16_ts_elect(dcol + (uint32_t)(m * kN), tmem + kACol + (uint32_t)(8 * m), bd,
+                                                      idesc, 0u);
+                            else
+                                ptx::mma_f16_ss_elect(dcol + (uint32_t)(m * kN),
+                                                      ptx::smem_desc(a_base + (uint32_t)(m * 128 * 32), 128, 256), bd,
+                                                      idesc, 0u);
+                        }
                     }
-                ptx::mma_commit_elect(&sm.tfull[ts]);
-            } else if (lane == 0) {
-                ptx::mbar_arrive(&sm.tfull[ts]);
+                    ptx::mma_commit_elect(&sm.tfull[h][ts]);
+                } else if (lane == 0) {
+                    ptx::mbar_arrive(&sm.tfull[h][ts]);
+                }
+                __syncwarp();
+                if (TGS_RASTER_PROF) pf[3] += clock64() - ti0;
+                cs[h] = c + 1;
+                if (hseq < 0) {
+                    ended[h] = true;
+                    ++n_ended;
+                }
+                did = true;
             }
-            __syncwarp();
-            if (TGS_RASTER_PROF) pf[3] += clock64() - ti0;
-            if (hseq < 0) break;
+            if (did) {
+                idle0 = clock64();
+            } else {
+                __nanosleep(20);
+                if (clock64() - idle0 > 4000000000ll) ptx::watchdog_trap("mma/idle", (int)cs[0], n_ended);
+            }
         }
     } else {
         // ================================ epilogue ============================================
         // warp -> (lane quadrant q, tile half, slots k0 .. k0+SPW-1); slot i of a thread is a
         // pixel of member tile k0 + i
         const int q = warp & 3, half = (warp >> 2) & 1, k0 = (warp >> 3) * SPW;
+        const int hs = warp / kWPS;  // this warp's chunk stream
         // M-tile holding slot k of this warp
         auto mtile = [&](int k) { return kCompact ? 4 * (warp >> 2) + k : 2 * (k0 + k) + half; };
         int relx[SPW], rely[SPW];
@@ -665,10 +749,10 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
             const int s = (int)(c % kSS), ts = (int)(c % kTS);
             // this warp consumed the phase of chunk c - kTS itself, so the parity is unambiguous
             [[maybe_unused]] const long long tw0 = clock64();
-            ptx::mbar_wait_wd(&sm.tfull[ts], (c / kTS) & 1, "epilogue/tfull", (int)c, warp);
+            ptx::mbar_wait_wd(&sm.tfull[hs][ts], (c / kTS) & 1, "epilogue/tfull", (int)c, warp);
             if (TGS_RASTER_PROF) pf[1] += clock64() - tw0;
             ptx::tc_fence_after();
-            const ChunkHeader h = sm.hdr[s];
+            const ChunkHeader h = sm.hdr[hs][s];
             if (h.chunk != (int)c) {
                 if (lane == 0)
                     printf("EPI w%d header mismatch: expected chunk %d found %d (seq %d)\n", warp, (int)c, h.chunk, h.seq);
@@ -747,7 +831,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                     // raster_scalar.cpp:36-41) — the splat that drives T below t_terminate is
                     // blended, nothing after it.
                     auto blend = [&](int jj, const uint32_t* dk) {
-                        const float4 ej = sm.epi[s][j0 + jj];
+                        const float4 ej = sm.epi[hs][s][j0 + jj];
 #pragma unroll
                         for (int k = 0; k < SPW; ++k) {
                             const float dv = __uint_as_float(dk[k]);
@@ -827,7 +911,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                 if (dead != reported) ((volatile int*)sm.dead)[warp] = (cur << 4) | (int)dtiles;
                 __threadfence_block();
                 ((volatile int*)sm.wdone)[warp] = (int)c + 1;
-                atomicAdd(&sm.done_cnt[s], 1u);
+                atomicAdd(&sm.done_cnt[hs][s], 1u);
             }
             reported = dead;
         }

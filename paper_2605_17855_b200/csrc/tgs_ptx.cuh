@@ -47,6 +47,12 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
 
 // Bounded wait: a deadlock (a protocol bug) must become a reported kernel error, never a hung
 // GPU.  After ~4e9 cycles (~2 s) the waiter prints where it is stuck and traps.
+#ifndef TGS_MBAR_SPIN  // waits by lane-0 polling (1), polling with __nanosleep(n) (n > 1), or try_wait (0)
+#define TGS_MBAR_SPIN 1
+#endif
+#ifndef TGS_MBAR_HINT_NS
+#define TGS_MBAR_HINT_NS 20000
+#endif
 // non-blocking phase test
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
@@ -69,7 +75,7 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(20000u)
+        : "r"(smem_u32(bar)), "r"(parity), "r"((uint32_t)TGS_MBAR_HINT_NS)
         : "memory");
     return ok != 0;
 }
@@ -83,6 +89,17 @@ static __device__ __noinline__ void watchdog_trap(const char* what, int a0, int 
 // reconverges, so no lane reaches a .sync.aligned tcgen05 op / elect.sync / vote while others
 // are still in the loop.  Memory ordering for the other lanes comes from __syncwarp.
 __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, const char* what, int a0, int a1) {
+#if TGS_MBAR_SPIN
+    if ((threadIdx.x & 31) == 0 && !mbar_test(bar, parity)) {
+        const long long t0 = clock64();
+        while (!mbar_test(bar, parity)) {
+            if (TGS_MBAR_SPIN > 1) __nanosleep(TGS_MBAR_SPIN);
+            if (clock64() - t0 > 4000000000ll) watchdog_trap(what, a0, a1);
+        }
+    }
+    __syncwarp();
+    return;
+#endif
     if ((threadIdx.x & 31) == 0 && !mbar_try(bar, parity)) {
         const long long t0 = clock64();
         for (uint32_t i = 1;; ++i) {

@@ -143,7 +143,12 @@ tgs_status tgs_render_band(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camer
                            const tgs_options* opt, int group_row0, int group_row1, float* out_rgb,
                            tgs_stats* stats);
 
-/* Camera batch: n frames, out_rgb = n * width * height * 3 floats (all cameras share W,H). */
+/* Camera batch (BASELINE config 5; reference analogue: one gsr::render call per camera,
+ * render.hpp:30-31 / tools/gsrender.cpp:112-152): n frames, out_rgb = n * width * height * 3 floats
+ * (all cameras share W,H; NULL: no image copies).  Frames are pipelined over up to 3 internal lanes
+ * (extra streams + buffers on the same device, created on first use and owned by ctx), so one
+ * frame's image copy and latency-bound raster overlap the next frames' preprocess/sort/binning.
+ * Images are identical to n single renders. */
 tgs_status tgs_render_batch(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cams, int n,
                             const tgs_options* opt, float* out_rgb, tgs_stats* stats);
 

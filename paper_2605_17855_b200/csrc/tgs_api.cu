@@ -70,6 +70,7 @@ using namespace tgs;
 
 struct tgs_scene;
 struct tgs_ctx;
+constexpr int kBatchLanes = 3;  // frames in flight in tgs_render_batch
 
 struct tgs_scene {
     tgs_ctx* ctx = nullptr;
@@ -121,6 +122,10 @@ struct tgs_ctx {
     int last_band0 = 0, last_band1 = 0;
     int image_rows = 0;
     bool pending = false;
+    // camera-batch lanes: extra contexts (own stream and buffers) on the same device that render
+    // the parent's scenes, so frames of a batch overlap (tgs_render_batch)
+    tgs_ctx* lanes[kBatchLanes - 1] = {};
+    tgs_ctx* parent = nullptr;
     tgs_scene* scratch_scene = nullptr;
 };
 
@@ -191,7 +196,8 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
                          const tgs_options* opt, int band0, int band1) {
     tgs_status st = validate_options(cam, opt);
     if (st != TGS_OK) return st;
-    if (!scene || scene->ctx != ctx) return set_err(TGS_ERR_VALIDATION, "render: scene belongs to another context");
+    if (!scene || (scene->ctx != ctx && scene->ctx != ctx->parent))
+        return set_err(TGS_ERR_VALIDATION, "render: scene belongs to another context");
     const GroupGeom full = make_geom(opt->group_size, cam->width, cam->height, 0, 0);
     if (band1 <= 0) {
         band0 = 0;
@@ -471,6 +477,11 @@ void tgs_ctx_destroy(tgs_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->scratch_scene) tgs_scene_free(c->scratch_scene);
+    for (tgs_ctx*& l : c->lanes)
+        if (l) {
+            tgs_ctx_destroy(l);
+            l = nullptr;
+        }
     DBuf* bufs[] = {&c->fc, &c->proj, &c->pre_keys[0], &c->pre_keys[1], &c->pre_vals[0],
                     &c->pre_vals[1], &c->rect, &c->rrect, &c->list, &c->rowlist, &c->hist, &c->bsum, &c->ghist,
                     &c->offsets, &c->order, &c->ucost, &c->image, &c->scratch_records};
@@ -557,25 +568,56 @@ tgs_status tgs_render_band(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camer
 tgs_status tgs_render_batch(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cams, int n,
                             const tgs_options* opt, float* out_rgb, tgs_stats* stats) {
     if (!ctx || !cams || n < 0) return set_err(TGS_ERR_VALIDATION, "render_batch: bad arguments");
-    tgs_stats acc{};
-    for (int i = 0; i < n; ++i) {
+    for (int i = 0; i < n; ++i)
         if (cams[i].width != cams[0].width || cams[i].height != cams[0].height)
             return set_err(TGS_ERR_VALIDATION, "render_batch: all cameras must share width/height");
-        tgs_stats one{};
-        const size_t px = (size_t)cams[i].width * cams[i].height * 3;
-        tgs_status st = tgs_render(ctx, scene, &cams[i], opt, out_rgb ? out_rgb + px * i : nullptr, &one);
-        if (st != TGS_OK) return st;
-        acc.input += one.input;
-        acc.culled += one.culled;
-        acc.dropped_degenerate += one.dropped_degenerate;
-        acc.entries += one.entries;
-        acc.tile_appearances += one.tile_appearances;
-        acc.visible += one.visible;
-        acc.ms_preprocess += one.ms_preprocess;
-        acc.ms_binning += one.ms_binning;
-        acc.ms_sort += one.ms_sort;
-        acc.ms_raster += one.ms_raster;
-        acc.ms_total += one.ms_total;
+    cudaSetDevice(ctx->device);
+    // round-robin over up to kBatchLanes contexts: frame i is enqueued on lane i % L once the lane's
+    // previous frame (i - L) is retired and its image copied out, so the copies and one frame's
+    // latency-bound raster overlap other frames' preprocess/sort/binning
+    const int L = std::max(1, std::min(n, kBatchLanes));
+    tgs_ctx* lane[kBatchLanes] = {ctx};
+    for (int k = 1; k < L; ++k) {
+        if (!ctx->lanes[k - 1]) {
+            tgs_status st = tgs_ctx_create(ctx->device, &ctx->lanes[k - 1]);
+            if (st != TGS_OK) return st;
+            ctx->lanes[k - 1]->parent = ctx;
+        }
+        lane[k] = ctx->lanes[k - 1];
+    }
+    tgs_stats acc{};
+    const size_t px = n ? (size_t)cams[0].width * cams[0].height * 3 : 0;
+    for (int i = 0; i < n + L; ++i) {
+        if (i >= L) {
+            const int j = i - L;
+            tgs_ctx* c = lane[j % L];
+            tgs_stats one{};
+            tgs_status st = finish_frame(c, &one);
+            if (st == TGS_OK && out_rgb) st = copy_image_to_host(c, out_rgb + px * j);
+            if (st != TGS_OK) {
+                for (int k = 0; k < L; ++k) cudaStreamSynchronize(lane[k]->stream), lane[k]->pending = false;
+                return st;
+            }
+            acc.input += one.input;
+            acc.culled += one.culled;
+            acc.dropped_degenerate += one.dropped_degenerate;
+            acc.entries += one.entries;
+            acc.tile_appearances += one.tile_appearances;
+            acc.visible += one.visible;
+            acc.ms_preprocess += one.ms_preprocess;
+            acc.ms_binning += one.ms_binning;
+            acc.ms_sort += one.ms_sort;
+            acc.ms_raster += one.ms_raster;
+            acc.ms_total += one.ms_total;
+        }
+        if (i < n) {
+            tgs_status st = validate_options(&cams[i], opt);
+            if (st == TGS_OK) st = enqueue_frame(lane[i % L], scene, &cams[i], opt, 0, 0);
+            if (st != TGS_OK) {
+                for (int k = 0; k < L; ++k) cudaStreamSynchronize(lane[k]->stream), lane[k]->pending = false;
+                return st;
+            }
+        }
     }
     if (stats) *stats = acc;
     return TGS_OK;

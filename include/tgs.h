@@ -164,6 +164,14 @@ tgs_status tgs_read_lists(tgs_ctx* ctx, tgs_group_entry* out, int64_t cap, uint3
  * DESIGN.md §Roofline); computed by an instrumented pass, not by the timed kernels. */
 tgs_status tgs_count_pairs(tgs_ctx* ctx, uint64_t* walked, uint64_t* blended);
 
+/* ReuseReport of the last frame's group lists (reference: load_reduction, metrics.cpp:45-57):
+ * n_group = group entries, n_total = sum of their mask popcounts (tile appearances),
+ * load_reduction = 1 - n_group / n_total, hist[p] = entries whose mask has popcount p (1..16;
+ * hist[0] = 0).  Computed on the device from the splats' tile rectangles.  VALIDATION when the
+ * frame has no entries (the reference throws on an empty list). */
+tgs_status tgs_reuse_report(tgs_ctx* ctx, uint64_t* n_group, uint64_t* n_total, double* load_reduction,
+                            uint64_t hist[17]);
+
 /* Per tile of the last frame (band-local, row-major): how many entries of the tile's
  * mask-filtered list the slowest pixel walked before terminating (the tile's trip).  Tooling for
  * load-balance analysis; *n receives the tile count. */

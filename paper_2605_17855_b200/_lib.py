@@ -59,6 +59,8 @@ SIGNATURES = {
     "tgs_read_projected": (c_status, [P, P, C.c_int64, C.POINTER(C.c_int64)]),
     "tgs_read_lists": (c_status, [P, P, C.c_int64, P, C.c_int64, C.POINTER(C.c_int64)]),
     "tgs_count_pairs": (c_status, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "tgs_reuse_report": (c_status, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_uint64)]),
     "tgs_tile_trips": (c_status, [P, P, C.c_int64, C.POINTER(C.c_int64)]),
     "tgs_gen_synthetic_scene": (c_status, [C.c_uint64, C.c_int, C.c_float, C.c_float, C.c_float,
                                            C.c_uint64, F32P]),

@@ -737,6 +737,35 @@ tgs_status tgs_tile_trips(tgs_ctx* ctx, uint32_t* trips, int64_t cap, int64_t* n
     return TGS_OK;
 }
 
+tgs_status tgs_reuse_report(tgs_ctx* ctx, uint64_t* n_group, uint64_t* n_total, double* load_reduction,
+                            uint64_t hist[17]) {
+    if (!ctx || !n_group || !n_total || !load_reduction || !hist)
+        return set_err(TGS_ERR_VALIDATION, "reuse_report: null argument");
+    if (!ctx->last_scene) return set_err(TGS_ERR_VALIDATION, "reuse_report: no frame rendered yet");
+    cudaSetDevice(ctx->device);
+    DBuf tmp;
+    TGS_CUDA_OK(tmp.ensure(17 * sizeof(unsigned long long)));
+    launch_reuse_hist(ctx->fc.as<FrameCounters>(), ctx->rect.as<uint2>(), ctx->last_gg,
+                      (int)std::max<int64_t>(1, ctx->last_scene->n), tmp.as<unsigned long long>(), ctx->stream);
+    cudaError_t e = cudaGetLastError();
+    unsigned long long h[17];
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, tmp.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    tmp.release();
+    if (e != cudaSuccess) return cuda_fail(e, "reuse_report", __FILE__, __LINE__);
+    uint64_t ng = 0, nt = 0;
+    for (int p = 0; p < 17; ++p) {
+        hist[p] = h[p];
+        ng += h[p];
+        nt += (uint64_t)p * h[p];
+    }
+    if (ng == 0) return set_err(TGS_ERR_VALIDATION, "load_reduction: empty entry list has an undefined ratio");
+    *n_group = ng;
+    *n_total = nt;
+    *load_reduction = 1.0 - (double)ng / (double)nt;
+    return TGS_OK;
+}
+
 tgs_status tgs_count_pairs(tgs_ctx* ctx, uint64_t* walked, uint64_t* blended) {
     if (!ctx || !walked || !blended) return set_err(TGS_ERR_VALIDATION, "count_pairs: null argument");
     if (!ctx->last_scene) return set_err(TGS_ERR_VALIDATION, "count_pairs: no frame rendered yet");

@@ -790,6 +790,44 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
         launch(cols_place_kernel<16>);
 }
 
+// ReuseReport of the last frame's group lists (metrics.cpp:45-57) without materialising masks: a
+// splat's entry in group (gx, gy) has popcount wx(gx) * wy(gy), the numbers of its tile columns /
+// rows inside that group, so per splat the histogram is the product of two width histograms.
+__global__ void __launch_bounds__(256) reuse_hist_kernel(const FrameCounters* __restrict__ fc,
+                                                         const uint2* __restrict__ rect, GroupGeom gg,
+                                                         unsigned long long* __restrict__ hist) {
+    __shared__ unsigned long long h[17];
+    if (threadIdx.x < 17) h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t n = fc->n_input;
+    const int G = gg.g;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        int x0, x1, y0, y1;
+        const uint2 r = __ldg(&rect[i]);
+        if (r.x == kCulledRect && r.y == kCulledRect) continue;  // not projected
+        if (!decode_rect(r, x0, x1, y0, y1)) continue;
+        // band: keep tile rows of the band's group rows
+        y0 = max(y0, gg.band_gy0 * G);
+        y1 = min(y1, gg.band_gy1 * G - 1);
+        if (y1 < y0) continue;
+        uint32_t nx[5] = {0, 0, 0, 0, 0}, ny[5] = {0, 0, 0, 0, 0};
+        for (int g = x0 / G; g <= x1 / G; ++g) ++nx[min(x1, g * G + G - 1) - max(x0, g * G) + 1];
+        for (int g = y0 / G; g <= y1 / G; ++g) ++ny[min(y1, g * G + G - 1) - max(y0, g * G) + 1];
+        for (int wx = 1; wx <= G; ++wx)
+            for (int wy = 1; wy <= G; ++wy)
+                if (nx[wx] && ny[wy]) atomicAdd(&h[wx * wy], (unsigned long long)nx[wx] * ny[wy]);
+    }
+    __syncthreads();
+    if (threadIdx.x < 17 && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
+
+void launch_reuse_hist(const FrameCounters* fc, const uint2* rect, const GroupGeom& gg, int max_input,
+                       unsigned long long* hist, cudaStream_t st) {
+    cudaMemsetAsync(hist, 0, 17 * sizeof(unsigned long long), st);
+    const int blocks = std::max(1, std::min(148 * 4, (max_input + 255) / 256));
+    reuse_hist_kernel<<<blocks, 256, 0, st>>>(fc, rect, gg, hist);
+}
+
 void launch_lists_readback(const uint32_t* sorted_idx, const uint32_t* offsets, int n_groups,
                            DevProjected proj, GroupGeom gg, tgs_group_entry* out, cudaStream_t st) {
     if (n_groups > 0) lists_readback_kernel<<<n_groups, 256, 0, st>>>(sorted_idx, offsets, n_groups, proj, gg, out);

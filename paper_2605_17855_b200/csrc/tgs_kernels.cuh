@@ -95,6 +95,9 @@ void launch_unit_order(const uint32_t* offsets, const uint32_t* feedback, int n_
 void launch_raster_tensor(const RasterArgs& a, int num_sms, cudaStream_t st);
 // Instrumented walk: counts walked / alpha-contributing pairs (reference semantics, G=1 lists).
 void launch_count_pairs(const RasterArgs& a, cudaStream_t st);
+// mask-popcount histogram (17 bins, index = popcount) of the frame's group entries
+void launch_reuse_hist(const FrameCounters* fc, const uint2* rect, const GroupGeom& gg, int max_input,
+                       unsigned long long* hist, cudaStream_t st);
 void launch_encode_u8(const float* rgb, int64_t n, uint8_t* out, cudaStream_t st);
 
 }  // namespace tgs

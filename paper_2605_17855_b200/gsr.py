@@ -350,6 +350,14 @@ class Context:
         _check(self.lib.tgs_count_pairs(self.h, C.byref(w), C.byref(b)))
         return int(w.value), int(b.value)
 
+    def reuse_report(self) -> dict:
+        """ReuseReport of the last frame (reference load_reduction, metrics.cpp:45-57)."""
+        ng, nt, lr = C.c_uint64(), C.c_uint64(), C.c_double()
+        hist = (C.c_uint64 * 17)()
+        _check(self.lib.tgs_reuse_report(self.h, C.byref(ng), C.byref(nt), C.byref(lr), hist))
+        return {"n_group": int(ng.value), "n_total": int(nt.value), "load_reduction": float(lr.value),
+                "mask_popcount_hist": [int(v) for v in hist]}
+
     def encode_u8(self, img_device_ptr: int, n: int) -> np.ndarray:
         out = np.empty(n, np.uint8)
         _check(self.lib.tgs_encode_u8(self.h, C.c_void_p(img_device_ptr), n, out.ctypes.data))

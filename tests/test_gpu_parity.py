@@ -85,6 +85,26 @@ def test_lists_bitexact_vs_golden(gsr, ctx, golden, name, group):
 
 
 @pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("group", [1, 2, 4])
+def test_reuse_report_vs_golden_masks(gsr, ctx, golden, name, group):
+    """ReuseReport (metrics.cpp:45-57 load_reduction) is a pure function of the reference's entry
+    masks: recompute it from the golden lists and compare with the device-side report."""
+    g = golden[name]
+    cam = _cam(gsr, CASES[name]["camera"]())
+    ds = ctx.upload(g["records"])
+    ctx.render(ds, cam, _opt(gsr, 0 if group == 1 else 1, group))
+    ng = len(g[f"offsets_g{group}"]) - 1
+    ent, _ = ctx.read_lists(ng)
+    assert np.array_equal(ent.view(np.uint8), g[f"entries_g{group}"])
+    pc = np.unpackbits(np.ascontiguousarray(ent["mask"]).view(np.uint8).reshape(len(ent), -1), axis=1).sum(1)
+    hist = np.bincount(pc, minlength=17)[:17]
+    rep = ctx.reuse_report()
+    assert rep["mask_popcount_hist"] == [int(v) for v in hist]
+    assert rep["n_group"] == len(ent) and rep["n_total"] == int(pc.sum())
+    assert rep["load_reduction"] == pytest.approx(1.0 - len(ent) / int(pc.sum()), rel=0, abs=1e-15)
+
+
+@pytest.mark.parametrize("name", list(CASES))
 @pytest.mark.parametrize("backend,group,mode,tag", [
     (0, 1, 0, "scalar_g1"), (1, 1, 0, "tensor_g2"), (1, 2, 0, "tensor_g2"), (1, 4, 0, "tensor_g2"),
     (1, 2, 1, "tensor_g2"), (1, 4, 1, "tensor_g4_fp16")])

@@ -159,6 +159,8 @@ struct Smem {
         int tok, ticket, fill, s, open, emitted, done, nbat;
         uint32_t c, live;
     } ps;
+    int ring[8];              // per-stream producers: unit tickets, producer 0 -> producer 1
+    int ring_head, ring_tail;
 };
 
 template <int SLOTS>
@@ -345,6 +347,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
         sm.wdone[threadIdx.x] = threadIdx.x < kEpiWarps ? 0 : 0x7fffffff;
         sm.dead[threadIdx.x] = -1;
     }
+    if (threadIdx.x == 0) sm.ring_head = sm.ring_tail = 0;
     if (threadIdx.x == 0) {
         for (int h = 0; h < kNS; ++h) {
             for (int s = 0; s < kSS; ++s) {
@@ -382,7 +385,197 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
     [[maybe_unused]] unsigned long long pf[4] = {0, 0, 0, 0};
     [[maybe_unused]] const long long pf_start = clock64();
 
-    if (kNP == 2 && warp >= kProd && warp < kProd + kNP) {
+    if (kNS == 2 && kNP == 2 && warp >= kProd && warp < kProd + kNP) {
+        // ====================== one producer per chunk stream ====================================
+        // Producer h feeds stream h (member tiles 2h, 2h+1) only: it walks the unit's whole list
+        // but builds and places just the splats overlapping its tiles, and finishes the unit as
+        // soon as its own tiles are retired.  Producer 0 claims the units and hands the tickets to
+        // producer 1 through a small shared-memory ring, so both streams see the same unit order.
+        const int hs = warp - kProd;
+        const uint32_t my_tiles = hs == 0 ? 0x3u : 0xcu;
+        const float skip = a.alpha_skip, clampv = a.alpha_clamp;
+        const uint32_t lt = (1u << lane) - 1u;
+        uint32_t c = 0;
+        auto vld = [&](const int* p) { return *reinterpret_cast<const volatile int*>(p); };
+        auto open_stage = [&](uint32_t cc) {
+            const int s = (int)(cc % kSS);
+            if (cc >= (uint32_t)kSS && lane == 0) {
+                const unsigned int need = (unsigned int)kWPS * (cc / kSS);
+                if (ld_volatile_u32(&sm.done_cnt[hs][s]) < need) {
+                    const long long t0 = clock64();
+                    while (ld_volatile_u32(&sm.done_cnt[hs][s]) < need) {
+                        __nanosleep(32);
+                        if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producerS/done", (int)cc, s);
+                    }
+                    if (TGS_RASTER_PROF) pf[1] += clock64() - t0;
+                }
+            }
+            __syncwarp();
+            return s;
+        };
+        auto publish = [&](int s, int seq, int unit, int n_valid, uint32_t live) {
+            if (lane == 0) {
+                sm.hdr[hs][s].seq = seq;
+                sm.hdr[hs][s].unit = unit;
+                sm.hdr[hs][s].n_valid = n_valid;
+                sm.hdr[hs][s].live = (int)live;
+                sm.hdr[hs][s].chunk = (int)c;
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&sm.full[hs][s]);
+            __syncwarp();
+        };
+        for (int seq = 0;; ++seq) {
+            int t = 0;
+            if (lane == 0) {
+                const long long t0 = clock64();
+                if (hs == 0) {
+                    t = (int)atomicAdd(&a.fc->group_counter, 1u);
+                    while (vld(&sm.ring_head) - vld(&sm.ring_tail) >= 8)
+                        if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producerS/ring", seq, 0);
+                    sm.ring[seq & 7] = t;
+                    __threadfence_block();
+                    *reinterpret_cast<volatile int*>(&sm.ring_head) = seq + 1;
+                } else {
+                    while (vld(&sm.ring_head) <= seq)
+                        if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producerS/ring", seq, 1);
+                    t = vld(&sm.ring[seq & 7]);
+                    __threadfence_block();
+                    *reinterpret_cast<volatile int*>(&sm.ring_tail) = seq + 1;
+                }
+            }
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= n_units) break;
+            const int unit = a.order ? a.order[t] : t;
+            const UnitGeom ug = unit_geom<SLOTS>(gg, unit);
+            const uint32_t c_unit0 = c;
+            const uint32_t begin = a.offsets[ug.gid], end = a.offsets[ug.gid + 1];
+            const float ox = (float)(ug.tx0 * kTile) + centre, oy = (float)(ug.ty0 * kTile) + centre;
+            int fill = 0, s = 0;
+            bool open = false, emitted = false;
+            uint32_t live = ug.live;
+            const uint32_t nb = (end - begin + 31u) / 32u;
+            auto ld_idx = [&](uint32_t b) -> uint32_t {
+                const uint32_t e = begin + b * 32u + (uint32_t)lane;
+                return (b < nb && e < end) ? __ldg(&a.list[e]) : 0xffffffffu;
+            };
+            struct Rec {
+                float4 mc, co, col;
+                uint32_t idx;
+            };
+            auto ld_rec = [&](uint32_t idx) -> Rec {
+                Rec r;
+                r.idx = idx;
+                if (idx != 0xffffffffu) {
+                    r.mc = __ldg(&a.proj.mc[idx]);
+                    r.co = __ldg(&a.proj.co[idx]);
+                    r.col = __ldg(&a.proj.col[idx]);
+                } else {
+                    r.mc = r.co = r.col = make_float4(0, 0, 0, 0);
+                }
+                return r;
+            };
+            uint32_t n_batches = 0;
+            auto batch = [&](const Rec& cur) -> bool {
+                ++n_batches;
+                if (emitted) {  // this stream's tiles whose pixels all terminated
+                    uint32_t retired = 0xfu;
+#pragma unroll
+                    for (int w4 = 0; w4 < kEpiWarps; w4 += 4) {
+                        const int4 d = ld_volatile_v4(&sm.dead[w4]);
+                        const int dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int w = w4 + j;
+                            const uint32_t owned = 1u << (w >> 1);
+                            retired &= ((dd[j] >> 4) == seq ? (uint32_t)(dd[j] & 15) : 0u) | (0xfu & ~owned);
+                        }
+                    }
+                    retired = __shfl_sync(0xffffffffu, retired, 0);
+                    live &= ~retired;
+                    if ((live & my_tiles) == 0u) return true;
+                }
+                bool keep = false;
+                uint4 r0, r1;
+                float4 epi_v = make_float4(0, 0, 0, 0);
+                if (cur.idx != 0xffffffffu) {
+                    int x0, y0, x1, y1;
+                    tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1, y1);
+                    uint32_t cover = 0;
+#pragma unroll
+                    for (int k = 0; k < SLOTS; ++k) {
+                        const int tx = ug.tx0 + (k & 1), ty = ug.ty0 + (k >> 1);
+                        if (tx >= x0 && tx <= x1 && ty >= y0 && ty <= y1) cover |= 1u << k;
+                    }
+                    cover &= live;
+                    const float cj = fminf(clampv, cur.co.y);
+                    if ((cover & my_tiles) != 0u && !(cj < skip)) {
+                        keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox, oy,
+                                        cover, r0, r1);
+                        epi_v = make_float4(cur.col.x, cur.col.y, cur.col.z, cj);
+                    }
+                }
+                const uint32_t km = __ballot_sync(0xffffffffu, keep);
+                if (km == 0u) return false;
+                const int nk = __popc(km);
+                const int rank = __popc(km & lt);
+                if (!open) {
+                    s = open_stage(c);
+                    open = true;
+                    fill = 0;
+                }
+                int placed = 0;
+                for (;;) {
+                    const int room = kN - fill;
+                    if (keep && rank >= placed && rank - placed < room) {
+                        write_row(sm, hs, s, fill + rank - placed, r0, r1);
+                        sm.epi[hs][s][fill + rank - placed] = epi_v;
+                    }
+                    if (nk - placed < room) {
+                        fill += nk - placed;
+                        break;
+                    }
+                    publish(s, seq, unit, kN, live & my_tiles);
+                    ++c;
+                    emitted = true;
+                    s = open_stage(c);
+                    fill = 0;
+                    placed += room;
+                    if (placed == nk) break;
+                }
+                return false;
+            };
+            Rec qa = ld_rec(ld_idx(0)), qb = ld_rec(ld_idx(1));
+            uint32_t ia = ld_idx(2), ib = ld_idx(3);
+            for (uint32_t bi = 0; bi < nb; bi += 2) {
+                if (batch(qa)) break;
+                qa = ld_rec(ia);
+                ia = ld_idx(bi + 4);
+                if (bi + 1 >= nb) break;
+                if (batch(qb)) break;
+                qb = ld_rec(ib);
+                ib = ld_idx(bi + 5);
+            }
+            if (open && (fill > 0 || !emitted)) {
+                if (lane >= fill && lane < kN) {
+                    uint4 r0, r1;
+                    never_row(r0, r1);
+                    write_row(sm, hs, s, lane, r0, r1);
+                }
+                publish(s, seq, unit, fill, live & my_tiles);
+                ++c;
+            } else if (!open) {
+                s = open_stage(c);
+                publish(s, seq, unit, 0, live & my_tiles);
+                ++c;
+            }
+            if (hs == 0 && a.unit_cost && lane == 0)
+                a.unit_cost[unit] = 32u * n_batches + (uint32_t)kN * 2u * (c - c_unit0);
+        }
+        const int se = open_stage(c);  // end of stream
+        publish(se, -1, -1, 0, 0u);
+    } else if (kNS == 1 && kNP == 2 && warp >= kProd && warp < kProd + kNP) {
         // ======================== two producers (even / odd batches) ============================
         // Both warps walk the same unit: warp pw gathers and builds batches pw, pw+2, ...; a batch
         // is placed into the open chunk only when the shared token equals its index, so chunk

@@ -98,9 +98,8 @@ __device__ __forceinline__ void sh_color(const DevScene& s, int i, float dcr, fl
 // projection.cpp:79-114 project_gaussian (after frustum_cull passed).
 // Returns 1 kept, 0 degenerate (det <= 1e-12 or NaN), -1 non-positive scale.
 __device__ __forceinline__ int project_one(const DevScene& s, const DevCamera& cam, int i,
-                                           const float p[3], const float4& po, Proj& o) {
-    const float4 q = s.quat[i];
-    const float4 sd = s.scale_dcr[i];
+                                           const float p[3], const float4& po, const float4& q, const float4& sd,
+                                           const float2& gb, Proj& o) {
     // compute_cov3d (projection.cpp:36-43): Eigen minCoeff, then R * diag(s), M * M^T
     const float m12 = (sd.z < sd.y) ? sd.z : sd.y;
     const float mn = (m12 < sd.x) ? m12 : sd.x;
@@ -184,7 +183,6 @@ __device__ __forceinline__ int project_one(const DevScene& s, const DevCamera& c
         d[1] = fdiv(d[1], sn);
         d[2] = fdiv(d[2], sn);
     }
-    const float2 gb = s.dc_gb[i];
     float col[3];
     sh_color(s, i, sd.w, gb.x, gb.y, d, col);
     o.r = col[0];
@@ -210,7 +208,12 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a)
     Proj pr;
     float4 po = make_float4(0, 0, 0, 0);
     if (i < a.scene.n) {
+        // every SH0 plane is loaded up front (one memory latency instead of a dependent chain of
+        // three; the few culled splats waste 40 B each)
         po = a.scene.pos_op[i];
+        const float4 q = a.scene.quat[i];
+        const float4 sd = a.scene.scale_dcr[i];
+        const float2 gb = a.scene.dc_gb[i];
         float p[3];
         camera_space(a.cam, po.x, po.y, po.z, p);
         bool vis = p[2] > a.cam.near_ && p[2] < a.cam.far_;  // frustum_cull (projection.cpp:45-53)
@@ -223,7 +226,7 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a)
         if (!vis) {
             culled = true;
         } else {
-            const int rc = project_one(a.scene, a.cam, i, p, po, pr);
+            const int rc = project_one(a.scene, a.cam, i, p, po, q, sd, gb, pr);
             if (rc < 0) {
                 atomicOr(&a.fc->err_validation, 1u);
                 dropped = true;  // the reference throws; the host reports VALIDATION

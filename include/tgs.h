@@ -111,6 +111,13 @@ void tgs_ctx_destroy(tgs_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t) for callers that time with their own events. */
 void* tgs_ctx_stream(tgs_ctx* ctx);
 
+/* Rasteriser tile cull (default on, both backends): a splat is skipped for a tile (tensor: for a
+ * member tile of the unit) when the box of its alpha >= alpha_skip ellipse, padded half a pixel,
+ * misses the tile's pixel centres.  Images are identical either way (such a splat has
+ * alpha < alpha_skip on every pixel of the tile); off reproduces the reference's 3-sigma-square
+ * work (binning.cpp:32-44) for A/B measurement. */
+tgs_status tgs_set_tile_cull(tgs_ctx* ctx, int on);
+
 /* Persistent device-resident scene (SoA, float4 planes); amortises marshalling across frames. */
 tgs_status tgs_scene_upload(tgs_ctx* ctx, const float* records, int64_t count, int sh_degree,
                             tgs_scene** out);

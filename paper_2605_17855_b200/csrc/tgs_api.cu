@@ -126,6 +126,7 @@ struct tgs_ctx {
     // the parent's scenes, so frames of a batch overlap (tgs_render_batch)
     tgs_ctx* lanes[kBatchLanes - 1] = {};
     tgs_ctx* parent = nullptr;
+    int tile_cull = 1;  // tgs_set_tile_cull
     tgs_scene* scratch_scene = nullptr;
 };
 
@@ -319,6 +320,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     ra.fc = fc;
     ra.tile_trip = nullptr;
     ra.unit_cost = ctx->ucost.as<uint32_t>();
+    ra.tile_cull = ctx->tile_cull;
     static const bool skip_raster = std::getenv("TGS_DEBUG_SKIP_RASTER") != nullptr;  // bisection aid
     if (skip_raster) {
     } else if (opt->backend == TGS_BACKEND_SCALAR)
@@ -495,6 +497,14 @@ void tgs_ctx_destroy(tgs_ctx* c) {
 
 void* tgs_ctx_stream(tgs_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
+tgs_status tgs_set_tile_cull(tgs_ctx* ctx, int on) {
+    if (!ctx) return set_err(TGS_ERR_VALIDATION, "set_tile_cull: null context");
+    ctx->tile_cull = on ? 1 : 0;
+    for (tgs_ctx* l : ctx->lanes)
+        if (l) l->tile_cull = ctx->tile_cull;
+    return TGS_OK;
+}
+
 tgs_status tgs_scene_upload(tgs_ctx* ctx, const float* records, int64_t count, int sh_degree, tgs_scene** out) {
     if (!ctx || !out || (count > 0 && !records)) return set_err(TGS_ERR_VALIDATION, "scene_upload: null argument");
     tgs_scene* sc = new tgs_scene();
@@ -582,6 +592,7 @@ tgs_status tgs_render_batch(tgs_ctx* ctx, const tgs_scene* scene, const tgs_came
             tgs_status st = tgs_ctx_create(ctx->device, &ctx->lanes[k - 1]);
             if (st != TGS_OK) return st;
             ctx->lanes[k - 1]->parent = ctx;
+            ctx->lanes[k - 1]->tile_cull = ctx->tile_cull;
         }
         lane[k] = ctx->lanes[k - 1];
     }
@@ -728,6 +739,7 @@ tgs_status tgs_tile_trips(tgs_ctx* ctx, uint32_t* trips, int64_t cap, int64_t* n
     ra.fc = fc;
     ra.tile_trip = tmp.as<uint32_t>();
     ra.unit_cost = nullptr;
+    ra.tile_cull = 0;
     launch_count_pairs(ra, ctx->stream);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(trips, tmp.p, (size_t)tiles * 4, cudaMemcpyDeviceToHost, ctx->stream);
@@ -785,6 +797,7 @@ tgs_status tgs_count_pairs(tgs_ctx* ctx, uint64_t* walked, uint64_t* blended) {
     ra.fc = fc;
     ra.tile_trip = nullptr;
     ra.unit_cost = nullptr;
+    ra.tile_cull = 0;
     launch_count_pairs(ra, ctx->stream);
     TGS_CUDA_OK(cudaGetLastError());
     unsigned long long h[2];

@@ -131,6 +131,27 @@ __device__ __forceinline__ uint32_t group_mask(int gx, int gy, int g, int tx0, i
     return m;
 }
 
+// Member tiles whose pixel centres can see the splat at alpha >= alpha_skip: the axis-aligned box
+// of the ellipse  power >= ln(alpha_skip / o)  (conic (a, b, c); half-extents sqrt(2 lnt Sigma_xx),
+// sqrt(2 lnt Sigma_yy) with Sigma the 2D covariance), padded by half a pixel — far more than the
+// FP16 hi/lo error of D — so no pixel that could pass D >= log2(alpha_skip) is masked.  Tighter
+// than the reference's 3-sigma square (binning.cpp:32-44), which stays the list criterion.
+__device__ __forceinline__ uint32_t tight_cover(float mx, float my, float ca, float cb, float cc, float o,
+                                                float skip, int tx0, int ty0, int slots) {
+    const float det = ca * cc - cb * cb;
+    const float lnt = __logf(o / skip);
+    if (!(det > 0.0f) || !(lnt > 0.0f)) return (1u << slots) - 1u;  // keep the coarse test
+    const float s2 = 2.0f * lnt / det;
+    const float ex = sqrtf(s2 * cc) + 0.5f, ey = sqrtf(s2 * ca) + 0.5f;
+    uint32_t m = 0;
+    for (int k = 0; k < slots; ++k) {
+        const float px0 = (float)((tx0 + (k & 1)) * kTile) + 0.5f, py0 = (float)((ty0 + (k >> 1)) * kTile) + 0.5f;
+        if (mx - ex <= px0 + (kTile - 1) && mx + ex >= px0 && my - ey <= py0 + (kTile - 1) && my + ey >= py0)
+            m |= 1u << k;
+    }
+    return m;
+}
+
 }  // namespace tgs
 
 #define TGS_CUDA_OK(expr)                                                   \

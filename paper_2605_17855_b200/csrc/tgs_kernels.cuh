@@ -84,6 +84,7 @@ struct RasterArgs {
     FrameCounters* fc;
     uint32_t* tile_trip;      // optional (count_pairs): per tile, entries of its list walked until done
     uint32_t* unit_cost;      // optional: per unit, list entries walked (next frame's schedule)
+    int tile_cull;            // drop splats whose alpha_skip ellipse box misses the tile (tight_cover)
 };
 void launch_raster_scalar(const RasterArgs& a, cudaStream_t st);
 // LPT schedule for the rasterisers: work units (tile / group / quarter group, per_group units per

@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(256) raster_scalar_kernel(RasterArgs a) {
     __shared__ float4 s_geo[kBatch];  // mx, my, q1=-a/2*log2e, q2=-b*log2e
     __shared__ float4 s_gc[kBatch];   // q3=-c/2*log2e, opacity, r, g
     __shared__ float s_b[kBatch];     // b
+    __shared__ int s_wcnt[8];         // kept splats per warp of the staged batch
     const GroupGeom& gg = a.gg;
     const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;  // LPT order, as the tensor path
     const int tx = tile % gg.tiles_x, ty = tile / gg.tiles_x + gg.band_gy0;  // G == 1: group == tile
@@ -40,17 +41,40 @@ __global__ void __launch_bounds__(256) raster_scalar_kernel(RasterArgs a) {
     for (; base < end; base += kBatch) {
         if (__syncthreads_count(done) == kBatch) break;
         const uint32_t e = base + threadIdx.x;
+        // stage the batch, keeping (in list order) only splats that can reach alpha_skip on this
+        // tile: min(clamp, o) >= skip and the padded alpha_skip ellipse box meets the tile (the
+        // same test the tensor producer applies, tight_cover)
+        bool ok = false;
+        float4 G, H;
+        float B = 0.0f;
         if (e < end) {
             const uint32_t idx = a.list[e];
             const float4 mc = a.proj.mc[idx];
             const float4 co = a.proj.co[idx];
             const float4 col = a.proj.col[idx];
-            s_geo[threadIdx.x] = make_float4(mc.x, mc.y, -0.5f * mc.z * kLog2e, -mc.w * kLog2e);
-            s_gc[threadIdx.x] = make_float4(-0.5f * co.x * kLog2e, co.y, col.x, col.y);
-            s_b[threadIdx.x] = col.z;
+            ok = !(fminf(a.alpha_clamp, co.y) < a.alpha_skip) &&
+                 (!a.tile_cull || tight_cover(mc.x, mc.y, mc.z, mc.w, co.x, co.y, a.alpha_skip, tx, ty, 1) != 0u);
+            G = make_float4(mc.x, mc.y, -0.5f * mc.z * kLog2e, -mc.w * kLog2e);
+            H = make_float4(-0.5f * co.x * kLog2e, co.y, col.x, col.y);
+            B = col.z;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        if (lane == 0) s_wcnt[warp] = __popc(bal);
+        __syncthreads();
+        int pos = __popc(bal & ((1u << lane) - 1u)), n = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const int cw = s_wcnt[w];
+            if (w < warp) pos += cw;
+            n += cw;
+        }
+        if (ok) {
+            s_geo[pos] = G;
+            s_gc[pos] = H;
+            s_b[pos] = B;
         }
         __syncthreads();
-        const int n = (int)min((uint32_t)kBatch, end - base);
         if (!done) {
             for (int j = 0; j < n; ++j) {
                 const float4 g = s_geo[j];

@@ -278,6 +278,10 @@ class Context:
         except Exception:
             pass
 
+    def set_tile_cull(self, on: bool) -> None:
+        """Rasteriser tile cull by the alpha_skip ellipse box (default on; images identical)."""
+        _check(self.lib.tgs_set_tile_cull(self.h, 1 if on else 0))
+
     @property
     def stream(self) -> int:
         return int(self.lib.tgs_ctx_stream(self.h) or 0)

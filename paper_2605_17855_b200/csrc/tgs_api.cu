@@ -292,7 +292,9 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     ba.capacity = ctx->capacity;
     launch_binning(ba, n_alloc, s);
     {
-        const int per = gg.g == 4 ? 4 : 1;  // G=4 groups are rasterised as 2x2-tile quarters
+        // tensor G=4 groups are rasterised as 2x2-tile quarters (and G=2 groups as tile rows when
+        // built with half units); the CUDA-core baseline always walks whole lists
+        const int per = opt->backend == TGS_BACKEND_TENSOR ? raster_units_per_group(gg.g) : 1;
         // the previous frame's measured walks schedule this one when it had the same unit geometry
         // (same image, group size, band and backend): a camera path changes slowly
         const uint64_t key = ((uint64_t)(uint32_t)cam->width << 40) ^ ((uint64_t)(uint32_t)cam->height << 20) ^

@@ -94,6 +94,8 @@ void launch_raster_scalar(const RasterArgs& a, cudaStream_t st);
 void launch_unit_order(const uint32_t* offsets, const uint32_t* feedback, int n_units, int per_group, int* order,
                        cudaStream_t st);
 void launch_raster_tensor(const RasterArgs& a, int num_sms, cudaStream_t st);
+// raster work units per group list of the tensor path (schedule / feedback indexing)
+int raster_units_per_group(int g);
 // Instrumented walk: counts walked / alpha-contributing pairs (reference semantics, G=1 lists).
 void launch_count_pairs(const RasterArgs& a, cudaStream_t st);
 // mask-popcount histogram (17 bins, index = popcount) of the frame's group entries

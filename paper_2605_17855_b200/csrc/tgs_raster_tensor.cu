@@ -74,6 +74,21 @@ constexpr int kTS = TGS_RASTER_TS;  // TMEM accumulator stages
 #define TGS_RASTER_CTAS 1
 #endif
 constexpr int kCtasPerSm = TGS_RASTER_CTAS;  // resident CTAs per SM (TMEM columns must fit)
+#ifndef TGS_RASTER_CTAS_G1
+#define TGS_RASTER_CTAS_G1 1
+#endif
+#ifndef TGS_RASTER_SPW2
+#define TGS_RASTER_SPW2 4
+#endif
+#ifndef TGS_RASTER_HALF
+#define TGS_RASTER_HALF 0
+#endif
+// units per group and resident CTAs per SM of the SLOTS instance: SLOTS = 2 rasterises a G=2 group
+// as two half units (its top and bottom tile rows), two CTAs per SM (256 TMEM columns each)
+template <int SLOTS>
+constexpr int ctas_per_sm() { return SLOTS == 1 ? TGS_RASTER_CTAS_G1 : SLOTS == 2 ? 2 : kCtasPerSm; }
+template <int SLOTS>
+__host__ __device__ inline int units_per_group(int g) { return SLOTS == 2 ? 2 : (SLOTS == 4 && g == 4) ? 4 : 1; }
 #ifndef TGS_RASTER_JB
 #define TGS_RASTER_JB 16
 #endif
@@ -128,13 +143,13 @@ struct ChunkHeader {
 template <int SLOTS>
 struct Roles {
     static constexpr int kMT = 2 * SLOTS;
-    static constexpr int kSPW = SLOTS == 1 ? 1 : TGS_RASTER_SPW;  // slots (member tiles) per warp
+    static constexpr int kSPW = SLOTS == 1 ? 1 : SLOTS == 2 ? TGS_RASTER_SPW2 : TGS_RASTER_SPW;  // slots per warp
     static constexpr int kEpiWarps = 8 * SLOTS / kSPW;         // 16 (G>=2) or 8 (G=1)
     // producer warps: 2 split a unit's batches (even/odd) and place them in order by a token
     static constexpr int kNP = (SLOTS == 4 && TGS_RASTER_PRODUCERS == 2) ? 2 : 1;
     static constexpr int kThreads = (kEpiWarps + kNP + 1) * 32;
     static constexpr int kProd = kEpiWarps, kMma = kEpiWarps + kNP;
-    static constexpr bool kCompact = SLOTS == 4 && kSPW == 4 && TGS_RASTER_COMPACT;
+    static constexpr bool kCompact = SLOTS >= 2 && kSPW == 4 && TGS_RASTER_COMPACT;
     // chunk streams: with 2, the unit's top tile row (tiles 0,1: warps 0-3, M-tiles 0-3) and bottom
     // row (tiles 2,3: warps 4-7, M-tiles 4-7) get their own chunk streams carrying only the splats
     // that overlap them, and progress independently
@@ -293,22 +308,28 @@ __device__ __forceinline__ UnitGeom unit_geom(const GroupGeom& gg, int unit) {
         u.live = 1u;
         return u;
     }
-    // G == 2: unit == group; G == 4: unit == quarter (2x2 tiles) of a group
-    const int per = (gg.g == 4) ? 4 : 1;
+    // G == 2: unit == group (SLOTS 4) or tile row of a group (SLOTS 2); G == 4: unit == quarter
+    // (2x2 tiles) of a group
+    const int per = units_per_group<SLOTS>(gg.g);
     const int grp = unit / per, quarter = unit % per;
     const int gx = grp % gg.groups_x, gy = grp / gg.groups_x + gg.band_gy0;
-    u.tx0 = gx * gg.g + (quarter & 1) * 2;
-    u.ty0 = gy * gg.g + (quarter >> 1) * 2;
+    if (SLOTS == 2) {
+        u.tx0 = gx * gg.g;
+        u.ty0 = gy * gg.g + quarter;
+    } else {
+        u.tx0 = gx * gg.g + (quarter & 1) * 2;
+        u.ty0 = gy * gg.g + (quarter >> 1) * 2;
+    }
     u.gid = grp;
     u.live = 0u;
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
+    for (int t = 0; t < SLOTS; ++t)
         if (u.tx0 + (t & 1) < gg.tiles_x && u.ty0 + (t >> 1) < gg.tiles_y) u.live |= 1u << t;
     return u;
 }
 
 template <int SLOTS, int P2>
-__global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_tensor_kernel(RasterArgs a) {
+__global__ void __launch_bounds__(Roles<SLOTS>::kThreads, ctas_per_sm<SLOTS>()) raster_tensor_kernel(RasterArgs a) {
     using R = Roles<SLOTS>;
     constexpr int kMT = R::kMT, SPW = R::kSPW, kEpiWarps = R::kEpiWarps;
     constexpr int kProd = R::kProd, kMma = R::kMma, kNP = R::kNP;
@@ -321,7 +342,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
     Smem<SLOTS>& sm = *reinterpret_cast<Smem<SLOTS>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const GroupGeom& gg = a.gg;
-    const int n_units = (SLOTS == 1 || gg.g == 2) ? gg.n_groups_band : gg.n_groups_band * 4;
+    const int n_units = SLOTS == 1 ? gg.n_groups_band : gg.n_groups_band * units_per_group<SLOTS>(gg.g);
     const float centre = SLOTS == 1 ? 8.0f : 16.0f;
 
     // ---- setup: A operand (pixel monomials + tile one-hot), barriers, TMEM -----------------
@@ -1392,7 +1413,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                 // published in member-tile bits (compact: the warp's half of tile warp >> 1)
                 const uint32_t dtiles = kCompact ? (dead == (1u << SPW) - 1u ? 1u << (warp >> 1) : 0u) : dead << k0;
                 if (dead != reported) ((volatile int*)sm.dead)[warp] = (cur << 4) | (int)dtiles;
-                __threadfence_block();
+__threadfence_block();
                 ((volatile int*)sm.wdone)[warp] = (int)c + 1;
                 atomicAdd(&sm.done_cnt[hs][s], 1u);
             }
@@ -1427,7 +1448,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, kCtasPerSm) raster_ten
                 for (int u = 0; u < n_units && u < 65536; ++u)
                     if (g_ucyc[u] > best) { best = g_ucyc[u]; bu = u; }
                 if (bu < 0) break;
-                const int gid = SLOTS == 1 || gg.g == 2 ? bu : bu / 4;
+                const int gid = SLOTS == 1 ? bu : bu / units_per_group<SLOTS>(gg.g);
                 printf("RUNIT %d cycles %u chunks %u list %u started #%u | producer wait %u retire %u row %u place %u\n",
                        bu, best, g_uch[bu], a.offsets[gid + 1] - a.offsets[gid], g_uent[bu], g_uwait[bu],
                        g_usec[bu][0], g_usec[bu][1], g_usec[bu][2]);
@@ -1448,8 +1469,8 @@ template <int SLOTS, int P2>
 void launch_t(const RasterArgs& a, int num_sms, cudaStream_t st) {
     const size_t smem = sizeof(Smem<SLOTS>);
     cudaFuncSetAttribute(raster_tensor_kernel<SLOTS, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int n_units = (SLOTS == 1 || a.gg.g == 2) ? a.gg.n_groups_band : a.gg.n_groups_band * 4;
-    int grid = num_sms * kCtasPerSm;
+    const int n_units = SLOTS == 1 ? a.gg.n_groups_band : a.gg.n_groups_band * units_per_group<SLOTS>(a.gg.g);
+    int grid = num_sms * ctas_per_sm<SLOTS>();
     if (grid > n_units) grid = n_units;
     if (grid > 0) raster_tensor_kernel<SLOTS, P2><<<grid, Roles<SLOTS>::kThreads, smem, st>>>(a);
 }
@@ -1463,9 +1484,13 @@ void launch_raster_tensor(const RasterArgs& a, int num_sms, cudaStream_t st) {
     }();
     if (a.gg.g == 1)
         variant == 4 ? launch_t<1, 4>(a, num_sms, st) : launch_t<1, 0>(a, num_sms, st);
+    else if (a.gg.g == 2 && TGS_RASTER_HALF)
+        launch_t<2, 0>(a, num_sms, st);
     else
         variant == 4 ? launch_t<4, 4>(a, num_sms, st) : launch_t<4, 0>(a, num_sms, st);
 }
+
+int raster_units_per_group(int g) { return g == 1 ? 1 : (g == 2 && TGS_RASTER_HALF) ? 2 : g == 4 ? 4 : 1; }
 
 }  // namespace tgs
 

@@ -95,10 +95,12 @@ __device__ __forceinline__ float lg2_approx(float x) {
 __device__ __forceinline__ void tile_rect(float mx, float my, int radius, int tiles_x, int tiles_y,
                                           int& x0, int& y0, int& x1, int& y1) {
     const float r = (float)radius;
-    x0 = (int)floorf(__fdiv_rn(__fsub_rn(mx, r), 16.0f));
-    x1 = (int)floorf(__fdiv_rn(__fadd_rn(mx, r), 16.0f));
-    y0 = (int)floorf(__fdiv_rn(__fsub_rn(my, r), 16.0f));
-    y1 = (int)floorf(__fdiv_rn(__fadd_rn(my, r), 16.0f));
+    // x / 16 (binning.cpp:32-44) == x * 2^-4 exactly (same real value, same rounding), so the
+    // multiply is bit-identical to the reference's division and avoids the IEEE divide sequence
+    x0 = (int)floorf(__fmul_rn(__fsub_rn(mx, r), 0.0625f));
+    x1 = (int)floorf(__fmul_rn(__fadd_rn(mx, r), 0.0625f));
+    y0 = (int)floorf(__fmul_rn(__fsub_rn(my, r), 0.0625f));
+    y1 = (int)floorf(__fmul_rn(__fadd_rn(my, r), 0.0625f));
     x0 = max(x0, 0);
     y0 = max(y0, 0);
     x1 = min(x1, tiles_x - 1);

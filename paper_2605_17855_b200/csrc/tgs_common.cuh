@@ -140,11 +140,13 @@ __device__ __forceinline__ uint32_t group_mask(int gx, int gy, int g, int tx0, i
 // than the reference's 3-sigma square (binning.cpp:32-44), which stays the list criterion.
 __device__ __forceinline__ uint32_t tight_cover(float mx, float my, float ca, float cb, float cc, float o,
                                                 float skip, int tx0, int ty0, int slots) {
+    // approximate MUFU forms are fine here: the half-pixel pad dwarfs their ~1e-6 relative error
     const float det = ca * cc - cb * cb;
-    const float lnt = __logf(o / skip);
+    const float lnt = __logf(__fdividef(o, skip));
     if (!(det > 0.0f) || !(lnt > 0.0f)) return (1u << slots) - 1u;  // keep the coarse test
-    const float s2 = 2.0f * lnt / det;
-    const float ex = sqrtf(s2 * cc) + 0.5f, ey = sqrtf(s2 * ca) + 0.5f;
+    const float s2 = __fdividef(2.0f * lnt, det);
+    const float vx = s2 * cc, vy = s2 * ca;
+    const float ex = vx * rsqrtf(vx) + 0.5f, ey = vy * rsqrtf(vy) + 0.5f;
     uint32_t m = 0;
     for (int k = 0; k < slots; ++k) {
         const float px0 = (float)((tx0 + (k & 1)) * kTile) + 0.5f, py0 = (float)((ty0 + (k >> 1)) * kTile) + 0.5f;

@@ -92,9 +92,9 @@ __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, con
 #if TGS_MBAR_SPIN
     if ((threadIdx.x & 31) == 0 && !mbar_test(bar, parity)) {
         const long long t0 = clock64();
-        while (!mbar_test(bar, parity)) {
+        for (uint32_t i = 1; !mbar_test(bar, parity); ++i) {
             if (TGS_MBAR_SPIN > 1) __nanosleep(TGS_MBAR_SPIN);
-            if (clock64() - t0 > 4000000000ll) watchdog_trap(what, a0, a1);
+            if ((i & 63u) == 0u && clock64() - t0 > 4000000000ll) watchdog_trap(what, a0, a1);
         }
     }
     __syncwarp();

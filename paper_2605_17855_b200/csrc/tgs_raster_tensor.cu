@@ -122,12 +122,6 @@ constexpr bool kTightCover = TGS_RASTER_TIGHT;  // producer drops splats by the 
 #ifndef TGS_RASTER_PREFETCH4
 #define TGS_RASTER_PREFETCH4 0
 #endif
-#ifndef TGS_RASTER_PRODUCERS
-#define TGS_RASTER_PRODUCERS 1
-#endif
-#ifndef TGS_RASTER_PIPE
-#define TGS_RASTER_PIPE 0
-#endif
 #ifndef TGS_RASTER_STREAMS
 #define TGS_RASTER_STREAMS 1
 #endif
@@ -148,13 +142,8 @@ struct Roles {
     static constexpr int kMT = 2 * SLOTS;
     static constexpr int kSPW = SLOTS == 1 ? 1 : SLOTS == 2 ? TGS_RASTER_SPW2 : TGS_RASTER_SPW;  // slots per warp
     static constexpr int kEpiWarps = 8 * SLOTS / kSPW;         // 16 (G>=2) or 8 (G=1)
-    // producer warps: 2 split a unit's batches (even/odd) and place them in order by a token
-    static constexpr int kNP = (SLOTS == 4 && (TGS_RASTER_PRODUCERS == 2 || TGS_RASTER_PIPE)) ? 2 : 1;
-    // builder + placer: with TGS_RASTER_PIPE the two producer warps split each batch's work in a
-    // pipeline (gather/cover/rows -> ordered placement) through a shared-memory ring
-    static constexpr bool kPipe = kNP == 2 && TGS_RASTER_PIPE;
-    static constexpr int kThreads = (kEpiWarps + kNP + 1) * 32;
-    static constexpr int kProd = kEpiWarps, kMma = kEpiWarps + kNP;
+    static constexpr int kThreads = (kEpiWarps + 2) * 32;
+    static constexpr int kProd = kEpiWarps, kMma = kEpiWarps + 1;
     static constexpr bool kCompact = SLOTS >= 2 && kSPW == 4 && TGS_RASTER_COMPACT;
     // chunk streams: with 2, the unit's top tile row (tiles 0,1: warps 0-3, M-tiles 0-3) and bottom
     // row (tiles 2,3: warps 4-7, M-tiles 4-7) get their own chunk streams carrying only the splats
@@ -179,24 +168,6 @@ struct Smem {
     // once every epilogue warp's wdone passed the chunk that used it.
     unsigned int done_cnt[kNS][kSS];
     uint32_t tmem_base;
-    // shared producer state (two producer warps): placement token and the open chunk
-    struct {
-        int tok, ticket, fill, s, open, emitted, done, nbat;
-        uint32_t c, live;
-    } ps;
-    int ring[8];              // per-stream producers: unit tickets, producer 0 -> producer 1
-    int ring_head, ring_tail;
-    // builder -> placer ring (kPipe): per slot a batch of built rows or a unit boundary
-    static constexpr int kRing = (Roles<SLOTS>::kNP == 2 && TGS_RASTER_PIPE) ? 4 : 1;
-    struct PipeSlot {
-        uint4 r0[32], r1[32];
-        float4 epi[32];
-        uint32_t keep;   // lanes (list order) whose rows are valid
-        int kind;        // 0 batch, 1 unit begin, 2 unit end, 3 stream end
-        int unit, seq;
-        uint32_t live;
-    } pipe[kRing];
-    int pipe_full, pipe_free;  // slots published by the builder / released by the placer
 };
 
 template <int SLOTS>
@@ -349,9 +320,7 @@ template <int SLOTS, int P2>
 __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, ctas_per_sm<SLOTS>()) raster_tensor_kernel(RasterArgs a) {
     using R = Roles<SLOTS>;
     constexpr int kMT = R::kMT, SPW = R::kSPW, kEpiWarps = R::kEpiWarps;
-    constexpr int kProd = R::kProd, kMma = R::kMma, kNP = R::kNP;
-    constexpr bool kPipe = R::kPipe;
-    constexpr int kRing = Smem<SLOTS>::kRing;
+    constexpr int kProd = R::kProd, kMma = R::kMma;
     constexpr bool kCompact = R::kCompact;
     constexpr int kNS = R::kNS, kWPS = kEpiWarps / kNS, kMPS = kMT / kNS;  // warps, M-tiles per stream
     constexpr int kColsPerStage = kMT * kN;
@@ -391,7 +360,6 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, ctas_per_sm<SLOTS>()) 
         sm.wdone[threadIdx.x] = threadIdx.x < kEpiWarps ? 0 : 0x7fffffff;
         sm.dead[threadIdx.x] = -1;
     }
-    if (threadIdx.x == 0) sm.ring_head = sm.ring_tail = sm.pipe_full = sm.pipe_free = 0;
     if (threadIdx.x == 0) {
         for (int h = 0; h < kNS; ++h) {
             for (int s = 0; s < kSS; ++s) {
@@ -429,736 +397,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, ctas_per_sm<SLOTS>()) 
     [[maybe_unused]] unsigned long long pf[4] = {0, 0, 0, 0};
     [[maybe_unused]] const long long pf_start = clock64();
 
-    if (kPipe && warp >= kProd && warp < kProd + kNP) {
-        // ========================= builder + placer producer pipeline ============================
-        const bool builder = warp == kProd;
-        auto vld = [&](const int* p) { return *reinterpret_cast<const volatile int*>(p); };
-        auto vst = [&](int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; };
-        if (builder) {
-            const float skip = a.alpha_skip, clampv = a.alpha_clamp;
-            int nslot = 0;  // slots published
-            auto acquire = [&]() -> int {  // next free ring slot (lane 0 waits), returns index
-                if (lane == 0) {
-                    const long long t0 = clock64();
-                    while (nslot - vld(&sm.pipe_free) >= kRing) {
-                        if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("builder/ring", nslot, 0);
-                    }
-                }
-                __syncwarp();
-                return nslot % kRing;
-            };
-            auto release = [&]() {
-                __syncwarp();
-                if (lane == 0) {
-                    __threadfence_block();
-                    vst(&sm.pipe_full, ++nslot);
-                }
-                nslot = __shfl_sync(0xffffffffu, nslot, 0);
-            };
-            for (int seq = 0;; ++seq) {
-                int t = 0;
-                if (lane == 0) t = (int)atomicAdd(&a.fc->group_counter, 1u);
-                t = __shfl_sync(0xffffffffu, t, 0);
-                if (t >= n_units) break;
-                const int unit = a.order ? a.order[t] : t;
-                const UnitGeom ug = unit_geom<SLOTS>(gg, unit);
-                {
-                    const int k = acquire();
-                    if (lane == 0) {
-                        sm.pipe[k].kind = 1;
-                        sm.pipe[k].unit = unit;
-                        sm.pipe[k].seq = seq;
-                        sm.pipe[k].live = ug.live;
-                    }
-                    release();
-                }
-                const uint32_t begin = a.offsets[ug.gid], end = a.offsets[ug.gid + 1];
-                const float ox = (float)(ug.tx0 * kTile) + centre, oy = (float)(ug.ty0 * kTile) + centre;
-                uint32_t live = ug.live;
-                const uint32_t nb = (end - begin + 31u) / 32u;
-                auto ld_idx = [&](uint32_t b) -> uint32_t {
-                    const uint32_t e = begin + b * 32u + (uint32_t)lane;
-                    return (b < nb && e < end) ? __ldg(&a.list[e]) : 0xffffffffu;
-                };
-                struct Rec {
-                    float4 mc, co, col;
-                    uint32_t idx;
-                };
-                auto ld_rec = [&](uint32_t idx) -> Rec {
-                    Rec r;
-                    r.idx = idx;
-                    if (idx != 0xffffffffu) {
-                        r.mc = __ldg(&a.proj.mc[idx]);
-                        r.co = __ldg(&a.proj.co[idx]);
-                        r.col = __ldg(&a.proj.col[idx]);
-                    } else {
-                        r.mc = r.co = r.col = make_float4(0, 0, 0, 0);
-                    }
-                    return r;
-                };
-                uint32_t n_batches = 0;
-                auto batch = [&](const Rec& cur) -> bool {
-                    ++n_batches;
-                    {  // member tiles whose pixels all terminated (entries tagged with this unit)
-                        uint32_t retired = 0xfu;
-#pragma unroll
-                        for (int w4 = 0; w4 < kEpiWarps; w4 += 4) {
-                            const int4 d = ld_volatile_v4(&sm.dead[w4]);
-                            const int dd[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                const int w = w4 + j;
-                                const uint32_t owned = kCompact ? 1u << (w >> 1) : ((1u << SPW) - 1u) << ((w >> 3) * SPW);
-                                retired &= ((dd[j] >> 4) == seq ? (uint32_t)(dd[j] & 15) : 0u) | (0xfu & ~owned);
-                            }
-                        }
-                        retired = __shfl_sync(0xffffffffu, retired, 0);
-                        live &= ~retired;
-                        if (live == 0u) return true;
-                    }
-                    bool keep = false;
-                    uint4 r0, r1;
-                    float4 epi_v = make_float4(0, 0, 0, 0);
-                    if (cur.idx != 0xffffffffu) {
-                        int x0, y0, x1, y1;
-                        tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1, y1);
-                        uint32_t cover = 0;
-#pragma unroll
-                        for (int k = 0; k < SLOTS; ++k) {
-                            const int tx = ug.tx0 + (k & 1), ty = ug.ty0 + (k >> 1);
-                            if (tx >= x0 && tx <= x1 && ty >= y0 && ty <= y1) cover |= 1u << k;
-                        }
-                        cover &= live;
-                        const float cj = fminf(clampv, cur.co.y);
-                        if (kTightCover && a.tile_cull && cover != 0u && !(cj < skip))
-                            cover &= tight_cover(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, cur.co.y, skip,
-                                                 ug.tx0, ug.ty0, SLOTS);
-                        if (cover != 0u && !(cj < skip)) {
-                            keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox,
-                                            oy, cover, r0, r1);
-                            epi_v = make_float4(cur.col.x, cur.col.y, cur.col.z, cj);
-                        }
-                    }
-                    const uint32_t km = __ballot_sync(0xffffffffu, keep);
-                    if (km == 0u) return false;
-                    const int k = acquire();
-                    if (keep) {
-                        sm.pipe[k].r0[lane] = r0;
-                        sm.pipe[k].r1[lane] = r1;
-                        sm.pipe[k].epi[lane] = epi_v;
-                    }
-                    if (lane == 0) {
-                        sm.pipe[k].kind = 0;
-                        sm.pipe[k].keep = km;
-                        sm.pipe[k].live = live;
-                    }
-                    release();
-                    return false;
-                };
-                Rec qa = ld_rec(ld_idx(0)), qb = ld_rec(ld_idx(1));
-                uint32_t ia = ld_idx(2), ib = ld_idx(3);
-                for (uint32_t bi = 0; bi < nb; bi += 2) {
-                    if (batch(qa)) break;
-                    qa = ld_rec(ia);
-                    ia = ld_idx(bi + 4);
-                    if (bi + 1 >= nb) break;
-                    if (batch(qb)) break;
-                    qb = ld_rec(ib);
-                    ib = ld_idx(bi + 5);
-                }
-                {
-                    const int k = acquire();
-                    if (lane == 0) {
-                        sm.pipe[k].kind = 2;
-                        sm.pipe[k].unit = (int)n_batches;  // walked batches (schedule feedback)
-                        sm.pipe[k].live = live;
-                    }
-                    release();
-                }
-            }
-            const int k = acquire();
-            if (lane == 0) sm.pipe[k].kind = 3;
-            release();
-        } else {
-            // placer: consumes the ring in order and fills / publishes the chunks
-            const uint32_t lt = (1u << lane) - 1u;
-            uint32_t c = 0;
-            int ntaken = 0;
-            auto open_stage = [&](uint32_t cc) {
-                const int s = (int)(cc % kSS);
-                if (cc >= (uint32_t)kSS && lane == 0) {
-                    const unsigned int need = (unsigned int)kEpiWarps * (cc / kSS);
-                    if (ld_volatile_u32(&sm.done_cnt[0][s]) < need) {
-                        const long long t0 = clock64();
-                        while (ld_volatile_u32(&sm.done_cnt[0][s]) < need) {
-                            __nanosleep(32);
-                            if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("placer/done", (int)cc, s);
-                        }
-                    }
-                }
-                __syncwarp();
-                return s;
-            };
-            auto publish = [&](int s, int seq, int unit, int n_valid, uint32_t live) {
-                if (lane == 0) {
-                    sm.hdr[0][s].seq = seq;
-                    sm.hdr[0][s].unit = unit;
-                    sm.hdr[0][s].n_valid = n_valid;
-                    sm.hdr[0][s].live = (int)live;
-                    sm.hdr[0][s].chunk = (int)c;
-                }
-                ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&sm.full[0][s]);
-                __syncwarp();
-            };
-            int seq = 0, unit = 0, fill = 0, s = 0;
-            bool open = false, emitted = false;
-            uint32_t live = 0, c_unit0 = 0;
-            for (;;) {
-                if (lane == 0) {
-                    const long long t0 = clock64();
-                    while (vld(&sm.pipe_full) <= ntaken)
-                        if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("placer/ring", ntaken, 0);
-                }
-                __syncwarp();
-                __threadfence_block();
-                const int k = ntaken % kRing;
-                const int kind = __shfl_sync(0xffffffffu, lane == 0 ? vld(&sm.pipe[k].kind) : 0, 0);
-                if (kind == 3) break;
-                if (kind == 1) {
-                    unit = __shfl_sync(0xffffffffu, lane == 0 ? vld(&sm.pipe[k].unit) : 0, 0);
-                    seq = __shfl_sync(0xffffffffu, lane == 0 ? vld(&sm.pipe[k].seq) : 0, 0);
-                    live = (uint32_t)__shfl_sync(0xffffffffu, lane == 0 ? vld((const int*)&sm.pipe[k].live) : 0, 0);
-                    fill = 0;
-                    open = false;
-                    emitted = false;
-                    c_unit0 = c;
-                } else if (kind == 0) {
-                    const uint32_t km = (uint32_t)__shfl_sync(0xffffffffu, lane == 0 ? vld((const int*)&sm.pipe[k].keep) : 0, 0);
-                    live = (uint32_t)__shfl_sync(0xffffffffu, lane == 0 ? vld((const int*)&sm.pipe[k].live) : 0, 0);
-                    const bool keep = (km >> lane) & 1u;
-                    const int nk = __popc(km), rank = __popc(km & lt);
-                    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0;
-                    float4 epi_v = make_float4(0, 0, 0, 0);
-                    if (keep) {
-                        r0 = sm.pipe[k].r0[lane];
-                        r1 = sm.pipe[k].r1[lane];
-                        epi_v = sm.pipe[k].epi[lane];
-                    }
-                    if (!open) {
-                        s = open_stage(c);
-                        open = true;
-                        fill = 0;
-                    }
-                    int placed = 0;
-                    for (;;) {
-                        const int room = kN - fill;
-                        if (keep && rank >= placed && rank - placed < room) {
-                            write_row(sm, 0, s, fill + rank - placed, r0, r1);
-                            sm.epi[0][s][fill + rank - placed] = epi_v;
-                        }
-                        if (nk - placed < room) {
-                            fill += nk - placed;
-                            break;
-                        }
-                        publish(s, seq, unit, kN, live);
-                        ++c;
-                        emitted = true;
-                        s = open_stage(c);
-                        fill = 0;
-                        placed += room;
-                        if (placed == nk) break;
-                    }
-                } else {  // unit end
-                    const int nbat = __shfl_sync(0xffffffffu, lane == 0 ? vld(&sm.pipe[k].unit) : 0, 0);
-                    live = (uint32_t)__shfl_sync(0xffffffffu, lane == 0 ? vld((const int*)&sm.pipe[k].live) : 0, 0);
-                    if (open && (fill > 0 || !emitted)) {
-                        if (lane >= fill && lane < kN) {
-                            uint4 r0, r1;
-                            never_row(r0, r1);
-                            write_row(sm, 0, s, lane, r0, r1);
-                        }
-                        publish(s, seq, unit, fill, live);
-                        ++c;
-                    } else if (!open) {
-                        s = open_stage(c);
-                        publish(s, seq, unit, 0, live);
-                        ++c;
-                    }
-                    if (a.unit_cost && lane == 0) a.unit_cost[unit] = 32u * (uint32_t)nbat + (uint32_t)kN * (c - c_unit0);
-                }
-                __syncwarp();
-                ++ntaken;
-                if (lane == 0) vst(&sm.pipe_free, ntaken);
-            }
-            const int se = open_stage(c);  // end of stream
-            publish(se, -1, -1, 0, 0u);
-        }
-    } else if (kNS == 2 && kNP == 2 && warp >= kProd && warp < kProd + kNP) {
-        // ====================== one producer per chunk stream ====================================
-        // Producer h feeds stream h (member tiles 2h, 2h+1) only: it walks the unit's whole list
-        // but builds and places just the splats overlapping its tiles, and finishes the unit as
-        // soon as its own tiles are retired.  Producer 0 claims the units and hands the tickets to
-        // producer 1 through a small shared-memory ring, so both streams see the same unit order.
-        const int hs = warp - kProd;
-        const uint32_t my_tiles = hs == 0 ? 0x3u : 0xcu;
-        const float skip = a.alpha_skip, clampv = a.alpha_clamp;
-        const uint32_t lt = (1u << lane) - 1u;
-        uint32_t c = 0;
-        auto vld = [&](const int* p) { return *reinterpret_cast<const volatile int*>(p); };
-        auto open_stage = [&](uint32_t cc) {
-            const int s = (int)(cc % kSS);
-            if (cc >= (uint32_t)kSS && lane == 0) {
-                const unsigned int need = (unsigned int)kWPS * (cc / kSS);
-                if (ld_volatile_u32(&sm.done_cnt[hs][s]) < need) {
-                    const long long t0 = clock64();
-                    while (ld_volatile_u32(&sm.done_cnt[hs][s]) < need) {
-                        __nanosleep(32);
-                        if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producerS/done", (int)cc, s);
-                    }
-                    if (TGS_RASTER_PROF) pf[1] += clock64() - t0;
-                }
-            }
-            __syncwarp();
-            return s;
-        };
-        auto publish = [&](int s, int seq, int unit, int n_valid, uint32_t live) {
-            if (lane == 0) {
-                sm.hdr[hs][s].seq = seq;
-                sm.hdr[hs][s].unit = unit;
-                sm.hdr[hs][s].n_valid = n_valid;
-                sm.hdr[hs][s].live = (int)live;
-                sm.hdr[hs][s].chunk = (int)c;
-            }
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&sm.full[hs][s]);
-            __syncwarp();
-        };
-        for (int seq = 0;; ++seq) {
-            int t = 0;
-            if (lane == 0) {
-                const long long t0 = clock64();
-                if (hs == 0) {
-                    t = (int)atomicAdd(&a.fc->group_counter, 1u);
-                    while (vld(&sm.ring_head) - vld(&sm.ring_tail) >= 8)
-                        if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producerS/ring", seq, 0);
-                    sm.ring[seq & 7] = t;
-                    __threadfence_block();
-                    *reinterpret_cast<volatile int*>(&sm.ring_head) = seq + 1;
-                } else {
-                    while (vld(&sm.ring_head) <= seq)
-                        if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producerS/ring", seq, 1);
-                    t = vld(&sm.ring[seq & 7]);
-                    __threadfence_block();
-                    *reinterpret_cast<volatile int*>(&sm.ring_tail) = seq + 1;
-                }
-            }
-            t = __shfl_sync(0xffffffffu, t, 0);
-            if (t >= n_units) break;
-            const int unit = a.order ? a.order[t] : t;
-            const UnitGeom ug = unit_geom<SLOTS>(gg, unit);
-            const uint32_t c_unit0 = c;
-            const uint32_t begin = a.offsets[ug.gid], end = a.offsets[ug.gid + 1];
-            const float ox = (float)(ug.tx0 * kTile) + centre, oy = (float)(ug.ty0 * kTile) + centre;
-            int fill = 0, s = 0;
-            bool open = false, emitted = false;
-            uint32_t live = ug.live;
-            const uint32_t nb = (end - begin + 31u) / 32u;
-            auto ld_idx = [&](uint32_t b) -> uint32_t {
-                const uint32_t e = begin + b * 32u + (uint32_t)lane;
-                return (b < nb && e < end) ? __ldg(&a.list[e]) : 0xffffffffu;
-            };
-            struct Rec {
-                float4 mc, co, col;
-                uint32_t idx;
-            };
-            auto ld_rec = [&](uint32_t idx) -> Rec {
-                Rec r;
-                r.idx = idx;
-                if (idx != 0xffffffffu) {
-                    r.mc = __ldg(&a.proj.mc[idx]);
-                    r.co = __ldg(&a.proj.co[idx]);
-                    r.col = __ldg(&a.proj.col[idx]);
-                } else {
-                    r.mc = r.co = r.col = make_float4(0, 0, 0, 0);
-                }
-                return r;
-            };
-            uint32_t n_batches = 0;
-            auto batch = [&](const Rec& cur) -> bool {
-                ++n_batches;
-                if (emitted) {  // this stream's tiles whose pixels all terminated
-                    uint32_t retired = 0xfu;
-#pragma unroll
-                    for (int w4 = 0; w4 < kEpiWarps; w4 += 4) {
-                        const int4 d = ld_volatile_v4(&sm.dead[w4]);
-                        const int dd[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int w = w4 + j;
-                            const uint32_t owned = 1u << (w >> 1);
-                            retired &= ((dd[j] >> 4) == seq ? (uint32_t)(dd[j] & 15) : 0u) | (0xfu & ~owned);
-                        }
-                    }
-                    retired = __shfl_sync(0xffffffffu, retired, 0);
-                    live &= ~retired;
-                    if ((live & my_tiles) == 0u) return true;
-                }
-                bool keep = false;
-                uint4 r0, r1;
-                float4 epi_v = make_float4(0, 0, 0, 0);
-                if (cur.idx != 0xffffffffu) {
-                    int x0, y0, x1, y1;
-                    tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1, y1);
-                    uint32_t cover = 0;
-#pragma unroll
-                    for (int k = 0; k < SLOTS; ++k) {
-                        const int tx = ug.tx0 + (k & 1), ty = ug.ty0 + (k >> 1);
-                        if (tx >= x0 && tx <= x1 && ty >= y0 && ty <= y1) cover |= 1u << k;
-                    }
-                    cover &= live;
-                    const float cj = fminf(clampv, cur.co.y);
-                    if ((cover & my_tiles) != 0u && !(cj < skip)) {
-                        keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox, oy,
-                                        cover, r0, r1);
-                        epi_v = make_float4(cur.col.x, cur.col.y, cur.col.z, cj);
-                    }
-                }
-                const uint32_t km = __ballot_sync(0xffffffffu, keep);
-                if (km == 0u) return false;
-                const int nk = __popc(km);
-                const int rank = __popc(km & lt);
-                if (!open) {
-                    s = open_stage(c);
-                    open = true;
-                    fill = 0;
-                }
-                int placed = 0;
-                for (;;) {
-                    const int room = kN - fill;
-                    if (keep && rank >= placed && rank - placed < room) {
-                        write_row(sm, hs, s, fill + rank - placed, r0, r1);
-                        sm.epi[hs][s][fill + rank - placed] = epi_v;
-                    }
-                    if (nk - placed < room) {
-                        fill += nk - placed;
-                        break;
-                    }
-                    publish(s, seq, unit, kN, live & my_tiles);
-                    ++c;
-                    emitted = true;
-                    s = open_stage(c);
-                    fill = 0;
-                    placed += room;
-                    if (placed == nk) break;
-                }
-                return false;
-            };
-            Rec qa = ld_rec(ld_idx(0)), qb = ld_rec(ld_idx(1));
-            uint32_t ia = ld_idx(2), ib = ld_idx(3);
-            for (uint32_t bi = 0; bi < nb; bi += 2) {
-                if (batch(qa)) break;
-                qa = ld_rec(ia);
-                ia = ld_idx(bi + 4);
-                if (bi + 1 >= nb) break;
-                if (batch(qb)) break;
-                qb = ld_rec(ib);
-                ib = ld_idx(bi + 5);
-            }
-            if (open && (fill > 0 || !emitted)) {
-                if (lane >= fill && lane < kN) {
-                    uint4 r0, r1;
-                    never_row(r0, r1);
-                    write_row(sm, hs, s, lane, r0, r1);
-                }
-                publish(s, seq, unit, fill, live & my_tiles);
-                ++c;
-            } else if (!open) {
-                s = open_stage(c);
-                publish(s, seq, unit, 0, live & my_tiles);
-                ++c;
-            }
-            if (hs == 0 && a.unit_cost && lane == 0)
-                a.unit_cost[unit] = 32u * n_batches + (uint32_t)kN * 2u * (c - c_unit0);
-        }
-        const int se = open_stage(c);  // end of stream
-        publish(se, -1, -1, 0, 0u);
-    } else if (!kPipe && kNS == 1 && kNP == 2 && warp >= kProd && warp < kProd + kNP) {
-        // ======================== two producers (even / odd batches) ============================
-        // Both warps walk the same unit: warp pw gathers and builds batches pw, pw+2, ...; a batch
-        // is placed into the open chunk only when the shared token equals its index, so chunk
-        // contents keep list order.  The open-chunk state lives in shared memory and is handed
-        // over with the token; the warp that filled rows fences them to the async proxy before
-        // handing over, so whichever warp publishes the chunk publishes rows of both.
-        const int pw = warp - kProd;
-        const float skip = a.alpha_skip, clampv = a.alpha_clamp;
-        const uint32_t lt = (1u << lane) - 1u;
-        auto bar_prod = [&]() { asm volatile("bar.sync 1, 64;" ::: "memory"); };
-        auto vld = [&](const int* p) { return *reinterpret_cast<const volatile int*>(p); };
-        auto vst = [&](int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; };
-        auto open_stage = [&](uint32_t cc) {
-            const int s = (int)(cc % kSS);
-            if (cc >= (uint32_t)kSS && lane == 0) {
-                const unsigned int need = (unsigned int)kEpiWarps * (cc / kSS);
-                if (ld_volatile_u32(&sm.done_cnt[0][s]) < need) {
-                    const long long t0 = clock64();
-                    while (ld_volatile_u32(&sm.done_cnt[0][s]) < need) {
-                        __nanosleep(32);
-                        if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producer2/done", (int)cc, s);
-                    }
-                    if (TGS_RASTER_PROF) pf[1] += clock64() - t0;
-                }
-            }
-            __syncwarp();
-            return s;
-        };
-        auto publish = [&](int s, uint32_t cc, int seq, int unit, int n_valid, uint32_t live) {
-            if (lane == 0) {
-                sm.hdr[0][s].seq = seq;
-                sm.hdr[0][s].unit = unit;
-                sm.hdr[0][s].n_valid = n_valid;
-                sm.hdr[0][s].live = (int)live;
-                sm.hdr[0][s].chunk = (int)cc;
-            }
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&sm.full[0][s]);
-            __syncwarp();
-        };
-        if (pw == 0 && lane == 0) sm.ps.c = 0;
-        for (int seq = 0;; ++seq) {
-            if (pw == 0) {
-                int t = 0;
-                if (lane == 0) t = (int)atomicAdd(&a.fc->group_counter, 1u);
-                t = __shfl_sync(0xffffffffu, t, 0);
-                if (lane == 0) {
-                    sm.ps.ticket = t;
-                    sm.ps.tok = 0;
-                    sm.ps.fill = 0;
-                    sm.ps.s = 0;
-                    sm.ps.open = 0;
-                    sm.ps.emitted = 0;
-                    sm.ps.done = 0;
-                    sm.ps.nbat = 0;
-                    sm.ps.live = t < n_units ? unit_geom<SLOTS>(gg, a.order ? a.order[t] : t).live : 0u;
-                }
-                __syncwarp();
-            }
-            bar_prod();
-            const int t = __shfl_sync(0xffffffffu, lane == 0 ? vld(&sm.ps.ticket) : 0, 0);
-            if (t >= n_units) break;
-            const int unit = a.order ? a.order[t] : t;
-            const UnitGeom ug = unit_geom<SLOTS>(gg, unit);
-            const uint32_t begin = a.offsets[ug.gid], end = a.offsets[ug.gid + 1];
-            const float ox = (float)(ug.tx0 * kTile) + centre, oy = (float)(ug.ty0 * kTile) + centre;
-            const uint32_t nb = (end - begin + 31u) / 32u;
-            auto ld_idx = [&](uint32_t b) -> uint32_t {
-                const uint32_t e = begin + b * 32u + (uint32_t)lane;
-                return (b < nb && e < end) ? __ldg(&a.list[e]) : 0xffffffffu;
-            };
-            struct Rec {
-                float4 mc, co, col;
-                uint32_t idx;
-            };
-            auto ld_rec = [&](uint32_t idx) -> Rec {
-                Rec r;
-                r.idx = idx;
-                if (idx != 0xffffffffu) {
-                    r.mc = __ldg(&a.proj.mc[idx]);
-                    r.co = __ldg(&a.proj.co[idx]);
-                    r.col = __ldg(&a.proj.col[idx]);
-                } else {
-                    r.mc = r.co = r.col = make_float4(0, 0, 0, 0);
-                }
-                return r;
-            };
-            // one batch: retire check, row build, then ordered placement under the token
-            auto batch = [&](const Rec& cur, uint32_t bi) -> bool {
-                int done = 0, emitted = 0;
-                uint32_t live = 0;
-                if (lane == 0) {
-                    done = vld(&sm.ps.done);
-                    emitted = vld(&sm.ps.emitted);
-                    live = (uint32_t)vld(reinterpret_cast<const int*>(&sm.ps.live));
-                }
-                done = __shfl_sync(0xffffffffu, done, 0);
-                emitted = __shfl_sync(0xffffffffu, emitted, 0);
-                live = __shfl_sync(0xffffffffu, live, 0);
-                if (done) return true;
-                if (emitted) {  // drop member tiles whose pixels all terminated (all owner warps)
-                    uint32_t retired = 0xfu;
-#pragma unroll
-                    for (int w4 = 0; w4 < kEpiWarps; w4 += 4) {
-                        const int4 d = ld_volatile_v4(&sm.dead[w4]);
-                        const int dd[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int w = w4 + j;
-                            const uint32_t owned = kCompact ? 1u << (w >> 1) : ((1u << SPW) - 1u) << ((w >> 3) * SPW);
-                            retired &= ((dd[j] >> 4) == seq ? (uint32_t)(dd[j] & 15) : 0u) | (0xfu & ~owned);
-                        }
-                    }
-                    retired = __shfl_sync(0xffffffffu, retired, 0);
-                    live &= ~retired;
-                    if (live == 0u) {
-                        if (lane == 0) vst(&sm.ps.done, 1);
-                        return true;
-                    }
-                }
-                bool keep = false;
-                uint4 r0, r1;
-                float4 epi_v = make_float4(0, 0, 0, 0);
-                if (cur.idx != 0xffffffffu) {
-                    int x0, y0, x1, y1;
-                    tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1, y1);
-                    uint32_t cover = 0;
-#pragma unroll
-                    for (int k = 0; k < SLOTS; ++k) {
-                        const int tx = ug.tx0 + (k & 1), ty = ug.ty0 + (k >> 1);
-                        if (tx >= x0 && tx <= x1 && ty >= y0 && ty <= y1) cover |= 1u << k;
-                    }
-                    cover &= live;
-                    const float cj = fminf(clampv, cur.co.y);
-                    if (cover != 0u && !(cj < skip)) {
-                        keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox, oy,
-                                        cover, r0, r1);
-                        epi_v = make_float4(cur.col.x, cur.col.y, cur.col.z, cj);
-                    }
-                }
-                const uint32_t km = __ballot_sync(0xffffffffu, keep);
-                // wait for this batch's turn (or the unit's end)
-                if (lane == 0) {
-                    const long long t0 = clock64();
-                    while (vld(&sm.ps.tok) != (int)bi && !vld(&sm.ps.done)) {
-                        if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producer2/token", (int)bi, unit);
-                    }
-                    done = vld(&sm.ps.done);
-                }
-                done = __shfl_sync(0xffffffffu, done, 0);
-                if (done) return true;
-                // place under the token: open-chunk state from shared memory
-                int fill = 0, s = 0, open = 0;
-                uint32_t c = 0, slive = 0;
-                if (lane == 0) {
-                    fill = vld(&sm.ps.fill);
-                    s = vld(&sm.ps.s);
-                    open = vld(&sm.ps.open);
-                    emitted = vld(&sm.ps.emitted);
-                    c = (uint32_t)vld(reinterpret_cast<const int*>(&sm.ps.c));
-                    slive = (uint32_t)vld(reinterpret_cast<const int*>(&sm.ps.live)) & live;
-                }
-                fill = __shfl_sync(0xffffffffu, fill, 0);
-                s = __shfl_sync(0xffffffffu, s, 0);
-                open = __shfl_sync(0xffffffffu, open, 0);
-                emitted = __shfl_sync(0xffffffffu, emitted, 0);
-                c = __shfl_sync(0xffffffffu, c, 0);
-                slive = __shfl_sync(0xffffffffu, slive, 0);
-                if (km != 0u) {
-                    const int nk = __popc(km);
-                    const int rank = __popc(km & lt);
-                    if (!open) {
-                        s = open_stage(c);
-                        open = 1;
-                        fill = 0;
-                    }
-                    int placed = 0;
-                    for (;;) {
-                        const int room = kN - fill;
-                        if (keep && rank >= placed && rank - placed < room) {
-                            write_row(sm, 0, s, fill + rank - placed, r0, r1);
-                            sm.epi[0][s][fill + rank - placed] = epi_v;
-                        }
-                        if (nk - placed < room) {
-                            fill += nk - placed;
-                            break;
-                        }
-                        publish(s, c, seq, unit, kN, slive);
-                        ++c;
-                        emitted = 1;
-                        s = open_stage(c);
-                        fill = 0;
-                        placed += room;
-                        if (placed == nk) break;
-                    }
-                }
-                // rows of the open chunk must be visible to the async proxy whichever warp publishes
-                ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    vst(&sm.ps.fill, fill);
-                    vst(&sm.ps.s, s);
-                    vst(&sm.ps.open, open);
-                    vst(&sm.ps.emitted, emitted);
-                    vst(reinterpret_cast<int*>(&sm.ps.c), (int)c);
-                    vst(reinterpret_cast<int*>(&sm.ps.live), (int)slive);
-                    vst(&sm.ps.nbat, (int)bi + 1);
-                    __threadfence_block();
-                    vst(&sm.ps.tok, (int)bi + 1);
-                }
-                __syncwarp();
-                return false;
-            };
-            // my batches pw, pw + 2, ...: two record slots, refilled four batches ahead of use
-            const uint32_t b0 = (uint32_t)pw;
-            Rec qa = ld_rec(ld_idx(b0)), qb = ld_rec(ld_idx(b0 + 2));
-            uint32_t ia = ld_idx(b0 + 4), ib = ld_idx(b0 + 6);
-            for (uint32_t bi = b0; bi < nb; bi += 4) {
-                if (batch(qa, bi)) break;
-                qa = ld_rec(ia);
-                ia = ld_idx(bi + 8);
-                if (bi + 2 >= nb) break;
-                if (batch(qb, bi + 2)) break;
-                qb = ld_rec(ib);
-                ib = ld_idx(bi + 10);
-            }
-            bar_prod();  // every placement of the unit is done
-            if (pw == 0) {
-                // close the unit: pad and publish the partial chunk (or an empty one)
-                int fill = 0, s = 0, open = 0, emitted = 0, nbat = 0;
-                uint32_t c = 0, live = 0;
-                if (lane == 0) {
-                    fill = vld(&sm.ps.fill);
-                    s = vld(&sm.ps.s);
-                    open = vld(&sm.ps.open);
-                    emitted = vld(&sm.ps.emitted);
-                    nbat = vld(&sm.ps.nbat);
-                    c = (uint32_t)vld(reinterpret_cast<const int*>(&sm.ps.c));
-                    live = (uint32_t)vld(reinterpret_cast<const int*>(&sm.ps.live));
-                }
-                fill = __shfl_sync(0xffffffffu, fill, 0);
-                s = __shfl_sync(0xffffffffu, s, 0);
-                open = __shfl_sync(0xffffffffu, open, 0);
-                emitted = __shfl_sync(0xffffffffu, emitted, 0);
-                nbat = __shfl_sync(0xffffffffu, nbat, 0);
-                c = __shfl_sync(0xffffffffu, c, 0);
-                live = __shfl_sync(0xffffffffu, live, 0);
-                const uint32_t c_unit0 = c;
-                if (open && (fill > 0 || !emitted)) {
-                    if (lane >= fill && lane < kN) {
-                        uint4 r0, r1;
-                        never_row(r0, r1);
-                        write_row(sm, 0, s, lane, r0, r1);
-                    }
-                    publish(s, c, seq, unit, fill, live);
-                    ++c;
-                } else if (!open) {
-                    s = open_stage(c);
-                    publish(s, c, seq, unit, 0, live);
-                    ++c;
-                }
-                if (lane == 0) sm.ps.c = c;
-                if (a.unit_cost && lane == 0) a.unit_cost[unit] = 32u * (uint32_t)nbat + (uint32_t)kN * (c - c_unit0 + 1u);
-                __syncwarp();
-            }
-        }
-        if (pw == 0) {  // end of stream
-            const uint32_t c = (uint32_t)__shfl_sync(0xffffffffu, lane == 0 ? vld(reinterpret_cast<const int*>(&sm.ps.c)) : 0, 0);
-            const int se = open_stage(c);
-            publish(se, c, -1, -1, 0, 0u);
-        }
-    } else if (kNP == 1 && warp == kProd) {
+    if (warp == kProd) {
         // ================================ producer ===========================================
         const float skip = a.alpha_skip, clampv = a.alpha_clamp;
         uint32_t c[kNS];  // chunks emitted so far, per stream

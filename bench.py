@@ -285,7 +285,7 @@ def main():
     else:
         achieved = alg_bytes[dom] / (stages[dom] / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "kernel": {"binning": "rank_gather + rows_count/place + cols_count/place + scans",
+                "traffic": traffic, "kernel": {"binning": "rows_count/place + cols_count/place + scans",
                                                "sort": "depth presort (digit histograms + 4 one-sweep passes)",
                                                "preprocess": "preprocess_kernel"}[dom],
                 "algorithmic_bytes": alg_bytes[dom]}
@@ -351,10 +351,10 @@ def main():
         except Exception as e:  # reported, never fatal for the GPU number
             cpu = {"value": None, "unit": "frames/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
-    # our kernels per frame (profiles/r01/launches_bench_r01f.csv): preprocess 1; depth presort:
-    # digit histograms + 4 one-sweep passes; binning: rank gather, rows count, 3-kernel scan, rows
-    # meta, rows place, cols count, 3-kernel scan, offsets, cols place; unit order 1; raster 1
-    launches_per_frame = 1 + 5 + 13 + 1 + 1
+    # our kernels per frame: preprocess 1; depth presort: digit histograms + 4 one-sweep passes;
+    # binning: rows count (with the rank gather), 3-kernel scan, rows meta, rows place, cols count,
+    # 3-kernel scan, offsets, cols place; unit order 1; raster 1
+    launches_per_frame = 1 + 5 + 12 + 1 + 1
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",

@@ -6,8 +6,8 @@
 // on (group_id << 32) | f32_bits(depth) (ties: emission order = splat index).  Here the splats are
 // first radix-sorted by depth bits (tgs_sort.cu, values = splat index, so ties keep index order) —
 // their "rank" order.  Every group's list is then the rank-ordered subsequence of splats
-// overlapping it, built by two stable partitions that write each entry once:
-//   gather : rank-ordered tile rectangles (8 B per splat);
+// overlapping it, built by two stable partitions that write each entry once (the level-1 count
+// also gathers the rank-ordered tile rectangles, 8 B per splat, for the placement pass):
 //   level 1: splats -> group-row lists.  Each warp owns a contiguous rank range (chunk); per-row
 //            counts (1D difference array) -> scan over (row, chunk) -> every lane owns some rows
 //            and appends the chunk's splats to them in rank order (8-byte row entries: splat
@@ -65,16 +65,6 @@ __device__ __forceinline__ void chunk_range(uint32_t n, int n_chunks, int w, uin
     r1 = min(n, r0 + per);
 }
 
-__global__ void __launch_bounds__(256) rank_gather_kernel(BinArgs a) {
-    const uint32_t n = *a.visible;
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
-        a.rrect[r] = __ldg(&a.rect[__ldg(&a.sval[r])]);
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-
 // ---- level 1: splats -> group-row lists -----------------------------------------------------
 // A "chunk" is one warp's contiguous rank range.  Row entries are (splat index, gx0 | gx1 << 16)
 // and row y's list is the concatenation over chunks of the chunk's splats overlapping row y.
@@ -93,7 +83,10 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_count_kernel(BinArgs a) {
     uint32_t ent = 0;
     for (uint32_t r = r0 + lane; r < r1; r += 32) {
         int gx0, gx1, gy0, gy1;
-        if (!band_groups(a.gg, __ldg(&a.rrect[r]), gx0, gx1, gy0, gy1)) continue;
+        // gather the rank-ordered rectangle once here (rows_place reads it back coalesced)
+        const uint2 rr = __ldg(&a.rect[__ldg(&a.sval[r])]);
+        a.rrect[r] = rr;
+        if (!band_groups(a.gg, rr, gx0, gx1, gy0, gy1)) continue;
         atomicAdd(&D[gy0], 1);
         atomicAdd(&D[gy1 + 1], -1);
         ent += (uint32_t)((gx1 - gx0 + 1) * (gy1 - gy0 + 1));
@@ -739,8 +732,7 @@ void launch_exclusive_scan(uint32_t* x, size_t n, uint32_t* tmp, cudaStream_t st
 void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     const GroupGeom& gg = a.gg;
     const int rows = gg.band_gy1 - gg.band_gy0, gx = gg.groups_x;
-    const int gblocks = std::max(1, std::min(148 * 8, (max_visible + 255) / 256));
-    rank_gather_kernel<<<gblocks, 256, 0, st>>>(a);
+    (void)max_visible;
     // level 1
     const size_t n1 = bin_hist1_elems(gg);
     rows_count_kernel<<<kRowChunks / kBinWarps, kBinWarps * 32, kBinWarps * (rows + 1) * sizeof(int), st>>>(a);

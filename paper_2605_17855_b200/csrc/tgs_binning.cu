@@ -65,6 +65,10 @@ __device__ __forceinline__ void chunk_range(uint32_t n, int n_chunks, int w, uin
     r1 = min(n, r0 + per);
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
 // ---- level 1: splats -> group-row lists -----------------------------------------------------
 // A "chunk" is one warp's contiguous rank range.  Row entries are (splat index, gx0 | gx1 << 16)
 // and row y's list is the concatenation over chunks of the chunk's splats overlapping row y.

@@ -224,24 +224,22 @@ __device__ __forceinline__ bool make_row(float mx, float my, float qa, float qb,
     w[4] = fmaf(qb, dx, qc * dy) * kLog2e;
     const float quad = fmaf(ha * dx, dx, fmaf(qb * dx, dy, hc * dy * dy));
     w[5] = fmaf(-quad, kLog2e, lo2);
-    bool ok = true;
-    float h[6], l[6];
+    const float amax = fmaxf(fmaxf(fmaxf(fabsf(w[0]), fabsf(w[1])), fmaxf(fabsf(w[2]), fabsf(w[3]))),
+                             fmaxf(fabsf(w[4]), fabsf(w[5])));
+    const bool ok = amax <= 16384.0f;
+    // hi halves packed pairwise (RN, as element-wise __float2half_rn), lo = w - hi (exact), packed
+    uint32_t hp[3], lp[3];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-        ok = ok && fabsf(w[k]) <= 16384.0f;
-        h[k] = __half2float(__float2half_rn(w[k]));
-        l[k] = w[k] - h[k];
+    for (int k = 0; k < 3; ++k) {
+        const __half2 h2 = __floats2half2_rn(w[2 * k], w[2 * k + 1]);
+        const float2 hf = __half22float2(h2);
+        hp[k] = *reinterpret_cast<const uint32_t*>(&h2);
+        lp[k] = pack_half2(w[2 * k] - hf.x, w[2 * k + 1] - hf.y);
     }
     const float m0 = (cover & 1u) ? 0.0f : kNeverRow, m1 = (cover & 2u) ? 0.0f : kNeverRow;
     const float m2 = (cover & 4u) ? 0.0f : kNeverRow, m3 = (cover & 8u) ? 0.0f : kNeverRow;
-    r0.x = pack_half2(h[0], h[1]);
-    r0.y = pack_half2(h[2], h[3]);
-    r0.z = pack_half2(h[4], h[5]);
-    r0.w = pack_half2(l[0], l[1]);
-    r1.x = pack_half2(l[2], l[3]);
-    r1.y = pack_half2(l[4], l[5]);
-    r1.z = pack_half2(m0, m1);
-    r1.w = pack_half2(m2, m3);
+    r0 = make_uint4(hp[0], hp[1], hp[2], lp[0]);
+    r1 = make_uint4(lp[1], lp[2], pack_half2(m0, m1), pack_half2(m2, m3));
     return ok;
 }
 

@@ -256,6 +256,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     pa.rect = ctx->rect.as<uint2>();
     pa.gg = gg;
     pa.fc = fc;
+    pa.alpha_skip = opt->alpha_skip;
     launch_preprocess(pa, s);
     TGS_CUDA_OK(cudaGetLastError());
     TGS_CUDA_OK(cudaEventRecord(ctx->ev[1], s));

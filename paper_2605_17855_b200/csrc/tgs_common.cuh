@@ -133,24 +133,32 @@ __device__ __forceinline__ uint32_t group_mask(int gx, int gy, int g, int tx0, i
     return m;
 }
 
-// Member tiles whose pixel centres can see the splat at alpha >= alpha_skip: the axis-aligned box
-// of the ellipse  power >= ln(alpha_skip / o)  (conic (a, b, c); half-extents sqrt(2 lnt Sigma_xx),
-// sqrt(2 lnt Sigma_yy) with Sigma the 2D covariance), padded by half a pixel — far more than the
-// FP16 hi/lo error of D — so no pixel that could pass D >= log2(alpha_skip) is masked.  Tighter
-// than the reference's 3-sigma square (binning.cpp:32-44), which stays the list criterion.
-__device__ __forceinline__ uint32_t tight_cover(float mx, float my, float ca, float cb, float cc, float o,
-                                                float skip, int tx0, int ty0, int slots) {
-    // approximate MUFU forms are fine here: the half-pixel pad dwarfs their ~1e-6 relative error
+// Tile cull (rasterisers, tgs_set_tile_cull): the axis-aligned box of the ellipse
+// power >= ln(alpha_skip / o)  (conic (a, b, c); half-extents sqrt(2 lnt Sigma_xx), sqrt(2 lnt
+// Sigma_yy) with Sigma the 2D covariance) padded by half a pixel — far more than the FP16 hi/lo error
+// of the tensor path's D — contains every pixel centre where the splat can reach alpha_skip.  The
+// preprocess stores the padded half-extents as a half2 rounded up (a superset) in col.w; +inf
+// halves mean "no bound" (opacity at or below alpha_skip, degenerate conic).  Tighter than the
+// reference's 3-sigma square (binning.cpp:32-44), which stays the list criterion.
+__device__ __forceinline__ float tight_extents(float ca, float cb, float cc, float o, float skip) {
     const float det = ca * cc - cb * cb;
-    const float lnt = __logf(__fdividef(o, skip));
-    if (!(det > 0.0f) || !(lnt > 0.0f)) return (1u << slots) - 1u;  // keep the coarse test
-    const float s2 = __fdividef(2.0f * lnt, det);
-    const float vx = s2 * cc, vy = s2 * ca;
-    const float ex = vx * rsqrtf(vx) + 0.5f, ey = vy * rsqrtf(vy) + 0.5f;
+    const float lnt = logf(o / skip);
+    __half2 e = __halves2half2(__ushort_as_half((unsigned short)0x7c00u), __ushort_as_half((unsigned short)0x7c00u));
+    if (det > 0.0f && lnt > 0.0f) {
+        const float s2 = 2.0f * lnt / det;
+        e = __halves2half2(__float2half_ru(sqrtf(s2 * cc) + 0.5f), __float2half_ru(sqrtf(s2 * ca) + 0.5f));
+    }
+    return __uint_as_float(*reinterpret_cast<const uint32_t*>(&e));
+}
+
+// Member tiles (bit k: tile (tx0 + (k & 1), ty0 + (k >> 1))) whose pixel centres meet the box.
+__device__ __forceinline__ uint32_t tight_cover(float mx, float my, float ext, int tx0, int ty0, int slots) {
+    const uint32_t eb = __float_as_uint(ext);
+    const float2 e = __half22float2(*reinterpret_cast<const __half2*>(&eb));
     uint32_t m = 0;
     for (int k = 0; k < slots; ++k) {
         const float px0 = (float)((tx0 + (k & 1)) * kTile) + 0.5f, py0 = (float)((ty0 + (k >> 1)) * kTile) + 0.5f;
-        if (mx - ex <= px0 + (kTile - 1) && mx + ex >= px0 && my - ey <= py0 + (kTile - 1) && my + ey >= py0)
+        if (mx - e.x <= px0 + (kTile - 1) && mx + e.x >= px0 && my - e.y <= py0 + (kTile - 1) && my + e.y >= py0)
             m |= 1u << k;
     }
     return m;

@@ -15,6 +15,7 @@ struct PreprocessArgs {
                                    //     kCulledRect twice: not projected)
     GroupGeom gg;
     FrameCounters* fc;
+    float alpha_skip;              // for the tile-cull extents stored in col.w (tight_extents)
 };
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t st);
 

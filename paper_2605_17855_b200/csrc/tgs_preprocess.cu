@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a)
         if (keep) {
             a.out.mc[i] = make_float4(pr.mx, pr.my, pr.a, pr.b);
             a.out.co[i] = make_float4(pr.c, po.w, pr.depth, __int_as_float(pr.radius));
-            a.out.col[i] = make_float4(pr.r, pr.g, pr.bl, 0.0f);
+            a.out.col[i] = make_float4(pr.r, pr.g, pr.bl, tight_extents(pr.a, pr.b, pr.c, po.w, a.alpha_skip));
             a.depth_keys[i] = __float_as_uint(pr.depth);
             int tx0, ty0, tx1, ty1, gx0, gy0, gx1, gy1;
             const int ng = group_rect(pr.mx, pr.my, pr.radius, a.gg, tx0, ty0, tx1, ty1, gx0, gy0, gx1, gy1);

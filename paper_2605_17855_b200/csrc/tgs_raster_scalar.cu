@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256) raster_scalar_kernel(RasterArgs a) {
             const float4 co = a.proj.co[idx];
             const float4 col = a.proj.col[idx];
             ok = !(fminf(a.alpha_clamp, co.y) < a.alpha_skip) &&
-                 (!a.tile_cull || tight_cover(mc.x, mc.y, mc.z, mc.w, co.x, co.y, a.alpha_skip, tx, ty, 1) != 0u);
+                 (!a.tile_cull || tight_cover(mc.x, mc.y, col.w, tx, ty, 1) != 0u);
             G = make_float4(mc.x, mc.y, -0.5f * mc.z * kLog2e, -mc.w * kLog2e);
             H = make_float4(-0.5f * co.x * kLog2e, co.y, col.x, col.y);
             B = col.z;

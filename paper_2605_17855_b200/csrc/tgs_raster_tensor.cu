@@ -530,8 +530,7 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, ctas_per_sm<SLOTS>()) 
                         cover &= live;
                         const float cj = fminf(clampv, cur.co.y);
                         if (kTightCover && a.tile_cull && cover != 0u && !(cj < skip))
-                            cover &= tight_cover(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, cur.co.y, skip,
-                                                 ug.tx0, ug.ty0, SLOTS);
+                            cover &= tight_cover(cur.mc.x, cur.mc.y, cur.col.w, ug.tx0, ug.ty0, SLOTS);
                         if (cover != 0u && !(cj < skip)) {
                             keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox,
                                             oy, cover, r0, r1);

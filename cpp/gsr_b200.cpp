@@ -4,6 +4,9 @@
 // binning.cpp:22-30), and maps tgs_status onto the reference's exception types.
 #include "gsr_b200.hpp"
 
+#include <cmath>
+#include <fstream>
+#include <iterator>
 #include <cstring>
 #include <string>
 
@@ -161,4 +164,98 @@ RenderResult DeviceScene::render(const Camera& cam, const RenderOptions& opt) {
 }
 
 }  // namespace b200
+// ---- .gsb scene files (scene_io.cpp:43-136 semantics) ------------------------------------------
+namespace {
+constexpr char kGsbMagic[4] = {'G', 'S', 'B', '1'};
+constexpr size_t kGsbHeader = 16;
+
+std::uint32_t le_u32(const unsigned char* p) {
+    return (std::uint32_t)p[0] | ((std::uint32_t)p[1] << 8) | ((std::uint32_t)p[2] << 16) | ((std::uint32_t)p[3] << 24);
+}
+float le_f32(const unsigned char* p) {
+    const std::uint32_t u = le_u32(p);
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+void put_le(std::string& out, std::uint32_t v) {
+    for (int k = 0; k < 4; ++k) out.push_back(static_cast<char>((v >> (8 * k)) & 0xffu));
+}
+void put_le(std::string& out, float f) {
+    std::uint32_t u;
+    std::memcpy(&u, &f, 4);
+    put_le(out, u);
+}
+}  // namespace
+
+std::vector<Gaussian3D> load_scene(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw FormatError("cannot open scene file: " + path);
+    const std::string bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    const auto* b = reinterpret_cast<const unsigned char*>(bytes.data());
+    if (bytes.size() < kGsbHeader)
+        throw FormatError(path + ": truncated header at byte offset " + std::to_string(bytes.size()) + " (need 16)");
+    if (std::memcmp(b, kGsbMagic, 4) != 0) throw FormatError(path + ": bad magic at byte offset 0");
+    const std::uint32_t count = le_u32(b + 4), degree = le_u32(b + 8);
+    if (degree != 0 && degree != 3) throw FormatError(path + ": unsupported sh_degree at byte offset 8");
+    const size_t rec_bytes = (degree == 3 ? 59u : 14u) * 4u;
+    const size_t need = kGsbHeader + static_cast<size_t>(count) * rec_bytes;
+    if (bytes.size() < need)
+        throw FormatError(path + ": truncated payload at byte offset " + std::to_string(bytes.size()) + " (need " +
+                          std::to_string(need) + ")");
+    std::vector<Gaussian3D> scene(count);
+    for (std::uint32_t i = 0; i < count; ++i) {
+        const unsigned char* p = b + kGsbHeader + static_cast<size_t>(i) * rec_bytes;
+        Gaussian3D& g = scene[i];
+        g.mean = Eigen::Vector3f(le_f32(p), le_f32(p + 4), le_f32(p + 8));
+        g.scale = Eigen::Vector3f(le_f32(p + 12), le_f32(p + 16), le_f32(p + 20));
+        g.rotation = Eigen::Quaternionf(le_f32(p + 24), le_f32(p + 28), le_f32(p + 32), le_f32(p + 36));
+        g.opacity = le_f32(p + 40);
+        g.sh_dc = Eigen::Vector3f(le_f32(p + 44), le_f32(p + 48), le_f32(p + 52));
+        if (degree == 3) {
+            std::array<float, kShRestCoeffs> rest{};
+            for (int k = 0; k < kShRestCoeffs; ++k) rest[static_cast<size_t>(k)] = le_f32(p + 56 + 4 * k);
+            g.sh_rest = rest;
+        }
+        const std::string at = path + ": scene record " + std::to_string(i);
+        if (!(g.opacity >= 0.0f && g.opacity <= 1.0f)) throw ValidationError(at + ": opacity outside [0,1]");
+        if (!g.mean.allFinite() || !g.scale.allFinite()) throw ValidationError(at + ": non-finite mean or scale");
+        if (!(g.scale.minCoeff() > 0.0f)) throw ValidationError(at + ": non-positive scale");
+        // the reference renormalises only drifted quaternions, so unit ones round-trip bit-exactly
+        const float n = g.rotation.norm();
+        if (!(n > 0.0f) || !std::isfinite(n))
+            throw ValidationError("scene record " + std::to_string(i) + ": quaternion has non-finite or zero norm");
+        if (std::fabs(n - 1.0f) > 1e-6f) g.rotation.coeffs() /= n;
+    }
+    return scene;
+}
+
+void save_scene(const std::vector<Gaussian3D>& gaussians, const std::string& path) {
+    size_t with_rest = 0;
+    for (const auto& g : gaussians) with_rest += g.sh_rest.has_value() ? 1u : 0u;
+    if (with_rest != 0 && with_rest != gaussians.size())
+        throw ValidationError("save_scene: mixed sh_rest presence across records");
+    const std::uint32_t degree = with_rest != 0 ? 3u : 0u;
+    std::string out(kGsbMagic, 4);
+    put_le(out, static_cast<std::uint32_t>(gaussians.size()));
+    put_le(out, degree);
+    put_le(out, 0u);
+    for (const auto& g : gaussians) {
+        for (int k = 0; k < 3; ++k) put_le(out, g.mean[k]);
+        for (int k = 0; k < 3; ++k) put_le(out, g.scale[k]);
+        put_le(out, g.rotation.w());
+        put_le(out, g.rotation.x());
+        put_le(out, g.rotation.y());
+        put_le(out, g.rotation.z());
+        put_le(out, g.opacity);
+        for (int k = 0; k < 3; ++k) put_le(out, g.sh_dc[k]);
+        if (degree == 3)
+            for (float v : *g.sh_rest) put_le(out, v);
+    }
+    std::ofstream f(path, std::ios::binary | std::ios::trunc);
+    if (!f) throw FormatError("cannot open for writing: " + path);
+    f.write(out.data(), static_cast<std::streamsize>(out.size()));
+    if (!f) throw FormatError("write failed: " + path);
+}
+
 }  // namespace gsr

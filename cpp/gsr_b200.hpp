@@ -27,6 +27,7 @@
 #include <memory>
 #include <optional>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 namespace gsr {
@@ -129,6 +130,11 @@ struct RenderResult {
 /// Drop-in for the reference's gsr::render: uploads the scene, renders on the current B200
 /// (device 0 unless gsr::b200::set_device was called), downloads the image.
 RenderResult render(const std::vector<Gaussian3D>& scene, const Camera& cam, const RenderOptions& opt);
+
+// .gsb scene files (scene_io.hpp:42-43): same byte layout, checks, messages and quaternion
+// renormalisation as the reference (FormatError / ValidationError).
+std::vector<Gaussian3D> load_scene(const std::string& path);
+void save_scene(const std::vector<Gaussian3D>& gaussians, const std::string& path);
 
 namespace b200 {
 

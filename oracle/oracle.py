@@ -221,6 +221,27 @@ class Ref(_Base):
     def hardware_concurrency(self) -> int:
         return int(self.lib.gref_hardware_concurrency())
 
+    def save_scene(self, rec, path: str) -> None:
+        rec = np.ascontiguousarray(rec, dtype=np.float32)
+        deg = 3 if rec.shape[1] == 59 else 0
+        rc = self.lib.gref_save_scene(_f32p(rec), C.c_int64(len(rec)), C.c_int(deg), path.encode())
+        if rc:
+            raise RuntimeError(f"reference save_scene failed ({rc}): {self.last_error()}")
+
+    def load_scene(self, path: str):
+        """(records, None) or (None, (code, message)) when the reference throws."""
+        cnt, deg = C.c_int64(), C.c_int()
+        rc = self.lib.gref_load_scene(path.encode(), None, C.c_int64(0), C.byref(cnt), C.byref(deg))
+        if rc:
+            return None, (rc, self.last_error())
+        rf = 59 if deg.value == 3 else 14
+        out = np.zeros((cnt.value, rf), np.float32)
+        rc = self.lib.gref_load_scene(path.encode(), _f32p(out), C.c_int64(out.size), C.byref(cnt),
+                                      C.byref(deg))
+        if rc:
+            return None, (rc, self.last_error())
+        return out, None
+
     def raster_projected(self, proj, width, height, **opt):
         proj = np.ascontiguousarray(proj, dtype=PROJ_DTYPE)
         img = np.zeros((height, width, 3), dtype=np.float32)

@@ -356,6 +356,51 @@ int gref_load_reduction(const CProjected* proj, std::int64_t n, int width, int h
     }
 }
 
+// save_scene / load_scene (scene_io.cpp:43-136) through the reference, for the .gsb I/O parity
+// tests: records in .gsb order (14 or 59 floats per Gaussian).
+int gref_save_scene(const float* rec, std::int64_t n, int deg, const char* path) {
+    try {
+        gsr::save_scene(to_scene(rec, n, deg), path);
+        return 0;
+    } catch (const gsr::ValidationError& e) {
+        return fail(e, 1);
+    } catch (const gsr::FormatError& e) {
+        return fail(e, 2);
+    } catch (const std::exception& e) {
+        return fail(e, 9);
+    }
+}
+
+// *count / *deg of the file; out (cap floats) receives the records when large enough.
+int gref_load_scene(const char* path, float* out, std::int64_t cap, std::int64_t* count, int* deg) {
+    try {
+        const auto s = gsr::load_scene(path);
+        const int d = (!s.empty() && s[0].sh_rest) ? 3 : 0;
+        const int rf = d == 3 ? 59 : 14;
+        *count = static_cast<std::int64_t>(s.size());
+        *deg = d;
+        if (cap < *count * rf) return 0;
+        for (size_t i = 0; i < s.size(); ++i) {
+            float* p = out + i * rf;
+            const auto& g = s[i];
+            p[0] = g.mean.x(); p[1] = g.mean.y(); p[2] = g.mean.z();
+            p[3] = g.scale.x(); p[4] = g.scale.y(); p[5] = g.scale.z();
+            p[6] = g.rotation.w(); p[7] = g.rotation.x(); p[8] = g.rotation.y(); p[9] = g.rotation.z();
+            p[10] = g.opacity;
+            p[11] = g.sh_dc.x(); p[12] = g.sh_dc.y(); p[13] = g.sh_dc.z();
+            if (d == 3)
+                for (int k = 0; k < 45; ++k) p[14 + k] = (*g.sh_rest)[static_cast<size_t>(k)];
+        }
+        return 0;
+    } catch (const gsr::ValidationError& e) {
+        return fail(e, 1);
+    } catch (const gsr::FormatError& e) {
+        return fail(e, 2);
+    } catch (const std::exception& e) {
+        return fail(e, 9);
+    }
+}
+
 // encode_ppm (scene_io.cpp:253-263) payload bytes (header stripped) for parity of the u8 path.
 int gref_encode_ppm(const float* rgb, int width, int height, std::uint8_t* out) {
     gsr::ImageBuffer img(width, height);

@@ -489,6 +489,73 @@ def max_abs_diff(a, b) -> float:
     return float(np.max(np.abs(a - b))) if a.size else 0.0
 
 
+_GSB_MAGIC = b"GSB1"
+_GSB_HEADER = 16
+
+
+def save_scene(scene, path: str) -> None:
+    """save_scene (scene_io.cpp:103-136): 16-byte header (magic "GSB1", u32 count, u32 sh_degree,
+    u32 reserved 0) then little-endian float32 records (14, or 59 with sh_rest)."""
+    sc = as_scene(scene)
+    deg = sc.sh_degree if len(sc) else 0
+    head = _GSB_MAGIC + np.array([len(sc), deg, 0], dtype="<u4").tobytes()
+    try:
+        with open(path, "wb") as f:
+            f.write(head)
+            f.write(np.ascontiguousarray(sc.records, dtype="<f4").tobytes())
+    except OSError:
+        raise FormatError("cannot open for writing: " + path)
+
+
+def load_scene(path: str) -> Scene:
+    """load_scene (scene_io.cpp:43-101): the reference's header and payload checks (FormatError),
+    per-record validation in record order (ValidationError: opacity in [0,1], finite mean/scale,
+    positive scale, finite non-zero quaternion norm) and its renormalisation of quaternions whose
+    float32 norm (Eigen coefficient order x, y, z, w, packet sum (x2+z2)+(y2+w2)) drifts from 1 by
+    more than 1e-6."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        raise FormatError("cannot open scene file: " + path)
+    if len(data) < _GSB_HEADER:
+        raise FormatError(f"{path}: truncated header at byte offset {len(data)} (need 16)")
+    if data[:4] != _GSB_MAGIC:
+        raise FormatError(f"{path}: bad magic at byte offset 0")
+    count, degree = (int(v) for v in np.frombuffer(data, dtype="<u4", count=2, offset=4))
+    if degree not in (0, 3):
+        raise FormatError(f"{path}: unsupported sh_degree at byte offset 8")
+    rf = 59 if degree == 3 else 14
+    need = _GSB_HEADER + count * rf * 4
+    if len(data) < need:
+        raise FormatError(f"{path}: truncated payload at byte offset {len(data)} (need {need})")
+    rec = np.frombuffer(data, dtype="<f4", count=count * rf, offset=_GSB_HEADER).reshape(count, rf)
+    rec = rec.astype(np.float32, copy=True)
+    if count:
+        with np.errstate(invalid="ignore", over="ignore"):
+            op = rec[:, 10]
+            bad_op = ~((op >= 0.0) & (op <= 1.0))
+            bad_fin = ~np.isfinite(rec[:, 0:6]).all(axis=1)
+            bad_scale = ~(rec[:, 3:6].min(axis=1) > 0.0)
+            x, y, z, w = rec[:, 7], rec[:, 8], rec[:, 9], rec[:, 6]
+            n = np.sqrt((x * x + z * z) + (y * y + w * w), dtype=np.float32)
+            bad_q = ~((n > 0.0) & np.isfinite(n))
+        bad = bad_op | bad_fin | bad_scale | bad_q
+        if bad.any():
+            i = int(np.argmax(bad))
+            if bad_op[i]:
+                raise ValidationError(f"{path}: scene record {i}: opacity outside [0,1]")
+            if bad_fin[i]:
+                raise ValidationError(f"{path}: scene record {i}: non-finite mean or scale")
+            if bad_scale[i]:
+                raise ValidationError(f"{path}: scene record {i}: non-positive scale")
+            raise ValidationError(f"scene record {i}: quaternion has non-finite or zero norm")
+        drift = np.abs(n - np.float32(1.0)) > np.float32(1e-6)
+        if drift.any():
+            rec[drift, 6:10] = rec[drift, 6:10] / n[drift, None]
+    return Scene(rec)
+
+
 def encode_ppm(img) -> bytes:
     """encode_ppm (scene_io.cpp:253-263): P6 header + lrintf(clamp(v)*255) bytes."""
     rgb = img.rgb if isinstance(img, ImageBuffer) else img

@@ -115,6 +115,9 @@ __device__ unsigned int g_usec[65536][3];  // producer cycles: retire check, row
 #ifndef TGS_RASTER_COMPACT
 #define TGS_RASTER_COMPACT 1
 #endif
+#ifndef TGS_RASTER_PAIR  // producer batches built together before placement: 1, 2 or 4
+#define TGS_RASTER_PAIR 2
+#endif
 #ifndef TGS_RASTER_TIGHT
 #define TGS_RASTER_TIGHT 1
 #endif
@@ -489,98 +492,128 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, ctas_per_sm<SLOTS>()) 
             // batches ahead right after use; list indices four batches ahead.
             uint32_t n_batches = 0;
             // one batch: retire check, row build, ordered placement; true = unit finished
+            // producer work on one batch, in three parts: the retire check (drops member tiles
+            // whose pixels all terminated), the build (cover tests and coefficient rows per lane)
+            // and the ordered placement into the open chunk(s)
+            struct Built {
+                bool keep;
+                uint32_t cover;
+                uint4 r0, r1;
+                float4 epi;
+            };
+            auto retire_check = [&]() -> bool {  // true = every member tile retired
+                if (emitted) {
+                    uint32_t retired = 0xfu;
+#pragma unroll
+                    for (int w4 = 0; w4 < kEpiWarps; w4 += 4) {
+                        const int4 d = ld_volatile_v4(&sm.dead[w4]);
+                        const int dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int w = w4 + j;
+                            const uint32_t owned =
+                                kCompact ? 1u << (w >> 1) : ((1u << SPW) - 1u) << ((w >> 3) * SPW);
+                            retired &= ((dd[j] >> 4) == seq ? (uint32_t)(dd[j] & 15) : 0u) | (0xfu & ~owned);
+                        }
+                    }
+                    // sm.dead is written concurrently by the epilogue warps: take lane 0's view so
+                    // the whole warp makes the same decision (lanes may read it at different times)
+                    retired = __shfl_sync(0xffffffffu, retired, 0);
+                    live &= ~retired;
+                    if (live == 0u) return true;
+                }
+                return false;
+            };
+            auto build = [&](const Rec& cur, Built& bt) {
+                bt.keep = false;
+                bt.cover = 0;
+                bt.epi = make_float4(0, 0, 0, 0);
+                if (cur.idx != 0xffffffffu) {
+                    int x0, y0, x1, y1;
+                    tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1, y1);
+                    uint32_t cover = 0;
+#pragma unroll
+                    for (int k = 0; k < SLOTS; ++k) {
+                        const int tx = ug.tx0 + (k & 1), ty = ug.ty0 + (k >> 1);
+                        if (tx >= x0 && tx <= x1 && ty >= y0 && ty <= y1) cover |= 1u << k;
+                    }
+                    cover &= live;
+                    const float cj = fminf(clampv, cur.co.y);
+                    if (kTightCover && a.tile_cull && cover != 0u && !(cj < skip))
+                        cover &= tight_cover(cur.mc.x, cur.mc.y, cur.col.w, ug.tx0, ug.ty0, SLOTS);
+                    if (cover != 0u && !(cj < skip)) {
+                        bt.keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox,
+                                           oy, cover, bt.r0, bt.r1);
+                        bt.cover = cover;
+                        bt.epi = make_float4(cur.col.x, cur.col.y, cur.col.z, cj);
+                    }
+                }
+            };
+            auto place = [&](const Built& bt) {
+#pragma unroll
+                for (int h = 0; h < kNS; ++h) {
+                    const bool keep_h = bt.keep && (bt.cover & smask(h)) != 0u;
+                    const uint32_t km = __ballot_sync(0xffffffffu, keep_h);
+                    if (km == 0u) continue;
+                    const int nk = __popc(km);
+                    const int rank = __popc(km & lt);
+                    if (!open[h]) {
+                        s[h] = open_stage(h, c[h]);
+                        open[h] = true;
+                        fill[h] = 0;
+                    }
+                    // place the kept ranks in order; a full chunk is published and the next one
+                    // opened (a 32-lane batch spans at most 32 / kN + 1 chunks)
+                    int placed = 0;
+                    for (;;) {
+                        const int room = kN - fill[h];
+                        if (keep_h && rank >= placed && rank - placed < room) {
+                            write_row(sm, h, s[h], fill[h] + rank - placed, bt.r0, bt.r1);
+                            sm.epi[h][s[h]][fill[h] + rank - placed] = bt.epi;
+                        }
+                        if (nk - placed < room) {
+                            fill[h] += nk - placed;
+                            break;
+                        }
+                        publish(h, s[h], seq, unit, kN, live & smask(h));
+                        ++c[h];
+                        emitted = true;
+                        emitted_h[h] = true;
+                        s[h] = open_stage(h, c[h]);
+                        fill[h] = 0;
+                        placed += room;
+                        if (placed == nk) break;
+                    }
+                }
+            };
             auto batch = [&](const Rec& cur) -> bool {
                 ++n_batches;
                 [[maybe_unused]] const long long tb0 = TGS_RASTER_PROF ? clock64() : 0;
-                    if (emitted) {  // drop member tiles whose pixels all terminated (all owner warps)
-                        uint32_t retired = 0xfu;
-#pragma unroll
-                        for (int w4 = 0; w4 < kEpiWarps; w4 += 4) {
-                            const int4 d = ld_volatile_v4(&sm.dead[w4]);
-                            const int dd[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                const int w = w4 + j;
-                                const uint32_t owned =
-                                    kCompact ? 1u << (w >> 1) : ((1u << SPW) - 1u) << ((w >> 3) * SPW);
-                                retired &= ((dd[j] >> 4) == seq ? (uint32_t)(dd[j] & 15) : 0u) | (0xfu & ~owned);
-                            }
-                        }
-                        // sm.dead is written concurrently by the epilogue warps: take lane 0's view so
-                        // the whole warp makes the same decision (lanes may read it at different times)
-                        retired = __shfl_sync(0xffffffffu, retired, 0);
-                        live &= ~retired;
-                        if (live == 0u) return true;
-                    }
-                    [[maybe_unused]] const long long tb1 = TGS_RASTER_PROF ? clock64() : 0;
-                    bool keep = false;
-                    uint32_t cover_kept = 0;
-                    uint4 r0, r1;
-                    float4 epi_v = make_float4(0, 0, 0, 0);
-                    if (cur.idx != 0xffffffffu) {
-                        int x0, y0, x1, y1;
-                        tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1,
-                                  y1);
-                        uint32_t cover = 0;
-#pragma unroll
-                        for (int k = 0; k < SLOTS; ++k) {
-                            const int tx = ug.tx0 + (k & 1), ty = ug.ty0 + (k >> 1);
-                            if (tx >= x0 && tx <= x1 && ty >= y0 && ty <= y1) cover |= 1u << k;
-                        }
-                        cover &= live;
-                        const float cj = fminf(clampv, cur.co.y);
-                        if (kTightCover && a.tile_cull && cover != 0u && !(cj < skip))
-                            cover &= tight_cover(cur.mc.x, cur.mc.y, cur.col.w, ug.tx0, ug.ty0, SLOTS);
-                        if (cover != 0u && !(cj < skip)) {
-                            keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox,
-                                            oy, cover, r0, r1);
-                            cover_kept = cover;
-                            epi_v = make_float4(cur.col.x, cur.col.y, cur.col.z, cj);
-                        }
-                    }
-                    [[maybe_unused]] const long long tb2 = TGS_RASTER_PROF ? clock64() : 0;
-                    if (TGS_RASTER_PROF) {
-                        pf[2] += 1;
-                        sec[0] += tb1 - tb0;
-                        sec[1] += tb2 - tb1;
-                    }
-#pragma unroll
-                    for (int h = 0; h < kNS; ++h) {
-                        const bool keep_h = keep && (cover_kept & smask(h)) != 0u;
-                        const uint32_t km = __ballot_sync(0xffffffffu, keep_h);
-                        if (km == 0u) continue;
-                        const int nk = __popc(km);
-                        const int rank = __popc(km & lt);
-                        if (!open[h]) {
-                            s[h] = open_stage(h, c[h]);
-                            open[h] = true;
-                            fill[h] = 0;
-                        }
-                        // place the kept ranks in order; a full chunk is published and the next one
-                        // opened (a 32-lane batch spans at most 32 / kN + 1 chunks)
-                        int placed = 0;
-                        for (;;) {
-                            const int room = kN - fill[h];
-                            if (keep_h && rank >= placed && rank - placed < room) {
-                                write_row(sm, h, s[h], fill[h] + rank - placed, r0, r1);
-                                sm.epi[h][s[h]][fill[h] + rank - placed] = epi_v;
-                            }
-                            if (nk - placed < room) {
-                                fill[h] += nk - placed;
-                                break;
-                            }
-                            publish(h, s[h], seq, unit, kN, live & smask(h));
-                            ++c[h];
-                            emitted = true;
-                            emitted_h[h] = true;
-                            s[h] = open_stage(h, c[h]);
-                            fill[h] = 0;
-                            placed += room;
-                            if (placed == nk) break;
-                        }
-                    }
-                    if (TGS_RASTER_PROF) sec[2] += clock64() - tb2;
-                    return false;
+                if (retire_check()) return true;
+                [[maybe_unused]] const long long tb1 = TGS_RASTER_PROF ? clock64() : 0;
+                Built bt;
+                build(cur, bt);
+                [[maybe_unused]] const long long tb2 = TGS_RASTER_PROF ? clock64() : 0;
+                if (TGS_RASTER_PROF) {
+                    pf[2] += 1;
+                    sec[0] += tb1 - tb0;
+                    sec[1] += tb2 - tb1;
+                }
+                place(bt);
+                if (TGS_RASTER_PROF) sec[2] += clock64() - tb2;
+                return false;
+            };
+            // pair mode: two batches built back to back (independent work overlaps), then placed
+            // in list order
+            [[maybe_unused]] auto batch_pair = [&](const Rec& ca, const Rec& cb, bool has_b) -> bool {
+                n_batches += has_b ? 2u : 1u;
+                if (retire_check()) return true;
+                Built ba, bb;
+                build(ca, ba);
+                if (has_b) build(cb, bb);
+                place(ba);
+                if (has_b) place(bb);
+                return false;
             };
 #if TGS_RASTER_PREFETCH4
             Rec q0 = ld_rec(ld_idx(0)), q1 = ld_rec(ld_idx(1)), q2 = ld_rec(ld_idx(2)), q3 = ld_rec(ld_idx(3));
@@ -598,6 +631,40 @@ __global__ void __launch_bounds__(Roles<SLOTS>::kThreads, ctas_per_sm<SLOTS>()) 
                 if (bi + 3 >= nb || batch(q3)) break;
                 q3 = ld_rec(i3);
                 i3 = ld_idx(bi + 11);
+            }
+#elif TGS_RASTER_PAIR == 4
+            Rec q0 = ld_rec(ld_idx(0)), q1 = ld_rec(ld_idx(1)), q2 = ld_rec(ld_idx(2)), q3 = ld_rec(ld_idx(3));
+            uint32_t i0 = ld_idx(4), i1 = ld_idx(5), i2 = ld_idx(6), i3 = ld_idx(7);
+            for (uint32_t bi = 0; bi < nb; bi += 4) {
+                n_batches += min(4u, nb - bi);
+                if (retire_check()) break;
+                Built b0, b1, b2, b3;
+                build(q0, b0);
+                build(q1, b1);
+                build(q2, b2);
+                build(q3, b3);
+                place(b0);
+                place(b1);
+                place(b2);
+                place(b3);
+                q0 = ld_rec(i0);
+                q1 = ld_rec(i1);
+                q2 = ld_rec(i2);
+                q3 = ld_rec(i3);
+                i0 = ld_idx(bi + 8);
+                i1 = ld_idx(bi + 9);
+                i2 = ld_idx(bi + 10);
+                i3 = ld_idx(bi + 11);
+            }
+#elif TGS_RASTER_PAIR == 2
+            Rec qa = ld_rec(ld_idx(0)), qb = ld_rec(ld_idx(1));
+            uint32_t ia = ld_idx(2), ib = ld_idx(3);
+            for (uint32_t bi = 0; bi < nb; bi += 2) {
+                if (batch_pair(qa, qb, bi + 1 < nb)) break;
+                qa = ld_rec(ia);
+                qb = ld_rec(ib);
+                ia = ld_idx(bi + 4);
+                ib = ld_idx(bi + 5);
             }
 #else
             Rec qa = ld_rec(ld_idx(0)), qb = ld_rec(ld_idx(1));

@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
                     for (int t = 0; t < 4; ++t)
 #pragma unroll
                         for (int k = 0; k < KC; ++k)
-                            if ((v[t][1 + k] & lanebit) && j0 + t < n) {
+                            if (v[t][1 + k] & lanebit) {  // slots past n hold zero masks
                                 asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa[k]), "r"(v[t][0]) : "memory");
                                 sa[k] += 4u;
                             }

@@ -58,6 +58,8 @@ struct FrameCounters {
     unsigned int group_counter;     // persistent raster scheduler ticket
     unsigned long long walked;      // instrumented pair counters (tgs_count_pairs)
     unsigned long long blended;
+    unsigned int key_min_inv;       // ~min and max of the visible depth keys: the presort ranks
+    unsigned int key_max;           // (key - min), so passes above the key range are plain copies
 };
 
 // Group geometry (GroupConfig, binning.hpp:15-31) with an optional band of group rows.

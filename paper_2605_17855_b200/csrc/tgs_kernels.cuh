@@ -32,8 +32,11 @@ size_t sort_scratch_elems(size_t max_items);
 // *count_first items and, with drop_first, drops keys equal to kCulledKey; later passes cover
 // *count_rest items (device-side counts, <= max_items).  Result in keys[r]/vals[r], r returned.
 // want_keys_last == false skips writing keys in the last pass (only values are needed downstream).
+// key_min_inv (device, may be null) holds ~min over the sorted keys: digits are taken from
+// (key - min), which keeps the order and leaves the passes above the key range trivial (copies).
 int radix_sort(SortBuffers& b, const uint32_t* count_first, const uint32_t* count_rest, int nbits,
-               bool drop_first, bool want_keys_last, size_t max_items, cudaStream_t st);
+               bool drop_first, bool want_keys_last, size_t max_items, cudaStream_t st,
+               const uint32_t* key_min_inv = nullptr);
 
 // ---- binning: stable counting sort of (group, rank) entries ---------------------------------
 // The splats are presorted by (depth, index) (rank order); every warp of the count/scatter grids

@@ -198,7 +198,9 @@ constexpr int kPreBlock = 256;
 // only materialised on readback).  Counters are block-aggregated.
 __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a) {
     __shared__ unsigned long long s_cnt[4];
+    __shared__ unsigned int s_key[2];
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x < 2) s_key[threadIdx.x] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) a.fc->n_input = (unsigned)a.scene.n;
     __syncthreads();
     const int i = blockIdx.x * kPreBlock + threadIdx.x;
@@ -262,20 +264,31 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a)
     const unsigned long long nc = __popc(__ballot_sync(0xffffffffu, culled));
     const unsigned long long nd = __popc(__ballot_sync(0xffffffffu, dropped));
     const unsigned long long nk = __popc(__ballot_sync(0xffffffffu, keep));
+    const uint32_t kv = keep ? __float_as_uint(pr.depth) : 0u;
+    const uint32_t kmin_inv = __reduce_max_sync(0xffffffffu, keep ? ~kv : 0u);
+    const uint32_t kmax = __reduce_max_sync(0xffffffffu, kv);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) app += __shfl_xor_sync(0xffffffffu, app, o);
     if (lane == 0) {
         if (nc) atomicAdd(&s_cnt[0], nc);
         if (nd) atomicAdd(&s_cnt[1], nd);
         if (app) atomicAdd(&s_cnt[2], app);  // tile appearances (render.cpp:19-20)
-        if (nk) atomicAdd(&s_cnt[3], nk);
+        if (nk) {
+            atomicAdd(&s_cnt[3], nk);
+            atomicMax(&s_key[0], kmin_inv);
+            atomicMax(&s_key[1], kmax);
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         if (s_cnt[0]) atomicAdd(&a.fc->culled, s_cnt[0]);
         if (s_cnt[1]) atomicAdd(&a.fc->dropped, s_cnt[1]);
         if (s_cnt[2]) atomicAdd(&a.fc->appearances, s_cnt[2]);
-        if (s_cnt[3]) atomicAdd(&a.fc->visible, (unsigned)s_cnt[3]);
+        if (s_cnt[3]) {
+            atomicAdd(&a.fc->visible, (unsigned)s_cnt[3]);
+            atomicMax(&a.fc->key_min_inv, s_key[0]);
+            atomicMax(&a.fc->key_max, s_key[1]);
+        }
     }
 }
 

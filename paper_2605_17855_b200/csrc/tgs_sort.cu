@@ -61,18 +61,20 @@ __device__ __forceinline__ uint32_t match_digit(uint32_t d, bool valid) {
 // aggregation via match/ballots measured slower).
 __global__ void __launch_bounds__(kThreads) digits_kernel(const uint32_t* __restrict__ keys,
                                                           const uint32_t* count_ptr, int passes, bool drop,
+                                                          const uint32_t* key_min_inv,
                                                           uint32_t* __restrict__ scratch) {
     __shared__ uint32_t h[4][kRadix];
     for (int i = threadIdx.x; i < 4 * kRadix; i += kThreads) (&h[0][0])[i] = 0;
     __syncthreads();
     const uint32_t n = *count_ptr;
+    const uint32_t kb = key_min_inv ? ~*key_min_inv : 0u;
     const uint32_t stride = gridDim.x * kThreads;
     for (uint32_t base = blockIdx.x * kThreads; base < n; base += stride) {  // warp-uniform trip count
         const uint32_t i = base + threadIdx.x;
         const uint32_t k = i < n ? keys[i] : kCulledKey;
         const bool valid = i < n && !(drop && k == kCulledKey);
         if (valid)
-            for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xffu], 1u);
+            for (int p = 0; p < passes; ++p) atomicAdd(&h[p][((k - kb) >> (8 * p)) & 0xffu], 1u);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * kRadix; i += kThreads) {
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(kThreads) digits_kernel(const uint32_t* __rest
 __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, const uint32_t* count_ptr, int pass, bool write_keys, bool drop,
-    uint32_t* __restrict__ scratch) {
+    const uint32_t* key_min_inv, uint32_t* __restrict__ scratch) {
     __shared__ uint32_t wcnt[kWarps][kRadix];   // per-warp digit counts -> per-warp offsets
     __shared__ uint32_t tot[kRadix];            // tile digit totals
     __shared__ uint32_t lstart[kRadix];         // tile-local start of each digit
@@ -95,7 +97,17 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     const int shift = 8 * pass;
     uint32_t* status = scratch + kStatusOff;
     const uint32_t n = *count_ptr;
+    const uint32_t kb = key_min_inv ? ~*key_min_inv : 0u;
     const uint32_t lt = (1u << lane) - 1u;
+    // A pass whose digit is the same for every item (e.g. the top byte of depth keys that share
+    // their float exponent's high bits) is the identity permutation: copy instead of ranking.
+    if (!drop && __syncthreads_or(scratch[kHistOff + pass * kRadix + threadIdx.x] == n)) {
+        for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < n; i += gridDim.x * kThreads) {
+            if (write_keys) kout[i] = __ldcs(kin + i);
+            vout[i] = __ldcs(vin + i);
+        }
+        return;
+    }
     // persistent blocks claim tiles in order, so only ~gridDim tiles are in flight and look-back
     // walks stay short
     for (;;) {
@@ -123,7 +135,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     for (int s = 0; s < kSteps; ++s) {
         const uint32_t i = t0 + warp * (32 * kSteps) + s * 32 + lane;
         const bool valid = i < n && !(drop && k[s] == kCulledKey);
-        const uint32_t d = (k[s] >> shift) & 0xffu;
+        const uint32_t d = ((k[s] - kb) >> shift) & 0xffu;
         peers[s] = match_digit(d, valid);
         old[s] = 0;
         if (valid && (31 - __clz(peers[s])) == lane) old[s] = atomicAdd(&wcnt[warp][d], (uint32_t)__popc(peers[s]));
@@ -223,7 +235,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
 #pragma unroll
     for (int s = 0; s < kSteps; ++s) {
         if (rk[s] != 0xffffffffu) {
-            const uint32_t d = (k[s] >> shift) & 0xffu;
+            const uint32_t d = ((k[s] - kb) >> shift) & 0xffu;
             const uint32_t p = lstart[d] + wcnt[warp][d] + rk[s];
             skey[p] = k[s];
             sval[p] = v[s];
@@ -234,7 +246,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     const uint32_t m = s_n;
     for (uint32_t j = threadIdx.x; j < m; j += kThreads) {
         const uint32_t key = skey[j];
-        const uint32_t d = (key >> shift) & 0xffu;
+        const uint32_t d = ((key - kb) >> shift) & 0xffu;
         const uint32_t pos = gbase[d] + (j - lstart[d]);
         if (write_keys) kout[pos] = key;
         vout[pos] = sval[j];
@@ -250,11 +262,12 @@ size_t sort_scratch_elems(size_t max_items) {
 }
 
 int radix_sort(SortBuffers& b, const uint32_t* count_first, const uint32_t* count_rest, int nbits,
-               bool drop_first, bool want_keys_last, size_t max_items, cudaStream_t st) {
+               bool drop_first, bool want_keys_last, size_t max_items, cudaStream_t st,
+               const uint32_t* key_min_inv) {
     const int passes = std::max(1, std::min(4, (nbits + 7) / 8));
     const int tiles = (int)std::max<size_t>(1, (max_items + kTileItems - 1) / kTileItems);
     cudaMemsetAsync(b.ghist, 0, sort_scratch_elems(max_items) * sizeof(uint32_t), st);
-    digits_kernel<<<148 * 4, kThreads, 0, st>>>(b.keys[0], count_first, passes, drop_first, b.ghist);
+    digits_kernel<<<148 * 4, kThreads, 0, st>>>(b.keys[0], count_first, passes, drop_first, key_min_inv, b.ghist);
     int src = 0;
     for (int p = 0; p < passes; ++p) {
         const bool last = p == passes - 1;
@@ -262,7 +275,7 @@ int radix_sort(SortBuffers& b, const uint32_t* count_first, const uint32_t* coun
             cudaMemsetAsync(b.ghist + kStatusOff, 0, (size_t)tiles * kRadix * sizeof(uint32_t), st);
         onesweep_kernel<<<std::min(tiles, kSweepBlocks), kThreads, 0, st>>>(b.keys[src], b.vals[src], b.keys[src ^ 1], b.vals[src ^ 1],
                                                    p == 0 ? count_first : count_rest, p, !last || want_keys_last,
-                                                   p == 0 && drop_first, b.ghist);
+                                                   p == 0 && drop_first, key_min_inv, b.ghist);
         src ^= 1;
     }
     return src;

@@ -164,6 +164,29 @@ def test_config1_scale_vs_port(gsr, ctx, port):
     check_image(res1.image.rgb, img_p, "config1 scalar g1")
 
 
+@pytest.mark.parametrize("depths", ["ties", "narrow", "wide"])
+def test_presort_key_ranges_vs_port(gsr, ctx, port, depths):
+    """The presort ranks (key - min key): a key range of a few bits leaves passes 1-3 as copies,
+    equal depths leave every pass after the culling one trivial, a wide range needs all four."""
+    w, h = 240, 160
+    c = make_camera(w, h)
+    rec = np.array(port.gen_scene(41, 5000, 1.0, 0.01, 0.06, 0), np.float32)
+    rng = np.random.default_rng(7)
+    z = {"ties": np.full(5000, 3.0), "narrow": 2.0 + rng.random(5000) * 1e-3,
+         "wide": np.exp(rng.uniform(np.log(0.25), np.log(90.0), 5000))}[depths]
+    rec[:, 0] = rng.uniform(-0.6, 0.6, 5000) * z
+    rec[:, 1] = rng.uniform(-0.4, 0.4, 5000) * z
+    rec[:, 2] = z
+    rec[::97, 2] = -1.0  # some culled behind the camera
+    pp, _ = port.project(rec, c)
+    ds = ctx.upload(rec)
+    for group in (1, 2):
+        ctx.render(ds, _cam(gsr, c), _opt(gsr, 0 if group == 1 else 1, group))
+        ent_p, off_p, _ = port.bin_sort(pp, w, h, group)
+        ent, off = ctx.read_lists(len(off_p) - 1)
+        assert np.array_equal(off, off_p) and np.array_equal(ent.view(np.uint8), ent_p.view(np.uint8))
+
+
 # ---------------------------------------------------------------------------------------------
 # edge cases the reference tests
 # ---------------------------------------------------------------------------------------------

@@ -208,15 +208,27 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
 #pragma unroll
     for (int k = 0; k < KR; ++k) sa[k] = out0 + 8u * (P[k] + (pos[k] - base[k]));
     uint32_t* my = reinterpret_cast<uint32_t*>(&stage[wib][lane][0]);
+    uint32_t snext = 0u;
+    uint2 rnext = make_uint2(0u, 0u);
+    if (r0 + lane < r1) {
+        snext = __ldg(&a.sval[r0 + lane]);
+        rnext = __ldg(&a.rrect[r0 + lane]);
+    }
     for (uint32_t rb = r0; rb < r1; rb += 32) {
         const uint32_t r = rb + lane;
+        const uint32_t sv = snext;  // next batch in flight while this one is placed
+        const uint2 rr = rnext;
+        if (r + 32 < r1) {
+            snext = __ldg(&a.sval[r + 32]);
+            rnext = __ldg(&a.rrect[r + 32]);
+        }
         uint32_t w[4 * NW];
 #pragma unroll
         for (int i = 0; i < 4 * NW; ++i) w[i] = 0u;
         if (r < r1) {
             int gx0, gx1, gy0, gy1;
-            w[0] = __ldg(&a.sval[r]);
-            if (band_groups(a.gg, __ldg(&a.rrect[r]), gx0, gx1, gy0, gy1)) {
+            w[0] = sv;
+            if (band_groups(a.gg, rr, gx0, gx1, gy0, gy1)) {
                 w[1] = (uint32_t)gx0 | ((uint32_t)gx1 << 16);
 #pragma unroll
                 for (int k = 0; k < KR; ++k) w[2 + k] = range_mask(gy0, gy1, k);
@@ -284,17 +296,19 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
 // [column][segment] block, so the exclusive scan of hist2 (rows in order) is directly the global
 // start of every (group, segment) run and group g = (y, x) starts at its segment-0 slot.
 
+// Row y and segment s of global segment q (warp-collective): y = last row with nsegp[y] <= q, found
+// with independent loads + ballots instead of a dependent binary search (nsegp is non-decreasing,
+// nsegp[0] = 0).
 __device__ __forceinline__ void seg_locate(const uint32_t* nsegp, int rows, uint32_t q, int& y, uint32_t& s) {
-    int lo = 0, hi = rows - 1;  // last row with nsegp[y] <= q
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (nsegp[mid] <= q)
-            lo = mid;
-        else
-            hi = mid - 1;
+    const int lane = threadIdx.x & 31;
+    int cnt = 0;
+#pragma unroll 4
+    for (int b = 0; b < rows; b += 32) {
+        const int i = b + lane;
+        cnt += __popc(__ballot_sync(0xffffffffu, i < rows && __ldg(&nsegp[i]) <= q));
     }
-    y = lo;
-    s = q - nsegp[lo];
+    y = cnt - 1;
+    s = q - __ldg(&nsegp[y]);
 }
 
 __global__ void __launch_bounds__(kBinWarps * 32) cols_count_kernel(BinArgs a) {
@@ -365,29 +379,33 @@ __global__ void offsets_kernel(BinArgs a) {
 // Group placement.  A block takes one segment (kBinWarps slices of kSliceLen row entries, one per
 // warp); the segment's run of column x is one contiguous global range [base_x, base_x + len_x),
 // inside which warp w's part starts after the parts of warps < w (per-slice column counts, made
-// here in shared memory).  Lane l of every warp owns columns l, l + 32, ... (KC per lane); each
-// lane stages one row entry (splat index + column masks) in shared memory, then entries are read
-// back in batches (broadcast) and every owning column appends the splat — into the block's shared
-// output buffer, so that every column run is flushed with coalesced stores.  A block whose output
-// exceeds the buffer writes to global slots instead.
+// here in shared memory).  Lane per entry: each lane marks the columns of its entry in a per-warp
+// column bitmask; the entry's slot in column c is the column's running position plus the number of
+// earlier lanes (= earlier entries) that also cover c, and the highest such lane advances the
+// column.  Slots are in the block's shared output buffer (with each slot's column id), flushed
+// with one flat coalesced pass; a block whose output exceeds the buffer writes global slots.
 template <int KC>
 __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
-    constexpr int NW = (KC + 1 + 3) / 4;  // uint4 words per staged entry: idx, KC masks
-    __shared__ uint4 stage[kBinWarps][32][NW];
-    extern __shared__ uint32_t sout[];    // [kStage2] output, then [kBinWarps][gx + 1] slice counts
+    constexpr int kPer = kSliceLen / 32;  // row entries per lane
+    // [kStage2] output | [kStage2] u16 column ids | [gx + 1] column global bias |
+    // [kBinWarps][gx + 1] slice counts, column positions, column masks
+    extern __shared__ uint32_t sout[];
     if (a.fc->overflow) return;
     const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const uint32_t lanebit = 1u << lane;
+    const uint32_t lanebit = 1u << lane, lt = lanebit - 1u;
     const uint32_t* rowstart = a.meta;
     const uint32_t* nsegp = a.meta + rows + 1;
     const uint32_t* rowbase2 = a.meta + 2 * rows + 2;
     const uint32_t nq = nsegp[rows], h2 = rowbase2[rows], total = a.fc->n_entries;
-    int* cntw = reinterpret_cast<int*>(sout + kStage2);
+    uint16_t* scol = reinterpret_cast<uint16_t*>(sout + kStage2);
+    uint32_t* gbias = sout + kStage2 + kStage2 / 2;
+    int* cntw = reinterpret_cast<int*>(gbias + gx + 1);
     int* D = cntw + wib * (gx + 1);
-    uint32_t* my = reinterpret_cast<uint32_t*>(&stage[wib][lane][0]);
+    uint32_t* cpos = reinterpret_cast<uint32_t*>(cntw) + (kBinWarps + wib) * (gx + 1);
+    uint32_t* cmask = cpos + kBinWarps * (gx + 1);
     uint32_t* list = a.list;
-    const uint32_t out0 = smem_u32(sout);
+    const uint32_t out0 = smem_u32(sout), col0 = smem_u32(scol);
     auto h2at = [&](uint32_t i) { return i < h2 ? a.hist2[i] : total; };
     for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
         int y;
@@ -396,14 +414,30 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
         const uint32_t nseg = nsegp[y + 1] - nsegp[y];
         const uint32_t se0 = rowstart[y] + s * kSegLen, se1 = min(rowstart[y + 1], se0 + kSegLen);
         const uint32_t e0 = min(se1, se0 + (uint32_t)wib * kSliceLen), e1 = min(se1, e0 + kSliceLen);
-        // this warp's slice: per-column counts (difference array -> prefix)
+        // column runs of the segment, [base, base + len) globally (loads in flight during the counts)
+        uint32_t base[KC], len[KC];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            const int x = lane + 32 * k;
+            const uint32_t i0 = rowbase2[y] + (uint32_t)x * nseg + s;
+            base[k] = x < gx ? h2at(i0) : 0u;
+            len[k] = x < gx ? h2at(i0 + 1) : 0u;
+        }
+        // this warp's slice, loaded once: per-column counts (difference array -> prefix)
+        uint2 ent[kPer];
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const uint32_t e = e0 + lane + 32u * i;
+            ent[i] = e < e1 ? __ldg(&a.rowlist[e]) : make_uint2(0u, 0u);
+        }
         for (int i = lane; i <= gx; i += 32) D[i] = 0;
         __syncwarp();
-        for (uint32_t e = e0 + lane; e < e1; e += 32) {
-            const uint32_t xp = __ldg(&a.rowlist[e].y);
-            atomicAdd(&D[xp & 0xffffu], 1);
-            atomicAdd(&D[(xp >> 16) + 1], -1);
-        }
+#pragma unroll
+        for (int i = 0; i < kPer; ++i)
+            if (e0 + lane + 32u * i < e1) {
+                atomicAdd(&D[ent[i].y & 0xffffu], 1);
+                atomicAdd(&D[(ent[i].y >> 16) + 1], -1);
+            }
         __syncwarp();
         {
             int run = 0;
@@ -420,14 +454,12 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
             }
         }
         __syncthreads();
-        // column runs of the segment: [base, base + len) globally, local start P; this warp's part
-        uint32_t base[KC], len[KC], P[KC], off[KC], carry = 0;
+        // local start P of every column run; this warp's part starts off after earlier warps'
+        uint32_t P[KC], off[KC], carry = 0;
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
             const int x = lane + 32 * k;
-            const uint32_t i0 = rowbase2[y] + (uint32_t)x * nseg + s;
-            base[k] = x < gx ? h2at(i0) : 0u;
-            len[k] = x < gx ? h2at(i0 + 1) - base[k] : 0u;
+            len[k] -= base[k];
             off[k] = 0u;
             if (x < gx)
                 for (int w = 0; w < wib; ++w) off[k] += (uint32_t)cntw[w * (gx + 1) + x];
@@ -441,81 +473,54 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
             carry += __shfl_sync(0xffffffffu, incl, 31);
         }
         const bool staged = carry <= (uint32_t)kStage2;  // block-uniform
-        uint32_t sa[KC], pos[KC];
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
-            sa[k] = out0 + 4u * (P[k] + off[k]);
-            pos[k] = base[k] + off[k];
+            const int x = lane + 32 * k;
+            if (x < gx) {
+                cpos[x] = staged ? P[k] + off[k] : base[k] + off[k];
+                cmask[x] = 0u;
+                if (wib == 0) gbias[x] = base[k] - P[k];
+            }
         }
-        for (uint32_t eb = e0; eb < e1; eb += 32) {
-            const uint32_t e = eb + lane;
-            uint32_t w[4 * NW];
+        __syncwarp();
 #pragma unroll
-            for (int i = 0; i < 4 * NW; ++i) w[i] = 0u;
-            if (e < e1) {
-                const uint2 v = __ldg(&a.rowlist[e]);
-                w[0] = v.x;
-#pragma unroll
-                for (int k = 0; k < KC; ++k) w[1 + k] = range_mask((int)(v.y & 0xffffu), (int)(v.y >> 16), k);
+        for (int i = 0; i < kPer; ++i) {
+            if (e0 + 32u * i >= e1) break;  // warp-uniform
+            const uint2 v = ent[i];
+            int x0 = 0, span = 0;
+            if (e0 + lane + 32u * i < e1) {
+                x0 = (int)(v.y & 0xffffu);
+                span = (int)(v.y >> 16) - x0 + 1;
             }
+            const int ms = (int)__reduce_max_sync(0xffffffffu, (uint32_t)span);
+            for (int t = 0; t < ms; ++t)
+                if (t < span) atomicOr(&cmask[x0 + t], lanebit);
             __syncwarp();
-#pragma unroll
-            for (int i = 0; i < NW; ++i)
-                reinterpret_cast<uint4*>(my)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
-            __syncwarp();
-            const int n = (int)min(32u, e1 - eb);
-            if (staged) {
-                // batches of 4 entries: all broadcast loads first, then the appends
-                for (int j0 = 0; j0 < n; j0 += 4) {
-                    uint32_t v[4][4 * NW];
-#pragma unroll
-                    for (int t = 0; t < 4; ++t)
-#pragma unroll
-                        for (int i = 0; i < NW; ++i) {
-                            const uint4 qv = stage[wib][(j0 + t) & 31][i];
-                            v[t][4 * i] = qv.x;
-                            v[t][4 * i + 1] = qv.y;
-                            v[t][4 * i + 2] = qv.z;
-                            v[t][4 * i + 3] = qv.w;
-                        }
-#pragma unroll
-                    for (int t = 0; t < 4; ++t)
-#pragma unroll
-                        for (int k = 0; k < KC; ++k)
-                            if (v[t][1 + k] & lanebit) {  // slots past n hold zero masks
-                                asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa[k]), "r"(v[t][0]) : "memory");
-                                sa[k] += 4u;
-                            }
-                }
-            } else {
-#pragma unroll 4
-                for (int j = 0; j < n; ++j) {
-                    uint32_t v[4 * NW];
-#pragma unroll
-                    for (int i = 0; i < NW; ++i) {
-                        const uint4 qv = stage[wib][j][i];
-                        v[4 * i] = qv.x;
-                        v[4 * i + 1] = qv.y;
-                        v[4 * i + 2] = qv.z;
-                        v[4 * i + 3] = qv.w;
+            for (int t = 0; t < ms; ++t)
+                if (t < span) {
+                    const uint32_t p = cpos[x0 + t] + __popc(cmask[x0 + t] & lt);
+                    if (staged) {
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(out0 + 4u * p), "r"(v.x) : "memory");
+                        asm volatile("st.shared.u16 [%0], %1;" ::"r"(col0 + 2u * p), "h"((unsigned short)(x0 + t)) : "memory");
+                    } else {
+                        list[p] = v.x;
                     }
-#pragma unroll
-                    for (int k = 0; k < KC; ++k)
-                        if (v[1 + k] & lanebit) list[pos[k]++] = v[0];
                 }
-            }
+            __syncwarp();
+            for (int t = 0; t < ms; ++t)
+                if (t < span) {
+                    const uint32_t m = cmask[x0 + t];
+                    if ((m >> lane) == 1u) {
+                        cpos[x0 + t] += __popc(m);
+                        cmask[x0 + t] = 0u;
+                    }
+                }
+            __syncwarp();
         }
         __syncthreads();
         if (staged) {
-            // flush: warp w copies the runs of columns w, w + 8, ... (coalesced)
-#pragma unroll
-            for (int k = 0; k < KC; ++k)
-                for (int l = wib; l < 32; l += kBinWarps) {
-                    const uint32_t c = __shfl_sync(0xffffffffu, len[k], l);
-                    const uint32_t src = __shfl_sync(0xffffffffu, P[k], l);
-                    const uint32_t dst = __shfl_sync(0xffffffffu, base[k], l);
-                    for (uint32_t i = lane; i < c; i += 32) list[dst + i] = sout[src + i];
-                }
+            // flush: one flat pass, slot j of column c goes to gbias[c] + j (coalesced runs)
+            for (uint32_t j = threadIdx.x; j < carry; j += kBinWarps * 32) list[gbias[scol[j]] + j] = sout[j];
             __syncthreads();
         }
     }
@@ -769,7 +774,9 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     launch_exclusive_scan(a.hist2, n2, tmp, st, h2_len);
     offsets_kernel<<<(gg.n_groups_band + 256) / 256, 256, 0, st>>>(a);
     const int kc = (gx + 31) / 32, t2 = kBinWarps * 32;
-    const size_t so = (size_t)kStage2 * sizeof(uint32_t) + (size_t)kBinWarps * (gx + 1) * sizeof(int);
+    // output stage + column ids, column bias, per-warp slice counts / column positions / masks
+    const size_t so = (size_t)kStage2 * (sizeof(uint32_t) + sizeof(uint16_t)) +
+                      (size_t)(3 * kBinWarps + 1) * (gx + 1) * sizeof(int);
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)so);
         kern<<<qblocks, t2, so, st>>>(a);

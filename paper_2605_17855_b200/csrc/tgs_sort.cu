@@ -102,10 +102,16 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     // A pass whose digit is the same for every item (e.g. the top byte of depth keys that share
     // their float exponent's high bits) is the identity permutation: copy instead of ranking.
     if (!drop && __syncthreads_or(scratch[kHistOff + pass * kRadix + threadIdx.x] == n)) {
-        for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < n; i += gridDim.x * kThreads) {
-            if (write_keys) kout[i] = __ldcs(kin + i);
-            vout[i] = __ldcs(vin + i);
-        }
+        const uint32_t tid = blockIdx.x * kThreads + threadIdx.x, nt = gridDim.x * kThreads, n4 = n / 4u;
+        auto copy = [&](const uint32_t* __restrict__ src, uint32_t* __restrict__ dst) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(src);  // cudaMalloc'd: 16-byte aligned
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll 4
+            for (uint32_t i = tid; i < n4; i += nt) d4[i] = __ldcs(s4 + i);
+            for (uint32_t i = 4u * n4 + tid; i < n; i += nt) dst[i] = src[i];
+        };
+        if (write_keys) copy(kin, kout);
+        copy(vin, vout);
         return;
     }
     // persistent blocks claim tiles in order, so only ~gridDim tiles are in flight and look-back

@@ -192,30 +192,23 @@ __device__ __forceinline__ int project_one(const DevScene& s, const DevCamera& c
 }
 
 constexpr int kPreBlock = 256;
+#ifndef TGS_PRE_PER
+#define TGS_PRE_PER 2
+#endif
+constexpr int kPrePer = TGS_PRE_PER;
 
-// One thread per input Gaussian, outputs at the INPUT index (no compaction pass: the depth
-// presort drops culled splats, whose key is 0xffffffff, and project_scene's compacted order is
-// only materialised on readback).  Counters are block-aggregated.
-__global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a) {
-    __shared__ unsigned long long s_cnt[4];
-    __shared__ unsigned int s_key[2];
-    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
-    if (threadIdx.x < 2) s_key[threadIdx.x] = 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.fc->n_input = (unsigned)a.scene.n;
-    __syncthreads();
-    const int i = blockIdx.x * kPreBlock + threadIdx.x;
-    const int lane = threadIdx.x & 31;
+// Per-thread frame tallies (summed over the thread's Gaussians, then warp/block aggregated).
+struct PreTally {
+    uint32_t culled = 0, dropped = 0, kept = 0, kmin_inv = 0, kmax = 0;
+    unsigned long long app = 0;
+};
 
+// Projection + outputs of Gaussian i (i < n) from its SH0 planes.
+__device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int i, float4 po, float4 q, float4 sd,
+                                               float2 gb, PreTally& t) {
     bool keep = false, culled = false, dropped = false;
     Proj pr;
-    float4 po = make_float4(0, 0, 0, 0);
-    if (i < a.scene.n) {
-        // every SH0 plane is loaded up front (one memory latency instead of a dependent chain of
-        // three; the few culled splats waste 40 B each)
-        po = a.scene.pos_op[i];
-        const float4 q = a.scene.quat[i];
-        const float4 sd = a.scene.scale_dcr[i];
-        const float2 gb = a.scene.dc_gb[i];
+    {
         float p[3];
         camera_space(a.cam, po.x, po.y, po.z, p);
         bool vis = p[2] > a.cam.near_ && p[2] < a.cam.far_;  // frustum_cull (projection.cpp:45-53)
@@ -239,8 +232,7 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a)
             }
         }
     }
-    unsigned long long app = 0;
-    if (i < a.scene.n) {
+    {
         a.idx_vals[i] = (uint32_t)i;
         if (keep) {
             a.out.mc[i] = make_float4(pr.mx, pr.my, pr.a, pr.b);
@@ -253,7 +245,7 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a)
             a.rect[i] = (tx1 >= tx0 && ty1 >= ty0)
                             ? make_uint2((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16))
                             : make_uint2(0xffffu, 0u);
-            if (tx1 >= tx0 && ty1 >= ty0) app = (unsigned long long)(tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+            if (tx1 >= tx0 && ty1 >= ty0) t.app += (unsigned long long)(tx1 - tx0 + 1) * (ty1 - ty0 + 1);
             // sort_entries depth validation (binning.cpp:78-83) for splats that emit entries
             if (ng > 0 && !(isfinite(pr.depth) && pr.depth >= 0.0f)) atomicOr(&a.fc->err_validation, 2u);
         } else {
@@ -261,12 +253,54 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a)
             a.rect[i] = make_uint2(kCulledRect, kCulledRect);
         }
     }
-    const unsigned long long nc = __popc(__ballot_sync(0xffffffffu, culled));
-    const unsigned long long nd = __popc(__ballot_sync(0xffffffffu, dropped));
-    const unsigned long long nk = __popc(__ballot_sync(0xffffffffu, keep));
-    const uint32_t kv = keep ? __float_as_uint(pr.depth) : 0u;
-    const uint32_t kmin_inv = __reduce_max_sync(0xffffffffu, keep ? ~kv : 0u);
-    const uint32_t kmax = __reduce_max_sync(0xffffffffu, kv);
+    t.culled += culled;
+    t.dropped += dropped;
+    if (keep) {
+        const uint32_t kv = __float_as_uint(pr.depth);
+        t.kept += 1u;
+        t.kmin_inv = max(t.kmin_inv, ~kv);
+        t.kmax = max(t.kmax, kv);
+    }
+}
+
+// kPrePer Gaussians per thread, block-strided (all their SH0 planes are loaded up front, so the
+// second Gaussian's loads are in flight while the first is projected); outputs at the INPUT index
+// (no compaction pass: the depth presort drops culled splats, whose key is 0xffffffff, and
+// project_scene's compacted order is only materialised on readback).  Counters are
+// block-aggregated.
+__global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a) {
+    __shared__ unsigned long long s_cnt[4];
+    __shared__ unsigned int s_key[2];
+    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x < 2) s_key[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.fc->n_input = (unsigned)a.scene.n;
+    __syncthreads();
+    const int i0 = blockIdx.x * kPreBlock * kPrePer + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    float4 po[kPrePer], q[kPrePer], sd[kPrePer];
+    float2 gb[kPrePer];
+#pragma unroll
+    for (int u = 0; u < kPrePer; ++u) {
+        const int i = i0 + u * kPreBlock;
+        if (i < a.scene.n) {
+            po[u] = a.scene.pos_op[i];
+            q[u] = a.scene.quat[i];
+            sd[u] = a.scene.scale_dcr[i];
+            gb[u] = a.scene.dc_gb[i];
+        }
+    }
+    PreTally t;
+#pragma unroll
+    for (int u = 0; u < kPrePer; ++u) {
+        const int i = i0 + u * kPreBlock;
+        if (i < a.scene.n) preprocess_one(a, i, po[u], q[u], sd[u], gb[u], t);
+    }
+    const unsigned long long nc = __reduce_add_sync(0xffffffffu, t.culled);
+    const unsigned long long nd = __reduce_add_sync(0xffffffffu, t.dropped);
+    const unsigned long long nk = __reduce_add_sync(0xffffffffu, t.kept);
+    const uint32_t kmin_inv = __reduce_max_sync(0xffffffffu, t.kmin_inv);
+    const uint32_t kmax = __reduce_max_sync(0xffffffffu, t.kmax);
+    unsigned long long app = t.app;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) app += __shfl_xor_sync(0xffffffffu, app, o);
     if (lane == 0) {
@@ -295,7 +329,7 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a)
 }  // namespace
 
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t st) {
-    const int blocks = (a.scene.n + kPreBlock - 1) / kPreBlock;
+    const int blocks = (a.scene.n + kPreBlock * kPrePer - 1) / (kPreBlock * kPrePer);
     if (blocks > 0) preprocess_kernel<<<blocks, kPreBlock, 0, st>>>(a);
 }
 

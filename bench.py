@@ -352,9 +352,9 @@ def main():
             cpu = {"value": None, "unit": "frames/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
     # our kernels per frame: preprocess 1; depth presort: digit histograms + 4 one-sweep passes;
-    # binning: rows count (with the rank gather), 3-kernel scan, rows meta, rows place, cols count,
-    # 3-kernel scan, offsets, cols place; unit order 1; raster 1
-    launches_per_frame = 1 + 5 + 12 + 1 + 1
+    # binning: rows count (with the rank gather), scan,
+    # rows meta, rows place, cols count, scan, offsets, cols place; unit order 1; raster 1
+    launches_per_frame = 1 + 5 + 8 + 1 + 1
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",

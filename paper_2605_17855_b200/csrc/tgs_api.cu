@@ -252,7 +252,6 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     pa.cam = make_dev_camera(cam);
     pa.out = proj;
     pa.depth_keys = ctx->pre_keys[0].as<uint32_t>();
-    pa.idx_vals = ctx->pre_vals[0].as<uint32_t>();
     pa.rect = ctx->rect.as<uint2>();
     pa.gg = gg;
     pa.fc = fc;
@@ -270,7 +269,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     pb.ghist = ctx->ghist.as<uint32_t>();
     pb.scan_tmp = ctx->bsum.as<uint32_t>();
     // pass 1 covers all n splats and drops the culled ones (key kCulledKey); later passes the kept
-    const int pr = radix_sort(pb, &fc->n_input, &fc->visible, 32, true, false, (size_t)n_alloc, s, &fc->key_min_inv);
+    const int pr = radix_sort(pb, &fc->n_input, &fc->visible, 32, true, false, (size_t)n_alloc, s, &fc->key_min_inv, true);
     TGS_CUDA_OK(cudaGetLastError());
 
     TGS_CUDA_OK(cudaEventRecord(ctx->ev[2], s));

@@ -23,6 +23,8 @@
 #include "tgs_common.cuh"
 #include "tgs_kernels.cuh"
 
+#include <cstdio>
+
 #include <algorithm>
 
 namespace tgs {
@@ -558,93 +560,79 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& t
     return excl;
 }
 
-__global__ void __launch_bounds__(kScanBlock) scan_reduce_kernel(const uint32_t* __restrict__ x, size_t n,
-                                                                 const uint32_t* __restrict__ n_dev,
-                                                                 uint32_t* __restrict__ bsum) {
+// Single-pass exclusive scan (in place): tiles of kScanTile values are claimed in order from a
+// ticket; each tile publishes its aggregate, resolves its prefix by decoupled look-back over the
+// 32 preceding tiles per round (warp 0, one status word per lane), publishes its inclusive prefix
+// and writes its values.  tmp: [0] ticket, [2] total, status words (u64: flag << 32 | value) from
+// tmp + 4; zeroed by the launcher.  n_dev (device length, may be null) caps n.
+__global__ void __launch_bounds__(kScanBlock) scan_onepass_kernel(uint32_t* __restrict__ x, size_t n,
+                                                                  const uint32_t* __restrict__ n_dev,
+                                                                  uint32_t* __restrict__ tmp) {
     if (n_dev) n = min(n, (size_t)*n_dev);
-    if ((size_t)blockIdx.x * kScanTile >= n) {  // past the device-side length: empty block
-        if (threadIdx.x == 0) bsum[blockIdx.x] = 0u;
-        return;
-    }
-    const size_t base = (size_t)blockIdx.x * kScanTile + (size_t)threadIdx.x * kScanItems;
-    uint32_t s = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        const size_t i = base + k;
-        if (i < n) s += x[i];
-    }
-    uint32_t total = 0;
-    block_exclusive_scan(s, total);
-    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
-}
-
-// in-place exclusive scan of n values by one block (n = blocks + 1, the last slot is the total)
-__global__ void __launch_bounds__(1024) scan_small_kernel(uint32_t* data, int n) {
-    __shared__ uint32_t warp_tot[32];
-    __shared__ uint32_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
+    const uint32_t tiles = (uint32_t)((n + kScanTile - 1) / kScanTile);
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(tmp + 4);
+    constexpr unsigned long long kAgg = 1ull << 32, kPre = 2ull << 32;
+    __shared__ uint32_t s_tile, s_prefix;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int base = 0; base < n; base += 1024 * 4) {
-        uint32_t v[4], s = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = base + threadIdx.x * 4 + k;
-            v[k] = i < n ? data[i] : 0u;
-            s += v[k];
-        }
-        uint32_t incl = s;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) warp_tot[warp] = incl;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&tmp[0], 1u);
         __syncthreads();
+        const uint32_t tile = s_tile;
+        if (tile >= tiles) break;  // block-uniform
+        const size_t base = (size_t)tile * kScanTile + (size_t)threadIdx.x * kScanItems;
+        uint32_t v[kScanItems], sum = 0;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            const size_t i = base + k;
+            v[k] = i < n ? x[i] : 0u;
+            sum += v[k];
+        }
+        uint32_t total = 0;
+        const uint32_t excl = block_exclusive_scan(sum, total);
         if (warp == 0) {
-            const uint32_t w = warp_tot[lane];
-            uint32_t wi = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o) wi += t;
+            uint32_t prefix = 0;
+            if (tile == 0) {
+                if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(&status[0]) = kPre | total;
+            } else {
+                if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(&status[tile]) = kAgg | total;
+                int j = (int)tile - 1;
+                const long long t0 = clock64();
+                for (;;) {
+                    const int idx = j - lane;
+                    const unsigned long long w =
+                        idx >= 0 ? *reinterpret_cast<volatile unsigned long long*>(&status[idx]) : kPre;
+                    const uint32_t flag = (uint32_t)(w >> 32);
+                    const uint32_t pm = __ballot_sync(0xffffffffu, flag == 2u);
+                    const uint32_t nm = __ballot_sync(0xffffffffu, flag == 0u);
+                    const uint32_t upto = pm ? (pm & (0u - pm)) * 2u - 1u : 0xffffffffu;  // lanes <= first P
+                    if (nm & upto) {  // a needed predecessor has not published yet
+                        __nanosleep(32);
+                        if (clock64() - t0 > 4000000000ll) {
+                            if (lane == 0) printf("scan look-back stuck: tile %u\n", tile);
+                            __trap();
+                        }
+                        continue;
+                    }
+                    const uint32_t mine = (upto >> lane) & 1u ? (uint32_t)w : 0u;
+                    prefix += __reduce_add_sync(0xffffffffu, mine);
+                    if (pm) break;
+                    j -= 32;
+                }
+                if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(&status[tile]) = kPre | (prefix + total);
             }
-            warp_tot[lane] = wi - w;
+            if (lane == 0) {
+                s_prefix = prefix;
+                if (tile == tiles - 1) tmp[2] = prefix + total;
+            }
         }
         __syncthreads();
-        uint32_t run = carry + warp_tot[warp] + incl - s;
+        uint32_t run = s_prefix + excl;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = base + threadIdx.x * 4 + k;
-            if (i < n) data[i] = run;
+        for (int k = 0; k < kScanItems; ++k) {
+            const size_t i = base + k;
+            if (i < n) x[i] = run;
             run += v[k];
         }
-        __syncthreads();
-        if (threadIdx.x == 1023) carry = run;
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(kScanBlock) scan_apply_kernel(uint32_t* __restrict__ x, size_t n,
-                                                                const uint32_t* __restrict__ n_dev,
-                                                                const uint32_t* __restrict__ bsum) {
-    if (n_dev) n = min(n, (size_t)*n_dev);
-    if ((size_t)blockIdx.x * kScanTile >= n) return;
-    const size_t base = (size_t)blockIdx.x * kScanTile + (size_t)threadIdx.x * kScanItems;
-    uint32_t v[kScanItems], s = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        const size_t i = base + k;
-        v[k] = i < n ? x[i] : 0u;
-        s += v[k];
-    }
-    uint32_t total = 0;
-    uint32_t run = block_exclusive_scan(s, total) + bsum[blockIdx.x];
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        const size_t i = base + k;
-        if (i < n) x[i] = run;
-        run += v[k];
     }
 }
 
@@ -727,15 +715,14 @@ size_t bin_hist2_elems(const GroupGeom& gg, uint32_t capacity) {
 }
 size_t bin_meta_elems(const GroupGeom& gg) { return 4 * (size_t)(gg.band_gy1 - gg.band_gy0 + 1) + 1; }
 
-size_t scan_tmp_elems(size_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
+size_t scan_tmp_elems(size_t n) { return 4 + 2 * ((n + kScanTile - 1) / kScanTile); }
 
-void launch_exclusive_scan(uint32_t* x, size_t n, uint32_t* tmp, cudaStream_t st, const uint32_t* n_dev) {
-    const int blocks = (int)((n + kScanTile - 1) / kScanTile);
-    if (blocks == 0) return;
-    scan_reduce_kernel<<<blocks, kScanBlock, 0, st>>>(x, n, n_dev, tmp);
-    cudaMemsetAsync(tmp + blocks, 0, sizeof(uint32_t), st);
-    scan_small_kernel<<<1, 1024, 0, st>>>(tmp, blocks + 1);
-    scan_apply_kernel<<<blocks, kScanBlock, 0, st>>>(x, n, n_dev, tmp);
+const uint32_t* launch_exclusive_scan(uint32_t* x, size_t n, uint32_t* tmp, cudaStream_t st, const uint32_t* n_dev) {
+    const size_t tiles = (n + kScanTile - 1) / kScanTile;
+    cudaMemsetAsync(tmp, 0, scan_tmp_elems(n) * sizeof(uint32_t), st);
+    const int grid = (int)std::min<size_t>(tiles, 148 * 8);
+    if (grid > 0) scan_onepass_kernel<<<grid, kScanBlock, 0, st>>>(x, n, n_dev, tmp);
+    return tmp + 2;
 }
 
 void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
@@ -746,8 +733,7 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     const size_t n1 = bin_hist1_elems(gg);
     rows_count_kernel<<<kRowChunks / kBinWarps, kBinWarps * 32, kBinWarps * (rows + 1) * sizeof(int), st>>>(a);
     uint32_t* tmp = a.bsum;
-    launch_exclusive_scan(a.hist1, n1, tmp, st, nullptr);
-    const uint32_t* scan1_total = tmp + (n1 + kScanTile - 1) / kScanTile;
+    const uint32_t* scan1_total = launch_exclusive_scan(a.hist1, n1, tmp, st, nullptr);
     rows_meta_kernel<<<1, 32, 0, st>>>(a, scan1_total);
     const int kr = (rows + 31) / 32, b1 = kRowChunks / kBinWarps, t1 = kBinWarps * 32;
     const size_t so1 = (size_t)kStage1 * sizeof(uint2);

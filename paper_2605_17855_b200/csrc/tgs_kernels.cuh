@@ -10,7 +10,6 @@ struct PreprocessArgs {
     DevCamera cam;
     DevProjected out;
     uint32_t* depth_keys;          // [n] depth bits (presort keys; kCulledKey when not projected)
-    uint32_t* idx_vals;            // [n] input index (presort values)
     uint2* rect;                   // [n] tile rect: x0 | x1 << 16, y0 | y1 << 16 (x0 > x1: none;
                                    //     kCulledRect twice: not projected)
     GroupGeom gg;
@@ -34,9 +33,10 @@ size_t sort_scratch_elems(size_t max_items);
 // want_keys_last == false skips writing keys in the last pass (only values are needed downstream).
 // key_min_inv (device, may be null) holds ~min over the sorted keys: digits are taken from
 // (key - min), which keeps the order and leaves the passes above the key range trivial (copies).
+// index_vals: the first pass takes item i's value to be i (vals[0] is not read).
 int radix_sort(SortBuffers& b, const uint32_t* count_first, const uint32_t* count_rest, int nbits,
                bool drop_first, bool want_keys_last, size_t max_items, cudaStream_t st,
-               const uint32_t* key_min_inv = nullptr);
+               const uint32_t* key_min_inv = nullptr, bool index_vals = false);
 
 // ---- binning: stable counting sort of (group, rank) entries ---------------------------------
 // The splats are presorted by (depth, index) (rank order); every warp of the count/scatter grids
@@ -65,11 +65,12 @@ size_t bin_hist1_elems(const GroupGeom& gg);
 size_t bin_hist2_elems(const GroupGeom& gg, uint32_t capacity);
 size_t bin_meta_elems(const GroupGeom& gg);
 void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st);
-// In-place exclusive scan of n u32 (multi-block: block sums, one-block scan of the sums, apply);
-// tmp holds scan_tmp_elems(n) u32 and ends with the total.
+// In-place exclusive scan of n u32 (one pass, decoupled look-back); tmp holds scan_tmp_elems(n)
+// u32; returns the device address of the total.
 size_t scan_tmp_elems(size_t n);
 // n_dev (optional): device-side length <= n; elements past it are left untouched.
-void launch_exclusive_scan(uint32_t* x, size_t n, uint32_t* tmp, cudaStream_t st, const uint32_t* n_dev = nullptr);
+const uint32_t* launch_exclusive_scan(uint32_t* x, size_t n, uint32_t* tmp, cudaStream_t st,
+                                      const uint32_t* n_dev = nullptr);
 
 // Sorted lists -> GroupEntry array (for readback).
 void launch_lists_readback(const uint32_t* sorted_idx, const uint32_t* offsets, int n_groups,

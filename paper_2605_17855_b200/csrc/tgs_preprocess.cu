@@ -233,7 +233,6 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int i, f
         }
     }
     {
-        a.idx_vals[i] = (uint32_t)i;
         if (keep) {
             a.out.mc[i] = make_float4(pr.mx, pr.my, pr.a, pr.b);
             a.out.co[i] = make_float4(pr.c, po.w, pr.depth, __int_as_float(pr.radius));

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     const uint32_t lt = (1u << lane) - 1u;
     // A pass whose digit is the same for every item (e.g. the top byte of depth keys that share
     // their float exponent's high bits) is the identity permutation: copy instead of ranking.
-    if (!drop && __syncthreads_or(scratch[kHistOff + pass * kRadix + threadIdx.x] == n)) {
+    if (!drop && vin && __syncthreads_or(scratch[kHistOff + pass * kRadix + threadIdx.x] == n)) {
         const uint32_t tid = blockIdx.x * kThreads + threadIdx.x, nt = gridDim.x * kThreads, n4 = n / 4u;
         auto copy = [&](const uint32_t* __restrict__ src, uint32_t* __restrict__ dst) {
             const uint4* s4 = reinterpret_cast<const uint4*>(src);  // cudaMalloc'd: 16-byte aligned
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     for (int s = 0; s < kSteps; ++s) {
         const uint32_t i = t0 + warp * (32 * kSteps) + s * 32 + lane;
         k[s] = i < n ? kin[i] : kCulledKey;
-        v[s] = i < n ? vin[i] : 0u;
+        v[s] = i < n ? (vin ? vin[i] : i) : 0u;  // null vin: values are the item indices
     }
     // rank within the warp: per step, lanes with equal digits (ballot match); the highest such lane
     // adds the group to the warp's running digit counter with one shared atomic (program order per
@@ -269,7 +269,7 @@ size_t sort_scratch_elems(size_t max_items) {
 
 int radix_sort(SortBuffers& b, const uint32_t* count_first, const uint32_t* count_rest, int nbits,
                bool drop_first, bool want_keys_last, size_t max_items, cudaStream_t st,
-               const uint32_t* key_min_inv) {
+               const uint32_t* key_min_inv, bool index_vals) {
     const int passes = std::max(1, std::min(4, (nbits + 7) / 8));
     const int tiles = (int)std::max<size_t>(1, (max_items + kTileItems - 1) / kTileItems);
     cudaMemsetAsync(b.ghist, 0, sort_scratch_elems(max_items) * sizeof(uint32_t), st);
@@ -279,7 +279,7 @@ int radix_sort(SortBuffers& b, const uint32_t* count_first, const uint32_t* coun
         const bool last = p == passes - 1;
         if (p > 0)  // look-back status of the previous pass
             cudaMemsetAsync(b.ghist + kStatusOff, 0, (size_t)tiles * kRadix * sizeof(uint32_t), st);
-        onesweep_kernel<<<std::min(tiles, kSweepBlocks), kThreads, 0, st>>>(b.keys[src], b.vals[src], b.keys[src ^ 1], b.vals[src ^ 1],
+        onesweep_kernel<<<std::min(tiles, kSweepBlocks), kThreads, 0, st>>>(b.keys[src], p == 0 && index_vals ? nullptr : b.vals[src], b.keys[src ^ 1], b.vals[src ^ 1],
                                                    p == 0 ? count_first : count_rest, p, !last || want_keys_last,
                                                    p == 0 && drop_first, key_min_inv, b.ghist);
         src ^= 1;

@@ -12,7 +12,8 @@ import sys
 
 STAGE = {"preprocess_kernel": "preprocess", "hist_kernel": "sort", "scatter_kernel": "sort",
          "digits_kernel": "sort", "onesweep_kernel": "sort",
-         "scan_reduce_kernel": None, "scan_small_kernel": None, "scan_apply_kernel": None,
+         "scan_reduce_kernel": "binning", "scan_small_kernel": "binning", "scan_apply_kernel": "binning",
+         "scan_onepass_kernel": "binning",
          "rank_gather_kernel": "binning", "rows_count_kernel": "binning", "rows_meta_kernel": "binning",
          "rows_place_kernel": "binning", "cols_count_kernel": "binning", "offsets_kernel": "binning",
          "cols_place_kernel": "binning", "unit_order_kernel": "binning",

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--group", type=int, default=2)
     ap.add_argument("--backend", default="tensor")
     ap.add_argument("--cam", type=int, default=5)
+    ap.add_argument("--save", action="store_true", help="save the image to gpurun_out/ab_TAG.npy")
     a = ap.parse_args()
     ctx = gsr.Context(0)
     ds = ctx.upload(gsr.gen_synthetic_scene(3, 3_000_000, 1.0, (0.01, 0.05)))
@@ -32,9 +33,10 @@ def main():
         st = ctx.sync()
         rows.append((st.ms_preprocess, st.ms_sort, st.ms_binning, st.ms_raster, st.ms_total))
     med = np.median(np.array(rows[3:]), axis=0)
-    img = ctx.render(ds, cam, opt).image.rgb
-    os.makedirs("gpurun_out", exist_ok=True)
-    np.save(f"gpurun_out/ab_{a.tag}.npy", img)
+    if a.save:
+        img = ctx.render(ds, cam, opt).image.rgb
+        os.makedirs("gpurun_out", exist_ok=True)
+        np.save(f"gpurun_out/ab_{a.tag}.npy", img)
     print(f"AB {a.tag}: pre {med[0]:.3f} sort {med[1]:.3f} bin {med[2]:.3f} raster {med[3]:.3f} "
           f"total {med[4]:.3f} ms", flush=True)
 

@@ -37,7 +37,7 @@ sys.path.insert(0, ROOT)
 METRIC = "frames/sec & raster ms/frame @1080p 3M Gaussians; tensor-pipe util; multi-view fps 1–8 GPU"
 W, H, N_SPLATS, SEED = 1920, 1080, 3_000_000, 3
 N_CAMS = 256
-LANES = 3  # frames in flight per GPU (one context/stream each), as tgs_render_batch pipelines
+LANES = int(os.environ.get("TGS_BENCH_LANES", "3"))  # frames in flight per GPU (one context/stream each), as tgs_render_batch pipelines
 
 
 def dist_env():

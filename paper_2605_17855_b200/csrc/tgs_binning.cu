@@ -581,12 +581,22 @@ __global__ void __launch_bounds__(kScanBlock) scan_onepass_kernel(uint32_t* __re
         if (tile >= tiles) break;  // block-uniform
         const size_t base = (size_t)tile * kScanTile + (size_t)threadIdx.x * kScanItems;
         uint32_t v[kScanItems], sum = 0;
+        const bool full = base + kScanItems <= n;  // 16-byte vector loads/stores (x is 16-aligned)
+        if (full) {
 #pragma unroll
-        for (int k = 0; k < kScanItems; ++k) {
-            const size_t i = base + k;
-            v[k] = i < n ? x[i] : 0u;
-            sum += v[k];
+            for (int k = 0; k < kScanItems; k += 4) {
+                const uint4 q = *reinterpret_cast<const uint4*>(x + base + k);
+                v[k] = q.x;
+                v[k + 1] = q.y;
+                v[k + 2] = q.z;
+                v[k + 3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kScanItems; ++k) v[k] = base + k < n ? x[base + k] : 0u;
         }
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) sum += v[k];
         uint32_t total = 0;
         const uint32_t excl = block_exclusive_scan(sum, total);
         if (warp == 0) {
@@ -627,11 +637,23 @@ __global__ void __launch_bounds__(kScanBlock) scan_onepass_kernel(uint32_t* __re
         }
         __syncthreads();
         uint32_t run = s_prefix + excl;
+        if (full) {
 #pragma unroll
-        for (int k = 0; k < kScanItems; ++k) {
-            const size_t i = base + k;
-            if (i < n) x[i] = run;
-            run += v[k];
+            for (int k = 0; k < kScanItems; k += 4) {
+                uint4 q;
+                q.x = run;
+                q.y = run += v[k];
+                q.z = run += v[k + 1];
+                q.w = run += v[k + 2];
+                run += v[k + 3];
+                *reinterpret_cast<uint4*>(x + base + k) = q;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kScanItems; ++k) {
+                if (base + k < n) x[base + k] = run;
+                run += v[k];
+            }
         }
     }
 }

@@ -87,15 +87,25 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_count_kernel(BinArgs a) {
     uint32_t r0, r1;
     chunk_range(*a.visible, kRowChunks, chunk, r0, r1);
     uint32_t ent = 0;
-    for (uint32_t r = r0 + lane; r < r1; r += 32) {
-        int gx0, gx1, gy0, gy1;
-        // gather the rank-ordered rectangle once here (rows_place reads it back coalesced)
-        const uint2 rr = __ldg(&a.rect[__ldg(&a.sval[r])]);
-        a.rrect[r] = rr;
-        if (!band_groups(a.gg, rr, gx0, gx1, gy0, gy1)) continue;
-        atomicAdd(&D[gy0], 1);
-        atomicAdd(&D[gy1 + 1], -1);
-        ent += (uint32_t)((gx1 - gx0 + 1) * (gy1 - gy0 + 1));
+    for (uint32_t rb = r0 + lane; rb < r1; rb += 32 * 4) {  // 4 gathers in flight per lane
+        uint2 rr[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t r = rb + 32u * u;
+            // gather the rank-ordered rectangle once here (rows_place reads it back coalesced)
+            rr[u] = r < r1 ? __ldg(&a.rect[__ldg(&a.sval[r])]) : make_uint2(0xffffu, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t r = rb + 32u * u;
+            if (r >= r1) continue;
+            a.rrect[r] = rr[u];
+            int gx0, gx1, gy0, gy1;
+            if (!band_groups(a.gg, rr[u], gx0, gx1, gy0, gy1)) continue;
+            atomicAdd(&D[gy0], 1);
+            atomicAdd(&D[gy1 + 1], -1);
+            ent += (uint32_t)((gx1 - gx0 + 1) * (gy1 - gy0 + 1));
+        }
     }
     __syncwarp();
     int carry = 0;
@@ -331,10 +341,16 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_count_kernel(BinArgs a) {
         const uint32_t e0 = rowstart[y] + s * kSegLen, e1 = min(rowstart[y + 1], e0 + kSegLen);
         for (int i = lane; i <= gx; i += 32) D[i] = 0;
         __syncwarp();
-        for (uint32_t e = e0 + lane; e < e1; e += 32) {
-            const uint32_t xp = __ldg(&a.rowlist[e].y);
-            atomicAdd(&D[xp & 0xffffu], 1);
-            atomicAdd(&D[(xp >> 16) + 1], -1);
+        for (uint32_t eb = e0 + lane; eb < e1; eb += 32 * 8) {  // 8 loads in flight per lane
+            uint32_t xp[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) xp[u] = eb + 32u * u < e1 ? __ldg(&a.rowlist[eb + 32u * u].y) : 0xffffffffu;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (xp[u] != 0xffffffffu) {
+                    atomicAdd(&D[xp[u] & 0xffffu], 1);
+                    atomicAdd(&D[(xp[u] >> 16) + 1], -1);
+                }
         }
         __syncwarp();
         int carry = 0;

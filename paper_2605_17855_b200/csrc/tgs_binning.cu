@@ -198,6 +198,12 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
     };
     uint32_t r0, r1;
     chunk_range(*a.visible, kRowChunks, chunk, r0, r1);
+    uint32_t snext = 0u;  // the chunk's first batch is in flight during the row setup
+    uint2 rnext = make_uint2(0u, 0u);
+    if (r0 + lane < r1) {
+        snext = __ldg(&a.sval[r0 + lane]);
+        rnext = __ldg(&a.rrect[r0 + lane]);
+    }
     uint32_t base[KR], len[KR], P[KR], pos[KR], carry = 0;
 #pragma unroll
     for (int k = 0; k < KR; ++k) {
@@ -220,12 +226,6 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
 #pragma unroll
     for (int k = 0; k < KR; ++k) sa[k] = out0 + 8u * (P[k] + (pos[k] - base[k]));
     uint32_t* my = reinterpret_cast<uint32_t*>(&stage[wib][lane][0]);
-    uint32_t snext = 0u;
-    uint2 rnext = make_uint2(0u, 0u);
-    if (r0 + lane < r1) {
-        snext = __ldg(&a.sval[r0 + lane]);
-        rnext = __ldg(&a.rrect[r0 + lane]);
-    }
     for (uint32_t rb = r0; rb < r1; rb += 32) {
         const uint32_t r = rb + lane;
         const uint32_t sv = snext;  // next batch in flight while this one is placed

@@ -69,12 +69,20 @@ __global__ void __launch_bounds__(kThreads) digits_kernel(const uint32_t* __rest
     const uint32_t n = *count_ptr;
     const uint32_t kb = key_min_inv ? ~*key_min_inv : 0u;
     const uint32_t stride = gridDim.x * kThreads;
-    for (uint32_t base = blockIdx.x * kThreads; base < n; base += stride) {  // warp-uniform trip count
-        const uint32_t i = base + threadIdx.x;
-        const uint32_t k = i < n ? keys[i] : kCulledKey;
-        const bool valid = i < n && !(drop && k == kCulledKey);
-        if (valid)
-            for (int p = 0; p < passes; ++p) atomicAdd(&h[p][((k - kb) >> (8 * p)) & 0xffu], 1u);
+    for (uint32_t base = blockIdx.x * kThreads; base < n; base += 4 * stride) {  // 4 loads in flight
+        uint32_t k[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t i = base + u * stride + threadIdx.x;
+            k[u] = i < n ? keys[i] : kCulledKey;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t i = base + u * stride + threadIdx.x;
+            const bool valid = i < n && !(drop && k[u] == kCulledKey);
+            if (valid)
+                for (int p = 0; p < passes; ++p) atomicAdd(&h[p][((k[u] - kb) >> (8 * p)) & 0xffu], 1u);
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * kRadix; i += kThreads) {

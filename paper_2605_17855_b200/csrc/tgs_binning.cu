@@ -34,9 +34,15 @@ namespace {
 constexpr int kBinWarps = 8;          // warps per binning block (one chunk / segment per warp)
 constexpr int kRowChunks = 148 * 128;  // level-1 chunks (contiguous rank ranges, one warp each)
 constexpr int kStage1 = 8192;          // level-1 per-block output staging (row entries)
-constexpr uint32_t kSliceLen = 128;   // level-2 placement: row-list entries per warp
+#ifndef TGS_SLICE_LEN
+#define TGS_SLICE_LEN 128
+#endif
+constexpr uint32_t kSliceLen = TGS_SLICE_LEN;   // level-2 placement: row-list entries per warp
 constexpr uint32_t kSegLen = kSliceLen * kBinWarps;  // level-2 segment: one count warp / one placement block
-constexpr int kStage2 = 8192;         // level-2 per-block output staging (entries)
+#ifndef TGS_STAGE2
+#define TGS_STAGE2 6144
+#endif
+constexpr int kStage2 = TGS_STAGE2;         // level-2 per-block output staging (entries)
 constexpr int kScanItems = 16;        // per thread in the hist scan
 constexpr int kScanBlock = 256;
 constexpr int kScanTile = kScanItems * kScanBlock;

@@ -60,7 +60,7 @@ constexpr float kInf = __builtin_huge_valf();
 #endif
 constexpr int kN = TGS_RASTER_N;  // splats per chunk (MMA N): 16 or 32
 #ifndef TGS_RASTER_SS
-#define TGS_RASTER_SS 4
+#define TGS_RASTER_SS 3
 #endif
 constexpr int kSS = TGS_RASTER_SS;  // smem stages
 #ifndef TGS_RASTER_TS

@@ -33,16 +33,29 @@ namespace {
 
 constexpr int kBinWarps = 8;          // warps per binning block (one chunk / segment per warp)
 constexpr int kRowChunks = 148 * 128;  // level-1 chunks (contiguous rank ranges, one warp each)
-constexpr int kStage1 = 8192;          // level-1 per-block output staging (row entries)
+// level-1 per-block output staging (row entries), smaller for few rows (more resident blocks)
+#ifndef TGS_STAGE1
+#define TGS_STAGE1 6144
+#endif
+#ifndef TGS_STAGE1_WIDE
+#define TGS_STAGE1_WIDE 8192
+#endif
+constexpr int stage1_entries(int kr) { return kr <= 2 ? TGS_STAGE1 : TGS_STAGE1_WIDE; }
 #ifndef TGS_SLICE_LEN
 #define TGS_SLICE_LEN 128
 #endif
 constexpr uint32_t kSliceLen = TGS_SLICE_LEN;   // level-2 placement: row-list entries per warp
 constexpr uint32_t kSegLen = kSliceLen * kBinWarps;  // level-2 segment: one count warp / one placement block
+// level-2 per-block output staging (entries): one segment's output is ~kSegLen x the mean column
+// span, which grows with the columns per row; a smaller stage keeps more blocks resident (bench
+// G=2, 60 columns: 6144; G=1, 120 columns: 8192)
 #ifndef TGS_STAGE2
 #define TGS_STAGE2 6144
 #endif
-constexpr int kStage2 = TGS_STAGE2;         // level-2 per-block output staging (entries)
+#ifndef TGS_STAGE2_WIDE
+#define TGS_STAGE2_WIDE 8192
+#endif
+constexpr int stage2_entries(int kc) { return kc <= 2 ? TGS_STAGE2 : TGS_STAGE2_WIDE; }
 constexpr int kScanItems = 16;        // per thread in the hist scan
 constexpr int kScanBlock = 256;
 constexpr int kScanTile = kScanItems * kScanBlock;
@@ -191,6 +204,7 @@ template <int KR>
 __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
     constexpr int NW = (KR + 2 + 3) / 4;  // uint4 words per staged splat: idx, xp, KR masks
     __shared__ uint4 stage[kBinWarps][32][NW];
+    constexpr int kStage1 = stage1_entries(KR);
     extern __shared__ uint2 sout1[];      // [kStage1]
     if (a.fc->overflow) return;
     const int rows = a.gg.band_gy1 - a.gg.band_gy0;
@@ -411,7 +425,7 @@ __global__ void offsets_kernel(BinArgs a) {
 template <int KC>
 __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
     constexpr int kPer = kSliceLen / 32;  // row entries per lane
-    // [kStage2] output | [kStage2] u16 column ids | [gx + 1] column global bias |
+    // [stage2_entries(KC)] output | [same] u16 column ids | [gx + 1] column global bias |
     // [kBinWarps][gx + 1] slice counts, column positions, column masks
     extern __shared__ uint32_t sout[];
     if (a.fc->overflow) return;
@@ -422,6 +436,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
     const uint32_t* nsegp = a.meta + rows + 1;
     const uint32_t* rowbase2 = a.meta + 2 * rows + 2;
     const uint32_t nq = nsegp[rows], h2 = rowbase2[rows], total = a.fc->n_entries;
+    constexpr int kStage2 = stage2_entries(KC);
     uint16_t* scol = reinterpret_cast<uint16_t*>(sout + kStage2);
     uint32_t* gbias = sout + kStage2 + kStage2 / 2;
     int* cntw = reinterpret_cast<int*>(gbias + gx + 1);
@@ -780,7 +795,7 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     const uint32_t* scan1_total = launch_exclusive_scan(a.hist1, n1, tmp, st, nullptr);
     rows_meta_kernel<<<1, 32, 0, st>>>(a, scan1_total);
     const int kr = (rows + 31) / 32, b1 = kRowChunks / kBinWarps, t1 = kBinWarps * 32;
-    const size_t so1 = (size_t)kStage1 * sizeof(uint2);
+    const size_t so1 = (size_t)stage1_entries(kr) * sizeof(uint2);
     auto launch1 = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)so1);
         kern<<<b1, t1, so1, st>>>(a);
@@ -805,7 +820,7 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     offsets_kernel<<<(gg.n_groups_band + 256) / 256, 256, 0, st>>>(a);
     const int kc = (gx + 31) / 32, t2 = kBinWarps * 32;
     // output stage + column ids, column bias, per-warp slice counts / column positions / masks
-    const size_t so = (size_t)kStage2 * (sizeof(uint32_t) + sizeof(uint16_t)) +
+    const size_t so = (size_t)stage2_entries(kc) * (sizeof(uint32_t) + sizeof(uint16_t)) +
                       (size_t)(3 * kBinWarps + 1) * (gx + 1) * sizeof(int);
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)so);

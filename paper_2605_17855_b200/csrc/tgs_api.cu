@@ -228,7 +228,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     const uint32_t cap = std::max<uint32_t>(ctx->capacity, 1u);
     TGS_CUDA_OK(ctx->list.ensure((size_t)cap * 4));
     const size_t h1 = bin_hist1_elems(gg), h2 = bin_hist2_elems(gg, cap), hm = bin_meta_elems(gg);
-    TGS_CUDA_OK(ctx->hist.ensure((h1 + h2 + hm) * 4));
+    TGS_CUDA_OK(ctx->hist.ensure((h1 + h2 + hm + bin_segmap_elems(gg, cap)) * 4));
     TGS_CUDA_OK(ctx->rowlist.ensure((size_t)cap * sizeof(uint2)));
     TGS_CUDA_OK(ctx->bsum.ensure(
         std::max({scan_tmp_elems(h1), scan_tmp_elems(h2), scan_tmp_elems(sort_scratch_elems((size_t)n_alloc))}) * 4));
@@ -284,6 +284,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     ba.hist1 = ctx->hist.as<uint32_t>();
     ba.hist2 = ba.hist1 + h1;
     ba.meta = ba.hist2 + h2;
+    ba.segmap = ba.meta + bin_meta_elems(gg);
     ba.rowlist = ctx->rowlist.as<uint2>();
     ba.bsum = ctx->bsum.as<uint32_t>();
     ba.offsets = ctx->offsets.as<uint32_t>();

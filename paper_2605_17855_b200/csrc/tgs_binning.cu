@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_count_kernel(BinArgs a) {
         int y;
         uint32_t s;
         seg_locate(nsegp, rows, q, y, s);
+        if (lane == 0) a.segmap[q] = (uint32_t)y;  // cols_place reads the row back (one load)
         const uint32_t nseg = nsegp[y + 1] - nsegp[y];
         const uint32_t e0 = rowstart[y] + s * kSegLen, e1 = min(rowstart[y + 1], e0 + kSegLen);
         for (int i = lane; i <= gx; i += 32) D[i] = 0;
@@ -446,10 +447,12 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
     uint32_t* list = a.list;
     const uint32_t out0 = smem_u32(sout), col0 = smem_u32(scol);
     auto h2at = [&](uint32_t i) { return i < h2 ? a.hist2[i] : total; };
+    // the segment's group row comes from cols_count's map, loaded one segment ahead
+    uint32_t ynext = blockIdx.x < nq ? __ldg(&a.segmap[blockIdx.x]) : 0u;
     for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
-        int y;
-        uint32_t s;
-        seg_locate(nsegp, rows, q, y, s);
+        const int y = (int)ynext;
+        if (q + gridDim.x < nq) ynext = __ldg(&a.segmap[q + gridDim.x]);
+        const uint32_t s = q - nsegp[y];
         const uint32_t nseg = nsegp[y + 1] - nsegp[y];
         const uint32_t se0 = rowstart[y] + s * kSegLen, se1 = min(rowstart[y + 1], se0 + kSegLen);
         const uint32_t e0 = min(se1, se0 + (uint32_t)wib * kSliceLen), e1 = min(se1, e0 + kSliceLen);
@@ -773,6 +776,9 @@ size_t bin_hist2_elems(const GroupGeom& gg, uint32_t capacity) {
     return (size_t)gg.groups_x * (rows + capacity / kSegLen + 1);
 }
 size_t bin_meta_elems(const GroupGeom& gg) { return 4 * (size_t)(gg.band_gy1 - gg.band_gy0 + 1) + 1; }
+size_t bin_segmap_elems(const GroupGeom& gg, uint32_t capacity) {
+    return (size_t)std::max(1, gg.band_gy1 - gg.band_gy0) + capacity / kSegLen + 1;
+}
 
 size_t scan_tmp_elems(size_t n) { return 4 + 2 * ((n + kScanTile - 1) / kScanTile); }
 

@@ -57,12 +57,14 @@ struct BinArgs {
     uint2* rowlist;              // [capacity] group-row entries (splat index, gx0 | gx1 << 16)
     uint32_t* offsets;           // [n_groups_band + 1]
     uint32_t* list;              // [capacity] output entries (splat indices)
+    uint32_t* segmap;            // [bin_segmap_elems] level-2 segment -> group row (cols_count -> cols_place)
     FrameCounters* fc;
     uint32_t capacity;
 };
 int bin_chunks(int n_groups);                                      // level-1 chunks
 size_t bin_hist1_elems(const GroupGeom& gg);
 size_t bin_hist2_elems(const GroupGeom& gg, uint32_t capacity);
+size_t bin_segmap_elems(const GroupGeom& gg, uint32_t capacity);
 size_t bin_meta_elems(const GroupGeom& gg);
 void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st);
 // In-place exclusive scan of n u32 (one pass, decoupled look-back); tmp holds scan_tmp_elems(n)

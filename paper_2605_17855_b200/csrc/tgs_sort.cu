@@ -7,7 +7,7 @@
 // partitions the rank-ordered splats stably by group (tgs_binning.cu), which yields the reference's
 // (group, depth, index) lists bit for bit (tests/test_gpu_parity.py checks full list equality).
 //
-// One-sweep passes (8-bit digits, tiles of 4096 items):
+// One-sweep passes (8-bit digits, tiles of 3072 items):
 //   digits : one kernel reads the keys once and builds the histograms of every pass;
 //   pass   : one kernel per digit.  Tiles are claimed in order from a counter; each tile ranks its
 //            items stably (per-warp __match_any_sync against running digit counters, warps
@@ -28,11 +28,14 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kSteps = 16;                        // 32-item steps per warp per tile
-constexpr int kTileItems = kThreads * kSteps;     // 4096
+#ifndef TGS_SORT_STEPS
+#define TGS_SORT_STEPS 12  // 77 registers: 3 resident blocks per SM
+#endif
+constexpr int kSteps = TGS_SORT_STEPS;            // 32-item steps per warp per tile
+constexpr int kTileItems = kThreads * kSteps;     // 3072
 constexpr int kRadix = 256;
 #ifndef TGS_SWEEP_BLOCKS
-#define TGS_SWEEP_BLOCKS 2
+#define TGS_SWEEP_BLOCKS 3
 #endif
 constexpr int kSweepBlocks = 148 * TGS_SWEEP_BLOCKS;  // persistent one-sweep blocks
 
@@ -132,7 +135,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     const uint32_t t0 = tile * (uint32_t)kTileItems;
     if (t0 >= n) return;
 
-    // 1. load + stable per-warp ranking (warp w owns items [w * 512, w * 512 + 512) of the tile)
+    // 1. load + stable per-warp ranking (warp w owns items [w * 32 kSteps, (w + 1) * 32 kSteps) of the tile)
     uint32_t k[kSteps], v[kSteps], rk[kSteps];
 #pragma unroll
     for (int s = 0; s < kSteps; ++s) {

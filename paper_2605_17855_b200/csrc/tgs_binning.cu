@@ -420,9 +420,10 @@ __global__ void offsets_kernel(BinArgs a) {
 // inside which warp w's part starts after the parts of warps < w (per-slice column counts, made
 // here in shared memory).  Lane per entry: each lane marks the columns of its entry in a per-warp
 // column bitmask; the entry's slot in column c is the column's running position plus the number of
-// earlier lanes (= earlier entries) that also cover c, and the highest such lane advances the
-// column.  Slots are in the block's shared output buffer (with each slot's column id), flushed
-// with one flat coalesced pass; a block whose output exceeds the buffer writes global slots.
+// earlier lanes (= earlier entries) that also cover c; after each 32-entry chunk every column
+// advances by its mask's population.  Slots are in the block's shared output buffer (with each
+// slot's column id), flushed with one flat coalesced pass; a block whose output exceeds the buffer
+// writes global slots.
 template <int KC>
 __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
     constexpr int kPer = kSliceLen / 32;  // row entries per lane
@@ -549,14 +550,14 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_place_kernel(BinArgs a) {
                     }
                 }
             __syncwarp();
-            for (int t = 0; t < ms; ++t)
-                if (t < span) {
-                    const uint32_t m = cmask[x0 + t];
-                    if ((m >> lane) == 1u) {
-                        cpos[x0 + t] += __popc(m);
-                        cmask[x0 + t] = 0u;
-                    }
+            // advance every column by its entries in this chunk (lane-owned columns, race-free)
+            for (int x = lane; x < gx; x += 32) {
+                const uint32_t m = cmask[x];
+                if (m) {
+                    cpos[x] += __popc(m);
+                    cmask[x] = 0u;
                 }
+            }
             __syncwarp();
         }
         __syncthreads();

@@ -191,7 +191,10 @@ __device__ __forceinline__ int project_one(const DevScene& s, const DevCamera& c
     return 1;
 }
 
-constexpr int kPreBlock = 256;
+#ifndef TGS_PRE_BLOCK
+#define TGS_PRE_BLOCK 128
+#endif
+constexpr int kPreBlock = TGS_PRE_BLOCK;
 #ifndef TGS_PRE_PER
 #define TGS_PRE_PER 2
 #endif

@@ -181,6 +181,26 @@ class Port(_Base):
     prefix = "tor_"
     so_path = PORT_SO
 
+    def bin_sort_fast(self, proj, width, height, g):
+        """tor_bin_sort_fast: the same lists in O(entries) (full-size frames)."""
+        proj = np.ascontiguousarray(proj, dtype=PROJ_DTYPE)
+        f = self.lib.tor_bin_sort_fast
+        f.restype = C.c_int64
+        f.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64,
+                      C.c_void_p, C.c_void_p]
+        app = np.zeros(1, dtype=np.uint64)
+        total = f(proj.ctypes.data, len(proj), width, height, g, None, 0, None, app.ctypes.data)
+        if total < 0:
+            raise ValueError("bin_sort_fast failed")
+        tiles_x, tiles_y = (width + 15) // 16, (height + 15) // 16
+        ng = ((tiles_x + g - 1) // g) * ((tiles_y + g - 1) // g)
+        ent = np.zeros(max(total, 1), dtype=ENTRY_DTYPE)
+        off = np.zeros(ng + 1, dtype=np.uint32)
+        t2 = f(proj.ctypes.data, len(proj), width, height, g, ent.ctypes.data, total, off.ctypes.data, None)
+        if t2 != total:
+            raise ValueError("bin_sort_fast failed (second pass)")
+        return ent[:total], off, int(app[0])
+
     def rasterize(self, entries, offsets, proj, width, height, **opt):
         """Rasterise sorted lists; returns (image, counters dict incl. walked/blended pairs)."""
         entries = np.ascontiguousarray(entries, dtype=ENTRY_DTYPE)

@@ -421,6 +421,92 @@ int64_t tor_bin_sort(const tor_projected* p, int64_t n, int width, int height, i
     }
 }
 
+/* Same lists as tor_bin_sort, in O(entries) instead of a comparison sort of every entry, so the
+ * oracle can check full-size frames (C3 G=1: 195M entries).  build_group_entries emits a
+ * Gaussian's entries in index order and at most one per group; std::stable_sort on
+ * (gid << 32 | depth bits) (binning.cpp:86-91) therefore leaves group g's list = the Gaussians
+ * overlapping g ordered by (depth bits, index).  So: order the Gaussians by (depth bits, index)
+ * once, then distribute them into the groups they overlap (a stable counting sort by gid).
+ * Pinned against tor_bin_sort by tests/test_oracle.py. */
+typedef struct { uint32_t key; uint32_t idx; } dpair;
+
+static int dpair_cmp(const void* a, const void* b) {
+    const dpair* x = (const dpair*)a;
+    const dpair* y = (const dpair*)b;
+    if (x->key != y->key) return x->key < y->key ? -1 : 1;
+    return x->idx < y->idx ? -1 : (x->idx > y->idx ? 1 : 0);
+}
+
+int64_t tor_bin_sort_fast(const tor_projected* p, int64_t n, int width, int height, int g,
+                          tor_entry* out, int64_t cap, uint32_t* offsets, uint64_t* appearances) {
+    gcfg c;
+    int64_t total = 0, i;
+    uint64_t app = 0;
+    dpair* ord;
+    uint64_t* cur;
+    int ng;
+    if (gcfg_make(g, width, height, &c) != 0) return -1;
+    ng = c.groups_x * c.groups_y;
+    for (i = 0; i < n; ++i) {
+        int r[4];
+        tile_rect(&p[i], &c, r);
+        if (r[2] < r[0] || r[3] < r[1]) continue;
+        total += (int64_t)(r[2] / g - r[0] / g + 1) * (r[3] / g - r[1] / g + 1);
+        app += (uint64_t)(r[2] - r[0] + 1) * (uint64_t)(r[3] - r[1] + 1);
+    }
+    if (appearances) *appearances = app;
+    if (!out || total > cap) return total;
+    ord = (dpair*)malloc((size_t)(n ? n : 1) * sizeof(dpair));
+    cur = (uint64_t*)calloc((size_t)ng + 1, sizeof(uint64_t));
+    if (!ord || !cur) { free(ord); free(cur); return -2; }
+    for (i = 0; i < n; ++i) {
+        int r[4];
+        tile_rect(&p[i], &c, r);
+        if (r[2] < r[0] || r[3] < r[1]) { ord[i].key = 0; ord[i].idx = (uint32_t)i; continue; }
+        if (!isfinite(p[i].depth) || p[i].depth < 0.0f) { free(ord); free(cur); return -1; }
+        ord[i].key = f2u(p[i].depth);
+        ord[i].idx = (uint32_t)i;
+        {
+            const int gx0 = r[0] / g, gx1 = r[2] / g, gy0 = r[1] / g, gy1 = r[3] / g;
+            int gy, gx;
+            for (gy = gy0; gy <= gy1; ++gy)
+                for (gx = gx0; gx <= gx1; ++gx) ++cur[gy * c.groups_x + gx + 1];
+        }
+    }
+    for (i = 1; i <= ng; ++i) cur[i] += cur[i - 1];
+    for (i = 0; i <= ng; ++i) offsets[i] = (uint32_t)cur[i];
+    qsort(ord, (size_t)n, sizeof(dpair), dpair_cmp);
+    for (i = 0; i < n; ++i) {
+        const tor_projected* q = &p[ord[i].idx];
+        int r[4];
+        tile_rect(q, &c, r);
+        if (r[2] < r[0] || r[3] < r[1]) continue;
+        {
+            const int gx0 = r[0] / g, gx1 = r[2] / g, gy0 = r[1] / g, gy1 = r[3] / g;
+            int gy, gx;
+            for (gy = gy0; gy <= gy1; ++gy)
+                for (gx = gx0; gx <= gx1; ++gx) {
+                    const int gid = gy * c.groups_x + gx;
+                    tor_entry* o = &out[cur[gid]++];
+                    uint32_t mask = 0;
+                    const int ty0 = r[1] > gy * g ? r[1] : gy * g;
+                    const int ty1 = r[3] < gy * g + g - 1 ? r[3] : gy * g + g - 1;
+                    const int tx0 = r[0] > gx * g ? r[0] : gx * g;
+                    const int tx1 = r[2] < gx * g + g - 1 ? r[2] : gx * g + g - 1;
+                    int ty, tx;
+                    for (ty = ty0; ty <= ty1; ++ty)
+                        for (tx = tx0; tx <= tx1; ++tx) mask |= 1u << ((ty - gy * g) * g + (tx - gx * g));
+                    o->gaussian_index = ord[i].idx;
+                    o->depth = q->depth;
+                    o->mask = mask;
+                }
+        }
+    }
+    free(ord);
+    free(cur);
+    return total;
+}
+
 /* ------------------------------------------------------------------------------------------ */
 /* operands.hpp:16-72, raster_scalar.hpp:29-55 — staged operands, canonical power, alpha, blend */
 /* ------------------------------------------------------------------------------------------ */

@@ -63,6 +63,10 @@ int64_t tor_project(const float* rec, int64_t n, int deg, const tor_camera* cam,
 /* binning.cpp:46-100. Returns total entries; writes when total <= cap. */
 int64_t tor_bin_sort(const tor_projected* p, int64_t n, int width, int height, int g,
                      tor_entry* out, int64_t cap, uint32_t* offsets, uint64_t* appearances);
+/* Same result as tor_bin_sort in O(entries): (depth, index) order + stable distribution by group.
+ * One call: returns total; writes entries/offsets when out != NULL and total <= cap. */
+int64_t tor_bin_sort_fast(const tor_projected* p, int64_t n, int width, int height, int g,
+                          tor_entry* out, int64_t cap, uint32_t* offsets, uint64_t* appearances);
 
 /* raster_scalar.cpp:52-71 (backend 0, G must be 1) or raster_tensor.cpp:173-191 (backend 1).
  * Works on already-sorted lists; counters may be NULL. Returns 0 or -1 (validation). */

@@ -102,3 +102,29 @@ def test_load_reduction_constructed(port):
     assert len(ent) == 64 and app == 256 and 1.0 - len(ent) / app == 0.75
     assert np.all(ent["mask"] == 0b1111)
     assert ENTRY_DTYPE.itemsize == 12
+
+
+@pytest.mark.parametrize("seed,count,smin,smax,rot", [(61, 20000, 0.01, 0.05, False), (62, 8000, 0.02, 0.2, True),
+                                                      (63, 5000, 0.01, 0.08, True)])
+def test_fast_bin_sort_matches_sort_entries(port, seed, count, smin, smax, rot):
+    """tor_bin_sort_fast (presort by (depth, index) + stable distribution by group, used by the
+    full-size GPU parity tests) equals the restatement of build_group_entries + std::stable_sort
+    (binning.cpp:46-100) entry for entry, including depth ties."""
+    cam = rotated_camera(480, 270, yaw_deg=9.0, pitch_deg=-4.0) if rot else make_camera(480, 270)
+    rec = np.array(port.gen_scene(seed, count, 1.0, smin, smax, 0), np.float32)
+    rec[::7, 2] = rec[3, 2]  # depth ties across many splats
+    pp, _ = port.project(rec, cam)
+    for g in (1, 2, 4):
+        ea, oa, xa = port.bin_sort(pp, cam.width, cam.height, g)
+        eb, ob, xb = port.bin_sort_fast(pp, cam.width, cam.height, g)
+        assert np.array_equal(_bits(ea), _bits(eb)) and np.array_equal(oa, ob) and xa == xb
+
+
+def test_fast_bin_sort_matches_reference_build(port, ref):
+    cam = rotated_camera(320, 200, yaw_deg=-13.0, pitch_deg=6.0)
+    rec = port.gen_scene(64, 6000, 1.0, 0.01, 0.1, 0)
+    pp, _ = port.project(rec, cam)
+    for g in (1, 2, 4):
+        ea, oa, xa = ref.bin_sort(pp, cam.width, cam.height, g)
+        eb, ob, xb = port.bin_sort_fast(pp, cam.width, cam.height, g)
+        assert np.array_equal(_bits(ea), _bits(eb)) and np.array_equal(oa, ob) and xa == xb

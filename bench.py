@@ -48,29 +48,54 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+    """SM clocks + throttle reasons sampled while the timed region runs: NVML polled every
+    ~0.5 ms from a thread (the timed region of a default run is ~20 ms), nvidia-smi as fallback."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReasons bits (nvml.h): hw_slowdown 0x8, sw_thermal 0x20, hw_thermal 0x40,
+    # sw_power_cap 0x4
+    REASON_BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                   "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device = device
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons set)
         self._stop = threading.Event()
         self._t = None
+        self._nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(device))
+        except Exception:
+            self._nv = None
+
+    def _sample_nvml(self):
+        nv, h = self._nv
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        return float(sm), float(mx), {k for k, b in self.REASON_BITS.items() if bits & b}
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,"
+                              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        f = [x.strip() for x in out.split(",")]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        return float(f[0]), float(f[1]), {names[i] for i in range(4) if f[2 + i].lower() == "active"}
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self.samples.append(self._sample_nvml() if self._nv else self._sample_smi())
             except Exception:
-                pass
-            self._stop.wait(0.2)
+                self._nv = None if self._nv else self._nv
+            self._stop.wait(0.0005 if self._nv else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -83,33 +108,28 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 4 + i and s[4 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [s[0] for s in self.samples]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
+                "sm_mhz_min": min(sm), "reasons": sorted(set().union(*(s[2] for s in self.samples))),
+                "samples": len(self.samples), "source": "nvml" if self._nv else "nvidia-smi"}
 
 
-def cpu_reference_sample(rec, cam_ns, group, backend, band_index, n_bands=8):
-    """One bounded sample of the reference's CPU path: a band of ~1/n_bands of the group rows,
-    through the reference's stage API (project_scene over all splats, then build_group_entries /
-    sort_entries / rasterize_* on the band).  Returns (frame_fraction, seconds, stage ms)."""
+def cpu_reference_frame(rec, cam_ns, group, backend, n_bands=1, band_first=0, band_count=None):
+    """The reference's CPU path on this host through its own stage API (oracle/_ref, all host
+    threads): project_scene ONCE, then build_group_entries / sort_entries / rasterize_* per
+    horizontal band of group rows (n_bands = 1: the whole frame, exactly render.cpp:7-35).
+    Returns (fraction of the frame covered, seconds charged, workers): the timed bands plus
+    project_scene's time scaled by that fraction (it runs once per frame)."""
     from oracle.oracle import Ref
     ref = Ref()
-    tiles_y = (cam_ns.height + 15) // 16
-    groups_y = (tiles_y + group - 1) // group
-    rows = [round(i * groups_y / n_bands) for i in range(n_bands + 1)]
-    g0, g1 = rows[band_index % n_bands], rows[band_index % n_bands + 1]
-    y0, y1 = g0 * group * 16, min(cam_ns.height, g1 * group * 16)
     workers = ref.hardware_concurrency()
-    t0 = time.perf_counter()
-    _, ms = ref.time_stages(rec, cam_ns, band_y0=y0, band_h=y1 - y0, backend=backend, group_size=group,
-                            workers=workers)
-    dt = time.perf_counter() - t0
-    return (y1 - y0) / cam_ns.height, dt, ms, workers
+    band_count = n_bands if band_count is None else band_count
+    rows, ms_proj, bands = ref.time_bands(rec, cam_ns, n_bands, band_first, band_count, backend=backend,
+                                          group_size=group, workers=workers)
+    frac = rows / cam_ns.height
+    sec = (ms_proj * frac + sum(sum(b) for b in bands)) / 1e3
+    return frac, sec, workers
 
 
 def run_reference(args):
@@ -129,10 +149,11 @@ def run_reference(args):
     fracs, secs = [], []
     workers = 1
     for i in range(args.warmup + args.steps):
-        c = cams[i % N_CAMS]
+        # step i: band i % 8 of orbit camera 5 + i // 8 (the cameras our arm renders)
+        c = cams[(5 + i // 8) % N_CAMS]
         cns = SimpleNamespace(view=c.view, focal_x=c.focal_x, focal_y=c.focal_y, width=W, height=H,
                               near=c.near, far=c.far)
-        frac, dt, ms, workers = cpu_reference_sample(rec, cns, 2, 1, i)
+        frac, dt, workers = cpu_reference_frame(rec, cns, 2, 1, n_bands=8, band_first=i % 8, band_count=1)
         if i >= args.warmup:
             fracs.append(frac)
             secs.append(dt)
@@ -146,8 +167,9 @@ def run_reference(args):
                    "(reference CPU path; each step one 1/8 band of a frame)", "global_batch": 1,
                    "seq_len": 0, "parallelism": "cpu"},
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": workers, "kind": "reference",
-                         "sample": "per step one 1/8-height band of a 3M/1080p frame: project_scene on all "
-                                   "splats + build_group_entries/sort_entries/rasterize_groups_tensor on the band"},
+                         "sample": "per step one 1/8-height band of a 3M/1080p orbit frame through the reference "
+                                   "stage API: build_group_entries/sort_entries/rasterize_groups_tensor on the "
+                                   "band, project_scene (run once per frame) charged 1/8"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -198,10 +220,13 @@ def main():
     lanes = [ctx] + [gsr.Context(local) for _ in range(LANES - 1)]
     lane_ds = [ds] + [c.upload(scene) for c in lanes[1:]]
     lane_streams = [torch.cuda.ExternalStream(c.stream, device=torch.device("cuda", local)) for c in lanes]
-    for k, c in enumerate(lanes[1:], 1):  # capacity sizing + schedule warm-up of the extra lanes
+    for k, c in enumerate(lanes[1:], 1):  # every lane sized on every camera it may render (untimed)
+        for cam in {id(x): x for x in mine}.values():
+            c.enqueue(lane_ds[k], cam, opt_t)
+            c.sync()
         for i in range(args.warmup):
             c.enqueue(lane_ds[k], mine[i], opt_t)
-            c.sync()
+        c.sync()
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in lanes]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in lanes]
     if world > 1:
@@ -215,6 +240,8 @@ def main():
             lanes[k].enqueue(lane_ds[k], mine[args.warmup + i], opt_t)
         for e, s in zip(ev1, lane_streams):
             e.record(s)
+        # tgs_sync raises if ANY frame enqueued on the lane since its last sync overflowed its
+        # entry buffers or failed validation (sticky device counters), so no blank frame is counted
         st_last = ctx.sync()
         for c in lanes[1:]:
             c.sync()
@@ -253,7 +280,7 @@ def main():
     ctx.sync()
     walked, blended = ctx.count_pairs()
 
-    # ---- roofline of the dominant kernel ----------------------------------------------------
+    # ---- rooflines (SURVEY.md §8(d) / BASELINE.md §2) ------------------------------------------
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -261,44 +288,58 @@ def main():
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     tflops = float(peaks.get("bf16_tflops", 1590.0))
-    peak_src = "measured" if peaks else "fallback"
-    stages = {k: st_t[k] for k in ("preprocess", "binning", "sort", "raster")}
-    dom = max(stages, key=stages.get)
+    peak_src = "measured (MEASURED_PEAKS.json)" if peaks else "fallback (B200_PROFILING.md)"
     n_vis = int(st_last.visible)
     ent = st_t["entries"]
-    # algorithmic bytes per launch of each HBM-bound stage: preprocess reads the
-    # 56-B SH0 record and writes the 64-B projected record (+ rect, key, value); the depth presort
-    # moves (key, value) pairs 4 times; binning writes every 4-B list entry once and reads the
-    # rank-ordered rect (8 B) twice plus the rank->index map (4 B)
-    alg_bytes = {"preprocess": (56 + 64) * N_SPLATS, "sort": 4 * 16 * n_vis, "binning": 4 * ent + 20 * n_vis}
+    clk_sum = clk.summary()
+    sm_mhz = clk_sum.get("sm_mhz") or float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+    # Raster (the kernel the paper targets): bound by the MUFU / FP32 pipes, the tensor pipe is a
+    # minor consumer.  W = walked pairs, C = alpha-contributing pairs (instrumented walk); per pipe
+    # algorithmic ops: tensor 12 W flops (unpadded 6-term contraction), MUFU C ex2, FP32 8 C + 2 W;
+    # peaks: FP32 = SMs x 128 lanes x clock, MUFU = SMs x 16 x clock (clock sampled in the timed
+    # region), tensor = measured dense bf16 (the f16 kind runs at the same rate)
+    t_r = st_t["raster"] / 1e3
+    pipes = {
+        "fp32": {"ops": 8.0 * blended + 2.0 * walked, "peak_tops": n_sm * 128 * sm_mhz * 1e6 / 1e12},
+        "mufu": {"ops": float(blended), "peak_tops": n_sm * 16 * sm_mhz * 1e6 / 1e12},
+        "tensor": {"ops": 12.0 * walked, "peak_tops": tflops},
+    }
+    for p in pipes.values():
+        p["achieved_tops"] = p["ops"] / t_r / 1e12
+        p["frac"] = p["achieved_tops"] / p["peak_tops"]
+    bound = max(pipes, key=lambda k: pipes[k]["frac"])
     traffic = None
     try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json"))).get(dom)
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json"))).get("raster")
     except Exception:
         pass
-    if dom == "raster":
-        # tensor pipe: 12 useful flops per walked (pixel, splat) pair (6-term contraction)
-        achieved = 12.0 * walked / (st_t["raster"] / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": tflops, "unit": "TFLOP/s",
-                "frac": achieved / tflops, "traffic": traffic, "kernel": "raster_tensor_kernel<4>",
-                "algorithmic": "12 flops per walked pixel-splat pair (6-term contraction)"}
-    else:
-        achieved = alg_bytes[dom] / (stages[dom] / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "kernel": {"binning": "rows_count/place + cols_count/place + scans",
-                                               "sort": "depth presort (digit histograms + 4 one-sweep passes)",
-                                               "preprocess": "preprocess_kernel"}[dom],
-                "algorithmic_bytes": alg_bytes[dom]}
-    roof["peak_source"] = peak_src
-    # raster pipes (the kernel the paper targets): FP32 / MUFU work per the survey's model
-    sm_mhz = clk.summary().get("sm_mhz") or 1965.0
-    lanes = 148 * 128 * sm_mhz * 1e6
-    fp32_ops = 8.0 * blended + 2.0 * walked
-    raster_pipes = {
-        "walked_pairs": walked, "blended_pairs": blended,
-        "fp32_frac": fp32_ops / (st_t["raster"] / 1e3) / lanes,
-        "mufu_frac": blended / (st_t["raster"] / 1e3) / (148 * 16 * sm_mhz * 1e6),
-        "tensor_frac": 32.0 * walked / (st_t["raster"] / 1e3) / (tflops * 1e12),
+    roof = {"bound": bound, "achieved": pipes[bound]["achieved_tops"], "peak": pipes[bound]["peak_tops"],
+            "unit": "TFLOP/s" if bound == "tensor" else "Tops/s", "frac": pipes[bound]["frac"],
+            "traffic": traffic, "kernel": "raster_tensor_kernel<4>",
+            "algorithmic": "max over pipes of ops / (pipe peak x raster time); W walked, C contributing pairs",
+            "walked_pairs": walked, "blended_pairs": blended, "sm_mhz": sm_mhz, "sms": n_sm,
+            "pipes": {k: {"achieved": v["achieved_tops"], "peak": v["peak_tops"], "frac": v["frac"]}
+                      for k, v in pipes.items()},
+            "peak_source": f"fp32/mufu: lanes x sampled clock; tensor: {peak_src}"}
+    # HBM-bound stages: algorithmic bytes under BASELINE.md's model (preprocess 56 B read + 44 B
+    # written per Gaussian; bin + sort 36 B per list entry) and under this implementation's own
+    # minimum (preprocess 56 + 64 B; presort 16 B per visible splat and pass x 4;
+    # binning 4 B per entry + 20 B per visible splat)
+    def frac(bytes_, ms):
+        gbs = bytes_ / (ms / 1e3) / 1e9
+        return {"bytes": bytes_, "ms": ms, "gbs": gbs, "frac": gbs / hbm}
+    stage_roofline = {
+        "peak_gbs": hbm, "peak_source": peak_src,
+        "baseline_model": {
+            "preprocess": frac((56 + 44) * N_SPLATS, st_t["preprocess"]),
+            "bin_sort": frac(36 * ent, st_t["binning"] + st_t["sort"]),
+        },
+        "implementation_model": {
+            "preprocess": frac((56 + 64) * N_SPLATS, st_t["preprocess"]),
+            "sort": frac(4 * 16 * n_vis, st_t["sort"]),
+            "binning": frac(4 * ent + 20 * n_vis, st_t["binning"]),
+        },
     }
 
     # ---- e2e through the C ABI with host buffers (gsr::render call shape) --------------------
@@ -328,7 +369,8 @@ def main():
                "d2h_bytes_per_step": int(W * H * 3 * 4),
                "api": "tgs_render_records (scene records + camera in, RGB float image out; pinned host buffers)"}
 
-    # ---- CPU baseline: the reference's own CPU path on this host (rank 0, N=1) ---------------
+    # ---- CPU baseline: the reference's own CPU path on this host (rank 0, N=1): one whole
+    # frame of the bench camera path through its stage API (render.cpp:7-35), all host threads --
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:
         try:
@@ -338,16 +380,11 @@ def main():
                 c = mine[args.warmup]
                 cns = SimpleNamespace(view=c.view, focal_x=c.focal_x, focal_y=c.focal_y, width=W, height=H,
                                       near=c.near, far=c.far)
-                fr, sec, nb = 0.0, 0.0, 0
-                workers = 1
-                while sec < 10.0 and nb < 8:
-                    f, dt, _, workers = cpu_reference_sample(scene.records, cns, 2, 1, nb)
-                    fr += f
-                    sec += dt
-                    nb += 1
+                fr, sec, workers = cpu_reference_frame(scene.records, cns, 2, 1)
                 cpu = {"value": fr / sec, "unit": "frames/s", "cores": workers, "kind": "reference",
-                       "sample": f"{nb} of 8 horizontal bands of one 3M/1080p frame (G=2 tensor fp32) "
-                                 "through the reference stage API (oracle/_ref), ~10 s of CPU work"}
+                       "sample": "one whole 3M/1080p orbit frame (G=2 tensor fp32) through the reference stage "
+                                 "API (oracle/_ref: project_scene, build_group_entries, sort_entries, "
+                                 "rasterize_groups_tensor), steady_clock per stage"}
         except Exception as e:  # reported, never fatal for the GPU number
             cpu = {"value": None, "unit": "frames/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
@@ -368,9 +405,9 @@ def main():
         "raster_no_tile_cull": {"tensor_ms": st_t_nc["raster"], "cuda_core_ms": st_s_nc["raster"],
                                 "speedup": speedup_nc},
         "stage_ms": st_t, "baseline_stage_ms": st_s,
-        "roofline": roof, "raster_pipes": raster_pipes,
+        "roofline": roof, "stage_roofline": stage_roofline,
         "cpu_baseline": cpu, "e2e": e2e,
-        "clocks": clk.summary(), "gpu_launches": launches_per_frame * args.steps,
+        "clocks": clk_sum, "gpu_launches": launches_per_frame * args.steps,
     }
     if rank == 0:
         print(json.dumps(line))

@@ -51,11 +51,11 @@ thread_local CtxHolder t_ctx;
 std::vector<float> to_records(const std::vector<Gaussian3D>& scene, int& sh_degree) {
     sh_degree = 0;
     if (!scene.empty()) {
-        const bool first = scene.front().sh_rest.has_value();
+        // eval_sh_color (projection.cpp:55-77) takes sh_rest per Gaussian: a scene where only
+        // some Gaussians carry it is uploaded as degree 3 with zero coefficients for the others,
+        // which adds only +-0 to their colour (bit-identical to the degree-0 evaluation)
         for (const auto& g : scene)
-            if (g.sh_rest.has_value() != first)
-                throw ValidationError("render: mixed sh_rest presence across Gaussians");
-        sh_degree = first ? 3 : 0;
+            if (g.sh_rest.has_value()) sh_degree = 3;
     }
     const size_t rf = sh_degree == 3 ? 59 : 14;
     std::vector<float> rec(scene.size() * rf);
@@ -67,7 +67,7 @@ std::vector<float> to_records(const std::vector<Gaussian3D>& scene, int& sh_degr
         r[6] = g.rotation.w(), r[7] = g.rotation.x(), r[8] = g.rotation.y(), r[9] = g.rotation.z();
         r[10] = g.opacity;
         r[11] = g.sh_dc.x(), r[12] = g.sh_dc.y(), r[13] = g.sh_dc.z();
-        if (sh_degree == 3) std::memcpy(r + 14, g.sh_rest->data(), sizeof(float) * kShRestCoeffs);
+        if (sh_degree == 3 && g.sh_rest.has_value()) std::memcpy(r + 14, g.sh_rest->data(), sizeof(float) * kShRestCoeffs);
     }
     return rec;
 }

@@ -287,6 +287,21 @@ class Ref(_Base):
             raise ValueError(self.last_error())
         return int(n), dict(zip(("project", "bin", "sort", "raster"), ms.tolist()))
 
+    def time_bands(self, rec, cam, n_bands, band_first, band_count, **opt):
+        """project_scene once, then bin/sort/raster per band (gref_time_bands):
+        (image rows covered, project ms, [(bin, sort, raster) ms per band])."""
+        rec = np.ascontiguousarray(rec, dtype=np.float32)
+        deg = 3 if rec.shape[1] == 59 else 0
+        ms = np.zeros(1 + 3 * band_count, dtype=np.float64)
+        f = self.lib.gref_time_bands
+        f.restype = C.c_int64
+        rows = f(_f32p(rec), C.c_int64(len(rec)), C.c_int(deg), C.byref(make_camera(cam)),
+                 C.byref(make_options(**opt)), C.c_int(n_bands), C.c_int(band_first), C.c_int(band_count),
+                 ms.ctypes.data_as(C.c_void_p))
+        if rows < 0:
+            raise ValueError(self.last_error())
+        return int(rows), float(ms[0]), [tuple(ms[1 + 3 * b: 4 + 3 * b]) for b in range(band_count)]
+
     def last_error(self) -> str:
         f = self.lib.gref_last_error
         f.restype = C.c_char_p

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <bit>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -329,6 +330,62 @@ std::int64_t gref_time_stages(const float* rec, std::int64_t n, int deg, const C
         }
         ms4[3] = ms_since(t0);
         return total;
+    } catch (const gsr::ValidationError& e) {
+        return fail(e, 1);
+    } catch (const std::exception& e) {
+        return fail(e, 9);
+    }
+}
+
+// The same stage API with project_scene run ONCE per frame and the remaining stages run per
+// horizontal band: band k of n_bands covers group rows [round(k*gy/n), round((k+1)*gy/n)).
+// Bands [band_first, band_first + band_count) are timed; ms = {project, then per timed band
+// bin, sort, raster}.  Returns the sum of the timed bands' image rows.  Each band copies and
+// shifts the projected list (untimed), exactly like gref_time_stages.
+std::int64_t gref_time_bands(const float* rec, std::int64_t n, int deg, const CCamera* cam, const COptions* opt,
+                             int n_bands, int band_first, int band_count, double* ms) {
+    try {
+        const auto scene = to_scene(rec, n, deg);
+        const gsr::RenderOptions o = to_opt(opt);
+        const gsr::Camera c = to_cam(cam);
+        auto t0 = std::chrono::steady_clock::now();
+        const auto pr_full = gsr::project_scene(scene, c, o.workers);
+        ms[0] = ms_since(t0);
+        const int g16 = o.group_size * 16;
+        const int gy = (c.height + g16 - 1) / g16;
+        std::int64_t rows = 0;
+        for (int b = 0; b < band_count; ++b) {
+            const int k = (band_first + b) % n_bands;
+            const int r0 = static_cast<int>(std::lround(static_cast<double>(k) * gy / n_bands));
+            const int r1 = static_cast<int>(std::lround(static_cast<double>(k + 1) * gy / n_bands));
+            const int y0 = r0 * g16, y1 = std::min(c.height, r1 * g16);
+            double* m = ms + 1 + 3 * b;
+            m[0] = m[1] = m[2] = 0.0;
+            if (y1 <= y0) continue;
+            rows += y1 - y0;
+            auto pr = pr_full;
+            for (auto& p : pr) p.mean2d.y() -= static_cast<float>(y0);
+            const auto cfg = gsr::GroupConfig::square(o.group_size, c.width, y1 - y0);
+            t0 = std::chrono::steady_clock::now();
+            auto entries = gsr::build_group_entries(pr, cfg);
+            m[0] = ms_since(t0);
+            t0 = std::chrono::steady_clock::now();
+            const auto lists = gsr::sort_entries(std::move(entries), cfg);
+            m[1] = ms_since(t0);
+            t0 = std::chrono::steady_clock::now();
+            if (o.backend == gsr::Backend::scalar) {
+                auto img = gsr::rasterize_tiles_scalar(lists, pr, cfg, o.constants, o.mode, o.workers);
+            } else {
+                gsr::TensorRasterOptions t;
+                t.constants = o.constants;
+                t.mode = o.mode;
+                t.chunk_len = o.chunk_len;
+                t.workers = o.workers;
+                auto img = gsr::rasterize_groups_tensor(lists, pr, cfg, t);
+            }
+            m[2] = ms_since(t0);
+        }
+        return rows;
     } catch (const gsr::ValidationError& e) {
         return fail(e, 1);
     } catch (const std::exception& e) {

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -127,6 +128,7 @@ struct tgs_ctx {
     tgs_ctx* lanes[kBatchLanes - 1] = {};
     tgs_ctx* parent = nullptr;
     int tile_cull = 1;  // tgs_set_tile_cull
+    uint32_t acked_overflow = 0, acked_invalid = 0;  // sticky frame-failure counters already reported
     tgs_scene* scratch_scene = nullptr;
 };
 
@@ -210,6 +212,12 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     const int n_groups = gg.n_groups_band;
     if (n_groups > 49152)
         return set_err(TGS_ERR_VALIDATION, "render: more than 49152 groups in one frame/band; use bands");
+    // binning lanes own group columns / band rows lane + 32k, k < 16 (tgs_binning.cu)
+    if (gg.groups_x > 512)
+        return set_err(TGS_ERR_VALIDATION, "render: more than 512 group columns (image wider than 8192 px at "
+                                           "G=1); use a larger group size");
+    if (band1 - band0 > 512)
+        return set_err(TGS_ERR_VALIDATION, "render: more than 512 group rows in one frame/band; use bands");
     cudaStream_t s = ctx->stream;
     const int64_t n = scene->n;
     const int n_alloc = (int)std::max<int64_t>(n, 1);
@@ -234,8 +242,11 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
         std::max({scan_tmp_elems(h1), scan_tmp_elems(h2), scan_tmp_elems(sort_scratch_elems((size_t)n_alloc))}) * 4));
     TGS_CUDA_OK(ctx->ghist.ensure(sort_scratch_elems((size_t)n_alloc) * 4));
     TGS_CUDA_OK(ctx->offsets.ensure((size_t)(n_groups + 1) * 4));
-    TGS_CUDA_OK(ctx->order.ensure((size_t)gg.tiles_x * gg.tiles_y * 4));
-    TGS_CUDA_OK(ctx->ucost.ensure((size_t)gg.tiles_x * gg.tiles_y * 4));
+    // raster work units: the tensor path splits G=4 groups into 2x2-tile quarters
+    const int units_per_group = opt->backend == TGS_BACKEND_TENSOR ? raster_units_per_group(gg.g) : 1;
+    const size_t n_units = (size_t)std::max(1, n_groups * units_per_group);
+    TGS_CUDA_OK(ctx->order.ensure(n_units * 4));
+    TGS_CUDA_OK(ctx->ucost.ensure(n_units * 4));
     const int row0 = band0 * gg.g * kTile;
     const int row1 = std::min(cam->height, band1 * gg.g * kTile);
     TGS_CUDA_OK(ctx->image.ensure((size_t)(row1 - row0) * cam->width * 3 * sizeof(float)));
@@ -244,7 +255,8 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     const DevProjected proj = dev_proj(ctx);
 
     TGS_CUDA_OK(cudaEventRecord(ctx->ev[0], s));
-    TGS_CUDA_OK(cudaMemsetAsync(fc, 0, sizeof(FrameCounters), s));
+    // the sticky counters at the end of FrameCounters survive across frames (tgs_sync checks them)
+    TGS_CUDA_OK(cudaMemsetAsync(fc, 0, offsetof(FrameCounters, sticky_overflow), s));
 
     // 1. preprocess + compaction
     PreprocessArgs pa;
@@ -295,14 +307,14 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     {
         // tensor G=4 groups are rasterised as 2x2-tile quarters (and G=2 groups as tile rows when
         // built with half units); the CUDA-core baseline always walks whole lists
-        const int per = opt->backend == TGS_BACKEND_TENSOR ? raster_units_per_group(gg.g) : 1;
+        const int per = units_per_group;
         // the previous frame's measured walks schedule this one when it had the same unit geometry
         // (same image, group size, band and backend): a camera path changes slowly
         const uint64_t key = ((uint64_t)(uint32_t)cam->width << 40) ^ ((uint64_t)(uint32_t)cam->height << 20) ^
                              ((uint64_t)band0 << 8) ^ ((uint64_t)band1 << 28) ^ ((uint64_t)gg.g << 4) ^
                              (uint64_t)opt->backend ^ (1ull << 63);
         const uint32_t* fb = (ctx->ucost_key == key) ? ctx->ucost.as<uint32_t>() : nullptr;
-        launch_unit_order(ctx->offsets.as<uint32_t>(), fb, n_groups * per, per, ctx->order.as<int>(), s);
+        launch_unit_order(ctx->offsets.as<uint32_t>(), fb, n_groups * per, per, ctx->order.as<int>(), fc, s);
         ctx->ucost_key = key;
     }
     TGS_CUDA_OK(cudaGetLastError());
@@ -324,9 +336,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     ra.tile_trip = nullptr;
     ra.unit_cost = ctx->ucost.as<uint32_t>();
     ra.tile_cull = ctx->tile_cull;
-    static const bool skip_raster = std::getenv("TGS_DEBUG_SKIP_RASTER") != nullptr;  // bisection aid
-    if (skip_raster) {
-    } else if (opt->backend == TGS_BACKEND_SCALAR)
+    if (opt->backend == TGS_BACKEND_SCALAR)
         launch_raster_scalar(ra, s);
     else
         launch_raster_tensor(ra, ctx->num_sms, s);
@@ -349,6 +359,20 @@ tgs_status finish_frame(tgs_ctx* ctx, tgs_stats* stats) {
     TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
     ctx->pending = false;
     const FrameCounters& f = *ctx->h_fc;
+    {
+        // frames enqueued since the last sync that overflowed their entry buffers or failed
+        // validation: only the last one is recovered (re-rendered / reported) below, an earlier
+        // one left an invalid image behind, so the whole sequence fails
+        const uint32_t of = f.sticky_overflow - ctx->acked_overflow, bad = f.sticky_invalid - ctx->acked_invalid;
+        ctx->acked_overflow = f.sticky_overflow;
+        ctx->acked_invalid = f.sticky_invalid;
+        if (of > (f.overflow ? 1u : 0u))
+            return set_err(TGS_ERR_OOM, "render: a frame enqueued before the last tgs_sync exceeded the entry "
+                                        "capacity (its lists were not built); size the context on every camera first");
+        if (bad > (f.err_validation ? 1u : 0u))
+            return set_err(TGS_ERR_VALIDATION, "render: a frame enqueued before the last tgs_sync failed validation "
+                                               "(non-positive scale or bad depth)");
+    }
     if (f.overflow) {
         // entry buffers too small: grow (25% headroom) and re-render this frame
         const uint64_t need = (uint64_t)f.n_entries + f.n_entries / 4 + 1024;
@@ -360,6 +384,8 @@ tgs_status finish_frame(tgs_ctx* ctx, tgs_stats* stats) {
         if (st != TGS_OK) return st;
         TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
         ctx->pending = false;
+        ctx->acked_overflow = ctx->h_fc->sticky_overflow;
+        ctx->acked_invalid = ctx->h_fc->sticky_invalid;
         if (ctx->h_fc->overflow) return set_err(TGS_ERR_OOM, "render: entry capacity overflow after growth");
     }
     const FrameCounters& g = *ctx->h_fc;

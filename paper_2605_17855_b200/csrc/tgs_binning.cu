@@ -738,7 +738,12 @@ __global__ void encode_u8_kernel(const float* __restrict__ rgb, int64_t n, uint8
 // 8 buckets per octave; equal keys keep unit order.
 __global__ void __launch_bounds__(1024) unit_order_kernel(const uint32_t* __restrict__ offsets,
                                                           const uint32_t* __restrict__ feedback, int n_units,
-                                                          int per_group, int* __restrict__ order) {
+                                                          int per_group, int* __restrict__ order,
+                                                          FrameCounters* __restrict__ fc) {
+    if (threadIdx.x == 0) {
+        if (fc->overflow) atomicAdd(&fc->sticky_overflow, 1u);
+        if (fc->err_validation) atomicAdd(&fc->sticky_invalid, 1u);
+    }
     constexpr int kBuckets = 264;
     __shared__ uint32_t cnt[kBuckets];
     for (int k = threadIdx.x; k < kBuckets; k += blockDim.x) cnt[k] = 0;
@@ -766,8 +771,8 @@ __global__ void __launch_bounds__(1024) unit_order_kernel(const uint32_t* __rest
 }  // namespace
 
 void launch_unit_order(const uint32_t* offsets, const uint32_t* feedback, int n_units, int per_group, int* order,
-                       cudaStream_t st) {
-    if (n_units > 0) unit_order_kernel<<<1, 1024, 0, st>>>(offsets, feedback, n_units, per_group, order);
+                       FrameCounters* fc, cudaStream_t st) {
+    unit_order_kernel<<<1, 1024, 0, st>>>(offsets, feedback, n_units, per_group, order, fc);
 }
 
 int bin_chunks(int) { return kRowChunks; }

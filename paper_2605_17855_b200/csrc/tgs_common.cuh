@@ -60,6 +60,10 @@ struct FrameCounters {
     unsigned long long blended;
     unsigned int key_min_inv;       // ~min and max of the visible depth keys: the presort ranks
     unsigned int key_max;           // (key - min), so passes above the key range are plain copies
+    // not zeroed per frame: frames of this context that overflowed / failed validation so far
+    // (counted by unit_order_kernel, checked by tgs_sync so no un-synced frame fails silently)
+    unsigned int sticky_overflow;
+    unsigned int sticky_invalid;
 };
 
 // Group geometry (GroupConfig, binning.hpp:15-31) with an optional band of group rows.

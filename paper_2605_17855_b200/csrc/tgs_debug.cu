@@ -225,3 +225,62 @@ extern "C" tgs_status tgs_debug_pipeline(int chunks, int mode, long long* cycles
     const cudaError_t e = tgs::debug_pipeline(chunks, mode, cycles);
     return e == cudaSuccess ? TGS_OK : TGS_ERR_CUDA;
 }
+
+// ---- self-test hook: one M=128 x N=32 x K=16 tcgen05.mma through the rasterizer's descriptors --
+namespace tgs {
+namespace {
+__device__ __forceinline__ uint32_t dbg_core_off(int row, int khalf) {
+    return (uint32_t)((row >> 3) * 256 + khalf * 128 + (row & 7) * 16);
+}
+__global__ void __launch_bounds__(128, 1) debug_mma_kernel(const uint16_t* __restrict__ a,
+                                                            const uint16_t* __restrict__ b,
+                                                            float* __restrict__ d) {
+    __shared__ __align__(1024) uint8_t sa[128 * 32];
+    __shared__ __align__(1024) uint8_t sb[32 * 32];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int t = threadIdx.x, warp = t >> 5;
+    // row t of A (16 halves) -> core-matrix layout
+    for (int kh = 0; kh < 2; ++kh) {
+        uint4 v = *reinterpret_cast<const uint4*>(a + t * 16 + kh * 8);
+        *reinterpret_cast<uint4*>(sa + dbg_core_off(t, kh)) = v;
+        if (t < 32) {
+            uint4 w = *reinterpret_cast<const uint4*>(b + t * 16 + kh * 8);
+            *reinterpret_cast<uint4*>(sb + dbg_core_off(t, kh)) = w;
+        }
+    }
+    if (t == 0) {
+        ptx::mbar_init(&bar, 1);
+        ptx::mbar_fence_init();
+    }
+    if (warp == 0) ptx::tmem_alloc<32>(&tbase);
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tm = tbase;
+    if (t == 0) {
+        ptx::mma_f16_ss(tm, ptx::smem_desc(ptx::smem_u32(sa), 128, 256), ptx::smem_desc(ptx::smem_u32(sb), 128, 256),
+                        ptx::idesc_f16(128, 32), 0u);
+        ptx::mma_commit(&bar);
+    }
+    ptx::mbar_wait(&bar, 0);
+    ptx::tc_fence_after();
+    uint32_t r[32];
+    ptx::tmem_ld16(tm + ((uint32_t)(warp * 32) << 16), r);
+    ptx::tmem_ld16(tm + ((uint32_t)(warp * 32) << 16) + 16, r + 16);
+    ptx::tmem_wait_ld();
+    ptx::reg_fence16(r);
+    ptx::reg_fence16(r + 16);
+    for (int j = 0; j < 32; ++j) d[t * 32 + j] = __uint_as_float(r[j]);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == 0) ptx::tmem_dealloc<32>(tm);
+}
+}  // namespace
+
+void launch_debug_mma(const uint16_t* a, const uint16_t* b, float* d, cudaStream_t st) {
+    debug_mma_kernel<<<1, 128, 0, st>>>(a, b, d);
+}
+}  // namespace tgs

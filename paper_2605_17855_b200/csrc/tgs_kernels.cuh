@@ -98,8 +98,9 @@ void launch_raster_scalar(const RasterArgs& a, cudaStream_t st);
 // group list) bucketed by floor(log2(list length)), longest first.
 // With `feedback` (per unit, entries walked by the previous frame of the same geometry) the cost
 // is the measured walk, else the list length.
+// Also folds the frame's overflow / validation flags into fc's sticky counters.
 void launch_unit_order(const uint32_t* offsets, const uint32_t* feedback, int n_units, int per_group, int* order,
-                       cudaStream_t st);
+                       FrameCounters* fc, cudaStream_t st);
 void launch_raster_tensor(const RasterArgs& a, int num_sms, cudaStream_t st);
 // raster work units per group list of the tensor path (schedule / feedback indexing)
 int raster_units_per_group(int g);

@@ -247,7 +247,9 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int i, f
             a.rect[i] = (tx1 >= tx0 && ty1 >= ty0)
                             ? make_uint2((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16))
                             : make_uint2(0xffffu, 0u);
-            if (tx1 >= tx0 && ty1 >= ty0) t.app += (unsigned long long)(tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+            // tile appearances of the band's tile rows only (the band's N_total, like its entries)
+            const int by0 = max(ty0, a.gg.band_gy0 * a.gg.g), by1 = min(ty1, a.gg.band_gy1 * a.gg.g - 1);
+            if (tx1 >= tx0 && by1 >= by0) t.app += (unsigned long long)(tx1 - tx0 + 1) * (by1 - by0 + 1);
             // sort_entries depth validation (binning.cpp:78-83) for splats that emit entries
             if (ng > 0 && !(isfinite(pr.depth) && pr.depth >= 0.0f)) atomicOr(&a.fc->err_validation, 2u);
         } else {

@@ -102,10 +102,13 @@ class Scene:
         gs = list(gs)
         if not gs:
             return Scene(np.zeros((0, 14), np.float32))
-        have = [g.sh_rest is not None for g in gs]
-        if any(have) and not all(have):
-            raise ValidationError("save_scene: mixed sh_rest presence across records")
-        return Scene(np.stack([g.record() for g in gs]))
+        # eval_sh_color (projection.cpp:55-77) takes sh_rest per Gaussian; a scene where only some
+        # Gaussians carry it becomes degree 3 with zero coefficients for the others (+-0 terms:
+        # their colours are bit-identical).  save_scene keeps the reference's mixed-presence error.
+        recs = [g.record() for g in gs]
+        if any(len(r) == 59 for r in recs):
+            recs = [r if len(r) == 59 else list(r) + [0.0] * kShRestCoeffs for r in recs]
+        return Scene(np.stack([np.asarray(r, np.float32) for r in recs]))
 
     def gaussian(self, i: int) -> Gaussian3D:
         r = self.records[i]
@@ -496,6 +499,11 @@ _GSB_HEADER = 16
 def save_scene(scene, path: str) -> None:
     """save_scene (scene_io.cpp:103-136): 16-byte header (magic "GSB1", u32 count, u32 sh_degree,
     u32 reserved 0) then little-endian float32 records (14, or 59 with sh_rest)."""
+    if not isinstance(scene, (Scene, np.ndarray)):
+        scene = list(scene)
+        have = [g.sh_rest is not None for g in scene]
+        if any(have) and not all(have):  # save_scene, scene_io.cpp:103-109
+            raise ValidationError("save_scene: mixed sh_rest presence across records")
     sc = as_scene(scene)
     deg = sc.sh_degree if len(sc) else 0
     head = _GSB_MAGIC + np.array([len(sc), deg, 0], dtype="<u4").tobytes()

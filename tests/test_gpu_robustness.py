@@ -1,0 +1,127 @@
+"""GPU tests of the C ABI's failure behaviour and input handling.
+
+* frames enqueued back to back without tgs_sync: an entry-capacity overflow of an EARLIER frame
+  must fail the sync (sticky device counters), never leave a silently blank image;
+* frame sizes the binning kernels cannot place (> 512 group columns / band rows) are rejected
+  with ValidationError instead of corrupting memory;
+* scenes where only some Gaussians carry sh_rest render like the reference's eval_sh_color
+  (projection.cpp:55-77): the degree-0 Gaussians' colours are bit-identical to a pure degree-0
+  scene's;
+* a thin image whose tensor G=4 unit count exceeds the tile count renders within tolerance
+  (order / feedback buffers sized by work units).
+"""
+import numpy as np
+import pytest
+
+from tests.cases import make_camera
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gsr():
+    from paper_2605_17855_b200 import gsr as g
+    return g
+
+
+def _cam(gsr, c):
+    return gsr.Camera(np.asarray(c.view, np.float32), c.focal_x, c.focal_y, c.width, c.height, c.near, c.far)
+
+
+def test_unsynced_overflow_is_reported(gsr, port):
+    ctx = gsr.Context(0)  # fresh context: entry capacity starts empty, so every frame overflows
+    try:
+        rec = port.gen_scene(11, 3000, 1.0, 0.01, 0.06, 0)
+        ds = ctx.upload(rec)
+        cam = gsr.make_camera(160, 128)
+        opt = gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 2)
+        ctx.enqueue(ds, cam, opt)
+        ctx.enqueue(ds, cam, opt)  # overwrites the first frame's bookkeeping before any sync
+        with pytest.raises(gsr.DeviceError, match="enqueued before the last tgs_sync"):
+            ctx.sync()
+        # the context recovers: the last frame was re-rendered with grown buffers, and a synced
+        # frame matches a fresh render
+        res = ctx.render(ds, cam, opt)
+        ref = gsr.Context(0)
+        try:
+            res2 = ref.render(ref.upload(rec), cam, opt)
+        finally:
+            ref.close()
+        assert np.array_equal(res.image.rgb, res2.image.rgb)
+    finally:
+        ctx.close()
+
+
+def test_single_overflow_recovers(gsr, port):
+    ctx = gsr.Context(0)
+    try:
+        rec = port.gen_scene(12, 2000, 1.0, 0.01, 0.06, 0)
+        ds = ctx.upload(rec)
+        cam = gsr.make_camera(128, 96)
+        opt = gsr.RenderOptions(gsr.Backend.scalar, gsr.PrecisionMode.fp32, 1)
+        ctx.enqueue(ds, cam, opt)
+        st = ctx.sync()  # the one overflowed frame is re-rendered, no error
+        assert st.entries > 0
+    finally:
+        ctx.close()
+
+
+@pytest.mark.parametrize("w,h,backend,group", [(8208, 16, 0, 1), (16, 8208, 0, 1), (16400, 32, 1, 2)])
+def test_oversized_grids_rejected(gsr, port, w, h, backend, group):
+    ctx = gsr.default_context(0)
+    rec = port.gen_scene(13, 100, 1.0, 0.01, 0.05, 0)
+    ds = ctx.upload(rec)
+    cam = gsr.make_camera(w, h)
+    with pytest.raises(gsr.ValidationError, match="512 group"):
+        ctx.render(ds, cam, gsr.RenderOptions(gsr.Backend(backend), gsr.PrecisionMode.fp32, group))
+
+
+def test_band_of_tall_frame_accepted(gsr, port):
+    """A frame taller than 512 group rows renders as bands of <= 512 rows."""
+    ctx = gsr.default_context(0)
+    rec = port.gen_scene(14, 500, 1.0, 0.01, 0.05, 0)
+    ds = ctx.upload(rec)
+    cam = gsr.make_camera(32, 8208)
+    img, st = ctx.render_band(ds, cam, gsr.RenderOptions(gsr.Backend.scalar, gsr.PrecisionMode.fp32, 1), 0, 512)
+    assert img.shape == (512 * 16, 32, 3)
+
+
+def test_mixed_sh_rest_scene(gsr, port):
+    rec3 = port.gen_scene(15, 400, 1.0, 0.01, 0.05, 5)   # degree 3
+    rec0 = np.ascontiguousarray(rec3[:, :14])            # the same Gaussians, degree 0
+    gs = []
+    for i, r in enumerate(rec3):
+        gs.append(gsr.Gaussian3D(tuple(r[0:3]), tuple(r[3:6]), tuple(r[6:10]), float(r[10]), tuple(r[11:14]),
+                                 tuple(r[14:59]) if i % 2 == 0 else None))
+    scene = gsr.Scene.from_gaussians(gs)  # promoted to degree 3, zero coefficients for odd i
+    assert scene.sh_degree == 3
+    cam = _cam(gsr, make_camera(96, 80))
+    ctx = gsr.default_context(0)
+    opt = gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 2)
+    ctx.render(ctx.upload(scene), cam, opt)
+    pm = ctx.read_projected()
+    ctx.render(ctx.upload(rec0), cam, opt)
+    p0 = ctx.read_projected()
+    ctx.render(ctx.upload(rec3), cam, opt)
+    p3 = ctx.read_projected()
+    # the generator's means all lie inside this camera's frustum, so the projected lists are in
+    # input order and complete
+    assert len(pm) == len(p0) == len(p3) == len(rec3)
+    c_m, c_0, c_3 = (x["color"].view(np.uint32) for x in (pm, p0, p3))
+    assert np.array_equal(c_m[1::2], c_0[1::2]), "degree-0 Gaussians of a mixed scene changed colour"
+    assert np.array_equal(c_m[0::2], c_3[0::2])
+    assert not np.array_equal(c_0, c_3)
+
+
+def test_thin_image_g4_units(gsr, port):
+    """16 px wide, G=4: 4 raster work units per group but only one tile column."""
+    rec = port.gen_scene(16, 800, 1.0, 0.02, 0.08, 0)
+    c = make_camera(16, 256)
+    cam = _cam(gsr, c)
+    ctx = gsr.default_context(0)
+    res = ctx.render(ctx.upload(rec), cam, gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 4))
+    proj_ref, _ = port.project(rec, c)
+    ent, off, _ = port.bin_sort(proj_ref, 16, 256, 4)
+    img_ref, _ = port.rasterize(ent, off, proj_ref, 16, 256, backend=1, group_size=4)
+    d = np.abs(res.image.rgb.astype(np.float64) - img_ref)
+    assert d.max() <= 2.0 / 255.0

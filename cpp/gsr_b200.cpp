@@ -126,6 +126,153 @@ RenderResult render(const std::vector<Gaussian3D>& scene, const Camera& cam, con
     return finish(cam, std::move(rgb), st);
 }
 
+// ---- stage API over the C ABI --------------------------------------------------------------
+namespace {
+tgs_projected to_c(const ProjectedGaussian& p) {
+    tgs_projected o{};
+    o.mean2d[0] = p.mean2d.x();
+    o.mean2d[1] = p.mean2d.y();
+    o.conic[0] = p.conic_a;
+    o.conic[1] = p.conic_b;
+    o.conic[2] = p.conic_c;
+    o.color[0] = p.color.x();
+    o.color[1] = p.color.y();
+    o.color[2] = p.color.z();
+    o.opacity = p.opacity;
+    o.depth = p.depth;
+    o.radius = p.radius;
+    return o;
+}
+ProjectedGaussian from_c(const tgs_projected& o) {
+    ProjectedGaussian p;
+    p.mean2d = Eigen::Vector2f(o.mean2d[0], o.mean2d[1]);
+    p.conic_a = o.conic[0];
+    p.conic_b = o.conic[1];
+    p.conic_c = o.conic[2];
+    p.color = Eigen::Vector3f(o.color[0], o.color[1], o.color[2]);
+    p.opacity = o.opacity;
+    p.depth = o.depth;
+    p.radius = o.radius;
+    return p;
+}
+std::vector<tgs_projected> to_c(const std::vector<ProjectedGaussian>& v) {
+    std::vector<tgs_projected> o(v.size());
+    for (size_t i = 0; i < v.size(); ++i) o[i] = to_c(v[i]);
+    return o;
+}
+static_assert(sizeof(GroupEntry) == sizeof(tgs_group_entry) && sizeof(KeyedEntry) == sizeof(tgs_keyed_entry),
+              "entry layouts must match the C ABI");
+
+ImageBuffer rasterize_lists(const SortedGroupLists& lists, const std::vector<ProjectedGaussian>& projected,
+                            const GroupConfig& cfg, Backend backend, const RasterConstants& k, PrecisionMode mode,
+                            int workers, int chunk_len) {
+    cfg.validate();
+    RenderOptions opt;
+    opt.backend = backend;
+    opt.mode = mode;
+    opt.group_size = cfg.group_h;
+    opt.workers = workers;
+    opt.chunk_len = chunk_len;
+    opt.constants = k;
+    const tgs_options o = to_c(opt);
+    const std::vector<tgs_projected> p = to_c(projected);
+    ImageBuffer img(cfg.image_width, cfg.image_height);
+    check(tgs_rasterize_lists(t_ctx.get(t_device), reinterpret_cast<const tgs_group_entry*>(lists.entries.data()),
+                              static_cast<int64_t>(lists.entries.size()), lists.offsets.data(),
+                              static_cast<int64_t>(lists.offsets.size()), p.data(), static_cast<int64_t>(p.size()),
+                              cfg.image_width, cfg.image_height, &o, img.rgb.data()));
+    return img;
+}
+}  // namespace
+
+std::vector<ProjectedGaussian> project_scene(const std::vector<Gaussian3D>& scene, const Camera& cam, int workers,
+                                             ProjectionStats* stats) {
+    if (workers < 1) throw ValidationError("project_scene: workers must be >= 1");
+    int deg = 0;
+    const std::vector<float> rec = to_records(scene, deg);
+    tgs_ctx* ctx = t_ctx.get(t_device);
+    const tgs_camera c = to_c(cam);
+    int64_t n = 0;
+    tgs_stats st{};
+    check(tgs_project_scene(ctx, rec.data(), static_cast<int64_t>(scene.size()), deg, &c, nullptr, 0, &n, &st));
+    std::vector<tgs_projected> out(static_cast<size_t>(n));
+    if (n) check(tgs_read_projected(ctx, out.data(), n, &n));
+    if (stats) {
+        stats->input = st.input;
+        stats->culled = st.culled;
+        stats->dropped_degenerate = st.dropped_degenerate;
+    }
+    std::vector<ProjectedGaussian> r(out.size());
+    for (size_t i = 0; i < out.size(); ++i) r[i] = from_c(out[i]);
+    return r;
+}
+
+GroupConfig GroupConfig::square(int g, int image_width, int image_height) {
+    GroupConfig cfg;
+    cfg.group_h = g;
+    cfg.group_w = g;
+    cfg.image_width = image_width;
+    cfg.image_height = image_height;
+    cfg.validate();
+    return cfg;
+}
+
+void GroupConfig::validate() const {
+    if (image_width <= 0 || image_height <= 0) throw ValidationError("GroupConfig: image dimensions must be positive");
+    if (!(group_h == group_w && (group_h == 1 || group_h == 2 || group_h == 4)))
+        throw ValidationError("GroupConfig: supported group sizes are 1x1, 2x2, 4x4");
+}
+
+TileRect tiles_overlapped(const ProjectedGaussian& p, const GroupConfig& cfg) {
+    // floor((mean -+ r) / 16): the same IEEE operations the GPU binning uses
+    const float r = static_cast<float>(p.radius);
+    TileRect t;
+    t.min_x = std::max(static_cast<int>(std::floor((p.mean2d.x() - r) / kTileSize)), 0);
+    t.max_x = std::min(static_cast<int>(std::floor((p.mean2d.x() + r) / kTileSize)), cfg.tiles_x() - 1);
+    t.min_y = std::max(static_cast<int>(std::floor((p.mean2d.y() - r) / kTileSize)), 0);
+    t.max_y = std::min(static_cast<int>(std::floor((p.mean2d.y() + r) / kTileSize)), cfg.tiles_y() - 1);
+    return t;
+}
+
+std::vector<KeyedEntry> build_group_entries(const std::vector<ProjectedGaussian>& projected, const GroupConfig& cfg) {
+    cfg.validate();
+    tgs_ctx* ctx = t_ctx.get(t_device);
+    const std::vector<tgs_projected> p = to_c(projected);
+    int64_t n = 0;
+    check(tgs_build_group_entries(ctx, p.data(), static_cast<int64_t>(p.size()), cfg.image_width, cfg.image_height,
+                                  cfg.group_h, nullptr, 0, &n));
+    std::vector<KeyedEntry> out(static_cast<size_t>(n));
+    if (n)
+        check(tgs_build_group_entries(ctx, p.data(), static_cast<int64_t>(p.size()), cfg.image_width,
+                                      cfg.image_height, cfg.group_h, reinterpret_cast<tgs_keyed_entry*>(out.data()),
+                                      n, &n));
+    return out;
+}
+
+SortedGroupLists sort_entries(std::vector<KeyedEntry> entries, const GroupConfig& cfg) {
+    cfg.validate();
+    SortedGroupLists lists;
+    lists.entries.resize(entries.size());
+    lists.offsets.assign(static_cast<size_t>(cfg.group_count()) + 1, 0u);
+    check(tgs_sort_entries(t_ctx.get(t_device), reinterpret_cast<const tgs_keyed_entry*>(entries.data()),
+                           static_cast<int64_t>(entries.size()), cfg.image_width, cfg.image_height, cfg.group_h,
+                           reinterpret_cast<tgs_group_entry*>(lists.entries.data()), lists.offsets.data(),
+                           static_cast<int64_t>(lists.offsets.size())));
+    return lists;
+}
+
+ImageBuffer rasterize_tiles_scalar(const SortedGroupLists& lists, const std::vector<ProjectedGaussian>& projected,
+                                   const GroupConfig& cfg, const RasterConstants& k, PrecisionMode mode, int workers) {
+    return rasterize_lists(lists, projected, cfg, Backend::scalar, k, mode, workers, kFragmentDim);
+}
+
+ImageBuffer rasterize_groups_tensor(const SortedGroupLists& lists, const std::vector<ProjectedGaussian>& projected,
+                                    const GroupConfig& cfg, const TensorRasterOptions& opt, OpReport* ops) {
+    (void)ops;
+    return rasterize_lists(lists, projected, cfg, Backend::tensor, opt.constants, opt.mode, opt.workers,
+                           opt.chunk_len);
+}
+
 namespace b200 {
 
 void set_device(int device) { t_device = device; }

@@ -127,6 +127,93 @@ struct RenderResult {
     std::uint64_t tile_appearances = 0;
 };
 
+// ---- stage API (projection.hpp, binning.hpp, raster_scalar.hpp, raster_tensor.hpp) ----------
+// Same declarations as the reference's public stage API; every stage runs on the GPU through the
+// C ABI on the caller's data (tgs_project_scene, tgs_build_group_entries, tgs_sort_entries,
+// tgs_rasterize_lists).  Lists and projected records are bit-exact with the reference; images are
+// within the FP16 tolerance.  `workers`/`chunk_len` are validated and otherwise ignored.
+
+/// Screen-space splat (projection.hpp:14-23).
+struct ProjectedGaussian {
+    Eigen::Vector2f mean2d = Eigen::Vector2f::Zero();
+    float conic_a = 0.0f;
+    float conic_b = 0.0f;
+    float conic_c = 0.0f;
+    Eigen::Vector3f color = Eigen::Vector3f::Zero();
+    float opacity = 0.0f;
+    float depth = 0.0f;
+    int radius = 0;
+};
+
+/// project_scene (projection.hpp:48-50).
+std::vector<ProjectedGaussian> project_scene(const std::vector<Gaussian3D>& scene, const Camera& cam, int workers,
+                                             ProjectionStats* stats = nullptr);
+
+inline constexpr int kTileSize = 16;
+
+/// GroupConfig (binning.hpp:15-31).
+struct GroupConfig {
+    int group_h = 2;
+    int group_w = 2;
+    int image_width = 0;
+    int image_height = 0;
+    static GroupConfig square(int g, int image_width, int image_height);
+    int tiles_x() const { return (image_width + kTileSize - 1) / kTileSize; }
+    int tiles_y() const { return (image_height + kTileSize - 1) / kTileSize; }
+    int groups_x() const { return (tiles_x() + group_w - 1) / group_w; }
+    int groups_y() const { return (tiles_y() + group_h - 1) / group_h; }
+    int group_count() const { return groups_x() * groups_y(); }
+    int tiles_per_group() const { return group_h * group_w; }
+    void validate() const;
+};
+
+/// TileRect (binning.hpp:34-37).
+struct TileRect {
+    int min_x = 0, min_y = 0, max_x = -1, max_y = -1;
+    bool empty() const { return max_x < min_x || max_y < min_y; }
+};
+
+/// GroupEntry / KeyedEntry / SortedGroupLists (binning.hpp:41-59).
+struct GroupEntry {
+    std::uint32_t gaussian_index = 0;
+    float depth = 0.0f;
+    std::uint32_t mask = 0;
+};
+struct KeyedEntry {
+    std::uint32_t group_id = 0;
+    GroupEntry entry;
+};
+struct SortedGroupLists {
+    std::vector<GroupEntry> entries;
+    std::vector<std::uint32_t> offsets;  // group_count + 1 prefix offsets
+    std::uint32_t group_begin(int group) const { return offsets[group]; }
+    std::uint32_t group_end(int group) const { return offsets[group + 1]; }
+};
+
+/// tiles_overlapped (binning.hpp:63-64): the splat's AABB clipped to the tile grid (host helper).
+TileRect tiles_overlapped(const ProjectedGaussian& p, const GroupConfig& cfg);
+/// build_group_entries (binning.hpp:68-69) — on the GPU.
+std::vector<KeyedEntry> build_group_entries(const std::vector<ProjectedGaussian>& projected, const GroupConfig& cfg);
+/// sort_entries (binning.hpp:72-73) — hand-written radix sort on the GPU.
+SortedGroupLists sort_entries(std::vector<KeyedEntry> entries, const GroupConfig& cfg);
+
+/// rasterize_tiles_scalar (raster_scalar.hpp:59-62) — the CUDA-core baseline kernel.
+ImageBuffer rasterize_tiles_scalar(const SortedGroupLists& lists, const std::vector<ProjectedGaussian>& projected,
+                                   const GroupConfig& cfg, const RasterConstants& k,
+                                   PrecisionMode mode = PrecisionMode::fp32, int workers = 1);
+
+/// TensorRasterOptions (raster_tensor.hpp:45-50).
+struct TensorRasterOptions {
+    RasterConstants constants{};
+    PrecisionMode mode = PrecisionMode::fp32;
+    int chunk_len = kFragmentDim;
+    int workers = 1;
+};
+/// rasterize_groups_tensor (raster_tensor.hpp:62-65) — the tcgen05 grouped kernel.  `ops` is
+/// left untouched (the CPU fragment-emulation counters have no GPU meaning).
+ImageBuffer rasterize_groups_tensor(const SortedGroupLists& lists, const std::vector<ProjectedGaussian>& projected,
+                                    const GroupConfig& cfg, const TensorRasterOptions& opt, OpReport* ops = nullptr);
+
 /// Drop-in for the reference's gsr::render: uploads the scene, renders on the current B200
 /// (device 0 unless gsr::b200::set_device was called), downloads the image.
 RenderResult render(const std::vector<Gaussian3D>& scene, const Camera& cam, const RenderOptions& opt);

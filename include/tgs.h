@@ -95,6 +95,12 @@ typedef struct {
     uint32_t mask; /* bit r*G+c per overlapped member tile */
 } tgs_group_entry;
 
+/* gsr::KeyedEntry (binning.hpp:47-50), 16 bytes: build_group_entries output, sort_entries input. */
+typedef struct {
+    uint32_t group_id;
+    tgs_group_entry entry;
+} tgs_keyed_entry;
+
 typedef struct tgs_ctx tgs_ctx;
 typedef struct tgs_scene tgs_scene;
 
@@ -166,6 +172,36 @@ tgs_status tgs_render_batch(tgs_ctx* ctx, const tgs_scene* scene, const tgs_came
 tgs_status tgs_read_projected(tgs_ctx* ctx, tgs_projected* out, int64_t cap, int64_t* n);
 tgs_status tgs_read_lists(tgs_ctx* ctx, tgs_group_entry* out, int64_t cap, uint32_t* offsets,
                           int64_t offsets_cap, int64_t* n);
+
+/* ---- The reference's public stage API on caller-provided data (one GPU call per stage). ------
+ * Each call is synchronous, uses the context's stream and scratch buffers, and validates like the
+ * reference (GroupConfig::validate binning.cpp:22-30 -> VALIDATION).  Variable-size outputs use
+ * the two-call pattern: *n receives the size, nothing is written when cap is too small. */
+
+/* project_scene(scene, cam, workers, &stats) (projection.hpp:48-50): compacted projected list in
+ * input order; stats receives input / culled / dropped_degenerate.  Non-positive scales of
+ * visible Gaussians -> VALIDATION (projection.cpp:37). */
+tgs_status tgs_project_scene(tgs_ctx* ctx, const float* records, int64_t count, int sh_degree,
+                             const tgs_camera* cam, tgs_projected* out, int64_t cap, int64_t* n,
+                             tgs_stats* stats);
+/* build_group_entries(projected, GroupConfig::square(G, width, height)) (binning.hpp:68-69): one
+ * KeyedEntry per (splat, overlapped group), splat order then group id (gy outer, gx inner). */
+tgs_status tgs_build_group_entries(tgs_ctx* ctx, const tgs_projected* proj, int64_t n, int width, int height,
+                                   int group_size, tgs_keyed_entry* out, int64_t cap, int64_t* n_out);
+/* sort_entries(entries, cfg) (binning.hpp:72-73): entries stably sorted by
+ * (group_id << 32) | f32_bits(depth), offsets = group_count + 1 prefix offsets.  A non-finite
+ * or negative depth -> VALIDATION (binning.cpp:78-83); a group id >= group_count -> VALIDATION. */
+tgs_status tgs_sort_entries(tgs_ctx* ctx, const tgs_keyed_entry* entries, int64_t n, int width, int height,
+                            int group_size, tgs_group_entry* out, uint32_t* offsets, int64_t offsets_cap);
+/* rasterize_tiles_scalar (opt->backend SCALAR, G must be 1: raster_scalar.cpp:56-57) /
+ * rasterize_groups_tensor (TENSOR) (raster_scalar.hpp:59-62, raster_tensor.hpp:62-65) on caller
+ * lists: entries/offsets as sort_entries returns them for GroupConfig::square(opt->group_size,
+ * width, height).  Every entry's mask must be the one build_group_entries derives from its
+ * splat (the GPU rasterisers recompute masks), its index must address proj -> VALIDATION
+ * otherwise.  out_rgb: width * height * 3 floats, clamped like ImageBuffer::finalize. */
+tgs_status tgs_rasterize_lists(tgs_ctx* ctx, const tgs_group_entry* entries, int64_t n_entries,
+                               const uint32_t* offsets, int64_t offsets_count, const tgs_projected* proj,
+                               int64_t n, int width, int height, const tgs_options* opt, float* out_rgb);
 
 /* Walked / alpha-contributing pair counts of the last frame (the raster roofline numerator,
  * DESIGN.md §Roofline); computed by an instrumented pass, not by the timed kernels. */

@@ -66,6 +66,13 @@ SIGNATURES = {
     "tgs_gen_synthetic_scene": (c_status, [C.c_uint64, C.c_int, C.c_float, C.c_float, C.c_float,
                                            C.c_uint64, F32P]),
     "tgs_encode_u8": (c_status, [P, P, C.c_int64, P]),
+    "tgs_project_scene": (c_status, [P, F32P, C.c_int64, C.c_int, C.POINTER(tgs_camera), P, C.c_int64,
+                                     C.POINTER(C.c_int64), C.POINTER(tgs_stats)]),
+    "tgs_build_group_entries": (c_status, [P, P, C.c_int64, C.c_int, C.c_int, C.c_int, P, C.c_int64,
+                                           C.POINTER(C.c_int64)]),
+    "tgs_sort_entries": (c_status, [P, P, C.c_int64, C.c_int, C.c_int, C.c_int, P, P, C.c_int64]),
+    "tgs_rasterize_lists": (c_status, [P, P, C.c_int64, P, C.c_int64, P, C.c_int64, C.c_int, C.c_int,
+                                       C.POINTER(tgs_options), F32P]),
     "tgs_debug_mma": (c_status, [P, P, P]),
     "tgs_debug_pipeline": (c_status, [C.c_int, C.c_int, C.POINTER(C.c_longlong)]),
     "tgs_debug_mma_rate": (c_status, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_longlong)]),

@@ -112,6 +112,7 @@ struct tgs_ctx {
     uint64_t ucost_key = 0;  // geometry the feedback belongs to (0: none)
     DBuf image;
     DBuf scratch_records;
+    DBuf stg[8];  // stage-API scratch (tgs_build_group_entries / tgs_sort_entries / tgs_rasterize_lists)
     FrameCounters* h_fc = nullptr;  // pinned
     uint32_t capacity = 0;          // entry capacity
     int64_t proj_cap = 0;
@@ -191,6 +192,7 @@ DevProjected dev_proj(tgs_ctx* ctx) {
     p.mc = b;
     p.co = b + ctx->proj_cap;
     p.col = b + 2 * ctx->proj_cap;
+    p.rr = reinterpret_cast<uint4*>(b + 3 * ctx->proj_cap);
     return p;
 }
 
@@ -224,7 +226,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
 
     // ---- buffers ----
     if (ctx->proj_cap < n_alloc) {
-        TGS_CUDA_OK(ctx->proj.ensure((size_t)n_alloc * 3 * sizeof(float4)));
+        TGS_CUDA_OK(ctx->proj.ensure((size_t)n_alloc * 4 * sizeof(float4)));
         ctx->proj_cap = n_alloc;
     }
     for (int i = 0; i < 2; ++i) {
@@ -268,6 +270,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     pa.gg = gg;
     pa.fc = fc;
     pa.alpha_skip = opt->alpha_skip;
+    pa.alpha_clamp = opt->alpha_clamp;
     launch_preprocess(pa, s);
     TGS_CUDA_OK(cudaGetLastError());
     TGS_CUDA_OK(cudaEventRecord(ctx->ev[1], s));
@@ -494,6 +497,8 @@ tgs_status tgs_ctx_create(int device, tgs_ctx** out) {
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     for (int i = 0; e == cudaSuccess && i < 6; ++i) e = cudaEventCreate(&c->ev[i]);
     if (e == cudaSuccess) e = c->fc.ensure(sizeof(FrameCounters));
+    // the sticky failure counters at the end of FrameCounters start at zero (never memset per frame)
+    if (e == cudaSuccess) e = cudaMemset(c->fc.p, 0, sizeof(FrameCounters));
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_fc, sizeof(FrameCounters));
     if (e != cudaSuccess) {
         tgs_ctx_destroy(c);
@@ -517,6 +522,7 @@ void tgs_ctx_destroy(tgs_ctx* c) {
                     &c->pre_vals[1], &c->rect, &c->rrect, &c->list, &c->rowlist, &c->hist, &c->bsum, &c->ghist,
                     &c->offsets, &c->order, &c->ucost, &c->image, &c->scratch_records};
     for (DBuf* b : bufs) b->release();
+    for (DBuf& b : c->stg) b.release();
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->h_fc) cudaFreeHost(c->h_fc);
@@ -847,6 +853,253 @@ tgs_status tgs_encode_u8(tgs_ctx* ctx, const float* rgb_device, int64_t n, uint8
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     tmp.release();
     if (e != cudaSuccess) return cuda_fail(e, "encode_u8", __FILE__, __LINE__);
+    return TGS_OK;
+}
+
+}  // extern "C"
+
+// ---- stage API on caller-provided data ------------------------------------------------------
+namespace tgs {
+namespace api {
+
+tgs_status validate_group_config(int g, int width, int height) {  // GroupConfig::validate (binning.cpp:22-30)
+    if (width <= 0 || height <= 0) return set_err(TGS_ERR_VALIDATION, "GroupConfig: image dimensions must be positive");
+    if (!(g == 1 || g == 2 || g == 4))
+        return set_err(TGS_ERR_VALIDATION, "GroupConfig: supported group sizes are 1x1, 2x2, 4x4");
+    return TGS_OK;
+}
+
+// Host -> device copy of n items into scratch buffer k (grown as needed).
+template <class T>
+tgs_status upload(tgs_ctx* ctx, int k, const T* host, size_t n, T** dev) {
+    TGS_CUDA_OK(ctx->stg[k].ensure(std::max<size_t>(n, 1) * sizeof(T)));
+    if (n) TGS_CUDA_OK(cudaMemcpyAsync(ctx->stg[k].p, host, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    *dev = ctx->stg[k].as<T>();
+    return TGS_OK;
+}
+
+}  // namespace api
+}  // namespace tgs
+
+extern "C" {
+
+tgs_status tgs_project_scene(tgs_ctx* ctx, const float* records, int64_t count, int sh_degree, const tgs_camera* cam,
+                             tgs_projected* out, int64_t cap, int64_t* n, tgs_stats* stats) {
+    if (!ctx || !cam || !n || (count > 0 && !records)) return set_err(TGS_ERR_VALIDATION, "project_scene: null argument");
+    cudaSetDevice(ctx->device);
+    if (!ctx->scratch_scene) ctx->scratch_scene = new tgs_scene();
+    tgs_status st = upload_into(ctx, ctx->scratch_scene, records, count, sh_degree);
+    if (st != TGS_OK) return st;
+    const int64_t na = std::max<int64_t>(count, 1);
+    if (ctx->proj_cap < na) {
+        TGS_CUDA_OK(ctx->proj.ensure((size_t)na * 4 * sizeof(float4)));
+        ctx->proj_cap = na;
+    }
+    TGS_CUDA_OK(ctx->pre_keys[0].ensure((size_t)na * 4));
+    TGS_CUDA_OK(ctx->rect.ensure((size_t)na * sizeof(uint2)));
+    const int w = std::max(cam->width, 1), h = std::max(cam->height, 1);
+    const GroupGeom gg = make_geom(1, w, h, 0, (h + kTile - 1) / kTile);
+    FrameCounters* fc = ctx->fc.as<FrameCounters>();
+    TGS_CUDA_OK(cudaMemsetAsync(fc, 0, offsetof(FrameCounters, sticky_overflow), ctx->stream));
+    PreprocessArgs pa;
+    pa.scene = ctx->scratch_scene->dev();
+    pa.cam = make_dev_camera(cam);
+    pa.out = dev_proj(ctx);
+    pa.depth_keys = ctx->pre_keys[0].as<uint32_t>();
+    pa.rect = ctx->rect.as<uint2>();
+    pa.gg = gg;
+    pa.fc = fc;
+    pa.alpha_skip = 1.0f / 255.0f;
+    pa.alpha_clamp = 0.99f;
+    launch_preprocess(pa, ctx->stream);
+    TGS_CUDA_OK(cudaGetLastError());
+    TGS_CUDA_OK(cudaMemcpyAsync(ctx->h_fc, fc, sizeof(FrameCounters), cudaMemcpyDeviceToHost, ctx->stream));
+    TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    ctx->acked_overflow = ctx->h_fc->sticky_overflow;
+    ctx->acked_invalid = ctx->h_fc->sticky_invalid;
+    if (ctx->h_fc->err_validation & 1u) return set_err(TGS_ERR_VALIDATION, "compute_cov3d: non-positive scale");
+    // the readback below reads the frame state of this call
+    ctx->last_scene = ctx->scratch_scene;
+    ctx->last_cam = *cam;
+    ctx->last_gg = gg;
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        stats->input = (uint64_t)count;
+        stats->culled = ctx->h_fc->culled;
+        stats->dropped_degenerate = ctx->h_fc->dropped;
+        stats->visible = ctx->h_fc->visible;
+    }
+    return tgs_read_projected(ctx, out, cap, n);
+}
+
+tgs_status tgs_build_group_entries(tgs_ctx* ctx, const tgs_projected* proj, int64_t n, int width, int height,
+                                   int group_size, tgs_keyed_entry* out, int64_t cap, int64_t* n_out) {
+    if (!ctx || !n_out || n < 0 || (n > 0 && !proj)) return set_err(TGS_ERR_VALIDATION, "build_group_entries: bad arguments");
+    tgs_status st = validate_group_config(group_size, width, height);
+    if (st != TGS_OK) return st;
+    cudaSetDevice(ctx->device);
+    const GroupGeom gg = make_geom(group_size, width, height, 0, 0);
+    tgs_projected* dp = nullptr;
+    st = upload(ctx, 0, proj, (size_t)n, &dp);
+    if (st != TGS_OK) return st;
+    TGS_CUDA_OK(ctx->stg[1].ensure((size_t)(n + 1) * 4));
+    uint32_t* counts = ctx->stg[1].as<uint32_t>();
+    TGS_CUDA_OK(ctx->stg[2].ensure(scan_tmp_elems((size_t)n + 1) * 4));
+    TGS_CUDA_OK(cudaMemsetAsync(counts, 0, (size_t)(n + 1) * 4, ctx->stream));
+    launch_entries_count(dp, n, gg, counts, ctx->stream);
+    launch_exclusive_scan(counts, (size_t)n + 1, ctx->stg[2].as<uint32_t>(), ctx->stream);
+    TGS_CUDA_OK(cudaGetLastError());
+    uint32_t total = 0;
+    TGS_CUDA_OK(cudaMemcpyAsync(&total, counts + n, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    *n_out = total;
+    if (!out || cap < (int64_t)total || total == 0) return TGS_OK;
+    TGS_CUDA_OK(ctx->stg[3].ensure((size_t)total * sizeof(tgs_keyed_entry)));
+    launch_entries_emit(dp, n, gg, counts, ctx->stg[3].as<tgs_keyed_entry>(), ctx->stream);
+    TGS_CUDA_OK(cudaGetLastError());
+    TGS_CUDA_OK(cudaMemcpyAsync(out, ctx->stg[3].p, (size_t)total * sizeof(tgs_keyed_entry), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+    TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    return TGS_OK;
+}
+
+tgs_status tgs_sort_entries(tgs_ctx* ctx, const tgs_keyed_entry* entries, int64_t n, int width, int height,
+                            int group_size, tgs_group_entry* out, uint32_t* offsets, int64_t offsets_cap) {
+    if (!ctx || n < 0 || (n > 0 && (!entries || !out)) || !offsets)
+        return set_err(TGS_ERR_VALIDATION, "sort_entries: bad arguments");
+    if (n > 0x7fffffffll) return set_err(TGS_ERR_VALIDATION, "sort_entries: more than 2^31 entries");
+    tgs_status st = validate_group_config(group_size, width, height);
+    if (st != TGS_OK) return st;
+    const GroupGeom gg = make_geom(group_size, width, height, 0, 0);
+    const uint32_t n_groups = (uint32_t)(gg.groups_x * gg.groups_y);
+    if (offsets_cap < (int64_t)n_groups + 1) return set_err(TGS_ERR_VALIDATION, "sort_entries: offsets too small");
+    cudaSetDevice(ctx->device);
+    const uint32_t m = (uint32_t)n;
+    tgs_keyed_entry* de = nullptr;
+    st = upload(ctx, 0, entries, (size_t)m, &de);
+    if (st != TGS_OK) return st;
+    const size_t cap = ((size_t)std::max<uint32_t>(m, 1) + 31) & ~(size_t)31;  // 16-byte aligned sub-arrays (vector loads)
+    // stg[1]: keys a | keys b | vals a | vals b | gids | flags+count ; stg[2]: sort scratch ; stg[3]: scan tmp
+    TGS_CUDA_OK(ctx->stg[1].ensure((5 * cap + 4) * 4));
+    uint32_t* u = ctx->stg[1].as<uint32_t>();
+    uint32_t *ka = u, *kb = u + cap, *va = u + 2 * cap, *vb = u + 3 * cap, *gid = u + 4 * cap, *flags = u + 5 * cap,
+             *count = flags + 1;
+    TGS_CUDA_OK(ctx->stg[2].ensure(sort_scratch_elems(cap) * 4));
+    TGS_CUDA_OK(ctx->stg[3].ensure(scan_tmp_elems(sort_scratch_elems(cap)) * 4));
+    TGS_CUDA_OK(cudaMemsetAsync(flags, 0, 8, ctx->stream));
+    launch_keyed_split(de, m, n_groups, ka, gid, flags, count, ctx->stream);
+    // pass A: stable by depth bits (values = entry positions); pass B: stable by group id
+    SortBuffers sb;
+    sb.keys[0] = ka;
+    sb.keys[1] = kb;
+    sb.vals[0] = va;
+    sb.vals[1] = vb;
+    sb.ghist = ctx->stg[2].as<uint32_t>();
+    sb.scan_tmp = ctx->stg[3].as<uint32_t>();
+    int r = radix_sort(sb, count, count, 32, false, false, cap, ctx->stream, nullptr, true);
+    uint32_t* perm = sb.vals[r];
+    uint32_t* k2 = sb.keys[r];  // free after pass A (keys not written in its last pass)
+    launch_gather_u32(gid, perm, m, k2, ctx->stream);
+    SortBuffers sb2 = sb;
+    sb2.keys[0] = k2;
+    sb2.keys[1] = sb.keys[r ^ 1];
+    sb2.vals[0] = perm;
+    sb2.vals[1] = sb.vals[r ^ 1];
+    const int gbits = std::max(1, ceil_log2((int)n_groups));
+    r = radix_sort(sb2, count, count, gbits, false, true, cap, ctx->stream, nullptr, false);
+    TGS_CUDA_OK(ctx->stg[4].ensure(cap * sizeof(tgs_group_entry)));
+    TGS_CUDA_OK(ctx->stg[5].ensure(cap * 4 + (size_t)(n_groups + 1) * 4));
+    uint32_t* gsorted = ctx->stg[5].as<uint32_t>();
+    uint32_t* doff = gsorted + cap;
+    launch_gather_entries(de, sb2.vals[r], m, ctx->stg[4].as<tgs_group_entry>(), gsorted, ctx->stream);
+    launch_offsets_from_sorted(gsorted, m, n_groups, doff, ctx->stream);
+    TGS_CUDA_OK(cudaGetLastError());
+    uint32_t hflags = 0;
+    TGS_CUDA_OK(cudaMemcpyAsync(&hflags, flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    if (hflags & 1u) return set_err(TGS_ERR_VALIDATION, "sort_entries: an entry has non-finite or negative depth");
+    if (hflags & 2u) return set_err(TGS_ERR_VALIDATION, "sort_entries: group id outside the GroupConfig");
+    if (m) TGS_CUDA_OK(cudaMemcpy(out, ctx->stg[4].p, (size_t)m * sizeof(tgs_group_entry), cudaMemcpyDeviceToHost));
+    TGS_CUDA_OK(cudaMemcpy(offsets, doff, (size_t)(n_groups + 1) * 4, cudaMemcpyDeviceToHost));
+    return TGS_OK;
+}
+
+tgs_status tgs_rasterize_lists(tgs_ctx* ctx, const tgs_group_entry* entries, int64_t n_entries, const uint32_t* offsets,
+                               int64_t offsets_count, const tgs_projected* proj, int64_t n, int width, int height,
+                               const tgs_options* opt, float* out_rgb) {
+    if (!ctx || !opt || !offsets || !out_rgb || n < 0 || n_entries < 0 || (n_entries > 0 && !entries) ||
+        (n > 0 && !proj))
+        return set_err(TGS_ERR_VALIDATION, "rasterize: bad arguments");
+    tgs_camera cam{};
+    cam.width = width;
+    cam.height = height;
+    tgs_status st = validate_options(&cam, opt);
+    if (st != TGS_OK) return st;
+    const GroupGeom gg = make_geom(opt->group_size, width, height, 0, (height + opt->group_size * kTile - 1) /
+                                                                           (opt->group_size * kTile));
+    if (gg.groups_x > 512 || gg.band_gy1 > 512 || gg.n_groups_band > 49152)
+        return set_err(TGS_ERR_VALIDATION, "rasterize: more than 512 group rows/columns; use a larger group size");
+    const int ng = gg.n_groups_band;
+    if (offsets_count != (int64_t)ng + 1 || offsets[0] != 0 || (int64_t)offsets[ng] != n_entries)
+        return set_err(TGS_ERR_VALIDATION, "rasterize: offsets must hold group_count + 1 prefix offsets of the entries");
+    cudaSetDevice(ctx->device);
+    const int64_t na = std::max<int64_t>(n, 1);
+    if (ctx->proj_cap < na) {
+        TGS_CUDA_OK(ctx->proj.ensure((size_t)na * 4 * sizeof(float4)));
+        ctx->proj_cap = na;
+    }
+    tgs_projected* dp = nullptr;
+    tgs_group_entry* de = nullptr;
+    uint32_t* doff = nullptr;
+    if ((st = upload(ctx, 0, proj, (size_t)n, &dp)) != TGS_OK) return st;
+    if ((st = upload(ctx, 1, entries, (size_t)n_entries, &de)) != TGS_OK) return st;
+    if ((st = upload(ctx, 2, offsets, (size_t)ng + 1, &doff)) != TGS_OK) return st;
+    TGS_CUDA_OK(ctx->list.ensure((size_t)std::max<int64_t>(n_entries, 1) * 4));
+    const int per = opt->backend == TGS_BACKEND_TENSOR ? raster_units_per_group(gg.g) : 1;
+    TGS_CUDA_OK(ctx->order.ensure((size_t)std::max(1, ng * per) * 4));
+    TGS_CUDA_OK(ctx->image.ensure((size_t)width * height * 3 * sizeof(float)));
+    TGS_CUDA_OK(ctx->stg[3].ensure(4));
+    uint32_t* flags = ctx->stg[3].as<uint32_t>();
+    FrameCounters* fc = ctx->fc.as<FrameCounters>();
+    TGS_CUDA_OK(cudaMemsetAsync(fc, 0, offsetof(FrameCounters, sticky_overflow), ctx->stream));
+    TGS_CUDA_OK(cudaMemsetAsync(flags, 0, 4, ctx->stream));
+    const DevProjected planes = dev_proj(ctx);
+    launch_projected_to_planes(dp, n, opt->alpha_skip, opt->alpha_clamp, gg, planes, ctx->stream);
+    launch_lists_check(de, doff, ng, dp, n, gg, ctx->list.as<uint32_t>(), flags, ctx->stream);
+    uint32_t hflags = 0;
+    TGS_CUDA_OK(cudaMemcpyAsync(&hflags, flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    if (hflags & 1u) return set_err(TGS_ERR_VALIDATION, "rasterize: an entry's gaussian_index is out of range");
+    if (hflags & 4u) return set_err(TGS_ERR_VALIDATION, "rasterize: offsets are not monotone");
+    if (hflags & 2u)
+        return set_err(TGS_ERR_VALIDATION, "rasterize: an entry's mask is not the one build_group_entries gives its "
+                                           "splat in that group");
+    launch_unit_order(doff, nullptr, ng * per, per, ctx->order.as<int>(), fc, ctx->stream);
+    RasterArgs ra;
+    ra.proj = planes;
+    ra.list = ctx->list.as<uint32_t>();
+    ra.offsets = doff;
+    ra.order = ctx->order.as<int>();
+    ra.gg = gg;
+    ra.image = ctx->image.as<float>();
+    ra.image_row0 = 0;
+    ra.alpha_skip = opt->alpha_skip;
+    ra.alpha_clamp = opt->alpha_clamp;
+    ra.t_terminate = opt->t_terminate;
+    ra.fc = fc;
+    ra.tile_trip = nullptr;
+    ra.unit_cost = nullptr;
+    ra.tile_cull = ctx->tile_cull;
+    if (opt->backend == TGS_BACKEND_SCALAR)
+        launch_raster_scalar(ra, ctx->stream);
+    else
+        launch_raster_tensor(ra, ctx->num_sms, ctx->stream);
+    TGS_CUDA_OK(cudaGetLastError());
+    TGS_CUDA_OK(cudaMemcpyAsync(out_rgb, ctx->image.p, (size_t)width * height * 3 * sizeof(float),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+    TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    // the context's frame state no longer describes a pipeline frame
+    ctx->ucost_key = 0;
     return TGS_OK;
 }
 

@@ -15,6 +15,7 @@ struct PreprocessArgs {
     GroupGeom gg;
     FrameCounters* fc;
     float alpha_skip;              // for the tile-cull extents stored in col.w (tight_extents)
+    float alpha_clamp;             // for the raster record (DevProjected::rr)
 };
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t st);
 
@@ -110,5 +111,22 @@ void launch_count_pairs(const RasterArgs& a, cudaStream_t st);
 void launch_reuse_hist(const FrameCounters* fc, const uint2* rect, const GroupGeom& gg, int max_input,
                        unsigned long long* hist, cudaStream_t st);
 void launch_encode_u8(const float* rgb, int64_t n, uint8_t* out, cudaStream_t st);
+
+// ---- stage API on caller-provided data (tgs_stage.cu) -------------------------------------
+void launch_entries_count(const tgs_projected* proj, int64_t n, const GroupGeom& gg, uint32_t* counts,
+                          cudaStream_t st);
+void launch_entries_emit(const tgs_projected* proj, int64_t n, const GroupGeom& gg, const uint32_t* start,
+                         tgs_keyed_entry* out, cudaStream_t st);
+void launch_keyed_split(const tgs_keyed_entry* e, uint32_t n, uint32_t n_groups, uint32_t* keys, uint32_t* gid,
+                        uint32_t* flags, uint32_t* count, cudaStream_t st);
+void launch_gather_u32(const uint32_t* src, const uint32_t* perm, uint32_t n, uint32_t* dst, cudaStream_t st);
+void launch_gather_entries(const tgs_keyed_entry* e, const uint32_t* perm, uint32_t n, tgs_group_entry* out,
+                           uint32_t* gid_sorted, cudaStream_t st);
+void launch_offsets_from_sorted(const uint32_t* gid, uint32_t n, uint32_t n_groups, uint32_t* offsets,
+                                cudaStream_t st);
+void launch_projected_to_planes(const tgs_projected* p, int64_t n, float alpha_skip, float alpha_clamp,
+                                const GroupGeom& gg, DevProjected out, cudaStream_t st);
+void launch_lists_check(const tgs_group_entry* e, const uint32_t* offsets, int n_groups, const tgs_projected* proj,
+                        int64_t n_proj, const GroupGeom& gg, uint32_t* list, uint32_t* flags, cudaStream_t st);
 
 }  // namespace tgs

@@ -239,10 +239,12 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int i, f
         if (keep) {
             a.out.mc[i] = make_float4(pr.mx, pr.my, pr.a, pr.b);
             a.out.co[i] = make_float4(pr.c, po.w, pr.depth, __int_as_float(pr.radius));
-            a.out.col[i] = make_float4(pr.r, pr.g, pr.bl, tight_extents(pr.a, pr.b, pr.c, po.w, a.alpha_skip));
+            const float ext = tight_extents(pr.a, pr.b, pr.c, po.w, a.alpha_skip);
+            a.out.col[i] = make_float4(pr.r, pr.g, pr.bl, ext);
             a.depth_keys[i] = __float_as_uint(pr.depth);
             int tx0, ty0, tx1, ty1, gx0, gy0, gx1, gy1;
             const int ng = group_rect(pr.mx, pr.my, pr.radius, a.gg, tx0, ty0, tx1, ty1, gx0, gy0, gx1, gy1);
+            a.out.rr[i] = raster_record(pr.mx, pr.my, ext, po.w, a.alpha_clamp, tx0, ty0, tx1, ty1);
             // tile rectangle (binning.cpp:32-44) for the group counting sort; empty -> x0 > x1
             a.rect[i] = (tx1 >= tx0 && ty1 >= ty0)
                             ? make_uint2((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16))

@@ -48,7 +48,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
 // Bounded wait: a deadlock (a protocol bug) must become a reported kernel error, never a hung
 // GPU.  After ~4e9 cycles (~2 s) the waiter prints where it is stuck and traps.
 #ifndef TGS_MBAR_SPIN  // waits by lane-0 polling (1), polling with __nanosleep(n) (n > 1), or try_wait (0)
-#define TGS_MBAR_SPIN 1
+#define TGS_MBAR_SPIN -1
 #endif
 #ifndef TGS_MBAR_HINT_NS
 #define TGS_MBAR_HINT_NS 20000
@@ -89,7 +89,22 @@ static __device__ __noinline__ void watchdog_trap(const char* what, int a0, int 
 // reconverges, so no lane reaches a .sync.aligned tcgen05 op / elect.sync / vote while others
 // are still in the loop.  Memory ordering for the other lanes comes from __syncwarp.
 __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, const char* what, int a0, int a1) {
-#if TGS_MBAR_SPIN
+#if TGS_MBAR_SPIN < 0
+    // every lane suspends in try_wait (warp-uniform, no reconvergence step); the loop body is
+    // just the re-test (a suspended warp is woken by barrier activity), the watchdog counts
+    // wake-ups and reads the clock only every 4096 of them
+    if (!mbar_try(bar, parity)) {
+        const long long t0 = clock64();
+        for (;;) {
+            bool ok = false;
+            for (int i = 0; i < 4096 && !ok; ++i) ok = mbar_try(bar, parity);
+            if (ok) break;
+            if (clock64() - t0 > 4000000000ll) watchdog_trap(what, a0, a1);
+        }
+    }
+    __syncwarp();
+    return;
+#elif TGS_MBAR_SPIN
     if ((threadIdx.x & 31) == 0 && !mbar_test(bar, parity)) {
         const long long t0 = clock64();
         for (uint32_t i = 1; !mbar_test(bar, parity); ++i) {

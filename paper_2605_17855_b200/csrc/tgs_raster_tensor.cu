@@ -56,17 +56,26 @@ namespace {
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kNeverRow = -30000.0f;
 constexpr float kInf = __builtin_huge_valf();
-constexpr int kN = 32;  // splats per chunk (MMA N)
+#ifndef TGS_RASTER_N
+#define TGS_RASTER_N 32
+#endif
+constexpr int kN = TGS_RASTER_N;  // splats per chunk (MMA N): 32, or 16 with 4 TMEM stages
 #ifndef TGS_RASTER_SS
 #define TGS_RASTER_SS 4
 #endif
 constexpr int kSS = TGS_RASTER_SS;  // shared-memory chunk ring (slack between member tiles)
-constexpr int kTS = 2;              // TMEM accumulator stages per warpgroup
+#ifndef TGS_RASTER_TS
+#define TGS_RASTER_TS 2
+#endif
+constexpr int kTS = TGS_RASTER_TS;  // TMEM accumulator stages per warpgroup
 constexpr int kJB = 16;             // accumulator columns per epilogue batch
 #ifndef TGS_RASTER_RING
 #define TGS_RASTER_RING 8
 #endif
 constexpr int kRing = TGS_RASTER_RING;  // producer gather ring: kRing - 1 batches of records in flight
+#ifndef TGS_RASTER_MMA_SLEEP
+#define TGS_RASTER_MMA_SLEEP 20  // MMA warp back-off (ns) when no warpgroup is ready
+#endif
 #ifndef TGS_RASTER_PROF
 #define TGS_RASTER_PROF 0
 #endif
@@ -74,16 +83,21 @@ constexpr int kRing = TGS_RASTER_RING;  // producer gather ring: kRing - 1 batch
 // role timing (tools builds only): [0] producer total [1] producer stage waits [2] MMA total
 // [3] epilogue total (sum over warps) [4] epilogue tfull waits [5] active (warp, splat) pairs
 // [6] (warp, splat) pairs tested [7] chunks
-__device__ unsigned long long g_rprof[8];
+__device__ unsigned long long g_rprof[16];
 __device__ unsigned int g_rprof_done;
 #endif
+
+#ifndef TGS_RASTER_NP
+#define TGS_RASTER_NP 1
+#endif
+constexpr int kNP = TGS_RASTER_NP;  // producer warps, each with its own chunk ring; units alternate
 
 template <int SLOTS>
 struct Cfg {
     static constexpr int kMT = 2 * SLOTS;  // M=128 tiles per unit (two per member tile)
     static constexpr int kEpiWarps = 4 * SLOTS;
-    static constexpr int kProd = kEpiWarps, kMma = kEpiWarps + 1;
-    static constexpr int kThreads = (kEpiWarps + 2) * 32;
+    static constexpr int kProd = kEpiWarps, kMma = kEpiWarps + kNP;  // producers kProd .. kProd + kNP - 1
+    static constexpr int kThreads = (kEpiWarps + kNP + 1) * 32;
     static constexpr int kCtasPerSm = SLOTS == 1 ? 3 : 1;
     static constexpr uint32_t kTmemCols = kTS * kMT * kN <= 128 ? 128 : kTS * kMT * kN <= 256 ? 256 : 512;
     static_assert(kTS * kMT * kN * kCtasPerSm <= 512, "TMEM columns per SM");
@@ -92,29 +106,64 @@ template <int SLOTS>
 __host__ __device__ inline int units_per_group(int g) { return (SLOTS == 4 && g == 4) ? 4 : 1; }
 
 struct ChunkHeader {
-    int seq;      // per-CTA unit sequence number, -1 = end of stream
+    int seq;      // per-CTA unit sequence number (kNP * k + producer), -1 = end of the ring's stream
     int unit;     // unit index (order-resolved)
     int n_valid;  // splats in the chunk (0: unit without contributing splats)
     int live;     // member tiles live when the chunk was produced (MMA skips the others)
-    int chunk;    // chunk number (protocol self-check)
+    int chunk;    // chunk number within its ring (protocol self-check)
+    int last;     // last chunk of its unit: consumers move on to the next ring
 };
 
 template <int SLOTS>
 struct Smem {
     alignas(128) uint8_t a[2 * SLOTS][128 * 32];  // pixel monomial rows (K-major, no swizzle)
-    alignas(128) uint8_t b[kSS][kN * 32];         // splat coefficient rows
-    float4 epi[kSS][kN];                          // r, g, b, min(alpha_clamp, opacity)
-    ChunkHeader hdr[kSS];
-    alignas(16) int wdone[16];  // chunks each epilogue warp has completed
+    alignas(128) uint8_t b[kNP][kSS][kN * 32];    // splat coefficient rows, per chunk ring
+    float4 epi[kNP][kSS][kN];                     // r, g, b, min(alpha_clamp, opacity)
+    ChunkHeader hdr[kNP][kSS];
+    alignas(16) int wdone[16];  // chunks each epilogue warp has completed (all rings)
     alignas(16) int dead[16];   // (seq << 1) | 1 once all pixels of the warp terminated in unit seq
-    uint64_t full[kSS];         // producer -> MMA
+    uint64_t full[kNP][kSS];    // producer -> MMA
     uint64_t tfull[SLOTS][kTS]; // MMA -> warpgroup (tcgen05.commit)
-    // smem stage s is free again once every epilogue warp finished the chunk that used it
-    unsigned int done_cnt[kSS];
+    // smem stage s of ring r is free again once every epilogue warp finished the chunk that used it
+    unsigned int done_cnt[kNP][kSS];
     uint32_t tmem_base;
-    // producer gather ring (cp.async): splat records of kRing batches and list indices of 2 kRing
-    float4 rmc[kRing][32], rco[kRing][32], rcol[kRing][32];
-    uint32_t ridx[2 * kRing][32];
+    int prod_done;  // highest unit seq whose chunks are all published (producer hand-over)
+    // producer gather rings (cp.async): splat records of kRing batches and list indices of 2 kRing
+    float4 rmc[kNP][kRing][32], rco[kNP][kRing][32], rcol[kNP][kRing][32];
+    uint4 rrr[kNP][kRing][32];
+    uint32_t ridx[kNP][2 * kRing][32];
+};
+
+// Consumer-side walk over the chunk rings: units alternate between the rings (seq = kNP k + r);
+// after a unit's last chunk, or a ring's end-of-stream marker, move to the next ring still open.
+struct RingCursor {
+    uint32_t g = 0;            // chunks consumed over all rings (TMEM stage / parity)
+    uint32_t cr[kNP] = {};     // chunks consumed per ring
+    uint32_t ended = 0;        // rings whose stream ended
+    int r = 0;                 // current ring, -1 when every ring ended
+    __device__ __forceinline__ uint32_t c() const {
+        uint32_t v = cr[0];
+#pragma unroll
+        for (int i = 1; i < kNP; ++i)
+            if (r == i) v = cr[i];
+        return v;
+    }
+    __device__ __forceinline__ void advance(bool end_marker, bool last) {
+        ++g;
+#pragma unroll
+        for (int i = 0; i < kNP; ++i)
+            if (r == i) ++cr[i];
+        if (end_marker) ended |= 1u << r;
+        if (end_marker || last) {
+            int nr = -1;
+#pragma unroll
+            for (int k = kNP; k >= 1; --k) {  // first open ring after r (cyclic), r itself last
+                const int cand = (r + k) % kNP;
+                if (!((ended >> cand) & 1u)) nr = cand;
+            }
+            r = nr;
+        }
+    }
 };
 
 // Pixel (relative to the unit's top-left) of row l of M-tile m = 2 t + k: member tile t, its
@@ -199,9 +248,9 @@ __device__ __forceinline__ void never_row(uint4& r0, uint4& r1) {
 }
 
 template <int SLOTS>
-__device__ __forceinline__ void write_row(Smem<SLOTS>& sm, int s, int slot, const uint4& r0, const uint4& r1) {
-    *reinterpret_cast<uint4*>(&sm.b[s][core_off(slot, 0)]) = r0;
-    *reinterpret_cast<uint4*>(&sm.b[s][core_off(slot, 1)]) = r1;
+__device__ __forceinline__ void write_row(Smem<SLOTS>& sm, int r, int s, int slot, const uint4& r0, const uint4& r1) {
+    *reinterpret_cast<uint4*>(&sm.b[r][s][core_off(slot, 0)]) = r0;
+    *reinterpret_cast<uint4*>(&sm.b[r][s][core_off(slot, 1)]) = r1;
 }
 
 // Unit geometry: the unit's top-left tile, the group whose list it walks, member-tile liveness.
@@ -271,12 +320,14 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
     if (threadIdx.x < 16) {
         sm.wdone[threadIdx.x] = 0;
         sm.dead[threadIdx.x] = -1;
+        if (threadIdx.x == 0) sm.prod_done = -1;
     }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kSS; ++s) {
-            ptx::mbar_init(&sm.full[s], 1);
-            sm.done_cnt[s] = 0;
-        }
+        for (int r = 0; r < kNP; ++r)
+            for (int s = 0; s < kSS; ++s) {
+                ptx::mbar_init(&sm.full[r][s], 1);
+                sm.done_cnt[r][s] = 0;
+            }
         for (int t = 0; t < SLOTS; ++t)
             for (int s = 0; s < kTS; ++s) ptx::mbar_init(&sm.tfull[t][s], 1);
         ptx::mbar_fence_init();
@@ -288,10 +339,12 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
     ptx::tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
     [[maybe_unused]] unsigned long long pf[4] = {0, 0, 0, 0};
+    [[maybe_unused]] unsigned long long pf_lock = 0;  // epilogue waits while its group held the TMEM stage
     [[maybe_unused]] const long long pf_start = clock64();
 
-    if (warp == kProd) {
-        // ================================ producer ===========================================
+    if (warp >= kProd && warp < kProd + kNP) {
+        // ================================ producers ==========================================
+        const int pr = warp - kProd;  // this producer's chunk ring
         const float skip = a.alpha_skip, clampv = a.alpha_clamp;
         uint32_t c = 0;  // chunks emitted so far
         const uint32_t lt = (1u << lane) - 1u;
@@ -301,9 +354,9 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
             const int s = (int)(cc % kSS);
             if (cc >= (uint32_t)kSS && lane == 0) {
                 const unsigned int need = (unsigned int)kEpiWarps * (cc / kSS);
-                if (ld_volatile_u32(&sm.done_cnt[s]) < need) {
+                if (ld_volatile_u32(&sm.done_cnt[pr][s]) < need) {
                     const long long t0 = clock64();
-                    while (ld_volatile_u32(&sm.done_cnt[s]) < need) {
+                    while (ld_volatile_u32(&sm.done_cnt[pr][s]) < need) {
                         __nanosleep(32);
                         if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producer/done", (int)cc, s);
                     }
@@ -313,20 +366,41 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
             __syncwarp();
             return s;
         };
-        auto publish = [&](int s, int seq, int unit, int n_valid, uint32_t live) {
+        auto publish = [&](int s, int seq, int unit, int n_valid, uint32_t live, int last) {
             if (lane == 0) {
-                sm.hdr[s].seq = seq;
-                sm.hdr[s].unit = unit;
-                sm.hdr[s].n_valid = n_valid;
-                sm.hdr[s].live = (int)live;
-                sm.hdr[s].chunk = (int)c;
+                ChunkHeader& h = sm.hdr[pr][s];
+                h.seq = seq;
+                h.unit = unit;
+                h.n_valid = n_valid;
+                h.live = (int)live;
+                h.chunk = (int)c;
+                h.last = last;
             }
             ptx::fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&sm.full[s]);
+            if (lane == 0) ptx::mbar_arrive(&sm.full[pr][s]);
             __syncwarp();
         };
-        for (int seq = 0;; ++seq) {
+        // units are handed out in sequence: a producer takes the ticket for unit seq only once
+        // unit seq - 1 is fully produced (the epilogue is then at most kSS chunks from needing
+        // it), so a CTA never holds more than one unit ahead of the one being rendered
+        auto wait_prev_produced = [&](int seq) {
+            if (seq > 0 && lane == 0 && ld_volatile_u32((const unsigned int*)&sm.prod_done) + 1u < (unsigned)seq) {
+                const long long t0 = clock64();
+                while (ld_volatile_u32((const unsigned int*)&sm.prod_done) + 1u < (unsigned)seq) {
+                    __nanosleep(64);
+                    if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producer/turn", seq, pr);
+                }
+            }
+            __syncwarp();
+        };
+        auto mark_produced = [&](int seq) {
+            __syncwarp();
+            if (lane == 0) ((volatile int*)&sm.prod_done)[0] = seq;
+        };
+        int seq = pr;
+        for (;; seq += kNP) {
+            wait_prev_produced(seq);
             int t = 0;
             if (lane == 0) t = (int)atomicAdd(&a.fc->group_counter, 1u);
             t = __shfl_sync(0xffffffffu, t, 0);
@@ -347,19 +421,21 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
             // commit group per step, so R - 1 batches of records are in flight.
             auto valid = [&](uint32_t b) { return b < nb && begin + b * 32u + (uint32_t)lane < end; };
             auto issue_idx = [&](uint32_t b) {
-                if (valid(b)) ptx::cp_async4(&sm.ridx[b % (2 * kRing)][lane], &a.list[begin + b * 32u + lane]);
+                if (valid(b)) ptx::cp_async4(&sm.ridx[pr][b % (2 * kRing)][lane], &a.list[begin + b * 32u + lane]);
             };
             auto issue_rec = [&](uint32_t b) {
                 if (valid(b)) {
-                    const uint32_t idx = sm.ridx[b % (2 * kRing)][lane];
+                    const uint32_t idx = sm.ridx[pr][b % (2 * kRing)][lane];
                     const int r = (int)(b % kRing);
-                    ptx::cp_async16(&sm.rmc[r][lane], &a.proj.mc[idx]);
-                    ptx::cp_async16(&sm.rco[r][lane], &a.proj.co[idx]);
-                    ptx::cp_async16(&sm.rcol[r][lane], &a.proj.col[idx]);
+                    ptx::cp_async16(&sm.rmc[pr][r][lane], &a.proj.mc[idx]);
+                    ptx::cp_async16(&sm.rco[pr][r][lane], &a.proj.co[idx]);
+                    ptx::cp_async16(&sm.rcol[pr][r][lane], &a.proj.col[idx]);
+                    ptx::cp_async16(&sm.rrr[pr][r][lane], &a.proj.rr[idx]);
                 }
             };
             struct Rec {
                 float4 mc, co, col;
+                uint4 rr;
                 uint32_t idx;
             };
             auto ld_rec = [&](uint32_t b) -> Rec {
@@ -367,12 +443,14 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                 if (valid(b)) {
                     const int k = (int)(b % kRing);
                     r.idx = 0u;
-                    r.mc = sm.rmc[k][lane];
-                    r.co = sm.rco[k][lane];
-                    r.col = sm.rcol[k][lane];
+                    r.mc = sm.rmc[pr][k][lane];
+                    r.co = sm.rco[pr][k][lane];
+                    r.col = sm.rcol[pr][k][lane];
+                    r.rr = sm.rrr[pr][k][lane];
                 } else {
                     r.idx = 0xffffffffu;
                     r.mc = r.co = r.col = make_float4(0, 0, 0, 0);
+                    r.rr = make_uint4(1u, 1u, 0u, 0u);
                 }
                 return r;
             };
@@ -407,8 +485,21 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                 bt.cover = 0;
                 bt.epi = make_float4(0, 0, 0, 0);
                 if (cur.idx != 0xffffffffu) {
+                    // member tiles the splat's list entry covers (binning.cpp:56-65), narrowed by the
+                    // tile cull to those whose pixel centres meet its alpha_skip box: the raster
+                    // record carries that tight rect (preprocess); without the cull, the 3-sigma rect
                     int x0, y0, x1, y1;
-                    tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1, y1);
+                    float cj, lo2;
+                    if (a.tile_cull) {
+                        x0 = (int)(cur.rr.x & 0xffffu), x1 = (int)(cur.rr.x >> 16);
+                        y0 = (int)(cur.rr.y & 0xffffu), y1 = (int)(cur.rr.y >> 16);
+                        lo2 = __uint_as_float(cur.rr.z);
+                        cj = __uint_as_float(cur.rr.w);
+                    } else {
+                        tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1, y1);
+                        lo2 = lg2_approx(cur.co.y);
+                        cj = fminf(clampv, cur.co.y);
+                    }
                     uint32_t cover = 0;
 #pragma unroll
                     for (int k = 0; k < SLOTS; ++k) {
@@ -416,12 +507,9 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                         if (tx >= x0 && tx <= x1 && ty >= y0 && ty <= y1) cover |= 1u << k;
                     }
                     cover &= live;
-                    const float cj = fminf(clampv, cur.co.y);
-                    if (a.tile_cull && cover != 0u && !(cj < skip))
-                        cover &= tight_cover(cur.mc.x, cur.mc.y, cur.col.w, ug.tx0, ug.ty0, SLOTS);
                     if (cover != 0u && !(cj < skip)) {
-                        bt.keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lg2_approx(cur.co.y), ox,
-                                           oy, cover, bt.r0, bt.r1);
+                        bt.keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lo2, ox, oy, cover, bt.r0,
+                                           bt.r1);
                         bt.cover = cover;
                         bt.epi = make_float4(cur.col.x, cur.col.y, cur.col.z, cj);
                     }
@@ -442,14 +530,14 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                 for (;;) {
                     const int room = kN - fill;
                     if (bt.keep && rank >= placed && rank - placed < room) {
-                        write_row(sm, s, fill + rank - placed, bt.r0, bt.r1);
-                        sm.epi[s][fill + rank - placed] = bt.epi;
+                        write_row(sm, pr, s, fill + rank - placed, bt.r0, bt.r1);
+                        sm.epi[pr][s][fill + rank - placed] = bt.epi;
                     }
                     if (nk - placed < room) {
                         fill += nk - placed;
                         break;
                     }
-                    publish(s, seq, unit, kN, live);
+                    publish(s, seq, unit, kN, live, 0);
                     ++c;
                     emitted = true;
                     s = open_stage(c);
@@ -458,96 +546,107 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                     if (placed == nk) break;
                 }
             };
-            for (uint32_t b = 0; b < 2u * kRing - 1u; ++b) issue_idx(b);
+            // two batches per step (independent builds overlap, then placement in list order);
+            // records of batches 2i + R - 2 and 2i + R - 1 are requested at step i into the slots
+            // the previous step consumed, one commit group per batch: R - 2 batches in flight
+            static_assert(kRing >= 4 && kRing % 2 == 0, "gather ring");
+            for (uint32_t b = 0; b < 2u * kRing - 2u; ++b) issue_idx(b);
             ptx::cp_async_commit();
             ptx::cp_async_wait<0>();
             __syncwarp();
-            for (uint32_t b = 0; b < kRing - 1u; ++b) {
+            for (uint32_t b = 0; b < kRing - 2u; ++b) {
                 issue_rec(b);
                 ptx::cp_async_commit();
             }
-            for (uint32_t bi = 0; bi < nb; ++bi) {
-                ptx::cp_async_wait<kRing - 2>();  // records of batch bi (and indices of bi + R - 1)
+            for (uint32_t bi = 0; bi < nb; bi += 2) {
+                [[maybe_unused]] const long long tc0 = TGS_RASTER_PROF ? clock64() : 0;
+                ptx::cp_async_wait<kRing - 4>();  // records of batches bi, bi + 1
+                if (TGS_RASTER_PROF) {
+                    pf[2] += clock64() - tc0;
+                    pf[3] += 2;
+                }
                 __syncwarp();
-                ++n_batches;
                 if (retire_check()) break;
-                const Rec cur = ld_rec(bi);
-                // refill: slot (bi - 1) % R was consumed by the previous step
+                const bool has_b = bi + 1 < nb;
+                n_batches += has_b ? 2u : 1u;
+                const Rec ca = ld_rec(bi), cb = ld_rec(bi + 1);
+                issue_idx(bi + 2u * kRing - 2u);
+                issue_rec(bi + kRing - 2u);
+                ptx::cp_async_commit();
                 issue_idx(bi + 2u * kRing - 1u);
                 issue_rec(bi + kRing - 1u);
                 ptx::cp_async_commit();
-                Built bt;
-                build(cur, bt);
-                place(bt);
+                Built ba, bb;
+                build(ca, ba);
+                build(cb, bb);
+                place(ba);
+                if (has_b) place(bb);
             }
             ptx::cp_async_wait<0>();  // nothing in flight into the ring when the next unit starts
             __syncwarp();
-            // close the unit: pad and publish the partial chunk (or an empty one so the
-            // epilogue still writes the unit's pixels)
-            if (open && (fill > 0 || !emitted)) {
-                if (lane >= fill) {
-                    uint4 r0, r1;
-                    never_row(r0, r1);
-                    write_row(sm, s, lane, r0, r1);
-                }
-                publish(s, seq, unit, fill, live);
-                ++c;
-            } else if (!open) {
-                s = open_stage(c);
-                publish(s, seq, unit, 0, live);
-                ++c;
+            // close the unit: exactly one chunk flagged `last` — the padded partial chunk, or an
+            // empty one (unit without kept splats, or kept rows ending on a chunk boundary)
+            if (!open) s = open_stage(c);
+            if (lane >= fill && lane < kN) {
+                uint4 r0, r1;
+                never_row(r0, r1);
+                write_row(sm, pr, s, lane, r0, r1);
             }
+            publish(s, seq, unit, fill, live, 1);
+            ++c;
+            mark_produced(seq);
             // schedule feedback: list entries this unit walked (batches) plus rows it staged
             if (a.unit_cost && lane == 0) a.unit_cost[unit] = 32u * n_batches + (uint32_t)kN * (c - unit_c0);
         }
-        {  // end of stream
+        if (TGS_RASTER_PROF) pf[0] = c;
+        {  // end of this ring's stream
             const int se = open_stage(c);
-            publish(se, -1, -1, 0, 0u);
+            publish(se, -1, -1, 0, 0u, 1);
+            mark_produced(seq);  // lets the other producer find the tickets exhausted too
         }
     } else if (warp == kMma) {
         // ================================ MMA issuer ==========================================
         constexpr uint32_t idesc = ptx::idesc_f16(128, kN);
         const uint32_t a_base = ptx::smem_u32(&sm.a[0][0]);
-        uint32_t cw[SLOTS];  // next chunk of each warpgroup
-        bool ended[SLOTS];
-#pragma unroll
-        for (int t = 0; t < SLOTS; ++t) {
-            cw[t] = 0;
-            ended[t] = false;
-        }
-        int n_ended = 0;
+        RingCursor cur[SLOTS];  // per warpgroup: its walk over the chunk rings
+        int n_done = 0;
         long long idle0 = clock64();
-        while (n_ended < SLOTS) {
+        while (n_done < SLOTS) {
             bool did = false;
 #pragma unroll
             for (int t = 0; t < SLOTS; ++t) {
-                if (ended[t]) continue;
-                const uint32_t c = cw[t];
-                const int s = (int)(c % kSS), ts = (int)(c % kTS);
+                RingCursor& rc = cur[t];
+                if (rc.r < 0) continue;
+                const int r = rc.r;
+                const uint32_t c = rc.c(), g = rc.g;
+                const int s = (int)(c % kSS), ts = (int)(g % kTS);
                 int ready = 0;
                 if (lane == 0) {
-                    // chunk published, and warpgroup t finished chunk c - kTS (its TMEM stage)
-                    ready = ptx::mbar_test(&sm.full[s], (c / kSS) & 1);
-                    if (ready && c >= (uint32_t)kTS) {
+                    // chunk published, and warpgroup t finished its chunk g - kTS (the TMEM stage)
+                    ready = ptx::mbar_test(&sm.full[r][s], (c / kSS) & 1);
+                    if (ready && g >= (uint32_t)kTS) {
                         const int4 d = ld_volatile_v4(&sm.wdone[4 * t]);
-                        ready = min(min(d.x, d.y), min(d.z, d.w)) >= (int)(c - kTS + 1);
+                        ready = min(min(d.x, d.y), min(d.z, d.w)) >= (int)(g - kTS + 1);
                     }
                 }
                 ready = __shfl_sync(0xffffffffu, ready, 0);
                 if (!ready) continue;
                 __syncwarp();
                 ptx::tc_fence_after();
-                const int hseq = __shfl_sync(0xffffffffu, sm.hdr[s].seq, 0);
-                const int hnv = __shfl_sync(0xffffffffu, sm.hdr[s].n_valid, 0);
-                const uint32_t hlive = __shfl_sync(0xffffffffu, (uint32_t)sm.hdr[s].live, 0);
-                const int hch = __shfl_sync(0xffffffffu, sm.hdr[s].chunk, 0);
+                const ChunkHeader& hs = sm.hdr[r][s];
+                const int hseq = __shfl_sync(0xffffffffu, hs.seq, 0);
+                const int hnv = __shfl_sync(0xffffffffu, hs.n_valid, 0);
+                const uint32_t hlive = __shfl_sync(0xffffffffu, (uint32_t)hs.live, 0);
+                const int hch = __shfl_sync(0xffffffffu, hs.chunk, 0);
+                const int hlast = __shfl_sync(0xffffffffu, hs.last, 0);
                 if (hch != (int)c) {
                     if (lane == 0)
-                        printf("libtgs MMA: warpgroup %d expected chunk %d found %d (seq %d)\n", t, (int)c, hch, hseq);
+                        printf("libtgs MMA: warpgroup %d ring %d expected chunk %d found %d (seq %d)\n", t, r, (int)c, hch,
+                               hseq);
                     __trap();
                 }
                 if (hseq >= 0 && hnv > 0 && ((hlive >> t) & 1u)) {
-                    const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[s][0]), 128, 256);
+                    const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[r][s][0]), 128, 256);
                     const uint32_t dcol = tmem + (uint32_t)(((ts * SLOTS + t) * 2) * kN);
 #pragma unroll
                     for (int k = 0; k < 2; ++k)
@@ -559,18 +658,15 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                     ptx::mbar_arrive(&sm.tfull[t][ts]);
                 }
                 __syncwarp();
-                cw[t] = c + 1;
-                if (hseq < 0) {
-                    ended[t] = true;
-                    ++n_ended;
-                }
+                rc.advance(hseq < 0, hlast != 0);
+                if (rc.r < 0) ++n_done;
                 did = true;
             }
             if (did) {
                 idle0 = clock64();
             } else {
-                __nanosleep(20);
-                if (clock64() - idle0 > 4000000000ll) ptx::watchdog_trap("mma/idle", (int)cw[0], n_ended);
+                if (TGS_RASTER_MMA_SLEEP) __nanosleep(TGS_RASTER_MMA_SLEEP);
+                if (clock64() - idle0 > 4000000000ll) ptx::watchdog_trap("mma/idle", (int)cur[0].g, n_done);
             }
         }
     } else {
@@ -585,7 +681,7 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
         int px[2], py[2];
         const float L = log2f(a.alpha_skip);
         const float tterm = a.t_terminate;
-        int cur = -1;
+        int cur = -1;            // unit being rendered (seq), -1 none
         uint32_t alive = 0;      // warp-uniform: slots with a non-terminated pixel
         bool reported = false;   // retirement of this warp published for `cur`
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
@@ -596,32 +692,36 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
         for (int k = 0; k < 2; ++k)
 #pragma unroll
             for (int j = 0; j < kJB; ++j) d[k][j] = 0u;
-        for (uint32_t c = 0;; ++c) {
-            const int s = (int)(c % kSS), ts = (int)(c % kTS);
-            // this warpgroup consumed the phase of chunk c - kTS itself, so the parity is unambiguous
+        RingCursor rcur;
+        while (rcur.r >= 0) {
+            const int r = rcur.r;
+            const uint32_t c = rcur.c(), g = rcur.g;
+            const int s = (int)(c % kSS), ts = (int)(g % kTS);
+            // this warpgroup consumed the phase of its chunk g - kTS itself, so the parity is unambiguous
             [[maybe_unused]] const long long tw0 = clock64();
-            ptx::mbar_wait_wd(&sm.tfull[t][ts], (c / kTS) & 1, "epilogue/tfull", (int)c, warp);
-            if (TGS_RASTER_PROF) pf[1] += clock64() - tw0;
+            // PROF: was the chunk still unpublished when this warp started waiting (producer-bound)?
+            [[maybe_unused]] const bool starved = TGS_RASTER_PROF && !ptx::mbar_test(&sm.full[r][s], (c / kSS) & 1);
+            [[maybe_unused]] bool lockstep = false;  // PROF: a warp of this group still holds the TMEM stage
+            if (TGS_RASTER_PROF && !starved && g >= (uint32_t)kTS) {
+                const int4 dd = ld_volatile_v4(&sm.wdone[4 * t]);
+                lockstep = min(min(dd.x, dd.y), min(dd.z, dd.w)) < (int)(g - kTS + 1);
+            }
+            ptx::mbar_wait_wd(&sm.tfull[t][ts], (g / kTS) & 1, "epilogue/tfull", (int)g, warp);
+            if (TGS_RASTER_PROF) {
+                const long long dw = clock64() - tw0;
+                pf[1] += dw;
+                if (starved) pf[0] += dw;
+                if (lockstep) pf_lock += dw;
+            }
             ptx::tc_fence_after();
-            const ChunkHeader h = sm.hdr[s];
+            const ChunkHeader h = sm.hdr[r][s];
             if (h.chunk != (int)c) {
                 if (lane == 0)
-                    printf("libtgs epilogue warp %d: expected chunk %d found %d (seq %d)\n", warp, (int)c, h.chunk,
-                           h.seq);
+                    printf("libtgs epilogue warp %d ring %d: expected chunk %d found %d (seq %d)\n", warp, r, (int)c,
+                           h.chunk, h.seq);
                 __trap();
             }
-            if (h.seq != cur) {
-                if (cur >= 0) {
-#pragma unroll
-                    for (int k = 0; k < 2; ++k)
-                        if (px[k] >= 0) {
-                            float* o = a.image + ((size_t)(py[k] - a.image_row0) * gg.width + px[k]) * 3;
-                            o[0] = fminf(fmaxf(cr[k], 0.0f), 1.0f);
-                            o[1] = fminf(fmaxf(cg[k], 0.0f), 1.0f);
-                            o[2] = fminf(fmaxf(cb[k], 0.0f), 1.0f);
-                        }
-                }
-                if (h.seq < 0) break;
+            if (h.seq >= 0 && h.seq != cur) {  // first chunk of a unit
                 cur = h.seq;
                 reported = false;
                 const UnitGeom ug = unit_geom<SLOTS>(gg, h.unit);
@@ -640,7 +740,7 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                 for (int k = 0; k < 2; ++k)
                     if (__any_sync(0xffffffffu, thr[k] != kInf)) alive |= 1u << k;
             }
-            const int nv = h.n_valid;
+            const int nv = h.seq >= 0 ? h.n_valid : 0;
             const uint32_t col0 = (uint32_t)(((ts * SLOTS + t) * 2) * kN);
             if (nv > 0 && alive != 0u) {
 #pragma unroll 1
@@ -673,7 +773,7 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
 #pragma unroll
                     for (int jj = 0; jj < kJB; ++jj)
                         if (M & (1u << jj)) {
-                            const float4 ej = sm.epi[s][j0 + jj];
+                            const float4 ej = sm.epi[r][s][j0 + jj];
 #pragma unroll
                             for (int k = 0; k < 2; ++k) {
                                 const float dv = __uint_as_float(d[k][jj]);
@@ -694,25 +794,39 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                 for (int k = 0; k < 2; ++k)
                     if (!__any_sync(0xffffffffu, thr[k] != kInf)) alive &= ~(1u << k);
             }
+            if (h.seq >= 0 && h.last) {  // unit complete: store its pixels (clamped, finalize)
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+                    if (px[k] >= 0) {
+                        float* o = a.image + ((size_t)(py[k] - a.image_row0) * gg.width + px[k]) * 3;
+                        o[0] = fminf(fmaxf(cr[k], 0.0f), 1.0f);
+                        o[1] = fminf(fmaxf(cg[k], 0.0f), 1.0f);
+                        o[2] = fminf(fmaxf(cb[k], 0.0f), 1.0f);
+                    }
+            }
             // TMEM stage and smem stage consumed (all tcgen05.ld of this warp completed above)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if (alive == 0u && !reported) ((volatile int*)sm.dead)[warp] = (cur << 1) | 1;
+                if (h.seq >= 0 && alive == 0u && !reported) ((volatile int*)sm.dead)[warp] = (cur << 1) | 1;
                 __threadfence_block();
-                ((volatile int*)sm.wdone)[warp] = (int)c + 1;
-                atomicAdd(&sm.done_cnt[s], 1u);
+                ((volatile int*)sm.wdone)[warp] = (int)g + 1;
+                atomicAdd(&sm.done_cnt[r][s], 1u);
             }
-            reported = alive == 0u;
+            reported = reported || (h.seq >= 0 && alive == 0u);
+            rcur.advance(h.seq < 0, h.last != 0);
         }
     }
 
 #if TGS_RASTER_PROF
     if (lane == 0) {
         const long long tot = clock64() - pf_start;
-        if (warp == kProd) {
+        if (warp >= kProd && warp < kProd + kNP) {
             atomicAdd(&g_rprof[0], (unsigned long long)tot);
             atomicAdd(&g_rprof[1], pf[1]);
+            atomicAdd(&g_rprof[8], pf[2]);   // cp.async data waits
+            atomicAdd(&g_rprof[9], pf[3]);   // batches
+            atomicAdd(&g_rprof[10], pf[0]);  // chunks
         } else if (warp == kMma) {
             atomicAdd(&g_rprof[2], (unsigned long long)tot);
         } else {
@@ -720,6 +834,8 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
             atomicAdd(&g_rprof[4], pf[1]);
             atomicAdd(&g_rprof[5], pf[2]);
             atomicAdd(&g_rprof[6], pf[3]);
+            atomicAdd(&g_rprof[7], pf[0]);
+            atomicAdd(&g_rprof[11], pf_lock);
         }
     }
 #endif
@@ -731,14 +847,17 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
     if (threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(&g_rprof_done, 1u) == gridDim.x - 1) {
-            unsigned long long v[8];
-            for (int i = 0; i < 8; ++i) v[i] = atomicExch(&g_rprof[i], 0ull);
+            unsigned long long v[16];
+            for (int i = 0; i < 16; ++i) v[i] = atomicExch(&g_rprof[i], 0ull);
+            printf("RPROF2 per CTA: producer gather waits %.0f batches %.0f chunks %.0f | epi/warp waits on its own "
+                   "group's TMEM stage %.0f\n", v[8] / (double)gridDim.x, v[9] / (double)gridDim.x,
+                   v[10] / (double)gridDim.x, v[11] / (double)gridDim.x / kEpiWarps);
             g_rprof_done = 0;
             const double n = (double)gridDim.x;
             printf("RPROF ctas %d | producer total %.0f wait %.0f | mma total %.0f | epi/warp total %.0f "
-                   "wtfull %.0f | active %.3f of %.0f (warp, splat) per warp\n",
+                   "wtfull %.0f (producer-starved %.0f) | active %.3f of %.0f (warp, splat) per warp\n",
                    gridDim.x, v[0] / n, v[1] / n, v[2] / n, v[3] / n / kEpiWarps, v[4] / n / kEpiWarps,
-                   (double)v[5] / (double)(v[6] ? v[6] : 1), v[6] / n / kEpiWarps);
+                   v[7] / n / kEpiWarps, (double)v[5] / (double)(v[6] ? v[6] : 1), v[6] / n / kEpiWarps);
         }
     }
 #endif

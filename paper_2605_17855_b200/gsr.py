@@ -432,21 +432,158 @@ def render(scene, cam: Camera, opt: RenderOptions = None, device: int = 0) -> Re
 
 def project_scene(scene, cam: Camera, workers: int = 1, stats: Optional[ProjectionStats] = None,
                   device: int = 0) -> np.ndarray:
-    """project_scene (projection.hpp:48-50): ProjectedGaussian records in input order."""
+    """project_scene (projection.hpp:48-50) on the GPU (tgs_project_scene): ProjectedGaussian
+    records (PROJ_DTYPE) in input order.  ValidationError for non-positive scales
+    (projection.cpp:37); workers is validated and ignored, like every launch-config knob here."""
     if workers < 1:
         raise ValidationError("project_scene: workers must be >= 1")
+    sc = as_scene(scene)
     ctx = default_context(device)
-    ds = ctx.upload(scene)
-    res = ctx.render(ds, cam, RenderOptions(Backend.tensor, group_size=2))
+    rec = sc.records if len(sc) else np.zeros((1, 14), np.float32)
+    n = C.c_int64()
+    st = _lib.tgs_stats()
+    _check(ctx.lib.tgs_project_scene(ctx.h, rec.ctypes.data_as(_lib.F32P), len(sc), sc.sh_degree,
+                                     C.byref(cam.to_c()), None, 0, C.byref(n), C.byref(st)))
+    out = np.zeros(max(n.value, 1), PROJ_DTYPE)
+    _check(ctx.lib.tgs_read_projected(ctx.h, out.ctypes.data, n.value, C.byref(n)))
     if stats is not None:
-        stats.input, stats.culled, stats.dropped_degenerate = (res.projection.input, res.projection.culled,
-                                                               res.projection.dropped_degenerate)
-    return ctx.read_projected()
+        stats.input, stats.culled, stats.dropped_degenerate = int(st.input), int(st.culled), \
+            int(st.dropped_degenerate)
+    return out[:n.value]
+
+
+@dataclass
+class GroupConfig:
+    """GroupConfig (binning.hpp:15-31): group_h x group_w blocks of 16x16 tiles."""
+    group_h: int = 2
+    group_w: int = 2
+    image_width: int = 0
+    image_height: int = 0
+
+    @staticmethod
+    def square(g: int, image_width: int, image_height: int) -> "GroupConfig":
+        cfg = GroupConfig(g, g, image_width, image_height)
+        cfg.validate()
+        return cfg
+
+    def tiles_x(self) -> int:
+        return (self.image_width + kTileSize - 1) // kTileSize
+
+    def tiles_y(self) -> int:
+        return (self.image_height + kTileSize - 1) // kTileSize
+
+    def groups_x(self) -> int:
+        return (self.tiles_x() + self.group_w - 1) // self.group_w
+
+    def groups_y(self) -> int:
+        return (self.tiles_y() + self.group_h - 1) // self.group_h
+
+    def group_count(self) -> int:
+        return self.groups_x() * self.groups_y()
+
+    def validate(self) -> None:  # binning.cpp:22-30
+        if self.image_width <= 0 or self.image_height <= 0:
+            raise ValidationError("GroupConfig: image dimensions must be positive")
+        if not (self.group_h == self.group_w and self.group_h in (1, 2, 4)):
+            raise ValidationError("GroupConfig: supported group sizes are 1x1, 2x2, 4x4")
+
+
+KEYED_DTYPE = np.dtype([("group_id", "<u4"), ("entry", ENTRY_DTYPE)])
+
+
+@dataclass
+class SortedGroupLists:
+    """SortedGroupLists (binning.hpp:53-59): (group, depth)-sorted entries + group offsets."""
+    entries: np.ndarray  # ENTRY_DTYPE
+    offsets: np.ndarray  # uint32, group_count + 1
+
+    def group_begin(self, g: int) -> int:
+        return int(self.offsets[g])
+
+    def group_end(self, g: int) -> int:
+        return int(self.offsets[g + 1])
+
+
+@dataclass
+class TensorRasterOptions:
+    """TensorRasterOptions (raster_tensor.hpp:45-50)."""
+    constants: RasterConstants = field(default_factory=RasterConstants)
+    mode: PrecisionMode = PrecisionMode.fp32
+    chunk_len: int = 16
+    workers: int = 1
+
+
+def _proj_array(projected) -> np.ndarray:
+    p = np.ascontiguousarray(projected, dtype=PROJ_DTYPE)
+    return p if len(p) else np.zeros(1, PROJ_DTYPE)
+
+
+def build_group_entries(projected, cfg: GroupConfig, device: int = 0) -> np.ndarray:
+    """build_group_entries (binning.hpp:68-69) on the GPU: KEYED_DTYPE entries in splat order,
+    then group id (gy outer, gx inner)."""
+    cfg.validate()
+    n = len(projected)
+    p = _proj_array(projected)
+    ctx = default_context(device)
+    m = C.c_int64()
+    _check(ctx.lib.tgs_build_group_entries(ctx.h, p.ctypes.data, n, cfg.image_width, cfg.image_height,
+                                           cfg.group_h, None, 0, C.byref(m)))
+    out = np.zeros(max(m.value, 1), KEYED_DTYPE)
+    if m.value:
+        _check(ctx.lib.tgs_build_group_entries(ctx.h, p.ctypes.data, n, cfg.image_width, cfg.image_height,
+                                               cfg.group_h, out.ctypes.data, m.value, C.byref(m)))
+    return out[:m.value]
+
+
+def sort_entries(entries, cfg: GroupConfig, device: int = 0) -> SortedGroupLists:
+    """sort_entries (binning.hpp:72-73) on the GPU: stable (group_id << 32 | depth bits) order;
+    ValidationError for a non-finite or negative depth (binning.cpp:78-83)."""
+    cfg.validate()
+    e = np.ascontiguousarray(entries, dtype=KEYED_DTYPE)
+    n = len(e)
+    ctx = default_context(device)
+    out = np.zeros(max(n, 1), ENTRY_DTYPE)
+    off = np.zeros(cfg.group_count() + 1, np.uint32)
+    ebuf = e if n else np.zeros(1, KEYED_DTYPE)
+    _check(ctx.lib.tgs_sort_entries(ctx.h, ebuf.ctypes.data, n, cfg.image_width, cfg.image_height, cfg.group_h,
+                                    out.ctypes.data, off.ctypes.data, len(off)))
+    return SortedGroupLists(out[:n], off)
+
+
+def _rasterize(lists: SortedGroupLists, projected, cfg: GroupConfig, backend: Backend, constants: RasterConstants,
+               mode: PrecisionMode, workers: int, chunk_len: int, device: int) -> ImageBuffer:
+    cfg.validate()
+    opt = RenderOptions(backend, mode, cfg.group_h, workers, chunk_len, constants)
+    ent = np.ascontiguousarray(lists.entries, dtype=ENTRY_DTYPE)
+    off = np.ascontiguousarray(lists.offsets, dtype=np.uint32)
+    p = _proj_array(projected)
+    img = np.empty((cfg.image_height, cfg.image_width, 3), np.float32)
+    ebuf = ent if len(ent) else np.zeros(1, ENTRY_DTYPE)
+    ctx = default_context(device)
+    _check(ctx.lib.tgs_rasterize_lists(ctx.h, ebuf.ctypes.data, len(ent), off.ctypes.data, len(off), p.ctypes.data,
+                                       len(projected), cfg.image_width, cfg.image_height, C.byref(opt.to_c()),
+                                       img.ctypes.data_as(_lib.F32P)))
+    return ImageBuffer(cfg.image_width, cfg.image_height, img)
+
+
+def rasterize_tiles_scalar(lists: SortedGroupLists, projected, cfg: GroupConfig, k: RasterConstants = None,
+                           mode: PrecisionMode = PrecisionMode.fp32, workers: int = 1, device: int = 0) -> ImageBuffer:
+    """rasterize_tiles_scalar (raster_scalar.hpp:59-62): the CUDA-core baseline kernel on caller
+    lists (1x1 groups required, raster_scalar.cpp:56-57)."""
+    return _rasterize(lists, projected, cfg, Backend.scalar, k or RasterConstants(), mode, workers, 16, device)
+
+
+def rasterize_groups_tensor(lists: SortedGroupLists, projected, cfg: GroupConfig,
+                            opt: TensorRasterOptions = None, device: int = 0) -> ImageBuffer:
+    """rasterize_groups_tensor (raster_tensor.hpp:62-65): the tcgen05 grouped kernel on caller lists."""
+    opt = opt or TensorRasterOptions()
+    return _rasterize(lists, projected, cfg, Backend.tensor, opt.constants, opt.mode, opt.workers, opt.chunk_len,
+                      device)
 
 
 def sorted_group_lists(scene, cam: Camera, group_size: int, device: int = 0):
-    """build_group_entries + sort_entries (binning.hpp:68-73) as the GPU produces them:
-    (entries[GroupEntry], offsets[group_count + 1], projected)."""
+    """The render path's own (fused) bin + sort of a frame, read back: (entries[GroupEntry],
+    offsets[group_count + 1], projected) — equal to sort_entries(build_group_entries(...))."""
     ctx = default_context(device)
     ds = ctx.upload(scene)
     opt = RenderOptions(Backend.scalar if group_size == 1 else Backend.tensor, group_size=group_size)

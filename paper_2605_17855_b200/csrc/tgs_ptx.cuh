@@ -88,8 +88,30 @@ static __device__ __noinline__ void watchdog_trap(const char* what, int a0, int 
 // Warp-wide bounded wait: lane 0 polls (hardware-suspending try_wait), then the warp
 // reconverges, so no lane reaches a .sync.aligned tcgen05 op / elect.sync / vote while others
 // are still in the loop.  Memory ordering for the other lanes comes from __syncwarp.
+#ifndef TGS_WAIT_NS0
+#define TGS_WAIT_NS0 32   // first back-off sleep of a waiting warp (ns), doubled up to TGS_WAIT_CAP
+#endif
+#ifndef TGS_WAIT_CAP
+#define TGS_WAIT_CAP 256
+#endif
 __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, const char* what, int a0, int a1) {
-#if TGS_MBAR_SPIN < 0
+#if TGS_MBAR_SPIN == -2
+    // test + __nanosleep with exponential back-off: a waiting warp is descheduled and costs no
+    // issue slots (try_wait's suspend is woken by any barrier traffic in the CTA and re-polls
+    // every few tens of cycles, which starved the working warps)
+    if (!mbar_test(bar, parity)) {
+        const long long t0 = clock64();
+        uint32_t ns = TGS_WAIT_NS0;
+        for (uint32_t i = 1;; ++i) {
+            __nanosleep(ns);
+            if (mbar_test(bar, parity)) break;
+            ns = ns < TGS_WAIT_CAP ? 2 * ns : ns;
+            if ((i & 1023u) == 0u && clock64() - t0 > 4000000000ll) watchdog_trap(what, a0, a1);
+        }
+    }
+    __syncwarp();
+    return;
+#elif TGS_MBAR_SPIN < 0
     // every lane suspends in try_wait (warp-uniform, no reconvergence step); the loop body is
     // just the re-test (a suspended warp is woken by barrier activity), the watchdog counts
     // wake-ups and reads the clock only every 4096 of them

@@ -176,6 +176,63 @@ def run_reference(args):
     return 0
 
 
+def run_bands(args, rank, world, local, coll_dev):
+    """BASELINE config 4: one 3840x2160 frame of the 6M-splat scene (seed 4), tensor G=2, split into
+    `world` screen bands of group rows balanced by per-row entry counts (tgs_group_row_entries);
+    rank r renders band r (tgs_render_band: full preprocess, binning/sort/raster of its rows only).
+    A step = one frame; value = frames/s with the frame time = max over ranks (strong scaling: the
+    total work is one frame whatever N is)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_17855_b200 import gsr, multigpu
+    W4, H4, N4, SEED4 = 3840, 2160, 6_000_000, 4
+    ctx = gsr.Context(local)
+    scene = gsr.gen_synthetic_scene(SEED4, N4, 1.0, (0.01, 0.05))
+    ds = ctx.upload(scene)
+    cam = gsr.make_camera(W4, H4)
+    opt = gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 2)
+    rows = ctx.group_row_entries(ds, cam, opt)
+    bands = multigpu.band_split(rows.astype(np.float64), world)
+    g0, g1 = bands[rank]
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    for _ in range(max(args.warmup, 3)):
+        ctx.render_band(ds, cam, opt, g0, g1, copy=False)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stage = []
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):  # the band image stays on its GPU (a gather is not timed)
+            _, st = ctx.render_band(ds, cam, opt, g0, g1, copy=False)
+            stage.append(st.ms_total)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = multigpu.max_over_ranks(ms_local, device=coll_dev)
+    full_ms = None
+    if world == 1:
+        full_ms = statistics.median(ctx.render(ds, cam, opt).stage_ms["total"] for _ in range(3))
+    line = {
+        "metric": "band-split frame time @4K, 6M Gaussians (C4)", "value": 1000.0 / ms, "unit": "frames/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 (fp16 hi/lo tensor-core contraction)",
+        "data": "synthetic (reference generator gen_synthetic_scene seed 4, scales 0.01-0.05)",
+        "config": {"workload": "C4: 6M splats, 3840x2160, identity camera, tensor G=2, screen bands of group rows",
+                   "global_batch": 1, "seq_len": 0, "parallelism": f"screen-bands x{world}",
+                   "bands": bands, "row_entries_total": int(rows.sum())},
+        "band_device_ms_median": statistics.median(stage), "full_frame_ms": full_ms,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -184,6 +241,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e/baseline extras (profiling runs)")
+    ap.add_argument("--mode", default="cameras", choices=["cameras", "bands"],
+                    help="cameras: the C3/C5 camera-batch line (default); bands: C4 single 4K frame split "
+                         "into screen bands across the ranks")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -192,9 +252,20 @@ def main():
     rank, world, local = dist_env()
     import torch
     import torch.distributed as dist
+    # TGS_BENCH_BACKEND=gloo: functional N>1 runs with several ranks on one GPU (NCCL needs one GPU
+    # per rank); the collectives are measurement-only either way
+    backend = os.environ.get("TGS_BENCH_BACKEND", "nccl")
+    if backend != "nccl" and torch.cuda.device_count() < world:
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    coll_dev = torch.device("cuda", local) if backend == "nccl" else None
+    if args.mode == "bands":
+        return run_bands(args, rank, world, local, coll_dev)
 
     from paper_2605_17855_b200 import gsr, _lib
     ctx = gsr.Context(local)
@@ -247,7 +318,7 @@ def main():
             c.sync()
         torch.cuda.synchronize()
     ms_local = max(ev0[0].elapsed_time(e) for e in ev1)
-    ms = multigpu.max_over_ranks(ms_local, device=torch.device("cuda", local))
+    ms = multigpu.max_over_ranks(ms_local, device=coll_dev)
     if world > 1:
         dist.barrier()
     frames = args.steps * world
@@ -363,7 +434,7 @@ def main():
                                         C.byref(mine[args.warmup + i % args.steps].to_c()), C.byref(oc),
                                         C.cast(out.data_ptr(), _lib.F32P), C.byref(st))
             assert rc == 0, _lib.last_error()
-        dt = multigpu.max_over_ranks(time.perf_counter() - t0, device=torch.device("cuda", local))
+        dt = multigpu.max_over_ranks(time.perf_counter() - t0, device=coll_dev)
         e2e = {"value": n_e2e * world / dt, "unit": "frames/s",
                "h2d_bytes_per_step": int(scene.records.nbytes + 88),
                "d2h_bytes_per_step": int(W * H * 3 * 4),

@@ -156,6 +156,13 @@ tgs_status tgs_render_band(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camer
                            const tgs_options* opt, int group_row0, int group_row1, float* out_rgb,
                            tgs_stats* stats);
 
+/* Screen-band work estimate: entries per group row of the frame (rows = ceil(H / (16 G))), i.e.
+ * the per-row totals of build_group_entries (binning.cpp:46-74), from one preprocess pass and a
+ * row histogram (no lists are built).  Every rank of a band-split frame computes the same counts
+ * and cuts its band with them (paper_2605_17855_b200/multigpu.py band_split). */
+tgs_status tgs_group_row_entries(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cam,
+                                 const tgs_options* opt, uint64_t* counts, int64_t cap, int64_t* n_rows);
+
 /* Camera batch (BASELINE config 5; reference analogue: one gsr::render call per camera,
  * render.hpp:30-31 / tools/gsrender.cpp:112-152): n frames, out_rgb = n * width * height * 3 floats
  * (all cameras share W,H; NULL: no image copies).  Frames are pipelined over up to 3 internal lanes

@@ -66,6 +66,8 @@ SIGNATURES = {
     "tgs_gen_synthetic_scene": (c_status, [C.c_uint64, C.c_int, C.c_float, C.c_float, C.c_float,
                                            C.c_uint64, F32P]),
     "tgs_encode_u8": (c_status, [P, P, C.c_int64, P]),
+    "tgs_group_row_entries": (c_status, [P, P, C.POINTER(tgs_camera), C.POINTER(tgs_options), P, C.c_int64,
+                                         C.POINTER(C.c_int64)]),
     "tgs_project_scene": (c_status, [P, F32P, C.c_int64, C.c_int, C.POINTER(tgs_camera), P, C.c_int64,
                                      C.POINTER(C.c_int64), C.POINTER(tgs_stats)]),
     "tgs_build_group_entries": (c_status, [P, P, C.c_int64, C.c_int, C.c_int, C.c_int, P, C.c_int64,

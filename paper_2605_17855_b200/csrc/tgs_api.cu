@@ -610,6 +610,46 @@ tgs_status tgs_render_band(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camer
     return out_rgb ? copy_image_to_host(ctx, out_rgb) : TGS_OK;
 }
 
+tgs_status tgs_group_row_entries(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cam, const tgs_options* opt,
+                                 uint64_t* counts, int64_t cap, int64_t* n_rows) {
+    if (!ctx || !n_rows) return set_err(TGS_ERR_VALIDATION, "group_row_entries: null argument");
+    tgs_status st = validate_options(cam, opt);
+    if (st != TGS_OK) return st;
+    if (!scene || (scene->ctx != ctx && scene->ctx != ctx->parent))
+        return set_err(TGS_ERR_VALIDATION, "group_row_entries: scene belongs to another context");
+    cudaSetDevice(ctx->device);
+    const GroupGeom full = make_geom(opt->group_size, cam->width, cam->height, 0, 0);
+    const GroupGeom gg = make_geom(opt->group_size, cam->width, cam->height, 0, full.groups_y);
+    *n_rows = gg.groups_y;
+    if (!counts || cap < gg.groups_y) return TGS_OK;
+    const int64_t na = std::max<int64_t>(scene->n, 1);
+    if (ctx->proj_cap < na) {
+        TGS_CUDA_OK(ctx->proj.ensure((size_t)na * 4 * sizeof(float4)));
+        ctx->proj_cap = na;
+    }
+    TGS_CUDA_OK(ctx->pre_keys[0].ensure((size_t)na * 4));
+    TGS_CUDA_OK(ctx->rect.ensure((size_t)na * sizeof(uint2)));
+    TGS_CUDA_OK(ctx->stg[6].ensure((size_t)gg.groups_y * sizeof(unsigned long long)));
+    FrameCounters* fc = ctx->fc.as<FrameCounters>();
+    TGS_CUDA_OK(cudaMemsetAsync(fc, 0, offsetof(FrameCounters, sticky_overflow), ctx->stream));
+    PreprocessArgs pa;
+    pa.scene = scene->dev();
+    pa.cam = make_dev_camera(cam);
+    pa.out = dev_proj(ctx);
+    pa.depth_keys = ctx->pre_keys[0].as<uint32_t>();
+    pa.rect = ctx->rect.as<uint2>();
+    pa.gg = gg;
+    pa.fc = fc;
+    pa.alpha_skip = opt->alpha_skip;
+    pa.alpha_clamp = opt->alpha_clamp;
+    launch_preprocess(pa, ctx->stream);
+    launch_row_entries(ctx->rect.as<uint2>(), &fc->n_input, gg, ctx->stg[6].as<unsigned long long>(), ctx->stream);
+    TGS_CUDA_OK(cudaGetLastError());
+    TGS_CUDA_OK(cudaMemcpyAsync(counts, ctx->stg[6].p, (size_t)gg.groups_y * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    return TGS_OK;
+}
+
 tgs_status tgs_render_batch(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cams, int n,
                             const tgs_options* opt, float* out_rgb, tgs_stats* stats) {
     if (!ctx || !cams || n < 0) return set_err(TGS_ERR_VALIDATION, "render_batch: bad arguments");

@@ -126,6 +126,9 @@ void launch_offsets_from_sorted(const uint32_t* gid, uint32_t n, uint32_t n_grou
                                 cudaStream_t st);
 void launch_projected_to_planes(const tgs_projected* p, int64_t n, float alpha_skip, float alpha_clamp,
                                 const GroupGeom& gg, DevProjected out, cudaStream_t st);
+// entries per group row of the frame whose splat rects are in `rect` (n = &fc->n_input)
+void launch_row_entries(const uint2* rect, const uint32_t* n, const GroupGeom& gg, unsigned long long* rows,
+                        cudaStream_t st);
 void launch_lists_check(const tgs_group_entry* e, const uint32_t* offsets, int n_groups, const tgs_projected* proj,
                         int64_t n_proj, const GroupGeom& gg, uint32_t* list, uint32_t* flags, cudaStream_t st);
 

@@ -136,9 +136,37 @@ __global__ void lists_check_kernel(const tgs_group_entry* __restrict__ e, const 
     }
 }
 
+// Entries per group row of a frame (screen-band work estimate): a splat with tile
+// rect [x0..x1] x [y0..y1] adds (x1/G - x0/G + 1) entries to every group row y0/G .. y1/G — the
+// row totals of build_group_entries (binning.cpp:46-74) without building a list.
+__global__ void __launch_bounds__(256) row_entries_kernel(const uint2* __restrict__ rect, const uint32_t* __restrict__ n,
+                                                          GroupGeom gg, unsigned long long* __restrict__ rows) {
+    extern __shared__ unsigned int srow[];  // one counter per group row
+    for (int k = threadIdx.x; k < gg.groups_y; k += blockDim.x) srow[k] = 0;
+    __syncthreads();
+    const uint32_t cnt = *n;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        const uint2 r = rect[i];
+        if (r.x == kCulledRect && r.y == kCulledRect) continue;
+        const int x0 = (int)(r.x & 0xffffu), x1 = (int)(r.x >> 16), y0 = (int)(r.y & 0xffffu), y1 = (int)(r.y >> 16);
+        if (x1 < x0 || y1 < y0) continue;
+        const unsigned int span = (unsigned int)(x1 / gg.g - x0 / gg.g + 1);
+        for (int gy = y0 / gg.g; gy <= y1 / gg.g; ++gy) atomicAdd(&srow[gy], span);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < gg.groups_y; k += blockDim.x)
+        if (srow[k]) atomicAdd(&rows[k], (unsigned long long)srow[k]);
+}
+
 constexpr int kBlocks = 148 * 4;
 
 }  // namespace
+
+void launch_row_entries(const uint2* rect, const uint32_t* n, const GroupGeom& gg, unsigned long long* rows,
+                        cudaStream_t st) {
+    cudaMemsetAsync(rows, 0, (size_t)gg.groups_y * sizeof(unsigned long long), st);
+    row_entries_kernel<<<kBlocks, 256, (size_t)gg.groups_y * sizeof(unsigned int), st>>>(rect, n, gg, rows);
+}
 
 void launch_entries_count(const tgs_projected* proj, int64_t n, const GroupGeom& gg, uint32_t* counts,
                           cudaStream_t st) {

@@ -302,15 +302,28 @@ class Context:
                                    img.ctypes.data_as(_lib.F32P), C.byref(st)))
         return _result(img, cam, st)
 
-    def render_band(self, dscene, cam: Camera, opt: RenderOptions, row0: int, row1: int):
+    def render_band(self, dscene, cam: Camera, opt: RenderOptions, row0: int, row1: int, copy: bool = True):
+        """Group rows [row0, row1) of the frame; copy=False leaves the band image on the device
+        (image_device_ptr) and returns (None, stats)."""
         g = opt.group_size
         y0 = row0 * g * kTileSize
         y1 = min(cam.height, row1 * g * kTileSize)
-        img = np.empty((y1 - y0, cam.width, 3), np.float32)
+        img = np.empty((y1 - y0, cam.width, 3), np.float32) if copy else None
         st = _lib.tgs_stats()
         _check(self.lib.tgs_render_band(self.h, dscene.h, C.byref(cam.to_c()), C.byref(opt.to_c()),
-                                        int(row0), int(row1), img.ctypes.data_as(_lib.F32P), C.byref(st)))
+                                        int(row0), int(row1), img.ctypes.data_as(_lib.F32P) if copy else None,
+                                        C.byref(st)))
         return img, st
+
+    def group_row_entries(self, dscene, cam: Camera, opt: RenderOptions) -> np.ndarray:
+        """Entries per group row of the frame (screen-band work estimate, tgs_group_row_entries)."""
+        n = C.c_int64()
+        _check(self.lib.tgs_group_row_entries(self.h, dscene.h, C.byref(cam.to_c()), C.byref(opt.to_c()), None, 0,
+                                              C.byref(n)))
+        out = np.zeros(max(n.value, 1), np.uint64)
+        _check(self.lib.tgs_group_row_entries(self.h, dscene.h, C.byref(cam.to_c()), C.byref(opt.to_c()),
+                                              out.ctypes.data, n.value, C.byref(n)))
+        return out[:n.value]
 
     def render_batch(self, dscene, cams: Sequence[Camera], opt: RenderOptions,
                      out: Optional[np.ndarray] = None):

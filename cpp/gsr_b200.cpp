@@ -108,6 +108,11 @@ RenderResult finish(const Camera& cam, std::vector<float>&& rgb, const tgs_stats
     res.projection.dropped_degenerate = st.dropped_degenerate;
     res.entries = st.entries;
     res.tile_appearances = st.tile_appearances;
+    res.ops.fragment_ops = st.fragment_ops;
+    res.ops.chunk_loads = st.chunk_loads;
+    res.ops.skipped_pairs = st.skipped_pairs;
+    res.ops.used_lanes = st.used_lanes;
+    res.ops.total_lanes = st.total_lanes;
     t_times = {st.ms_preprocess, st.ms_binning, st.ms_sort, st.ms_raster, st.ms_total};
     return res;
 }

@@ -13,9 +13,10 @@
 // own dependency, CMakeLists.txt:14) must be on the include path.
 //
 // Differences a caller can observe: images are within the stated FP16
-// tolerance of the reference's fp32 image instead of byte-identical; RenderResult::ops (the
-// emulated-fragment counters of the CPU tensor path) are not produced and stay zero; `workers`
-// and `chunk_len` are validated like the reference and otherwise ignored.
+// tolerance of the reference's fp32 image instead of byte-identical; RenderResult::ops counts the
+// GPU rasteriser's work in the reference's units (include/tgs.h tgs_stats: one tcgen05.mma
+// M=128 N=32 K=16 = 16 m16n16k16 fragments, chunks of 32 rows); `workers` and `chunk_len` are
+// validated like the reference and otherwise ignored.
 #pragma once
 
 #include <Eigen/Core>

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define TGS_ABI_VERSION 1
+#define TGS_ABI_VERSION 2
 
 typedef enum {
     TGS_OK = 0,
@@ -76,6 +76,13 @@ typedef struct {
     uint64_t tile_appearances; /* sum of mask popcounts N_total */
     uint64_t visible;          /* projected splats (input - culled - dropped) */
     float ms_preprocess, ms_binning, ms_sort, ms_raster, ms_total; /* CUDA-event times */
+    /* OpReport (metrics.hpp:49-69) of the tensor rasteriser (zero for the scalar backend), in the
+     * reference's units: chunk_loads = staged chunks (32 splat rows here, <= 16 there);
+     * fragment_ops = m16n16k16-equivalent MMA blocks (one tcgen05.mma M=128 N=32 K=16 = 16);
+     * skipped_pairs = (member tile, staged row) pairs whose mask excludes a live tile;
+     * used_lanes = rows x pixels x 12 productive K lanes (the hi/lo 6-term contraction), summed
+     * over MMAs; total_lanes = 16^3 per fragment. */
+    uint64_t fragment_ops, chunk_loads, skipped_pairs, used_lanes, total_lanes;
 } tgs_stats;
 
 /* gsr::ProjectedGaussian (projection.hpp:14-23), 44 bytes. */
@@ -232,18 +239,6 @@ tgs_status tgs_gen_synthetic_scene(uint64_t seed, int count, float extent, float
                                    float scale_max, uint64_t sh_seed, float* out_records);
 /* encode_ppm payload (scene_io.cpp:253-263) of a host RGB float image on the device. */
 tgs_status tgs_encode_u8(tgs_ctx* ctx, const float* rgb_device, int64_t n, uint8_t* out_host);
-
-/* Internal self-test of the tcgen05 operand path: one M=128 x N=32 x K=16 FP16 MMA through the
- * same smem descriptors / instruction descriptor the rasterizer uses (row-major A[128][16],
- * B[32][16] as binary16 bit patterns; D[128][32] = A . B^T in FP32). */
-tgs_status tgs_debug_mma(const uint16_t* a_128x16, const uint16_t* b_32x16, float* d_128x32);
-/* Internal microbenchmark of the rasterizer's chunk hand-off protocol (producer -> MMA ->
- * epilogue): device cycles for `chunks` chunks with no blending work; mode bits: 1 issue MMAs,
- * 2 tcgen05.ld the accumulators, 4 producer proxy fence. */
-tgs_status tgs_debug_pipeline(int chunks, int mode, long long* cycles);
-/* Internal probe of the tcgen05.mma issue/commit rate: n MMAs (M=128, N=ncols in {16,32,64},
- * K=16), a commit every per_commit MMAs (waited for when wait_each); device cycles. */
-tgs_status tgs_debug_mma_rate(int n, int per_commit, int wait_each, int ncols, long long* cycles);
 
 #ifdef __cplusplus
 }

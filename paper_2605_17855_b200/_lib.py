@@ -30,7 +30,9 @@ class tgs_stats(C.Structure):
     _fields_ = [("input", C.c_uint64), ("culled", C.c_uint64), ("dropped_degenerate", C.c_uint64),
                 ("entries", C.c_uint64), ("tile_appearances", C.c_uint64), ("visible", C.c_uint64),
                 ("ms_preprocess", C.c_float), ("ms_binning", C.c_float), ("ms_sort", C.c_float),
-                ("ms_raster", C.c_float), ("ms_total", C.c_float)]
+                ("ms_raster", C.c_float), ("ms_total", C.c_float),
+                ("fragment_ops", C.c_uint64), ("chunk_loads", C.c_uint64), ("skipped_pairs", C.c_uint64),
+                ("used_lanes", C.c_uint64), ("total_lanes", C.c_uint64)]
 
 
 P = C.c_void_p
@@ -75,9 +77,6 @@ SIGNATURES = {
     "tgs_sort_entries": (c_status, [P, P, C.c_int64, C.c_int, C.c_int, C.c_int, P, P, C.c_int64]),
     "tgs_rasterize_lists": (c_status, [P, P, C.c_int64, P, C.c_int64, P, C.c_int64, C.c_int, C.c_int,
                                        C.POINTER(tgs_options), F32P]),
-    "tgs_debug_mma": (c_status, [P, P, P]),
-    "tgs_debug_pipeline": (c_status, [C.c_int, C.c_int, C.POINTER(C.c_longlong)]),
-    "tgs_debug_mma_rate": (c_status, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_longlong)]),
 }
 
 
@@ -99,7 +98,7 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.tgs_abi_version() != 1:
+        if lib.tgs_abi_version() != 2:
             raise ImportError("libtgs ABI version mismatch")
         _LIB = lib
         return lib

@@ -22,8 +22,6 @@
 
 namespace tgs {
 
-void launch_debug_mma(const uint16_t* a, const uint16_t* b, float* d, cudaStream_t st);
-
 namespace err_state {
 thread_local std::string g_err;
 }
@@ -414,6 +412,11 @@ tgs_status finish_frame(tgs_ctx* ctx, tgs_stats* stats) {
         stats->ms_raster = ms;
         cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[4]);
         stats->ms_total = ms;
+        stats->chunk_loads = g.op_chunks;
+        stats->fragment_ops = 16ull * g.op_mmas;
+        stats->skipped_pairs = g.op_skipped;
+        stats->used_lanes = g.op_mma_rows * 128ull * 12ull;
+        stats->total_lanes = stats->fragment_ops * 16ull * 16ull * 16ull;
     }
     return TGS_OK;
 }
@@ -695,6 +698,11 @@ tgs_status tgs_render_batch(tgs_ctx* ctx, const tgs_scene* scene, const tgs_came
             acc.ms_sort += one.ms_sort;
             acc.ms_raster += one.ms_raster;
             acc.ms_total += one.ms_total;
+            acc.fragment_ops += one.fragment_ops;
+            acc.chunk_loads += one.chunk_loads;
+            acc.skipped_pairs += one.skipped_pairs;
+            acc.used_lanes += one.used_lanes;
+            acc.total_lanes += one.total_lanes;
         }
         if (i < n) {
             tgs_status st = validate_options(&cams[i], opt);
@@ -1140,24 +1148,6 @@ tgs_status tgs_rasterize_lists(tgs_ctx* ctx, const tgs_group_entry* entries, int
     TGS_CUDA_OK(cudaStreamSynchronize(ctx->stream));
     // the context's frame state no longer describes a pipeline frame
     ctx->ucost_key = 0;
-    return TGS_OK;
-}
-
-// Internal self-test of the tcgen05 operand descriptors (tests/test_gpu_tcgen05.py).
-tgs_status tgs_debug_mma(const uint16_t* a_host_128x16, const uint16_t* b_host_32x16, float* d_host_128x32) {
-    DBuf da, db, dd;
-    TGS_CUDA_OK(da.ensure(128 * 16 * 2));
-    TGS_CUDA_OK(db.ensure(32 * 16 * 2));
-    TGS_CUDA_OK(dd.ensure(128 * 32 * 4));
-    TGS_CUDA_OK(cudaMemcpy(da.p, a_host_128x16, 128 * 16 * 2, cudaMemcpyHostToDevice));
-    TGS_CUDA_OK(cudaMemcpy(db.p, b_host_32x16, 32 * 16 * 2, cudaMemcpyHostToDevice));
-    launch_debug_mma(da.as<uint16_t>(), db.as<uint16_t>(), dd.as<float>(), 0);
-    TGS_CUDA_OK(cudaGetLastError());
-    TGS_CUDA_OK(cudaDeviceSynchronize());
-    TGS_CUDA_OK(cudaMemcpy(d_host_128x32, dd.p, 128 * 32 * 4, cudaMemcpyDeviceToHost));
-    da.release();
-    db.release();
-    dd.release();
     return TGS_OK;
 }
 

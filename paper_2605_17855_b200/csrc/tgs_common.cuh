@@ -62,6 +62,9 @@ struct FrameCounters {
     unsigned long long blended;
     unsigned int key_min_inv;       // ~min and max of the visible depth keys: the presort ranks
     unsigned int key_max;           // (key - min), so passes above the key range are plain copies
+    // OpReport (metrics.hpp:49-69) of the tensor rasteriser: chunks staged, tcgen05.mma issued,
+    // splat rows those MMAs carried, (member tile, staged row) pairs the mask filtered out
+    unsigned long long op_chunks, op_mmas, op_mma_rows, op_skipped;
     // not zeroed per frame: frames of this context that overflowed / failed validation so far
     // (counted by unit_order_kernel, checked by tgs_sync so no un-synced frame fails silently)
     unsigned int sticky_overflow;

@@ -47,9 +47,6 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
 
 // Bounded wait: a deadlock (a protocol bug) must become a reported kernel error, never a hung
 // GPU.  After ~4e9 cycles (~2 s) the waiter prints where it is stuck and traps.
-#ifndef TGS_MBAR_SPIN  // waits by lane-0 polling (1), polling with __nanosleep(n) (n > 1), or try_wait (0)
-#define TGS_MBAR_SPIN -1
-#endif
 #ifndef TGS_MBAR_HINT_NS
 #define TGS_MBAR_HINT_NS 20000
 #endif
@@ -67,8 +64,8 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 }
 
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
-    // try_wait with a suspend-time hint: the thread sleeps in hardware until the phase completes
-    // or ~20 us pass, so waiting warps do not steal issue slots from working ones
+    // try_wait with a suspend-time hint: the thread is suspended in hardware until the phase
+    // completes (or barrier activity wakes it, or the hint expires)
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -82,39 +79,14 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 static __device__ __noinline__ void watchdog_trap(const char* what, int a0, int a1) {
     if ((threadIdx.x & 31) == 0)
         printf("libtgs watchdog: block %d thread %d stuck in %s (%d, %d)\n", (int)blockIdx.x, (int)threadIdx.x, what,
-           a0, a1);
+               a0, a1);
     __trap();
 }
-// Warp-wide bounded wait: lane 0 polls (hardware-suspending try_wait), then the warp
-// reconverges, so no lane reaches a .sync.aligned tcgen05 op / elect.sync / vote while others
-// are still in the loop.  Memory ordering for the other lanes comes from __syncwarp.
-#ifndef TGS_WAIT_NS0
-#define TGS_WAIT_NS0 32   // first back-off sleep of a waiting warp (ns), doubled up to TGS_WAIT_CAP
-#endif
-#ifndef TGS_WAIT_CAP
-#define TGS_WAIT_CAP 256
-#endif
+// Warp-wide bounded wait: every lane suspends in try_wait (warp-uniform, so no lane reaches a
+// .sync.aligned tcgen05 op / vote while others still wait); the loop body is just the re-test,
+// the watchdog reads the clock every 4096 wake-ups.  (Measured alternatives, DESIGN.md §3.1:
+// lane-0 polling of test_wait, test_wait + __nanosleep back-off — both slower.)
 __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, const char* what, int a0, int a1) {
-#if TGS_MBAR_SPIN == -2
-    // test + __nanosleep with exponential back-off: a waiting warp is descheduled and costs no
-    // issue slots (try_wait's suspend is woken by any barrier traffic in the CTA and re-polls
-    // every few tens of cycles, which starved the working warps)
-    if (!mbar_test(bar, parity)) {
-        const long long t0 = clock64();
-        uint32_t ns = TGS_WAIT_NS0;
-        for (uint32_t i = 1;; ++i) {
-            __nanosleep(ns);
-            if (mbar_test(bar, parity)) break;
-            ns = ns < TGS_WAIT_CAP ? 2 * ns : ns;
-            if ((i & 1023u) == 0u && clock64() - t0 > 4000000000ll) watchdog_trap(what, a0, a1);
-        }
-    }
-    __syncwarp();
-    return;
-#elif TGS_MBAR_SPIN < 0
-    // every lane suspends in try_wait (warp-uniform, no reconvergence step); the loop body is
-    // just the re-test (a suspended warp is woken by barrier activity), the watchdog counts
-    // wake-ups and reads the clock only every 4096 of them
     if (!mbar_try(bar, parity)) {
         const long long t0 = clock64();
         for (;;) {
@@ -122,26 +94,6 @@ __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, con
             for (int i = 0; i < 4096 && !ok; ++i) ok = mbar_try(bar, parity);
             if (ok) break;
             if (clock64() - t0 > 4000000000ll) watchdog_trap(what, a0, a1);
-        }
-    }
-    __syncwarp();
-    return;
-#elif TGS_MBAR_SPIN
-    if ((threadIdx.x & 31) == 0 && !mbar_test(bar, parity)) {
-        const long long t0 = clock64();
-        for (uint32_t i = 1; !mbar_test(bar, parity); ++i) {
-            if (TGS_MBAR_SPIN > 1) __nanosleep(TGS_MBAR_SPIN);
-            if ((i & 63u) == 0u && clock64() - t0 > 4000000000ll) watchdog_trap(what, a0, a1);
-        }
-    }
-    __syncwarp();
-    return;
-#endif
-    if ((threadIdx.x & 31) == 0 && !mbar_try(bar, parity)) {
-        const long long t0 = clock64();
-        for (uint32_t i = 1;; ++i) {
-            if (mbar_try(bar, parity)) break;
-            if ((i & 255u) == 0u && clock64() - t0 > 4000000000ll) watchdog_trap(what, a0, a1);
         }
     }
     __syncwarp();

@@ -56,35 +56,15 @@ namespace {
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kNeverRow = -30000.0f;
 constexpr float kInf = __builtin_huge_valf();
-#ifndef TGS_RASTER_N
-#define TGS_RASTER_N 32
-#endif
-constexpr int kN = TGS_RASTER_N;  // splats per chunk (MMA N): 32, or 16 with 4 TMEM stages
-#ifndef TGS_RASTER_SS
-#define TGS_RASTER_SS 4
-#endif
-constexpr int kSS = TGS_RASTER_SS;  // shared-memory chunk ring (slack between member tiles)
-#ifndef TGS_RASTER_TS
-#define TGS_RASTER_TS 2
-#endif
-constexpr int kTS = TGS_RASTER_TS;  // TMEM accumulator stages per warpgroup
-constexpr int kJB = 16;             // accumulator columns per epilogue batch
-#ifndef TGS_RASTER_RING
-#define TGS_RASTER_RING 8
-#endif
-constexpr int kRing = TGS_RASTER_RING;  // producer gather ring: kRing - 1 batches of records in flight
-#ifndef TGS_RASTER_CTRL_FIRST
-#define TGS_RASTER_CTRL_FIRST 1
-#endif
-#ifndef TGS_RASTER_NOBLEND
-#define TGS_RASTER_NOBLEND 0  // timing probe (tools builds): skip every blend, images are wrong
-#endif
-#ifndef TGS_RASTER_MMA_SLEEP
-#define TGS_RASTER_MMA_SLEEP 16  // MMA warp first back-off (ns) when no warpgroup is ready
-#endif
-#ifndef TGS_RASTER_MMA_CAP
-#define TGS_RASTER_MMA_CAP 128   // ... doubled up to this
-#endif
+// Tuned on the C3 bench frame (DESIGN.md §3.1 lists the measured alternatives): chunks of 32
+// splats (MMA N), a ring of 4 shared-memory chunk stages, 2 TMEM stages per warpgroup, a gather
+// ring of 8 batches.
+constexpr int kN = 32;      // splats per chunk (MMA N)
+constexpr int kSS = 4;      // shared-memory chunk ring (slack between member tiles)
+constexpr int kTS = 2;      // TMEM accumulator stages per warpgroup
+constexpr int kJB = 16;     // accumulator columns per epilogue batch
+constexpr int kRing = 8;    // producer gather ring: kRing - 2 batches of records in flight
+constexpr uint32_t kMmaSleep0 = 16, kMmaSleepCap = 128;  // MMA warp back-off (ns) when nothing is ready
 #ifndef TGS_RASTER_PROF
 #define TGS_RASTER_PROF 0
 #endif
@@ -97,21 +77,13 @@ __device__ unsigned int g_rprof_done;
 __device__ unsigned long long g_rprof_issue, g_rprof_seen, g_rprof_iters;
 #endif
 
-#ifndef TGS_RASTER_NP
-#define TGS_RASTER_NP 1
-#endif
-constexpr int kNP = TGS_RASTER_NP;  // producer warps, each with its own chunk ring; units alternate
-
 template <int SLOTS>
 struct Cfg {
     static constexpr int kMT = 2 * SLOTS;  // M=128 tiles per unit (two per member tile)
     static constexpr int kEpiWarps = 4 * SLOTS;
-    // warp layout: control warps first when TGS_RASTER_CTRL_FIRST (producers, then the MMA warp),
-    // then the epilogue warps; otherwise epilogue warps first
-    static constexpr int kProd = TGS_RASTER_CTRL_FIRST ? 0 : kEpiWarps;  // producers kProd .. kProd + kNP - 1
-    static constexpr int kMma = kProd + kNP;
-    static constexpr int kEpi0 = TGS_RASTER_CTRL_FIRST ? kNP + 1 : 0;     // first epilogue warp
-    static constexpr int kThreads = (kEpiWarps + kNP + 1) * 32;
+    // warp layout: the producer, the MMA warp, then the epilogue warps
+    static constexpr int kProd = 0, kMma = 1, kEpi0 = 2;
+    static constexpr int kThreads = (kEpiWarps + 2) * 32;
     static constexpr int kCtasPerSm = SLOTS == 1 ? 3 : 1;
     static constexpr uint32_t kTmemCols = kTS * kMT * kN <= 128 ? 128 : kTS * kMT * kN <= 256 ? 256 : 512;
     static_assert(kTS * kMT * kN * kCtasPerSm <= 512, "TMEM columns per SM");
@@ -120,67 +92,34 @@ template <int SLOTS>
 __host__ __device__ inline int units_per_group(int g) { return (SLOTS == 4 && g == 4) ? 4 : 1; }
 
 struct ChunkHeader {
-    int seq;      // per-CTA unit sequence number (kNP * k + producer), -1 = end of the ring's stream
+    int seq;      // per-CTA unit sequence number, -1 = end of the stream
     int unit;     // unit index (order-resolved)
     int n_valid;  // splats in the chunk (0: unit without contributing splats)
     int live;     // member tiles live when the chunk was produced (MMA skips the others)
-    int chunk;    // chunk number within its ring (protocol self-check)
-    int last;     // last chunk of its unit: consumers move on to the next ring
+    int chunk;    // chunk number (protocol self-check)
+    int last;     // last chunk of its unit (the epilogue stores the unit's pixels)
 };
 
 template <int SLOTS>
 struct Smem {
     alignas(128) uint8_t a[2 * SLOTS][128 * 32];  // pixel monomial rows (K-major, no swizzle)
-    alignas(128) uint8_t b[kNP][kSS][kN * 32];    // splat coefficient rows, per chunk ring
-    float4 epi[kNP][kSS][kN];                     // r, g, b, min(alpha_clamp, opacity)
-    ChunkHeader hdr[kNP][kSS];
-    alignas(16) int wdone[16];  // chunks each epilogue warp has completed (all rings)
+    alignas(128) uint8_t b[kSS][kN * 32];         // splat coefficient rows
+    float4 epi[kSS][kN];                          // r, g, b, min(alpha_clamp, opacity)
+    ChunkHeader hdr[kSS];
+    alignas(16) int wdone[16];  // chunks each epilogue warp has completed
     alignas(16) int dead[16];   // (seq << 1) | 1 once all pixels of the warp terminated in unit seq
-    uint64_t full[kNP][kSS];    // producer -> MMA
+    uint64_t full[kSS];         // producer -> MMA
     uint64_t tfull[SLOTS][kTS]; // MMA -> warpgroup (tcgen05.commit)
-    // smem stage s of ring r is free again once every epilogue warp finished the chunk that used it
-    unsigned int done_cnt[kNP][kSS];
+    // smem stage s is free again once every epilogue warp finished the chunk that used it
+    unsigned int done_cnt[kSS];
     uint32_t tmem_base;
-    int prod_done;  // highest unit seq whose chunks are all published (producer hand-over)
 #if TGS_RASTER_PROF
-    unsigned long long t_rel[4][kTS], t_iss[4][kTS], t_pub[kNP][kSS];  // PROF timestamps
+    unsigned long long t_rel[4][kTS], t_iss[4][kTS], t_pub[kSS];  // PROF timestamps
 #endif
-    // producer gather rings (cp.async): splat records of kRing batches and list indices of 2 kRing
-    float4 rmc[kNP][kRing][32], rco[kNP][kRing][32], rcol[kNP][kRing][32];
-    uint4 rrr[kNP][kRing][32];
-    uint32_t ridx[kNP][2 * kRing][32];
-};
-
-// Consumer-side walk over the chunk rings: units alternate between the rings (seq = kNP k + r);
-// after a unit's last chunk, or a ring's end-of-stream marker, move to the next ring still open.
-struct RingCursor {
-    uint32_t g = 0;            // chunks consumed over all rings (TMEM stage / parity)
-    uint32_t cr[kNP] = {};     // chunks consumed per ring
-    uint32_t ended = 0;        // rings whose stream ended
-    int r = 0;                 // current ring, -1 when every ring ended
-    __device__ __forceinline__ uint32_t c() const {
-        uint32_t v = cr[0];
-#pragma unroll
-        for (int i = 1; i < kNP; ++i)
-            if (r == i) v = cr[i];
-        return v;
-    }
-    __device__ __forceinline__ void advance(bool end_marker, bool last) {
-        ++g;
-#pragma unroll
-        for (int i = 0; i < kNP; ++i)
-            if (r == i) ++cr[i];
-        if (end_marker) ended |= 1u << r;
-        if (end_marker || last) {
-            int nr = -1;
-#pragma unroll
-            for (int k = kNP; k >= 1; --k) {  // first open ring after r (cyclic), r itself last
-                const int cand = (r + k) % kNP;
-                if (!((ended >> cand) & 1u)) nr = cand;
-            }
-            r = nr;
-        }
-    }
+    // producer gather ring (cp.async): splat records of kRing batches and list indices of 2 kRing
+    float4 rmc[kRing][32], rco[kRing][32], rcol[kRing][32];
+    uint4 rrr[kRing][32];
+    uint32_t ridx[2 * kRing][32];
 };
 
 // Pixel (relative to the unit's top-left) of row l of M-tile m = 2 t + k: member tile t, its
@@ -265,9 +204,9 @@ __device__ __forceinline__ void never_row(uint4& r0, uint4& r1) {
 }
 
 template <int SLOTS>
-__device__ __forceinline__ void write_row(Smem<SLOTS>& sm, int r, int s, int slot, const uint4& r0, const uint4& r1) {
-    *reinterpret_cast<uint4*>(&sm.b[r][s][core_off(slot, 0)]) = r0;
-    *reinterpret_cast<uint4*>(&sm.b[r][s][core_off(slot, 1)]) = r1;
+__device__ __forceinline__ void write_row(Smem<SLOTS>& sm, int s, int slot, const uint4& r0, const uint4& r1) {
+    *reinterpret_cast<uint4*>(&sm.b[s][core_off(slot, 0)]) = r0;
+    *reinterpret_cast<uint4*>(&sm.b[s][core_off(slot, 1)]) = r1;
 }
 
 // Unit geometry: the unit's top-left tile, the group whose list it walks, member-tile liveness.
@@ -337,18 +276,16 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
     if (threadIdx.x < 16) {
         sm.wdone[threadIdx.x] = 0;
         sm.dead[threadIdx.x] = -1;
-        if (threadIdx.x == 0) sm.prod_done = -1;
 #if TGS_RASTER_PROF
         if (threadIdx.x < 4 * kTS) sm.t_rel[threadIdx.x / kTS][threadIdx.x % kTS] = 0, sm.t_iss[threadIdx.x / kTS][threadIdx.x % kTS] = 0;
-        if (threadIdx.x < kNP * kSS) sm.t_pub[threadIdx.x / kSS][threadIdx.x % kSS] = 0;
+        if (threadIdx.x < kSS) sm.t_pub[threadIdx.x] = 0;
 #endif
     }
     if (threadIdx.x == 0) {
-        for (int r = 0; r < kNP; ++r)
-            for (int s = 0; s < kSS; ++s) {
-                ptx::mbar_init(&sm.full[r][s], 1);
-                sm.done_cnt[r][s] = 0;
-            }
+        for (int s = 0; s < kSS; ++s) {
+            ptx::mbar_init(&sm.full[s], 1);
+            sm.done_cnt[s] = 0;
+        }
         for (int t = 0; t < SLOTS; ++t)
             for (int s = 0; s < kTS; ++s) ptx::mbar_init(&sm.tfull[t][s], 1);
         ptx::mbar_fence_init();
@@ -364,9 +301,8 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
     [[maybe_unused]] unsigned long long pf_wake = 0, pf_wake_n = 0;  // MMA commit -> epilogue wake-up
     [[maybe_unused]] const long long pf_start = clock64();
 
-    if (warp >= kProd && warp < kProd + kNP) {
-        // ================================ producers ==========================================
-        const int pr = warp - kProd;  // this producer's chunk ring
+    if (warp == kProd) {
+        // ================================ producer ===========================================
         const float skip = a.alpha_skip, clampv = a.alpha_clamp;
         uint32_t c = 0;  // chunks emitted so far
         const uint32_t lt = (1u << lane) - 1u;
@@ -376,9 +312,9 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
             const int s = (int)(cc % kSS);
             if (cc >= (uint32_t)kSS && lane == 0) {
                 const unsigned int need = (unsigned int)kEpiWarps * (cc / kSS);
-                if (ld_volatile_u32(&sm.done_cnt[pr][s]) < need) {
+                if (ld_volatile_u32(&sm.done_cnt[s]) < need) {
                     const long long t0 = clock64();
-                    while (ld_volatile_u32(&sm.done_cnt[pr][s]) < need) {
+                    while (ld_volatile_u32(&sm.done_cnt[s]) < need) {
                         __nanosleep(32);
                         if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producer/done", (int)cc, s);
                     }
@@ -388,9 +324,11 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
             __syncwarp();
             return s;
         };
+        unsigned long long op_chunks = 0, op_skipped = 0;  // OpReport (lane 0)
         auto publish = [&](int s, int seq, int unit, int n_valid, uint32_t live, int last) {
             if (lane == 0) {
-                ChunkHeader& h = sm.hdr[pr][s];
+                op_chunks += (seq >= 0 && n_valid > 0) ? 1u : 0u;
+                ChunkHeader& h = sm.hdr[s];
                 h.seq = seq;
                 h.unit = unit;
                 h.n_valid = n_valid;
@@ -401,31 +339,12 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
             ptx::fence_proxy_async_smem();
             __syncwarp();
 #if TGS_RASTER_PROF
-            if (lane == 0) sm.t_pub[pr][s] = (unsigned long long)clock64();
+            if (lane == 0) sm.t_pub[s] = (unsigned long long)clock64();
 #endif
-            if (lane == 0) ptx::mbar_arrive(&sm.full[pr][s]);
+            if (lane == 0) ptx::mbar_arrive(&sm.full[s]);
             __syncwarp();
         };
-        // units are handed out in sequence: a producer takes the ticket for unit seq only once
-        // unit seq - 1 is fully produced (the epilogue is then at most kSS chunks from needing
-        // it), so a CTA never holds more than one unit ahead of the one being rendered
-        auto wait_prev_produced = [&](int seq) {
-            if (seq > 0 && lane == 0 && ld_volatile_u32((const unsigned int*)&sm.prod_done) + 1u < (unsigned)seq) {
-                const long long t0 = clock64();
-                while (ld_volatile_u32((const unsigned int*)&sm.prod_done) + 1u < (unsigned)seq) {
-                    __nanosleep(64);
-                    if (clock64() - t0 > 4000000000ll) ptx::watchdog_trap("producer/turn", seq, pr);
-                }
-            }
-            __syncwarp();
-        };
-        auto mark_produced = [&](int seq) {
-            __syncwarp();
-            if (lane == 0) ((volatile int*)&sm.prod_done)[0] = seq;
-        };
-        int seq = pr;
-        for (;; seq += kNP) {
-            wait_prev_produced(seq);
+        for (int seq = 0;; ++seq) {
             int t = 0;
             if (lane == 0) t = (int)atomicAdd(&a.fc->group_counter, 1u);
             t = __shfl_sync(0xffffffffu, t, 0);
@@ -446,16 +365,16 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
             // commit group per step, so R - 1 batches of records are in flight.
             auto valid = [&](uint32_t b) { return b < nb && begin + b * 32u + (uint32_t)lane < end; };
             auto issue_idx = [&](uint32_t b) {
-                if (valid(b)) ptx::cp_async4(&sm.ridx[pr][b % (2 * kRing)][lane], &a.list[begin + b * 32u + lane]);
+                if (valid(b)) ptx::cp_async4(&sm.ridx[b % (2 * kRing)][lane], &a.list[begin + b * 32u + lane]);
             };
             auto issue_rec = [&](uint32_t b) {
                 if (valid(b)) {
-                    const uint32_t idx = sm.ridx[pr][b % (2 * kRing)][lane];
+                    const uint32_t idx = sm.ridx[b % (2 * kRing)][lane];
                     const int r = (int)(b % kRing);
-                    ptx::cp_async16(&sm.rmc[pr][r][lane], &a.proj.mc[idx]);
-                    ptx::cp_async16(&sm.rco[pr][r][lane], &a.proj.co[idx]);
-                    ptx::cp_async16(&sm.rcol[pr][r][lane], &a.proj.col[idx]);
-                    ptx::cp_async16(&sm.rrr[pr][r][lane], &a.proj.rr[idx]);
+                    ptx::cp_async16(&sm.rmc[r][lane], &a.proj.mc[idx]);
+                    ptx::cp_async16(&sm.rco[r][lane], &a.proj.co[idx]);
+                    ptx::cp_async16(&sm.rcol[r][lane], &a.proj.col[idx]);
+                    ptx::cp_async16(&sm.rrr[r][lane], &a.proj.rr[idx]);
                 }
             };
             struct Rec {
@@ -468,10 +387,10 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                 if (valid(b)) {
                     const int k = (int)(b % kRing);
                     r.idx = 0u;
-                    r.mc = sm.rmc[pr][k][lane];
-                    r.co = sm.rco[pr][k][lane];
-                    r.col = sm.rcol[pr][k][lane];
-                    r.rr = sm.rrr[pr][k][lane];
+                    r.mc = sm.rmc[k][lane];
+                    r.co = sm.rco[k][lane];
+                    r.col = sm.rcol[k][lane];
+                    r.rr = sm.rrr[k][lane];
                 } else {
                     r.idx = 0xffffffffu;
                     r.mc = r.co = r.col = make_float4(0, 0, 0, 0);
@@ -543,6 +462,9 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
             auto place = [&](const Built& bt) {
                 const uint32_t km = __ballot_sync(0xffffffffu, bt.keep);
                 if (km == 0u) return;
+                // OpReport skipped_pairs: live member tiles a staged row's mask leaves out
+                const uint32_t sk = __reduce_add_sync(0xffffffffu, bt.keep ? __popc(live & ~bt.cover) : 0u);
+                if (lane == 0) op_skipped += sk;
                 const int nk = __popc(km);
                 const int rank = __popc(km & lt);
                 if (!open) {
@@ -555,8 +477,8 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                 for (;;) {
                     const int room = kN - fill;
                     if (bt.keep && rank >= placed && rank - placed < room) {
-                        write_row(sm, pr, s, fill + rank - placed, bt.r0, bt.r1);
-                        sm.epi[pr][s][fill + rank - placed] = bt.epi;
+                        write_row(sm, s, fill + rank - placed, bt.r0, bt.r1);
+                        sm.epi[s][fill + rank - placed] = bt.epi;
                     }
                     if (nk - placed < room) {
                         fill += nk - placed;
@@ -615,28 +537,37 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
             if (lane >= fill && lane < kN) {
                 uint4 r0, r1;
                 never_row(r0, r1);
-                write_row(sm, pr, s, lane, r0, r1);
+                write_row(sm, s, lane, r0, r1);
             }
             publish(s, seq, unit, fill, live, 1);
             ++c;
-            mark_produced(seq);
             // schedule feedback: list entries this unit walked (batches) plus rows it staged
             if (a.unit_cost && lane == 0) a.unit_cost[unit] = 32u * n_batches + (uint32_t)kN * (c - unit_c0);
         }
         if (TGS_RASTER_PROF) pf[0] = c;
-        {  // end of this ring's stream
+        {  // end of the stream
             const int se = open_stage(c);
             publish(se, -1, -1, 0, 0u, 1);
-            mark_produced(seq);  // lets the other producer find the tickets exhausted too
+        }
+        if (lane == 0) {
+            atomicAdd(&a.fc->op_chunks, op_chunks);
+            atomicAdd(&a.fc->op_skipped, op_skipped);
         }
     } else if (warp == kMma) {
         // ================================ MMA issuer ==========================================
         constexpr uint32_t idesc = ptx::idesc_f16(128, kN);
         const uint32_t a_base = ptx::smem_u32(&sm.a[0][0]);
-        RingCursor cur[SLOTS];  // per warpgroup: its walk over the chunk rings
+        uint32_t cg[SLOTS];   // next chunk of each warpgroup
+        bool ended[SLOTS];
+#pragma unroll
+        for (int t = 0; t < SLOTS; ++t) {
+            cg[t] = 0;
+            ended[t] = false;
+        }
         int n_done = 0;
+        unsigned long long op_mmas = 0, op_mma_rows = 0;  // OpReport
         long long idle0 = clock64();
-        uint32_t backoff = TGS_RASTER_MMA_SLEEP;
+        uint32_t backoff = kMmaSleep0;
 #if TGS_RASTER_PROF
         unsigned long long mma_iters = 0;
 #endif
@@ -648,18 +579,16 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
 #endif
 #pragma unroll
             for (int t = 0; t < SLOTS; ++t) {
-                RingCursor& rc = cur[t];
-                if (rc.r < 0) continue;
-                const int r = rc.r;
-                const uint32_t c = rc.c(), g = rc.g;
-                const int s = (int)(c % kSS), ts = (int)(g % kTS);
+                if (ended[t]) continue;
+                const uint32_t c = cg[t];
+                const int s = (int)(c % kSS), ts = (int)(c % kTS);
                 int ready = 0;
                 if (lane == 0) {
-                    // chunk published, and warpgroup t finished its chunk g - kTS (the TMEM stage)
-                    ready = ptx::mbar_test(&sm.full[r][s], (c / kSS) & 1);
-                    if (ready && g >= (uint32_t)kTS) {
+                    // chunk published, and warpgroup t finished chunk c - kTS (its TMEM stage)
+                    ready = ptx::mbar_test(&sm.full[s], (c / kSS) & 1);
+                    if (ready && c >= (uint32_t)kTS) {
                         const int4 d = ld_volatile_v4(&sm.wdone[4 * t]);
-                        ready = min(min(d.x, d.y), min(d.z, d.w)) >= (int)(g - kTS + 1);
+                        ready = min(min(d.x, d.y), min(d.z, d.w)) >= (int)(c - kTS + 1);
                     }
                 }
                 ready = __shfl_sync(0xffffffffu, ready, 0);
@@ -667,21 +596,19 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                 [[maybe_unused]] const long long t_seen = TGS_RASTER_PROF ? clock64() : 0;
                 __syncwarp();
                 ptx::tc_fence_after();
-                const ChunkHeader& hs = sm.hdr[r][s];
+                const ChunkHeader& hs = sm.hdr[s];
                 const int hseq = __shfl_sync(0xffffffffu, hs.seq, 0);
                 const int hnv = __shfl_sync(0xffffffffu, hs.n_valid, 0);
                 const uint32_t hlive = __shfl_sync(0xffffffffu, (uint32_t)hs.live, 0);
                 const int hch = __shfl_sync(0xffffffffu, hs.chunk, 0);
-                const int hlast = __shfl_sync(0xffffffffu, hs.last, 0);
                 if (hch != (int)c) {
                     if (lane == 0)
-                        printf("libtgs MMA: warpgroup %d ring %d expected chunk %d found %d (seq %d)\n", t, r, (int)c, hch,
-                               hseq);
+                        printf("libtgs MMA: warpgroup %d expected chunk %d found %d (seq %d)\n", t, (int)c, hch, hseq);
                     __trap();
                 }
                 if (hseq >= 0 && hnv > 0 && ((hlive >> t) & 1u)) {
                     [[maybe_unused]] const long long ti0 = TGS_RASTER_PROF ? clock64() : 0;
-                    const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[r][s][0]), 128, 256);
+                    const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[s][0]), 128, 256);
                     const uint32_t dcol = tmem + (uint32_t)(((ts * SLOTS + t) * 2) * kN);
 #pragma unroll
                     for (int k = 0; k < 2; ++k)
@@ -689,11 +616,13 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                                               ptx::smem_desc(a_base + (uint32_t)((2 * t + k) * 128 * 32), 128, 256), bd,
                                               idesc, 0u);
                     ptx::mma_commit_elect(&sm.tfull[t][ts]);
+                    op_mmas += 2;
+                    op_mma_rows += 2u * (uint32_t)hnv;
 #if TGS_RASTER_PROF
                     if (lane == 0) {
                         const unsigned long long now = (unsigned long long)clock64();
                         const unsigned long long rdy =
-                            g >= (uint32_t)kTS ? max(sm.t_rel[t][ts], sm.t_pub[r][s]) : sm.t_pub[r][s];
+                            c >= (uint32_t)kTS ? max(sm.t_rel[t][ts], sm.t_pub[s]) : sm.t_pub[s];
                         pf[0] += now > rdy ? now - rdy : 0ull;  // ready -> MMAs issued and committed
                         pf[1] += (unsigned long long)t_seen > rdy ? (unsigned long long)t_seen - rdy : 0ull;
                         pf[2] += 1;
@@ -705,22 +634,27 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                     ptx::mbar_arrive(&sm.tfull[t][ts]);
                 }
                 __syncwarp();
-                rc.advance(hseq < 0, hlast != 0);
-                if (rc.r < 0) ++n_done;
+                cg[t] = c + 1;
+                if (hseq < 0) {
+                    ended[t] = true;
+                    ++n_done;
+                }
                 did = true;
             }
             if (did) {
                 idle0 = clock64();
-                backoff = TGS_RASTER_MMA_SLEEP;
+                backoff = kMmaSleep0;
             } else {
                 // idle: back off exponentially so the polls do not take issue slots from the
                 // epilogue warps of this SMSP (the MMA warp has the highest arbitration rank)
-                if (TGS_RASTER_MMA_SLEEP) {
-                    __nanosleep(backoff);
-                    backoff = backoff < TGS_RASTER_MMA_CAP ? 2 * backoff : backoff;
-                }
-                if (clock64() - idle0 > 4000000000ll) ptx::watchdog_trap("mma/idle", (int)cur[0].g, n_done);
+                __nanosleep(backoff);
+                backoff = backoff < kMmaSleepCap ? 2 * backoff : backoff;
+                if (clock64() - idle0 > 4000000000ll) ptx::watchdog_trap("mma/idle", (int)cg[0], n_done);
             }
+        }
+        if (lane == 0) {
+            atomicAdd(&a.fc->op_mmas, op_mmas);
+            atomicAdd(&a.fc->op_mma_rows, op_mma_rows);
         }
 #if TGS_RASTER_PROF
         if (lane == 0) atomicAdd(&g_rprof_iters, mma_iters);
@@ -755,21 +689,18 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
         for (int k = 0; k < 2; ++k)
 #pragma unroll
             for (int j = 0; j < kJB; ++j) d[k][j] = 0u;
-        RingCursor rcur;
-        while (rcur.r >= 0) {
-            const int r = rcur.r;
-            const uint32_t c = rcur.c(), g = rcur.g;
-            const int s = (int)(c % kSS), ts = (int)(g % kTS);
-            // this warpgroup consumed the phase of its chunk g - kTS itself, so the parity is unambiguous
+        for (uint32_t c = 0;; ++c) {
+            const int s = (int)(c % kSS), ts = (int)(c % kTS);
+            // this warpgroup consumed the phase of chunk c - kTS itself, so the parity is unambiguous
             [[maybe_unused]] const long long tw0 = clock64();
             // PROF: was the chunk still unpublished when this warp started waiting (producer-bound)?
-            [[maybe_unused]] const bool starved = TGS_RASTER_PROF && !ptx::mbar_test(&sm.full[r][s], (c / kSS) & 1);
+            [[maybe_unused]] const bool starved = TGS_RASTER_PROF && !ptx::mbar_test(&sm.full[s], (c / kSS) & 1);
             [[maybe_unused]] bool lockstep = false;  // PROF: a warp of this group still holds the TMEM stage
-            if (TGS_RASTER_PROF && !starved && g >= (uint32_t)kTS) {
+            if (TGS_RASTER_PROF && !starved && c >= (uint32_t)kTS) {
                 const int4 dd = ld_volatile_v4(&sm.wdone[4 * t]);
-                lockstep = min(min(dd.x, dd.y), min(dd.z, dd.w)) < (int)(g - kTS + 1);
+                lockstep = min(min(dd.x, dd.y), min(dd.z, dd.w)) < (int)(c - kTS + 1);
             }
-            ptx::mbar_wait_wd(&sm.tfull[t][ts], (g / kTS) & 1, "epilogue/tfull", (int)g, warp);
+            ptx::mbar_wait_wd(&sm.tfull[t][ts], (c / kTS) & 1, "epilogue/tfull", (int)c, warp);
             if (TGS_RASTER_PROF) {
                 const long long dw = clock64() - tw0;
                 pf[1] += dw;
@@ -784,11 +715,11 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
 #endif
             }
             ptx::tc_fence_after();
-            const ChunkHeader h = sm.hdr[r][s];
+            const ChunkHeader h = sm.hdr[s];
             if (h.chunk != (int)c) {
                 if (lane == 0)
-                    printf("libtgs epilogue warp %d ring %d: expected chunk %d found %d (seq %d)\n", warp, r, (int)c,
-                           h.chunk, h.seq);
+                    printf("libtgs epilogue warp %d: expected chunk %d found %d (seq %d)\n", warp, (int)c, h.chunk,
+                           h.seq);
                 __trap();
             }
             if (h.seq >= 0 && h.seq != cur) {  // first chunk of a unit
@@ -827,7 +758,7 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                         // before blending, so the next MMA into it overlaps this blend
                         ptx::tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) ((volatile int*)sm.wdone)[slot] = (int)g + 1;
+                        if (lane == 0) ((volatile int*)sm.wdone)[slot] = (int)c + 1;
 #if TGS_RASTER_PROF
                         if (lane == 0) atomicMax(&sm.t_rel[t][ts], (unsigned long long)clock64());
 #endif
@@ -842,7 +773,7 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                                            fset_ge(__uint_as_float(d[1][jj]), thr[1]);
                         mk |= p & (1u << jj);
                     }
-                    const uint32_t M = TGS_RASTER_NOBLEND ? 0u : __reduce_or_sync(0xffffffffu, mk);  // NOBLEND: timing probe only
+                    const uint32_t M = __reduce_or_sync(0xffffffffu, mk);
                     if (TGS_RASTER_PROF) {
                         pf[2] += __popc(M);
                         pf[3] += kJB;
@@ -855,7 +786,7 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
 #pragma unroll
                     for (int jj = 0; jj < kJB; ++jj)
                         if (M & (1u << jj)) {
-                            const float4 ej = sm.epi[r][s][j0 + jj];
+                            const float4 ej = sm.epi[s][j0 + jj];
 #pragma unroll
                             for (int k = 0; k < 2; ++k) {
                                 const float dv = __uint_as_float(d[k][jj]);
@@ -892,21 +823,21 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
             if (lane == 0) {
                 if (h.seq >= 0 && alive == 0u && !reported) ((volatile int*)sm.dead)[slot] = (cur << 1) | 1;
                 __threadfence_block();
-                if (!tmem_released) ((volatile int*)sm.wdone)[slot] = (int)g + 1;
+                if (!tmem_released) ((volatile int*)sm.wdone)[slot] = (int)c + 1;
 #if TGS_RASTER_PROF
                 if (!tmem_released) atomicMax(&sm.t_rel[t][ts], (unsigned long long)clock64());
 #endif
-                atomicAdd(&sm.done_cnt[r][s], 1u);
+                atomicAdd(&sm.done_cnt[s], 1u);
             }
             reported = reported || (h.seq >= 0 && alive == 0u);
-            rcur.advance(h.seq < 0, h.last != 0);
+            if (h.seq < 0) break;
         }
     }
 
 #if TGS_RASTER_PROF
     if (lane == 0) {
         const long long tot = clock64() - pf_start;
-        if (warp >= kProd && warp < kProd + kNP) {
+        if (warp == kProd) {
             atomicAdd(&g_rprof[0], (unsigned long long)tot);
             atomicAdd(&g_rprof[1], pf[1]);
             atomicAdd(&g_rprof[8], pf[2]);   // cp.async data waits

@@ -250,6 +250,20 @@ class RenderResult:
     entries: int = 0           # group-level entries (N_group)
     tile_appearances: int = 0  # tile-level appearances (N_total)
     stage_ms: dict = field(default_factory=dict)
+    ops: "OpReport" = None     # OpReport (metrics.hpp:49-69) of the tensor rasteriser
+
+
+@dataclass
+class OpReport:
+    """OpReport (metrics.hpp:49-69) in the reference's units (include/tgs.h tgs_stats)."""
+    fragment_ops: int = 0
+    chunk_loads: int = 0
+    skipped_pairs: int = 0
+    used_lanes: int = 0
+    total_lanes: int = 0
+
+    def padding_waste(self) -> float:
+        return 1.0 - self.used_lanes / self.total_lanes if self.total_lanes else 0.0
 
 
 PROJ_DTYPE = np.dtype([("mean2d", "<f4", 2), ("conic", "<f4", 3), ("color", "<f4", 3),
@@ -420,7 +434,9 @@ def _result(img: np.ndarray, cam: Camera, st: _lib.tgs_stats) -> RenderResult:
         ProjectionStats(int(st.input), int(st.culled), int(st.dropped_degenerate)),
         int(st.entries), int(st.tile_appearances),
         {"preprocess": st.ms_preprocess, "binning": st.ms_binning, "sort": st.ms_sort,
-         "raster": st.ms_raster, "total": st.ms_total})
+         "raster": st.ms_raster, "total": st.ms_total},
+        OpReport(int(st.fragment_ops), int(st.chunk_loads), int(st.skipped_pairs), int(st.used_lanes),
+                 int(st.total_lanes)))
 
 
 # --------------------------------------------------------------------------------------------

@@ -165,3 +165,25 @@ def test_c4_bands_stitch_bit_identical(gsr, world):
     assert entries == full.entries
     stitched = np.concatenate(parts, axis=0)
     assert np.array_equal(stitched.view(np.uint32), full.image.rgb.view(np.uint32))
+
+
+def test_op_report_counters(gsr, port):
+    """RenderResult.ops (OpReport, metrics.hpp:49-69) of the tensor rasteriser: consistent units
+    (16 fragments per tcgen05.mma, 16^3 lanes per fragment), non-trivial skipped pairs, zero for
+    the CUDA-core baseline; deterministic across identical renders."""
+    rec = port.gen_scene(18, 4000, 1.0, 0.01, 0.08, 0)
+    cam = gsr.make_camera(256, 192)
+    ctx = gsr.default_context(0)
+    ds = ctx.upload(rec)
+    res = ctx.render(ds, cam, gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 2))
+    ops = res.ops
+    assert ops.chunk_loads > 0 and ops.fragment_ops > 0 and ops.fragment_ops % 32 == 0
+    assert ops.total_lanes == ops.fragment_ops * 16 ** 3
+    assert 0 < ops.used_lanes < ops.total_lanes and 0.0 < ops.padding_waste() < 1.0
+    assert ops.skipped_pairs > 0
+    # each chunk carries at most 32 rows to at most 4 member tiles (2 MMAs of 16 fragments each)
+    assert ops.fragment_ops <= ops.chunk_loads * 4 * 2 * 16
+    again = ctx.render(ds, cam, gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 2)).ops
+    assert again == ops
+    base = ctx.render(ds, cam, gsr.RenderOptions(gsr.Backend.scalar, gsr.PrecisionMode.fp32, 1)).ops
+    assert base.fragment_ops == base.chunk_loads == base.total_lanes == 0

@@ -1,9 +1,12 @@
-// Microbenchmark of the rasterizer's chunk hand-off protocol (producer -> MMA -> epilogue ->
-// producer) with no blending work, to measure per-chunk pipeline latency on the device.
-// Exposed as tgs_debug_pipeline (include/tgs.h, internal).
-#include "tgs_common.cuh"
-#include "tgs_kernels.cuh"
-#include "tgs_ptx.cuh"
+// TOOLS ONLY (libtgs_debug.so, built by tools/debug/build.py; not part of libtgs.so or its ABI):
+// microbenchmarks of the rasterizer's tcgen05 building blocks —
+//   tgs_debug_pipeline: per-chunk latency of the producer -> MMA -> epilogue hand-off (no blending),
+//   tgs_debug_mma_rate: tcgen05.mma issue rate / group latency in isolation,
+//   tgs_debug_mma:      one M=128 x N=32 x K=16 MMA through the rasterizer's descriptors
+//                       (tests/test_gpu_tcgen05.py checks it against float64).
+#include "../../paper_2605_17855_b200/csrc/tgs_common.cuh"
+#include "../../paper_2605_17855_b200/csrc/tgs_ptx.cuh"
+#include "tgs_debug.h"
 
 namespace tgs {
 namespace {
@@ -228,7 +231,6 @@ extern "C" tgs_status tgs_debug_pipeline(int chunks, int mode, long long* cycles
 
 // ---- self-test hook: one M=128 x N=32 x K=16 tcgen05.mma through the rasterizer's descriptors --
 namespace tgs {
-namespace {
 __device__ __forceinline__ uint32_t dbg_core_off(int row, int khalf) {
     return (uint32_t)((row >> 3) * 256 + khalf * 128 + (row & 7) * 16);
 }
@@ -278,9 +280,23 @@ __global__ void __launch_bounds__(128, 1) debug_mma_kernel(const uint16_t* __res
     ptx::tc_fence_after();
     if (warp == 0) ptx::tmem_dealloc<32>(tm);
 }
-}  // namespace
-
-void launch_debug_mma(const uint16_t* a, const uint16_t* b, float* d, cudaStream_t st) {
-    debug_mma_kernel<<<1, 128, 0, st>>>(a, b, d);
-}
 }  // namespace tgs
+
+extern "C" tgs_status tgs_debug_mma(const uint16_t* a_host_128x16, const uint16_t* b_host_32x16, float* d_host_128x32) {
+    uint16_t *a = nullptr, *b = nullptr;
+    float* d = nullptr;
+    cudaError_t e = cudaMalloc(&a, 128 * 16 * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&b, 32 * 16 * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&d, 128 * 32 * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(a, a_host_128x16, 128 * 16 * 2, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(b, b_host_32x16, 32 * 16 * 2, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        tgs::debug_mma_kernel<<<1, 128>>>(a, b, d);
+        e = cudaDeviceSynchronize();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(d_host_128x32, d, 128 * 32 * 4, cudaMemcpyDeviceToHost);
+    cudaFree(a);
+    cudaFree(b);
+    cudaFree(d);
+    return e == cudaSuccess ? TGS_OK : TGS_ERR_CUDA;
+}

@@ -6,18 +6,18 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2605_17855_b200 import _lib  # noqa: E402
+from tools.debug.build import load  # noqa: E402
 
 
 def main():
-    lib = _lib.load()
+    lib = load()
     for ncols in (16, 32, 64):
         for per, wait in ((8, 0), (8, 1), (1, 1)):
             n = 4096
             cyc = C.c_longlong()
             variant = 4 << 16  # warp-uniform elected issue, as the rasteriser
             rc = lib.tgs_debug_mma_rate(n, variant | per, wait, ncols, C.byref(cyc))
-            assert rc == 0, _lib.last_error()
+            assert rc == 0
             print(f"MMA N={ncols:2d} commit every {per} wait={wait}: {cyc.value / n:7.1f} cycles per MMA "
                   f"({cyc.value / n * per:8.1f} per group)", flush=True)
 

@@ -42,7 +42,7 @@ def test_cubin_is_sm100a_with_tcgen05():
 
 def test_loads_and_abi_version():
     lib = _lib.load()
-    assert lib.tgs_abi_version() == 1
+    assert lib.tgs_abi_version() == 2
 
 
 def test_generator_matches_port(port):

@@ -176,6 +176,43 @@ def run_reference(args):
     return 0
 
 
+CONFIGS = {  # BASELINE.json configs: seed, splats, SH seed, width, height
+    "C1": (1, 100_000, 5, 800, 800),
+    "C2": (2, 1_000_000, 0, 1920, 1080),
+    "C3": (3, 3_000_000, 0, 1920, 1080),
+    "C4": (4, 6_000_000, 0, 3840, 2160),
+}
+
+
+def run_configs(args, local):
+    """Per-stage ms of one frame (identity camera, testutil.hpp:14-24) for every BASELINE config:
+    tensor G=2 and the CUDA-core baseline G=1, median of `steps` synced frames after `warmup`;
+    one JSON line per config.  Not the driver's bench line (that is --mode cameras)."""
+    from paper_2605_17855_b200 import gsr
+    ctx = gsr.Context(local)
+    for name, (seed, n, sh, w, h) in CONFIGS.items():
+        ds = ctx.upload(gsr.gen_synthetic_scene(seed, n, 1.0, (0.01, 0.05), sh_seed=sh))
+        cam = gsr.make_camera(w, h)
+        out = {"config": name, "splats": n, "sh_degree": 3 if sh else 0, "width": w, "height": h}
+        for label, opt in (("tensor_g2", gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 2)),
+                           ("cuda_core_g1", gsr.RenderOptions(gsr.Backend.scalar, gsr.PrecisionMode.fp32, 1))):
+            rows = []
+            for i in range(max(args.warmup, 3) + args.steps):
+                ctx.enqueue(ds, cam, opt)
+                st = ctx.sync()
+                if i >= max(args.warmup, 3):
+                    rows.append((st.ms_preprocess, st.ms_sort, st.ms_binning, st.ms_raster, st.ms_total))
+            med = [statistics.median(r[k] for r in rows) for k in range(5)]
+            out[label] = {"preprocess": med[0], "sort": med[1], "binning": med[2], "raster": med[3],
+                          "total": med[4], "frames_per_s": 1000.0 / med[4], "entries": int(st.entries)}
+        walked, blended = ctx.count_pairs()
+        out["walked_pairs"], out["blended_pairs"] = walked, blended
+        out["raster_speedup_vs_cuda_core"] = out["cuda_core_g1"]["raster"] / out["tensor_g2"]["raster"]
+        print(json.dumps(out), flush=True)
+        ds.free()
+    return 0
+
+
 def run_bands(args, rank, world, local, coll_dev):
     """BASELINE config 4: one 3840x2160 frame of the 6M-splat scene (seed 4), tensor G=2, split into
     `world` screen bands of group rows balanced by per-row entry counts (tgs_group_row_entries);
@@ -241,7 +278,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e/baseline extras (profiling runs)")
-    ap.add_argument("--mode", default="cameras", choices=["cameras", "bands"],
+    ap.add_argument("--mode", default="cameras", choices=["cameras", "bands", "configs"],
                     help="cameras: the C3/C5 camera-batch line (default); bands: C4 single 4K frame split "
                          "into screen bands across the ranks")
     args = ap.parse_args()
@@ -266,6 +303,8 @@ def main():
     coll_dev = torch.device("cuda", local) if backend == "nccl" else None
     if args.mode == "bands":
         return run_bands(args, rank, world, local, coll_dev)
+    if args.mode == "configs":
+        return run_configs(args, local)
 
     from paper_2605_17855_b200 import gsr, _lib
     ctx = gsr.Context(local)

@@ -54,8 +54,10 @@ typedef struct {
 /* gsr::RenderOptions (render.hpp:10-17) + RasterConstants (raster_scalar.hpp:14-18).
  * backend: TGS_BACKEND_SCALAR runs the CUDA-core baseline rasterizer (requires group_size 1,
  * like raster_scalar.cpp:56-57); TGS_BACKEND_TENSOR runs the tcgen05 grouped rasterizer.
- * mode: both modes run the FP16 hi/lo monomial contraction; the
- * reference's emulated fp16 operand quantisation is not reproduced.  workers and chunk_len are
+ * mode: TGS_MODE_FP32 runs the fast rasterisers (tensor: FP16 hi/lo monomial contraction on the
+ * tensor cores, images within the tolerance of DESIGN.md §Precision); TGS_MODE_FP16 runs the
+ * exact-emulation rasteriser, which reproduces the reference's fp16 lanes (operands.hpp:27-72)
+ * bit for bit for either backend and any G.  workers and chunk_len are
  * accepted for source compatibility; the image does not depend on either (the reference pins
  * both invariances: acceptance.cpp:227-238, :359-382). */
 typedef struct {
@@ -130,6 +132,16 @@ void* tgs_ctx_stream(tgs_ctx* ctx);
  * alpha < alpha_skip on every pixel of the tile); off reproduces the reference's 3-sigma-square
  * work (binning.cpp:32-44) for A/B measurement. */
 tgs_status tgs_set_tile_cull(tgs_ctx* ctx, int on);
+
+/* Exact emulation (default off): fp32-mode frames also go through the exact-emulation rasteriser,
+ * whose images equal the reference CPU build's bit for bit (CUDA cores; a validation mode). */
+tgs_status tgs_set_exact_emulation(tgs_ctx* ctx, int on);
+
+/* CUDA-graph frames (default on): the second frame of an unchanged configuration (scene, image
+ * size, options, band, buffer capacities) captures the per-frame launch sequence (preprocess,
+ * presort, binning, unit order, raster, ~20 launches / memsets / event records) into a graph;
+ * later frames replay it with only the camera argument updated.  Images are identical either way. */
+tgs_status tgs_set_graphs(tgs_ctx* ctx, int on);
 
 /* Persistent device-resident scene (SoA, float4 planes); amortises marshalling across frames. */
 tgs_status tgs_scene_upload(tgs_ctx* ctx, const float* records, int64_t count, int sh_degree,

@@ -46,6 +46,8 @@ SIGNATURES = {
     "tgs_ctx_destroy": (None, [P]),
     "tgs_ctx_stream": (P, [P]),
     "tgs_set_tile_cull": (c_status, [P, C.c_int]),
+    "tgs_set_graphs": (c_status, [P, C.c_int]),
+    "tgs_set_exact_emulation": (c_status, [P, C.c_int]),
     "tgs_scene_upload": (c_status, [P, F32P, C.c_int64, C.c_int, C.POINTER(P)]),
     "tgs_scene_free": (None, [P]),
     "tgs_render": (c_status, [P, P, C.POINTER(tgs_camera), C.POINTER(tgs_options), F32P,

@@ -127,6 +127,16 @@ struct tgs_ctx {
     tgs_ctx* lanes[kBatchLanes - 1] = {};
     tgs_ctx* parent = nullptr;
     int tile_cull = 1;  // tgs_set_tile_cull
+    // CUDA graph of the per-frame launch sequence (tgs_set_graphs): captured on the second frame
+    // of an unchanged configuration, replayed with the camera argument of preprocess updated
+    int graphs = 1;
+    int exact = 0;  // tgs_set_exact_emulation: fp32 frames through the exact-emulation rasteriser
+    cudaGraphExec_t gexec = nullptr;
+    cudaGraph_t ggraph = nullptr;
+    cudaGraphNode_t gpre = nullptr;   // preprocess kernel node
+    PreprocessArgs gpa{};             // its captured arguments (camera replaced per launch)
+    std::string gkey;                 // configuration the graph was captured for
+    std::string pkey;                 // configuration of the previous frame
     uint32_t acked_overflow = 0, acked_invalid = 0;  // sticky frame-failure counters already reported
     tgs_scene* scratch_scene = nullptr;
 };
@@ -194,6 +204,20 @@ DevProjected dev_proj(tgs_ctx* ctx) {
     return p;
 }
 
+tgs_status record_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cam, const tgs_options* opt,
+                        const GroupGeom& gg, bool feedback, int row0, size_t h1, size_t h2, int n_alloc,
+                        int units_per_group);
+
+// Stage events: recorded as event-record nodes when the frame is captured into a graph (a plain
+// cudaEventRecord on a capturing stream only expresses a dependency and leaves the event unset).
+cudaError_t record_event(cudaEvent_t ev, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(s, &cs);
+    if (e != cudaSuccess) return e;
+    return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal)
+                                               : cudaEventRecord(ev, s);
+}
+
 // Enqueue one frame (or band) on ctx->stream.
 tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cam,
                          const tgs_options* opt, int band0, int band1) {
@@ -251,10 +275,108 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     const int row1 = std::min(cam->height, band1 * gg.g * kTile);
     TGS_CUDA_OK(ctx->image.ensure((size_t)(row1 - row0) * cam->width * 3 * sizeof(float)));
 
+    // the previous frame's measured walks schedule this one when it had the same unit geometry
+    // (same image, group size, band and backend): a camera path changes slowly
+    const uint64_t ukey = ((uint64_t)(uint32_t)cam->width << 40) ^ ((uint64_t)(uint32_t)cam->height << 20) ^
+                          ((uint64_t)band0 << 8) ^ ((uint64_t)band1 << 28) ^ ((uint64_t)gg.g << 4) ^
+                          (uint64_t)opt->backend ^ (1ull << 63);
+    const bool feedback = ctx->ucost_key == ukey;
+    ctx->ucost_key = ukey;
+    // everything the launch sequence depends on except the camera pose / intrinsics
+    char kbuf[640];
+    int kl = std::snprintf(kbuf, sizeof(kbuf), "%p %lld %d %d %d %d %d %d %d %a %a %a %d %d %u %lld", (const void*)scene,
+                           (long long)scene->n, cam->width, cam->height, opt->backend, opt->mode, opt->group_size,
+                           band0, band1,
+                           opt->alpha_skip, opt->alpha_clamp, opt->t_terminate, ctx->tile_cull * 2 + ctx->exact,
+                           feedback ? 1 : 0,
+                           ctx->capacity, (long long)ctx->proj_cap);
+    // ... and every buffer address the captured launches bake in (buffers only ever grow)
+    const DBuf* fbufs[] = {&ctx->proj, &ctx->pre_keys[0], &ctx->pre_keys[1], &ctx->pre_vals[0], &ctx->pre_vals[1],
+                           &ctx->rect, &ctx->rrect, &ctx->list, &ctx->rowlist, &ctx->hist, &ctx->bsum, &ctx->ghist,
+                           &ctx->offsets, &ctx->order, &ctx->ucost, &ctx->image};
+    for (const DBuf* b : fbufs) kl += std::snprintf(kbuf + kl, sizeof(kbuf) - (size_t)kl, " %p", b->p);
+    const std::string key(kbuf);
+    const bool same_as_prev = key == ctx->pkey;
+    ctx->pkey = key;
+    if (ctx->graphs && ctx->gexec && key == ctx->gkey) {
+        // replay: only the camera changes
+        PreprocessArgs pa = ctx->gpa;
+        pa.cam = make_dev_camera(cam);
+        cudaKernelNodeParams kp;
+        TGS_CUDA_OK(cudaGraphKernelNodeGetParams(ctx->gpre, &kp));
+        void* args[1] = {&pa};
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        TGS_CUDA_OK(cudaGraphExecKernelNodeSetParams(ctx->gexec, ctx->gpre, &kp));
+        TGS_CUDA_OK(cudaGraphLaunch(ctx->gexec, s));
+    } else if (ctx->graphs && same_as_prev) {
+        // the configuration repeated: capture the launch sequence once, then replay it
+        cudaGraph_t graph = nullptr;
+        TGS_CUDA_OK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+        const tgs_status rs = record_frame(ctx, scene, cam, opt, gg, feedback, row0, h1, h2, n_alloc, units_per_group);
+        const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+        if (rs != TGS_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return rs;
+        }
+        TGS_CUDA_OK(ce);
+        if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+        ctx->gexec = nullptr;
+        ctx->gpre = nullptr;
+        cudaError_t e = cudaGraphInstantiate(&ctx->gexec, graph, 0);
+        if (e == cudaSuccess) {
+            size_t nn = 0;
+            cudaGraphGetNodes(graph, nullptr, &nn);
+            std::vector<cudaGraphNode_t> nodes(nn);
+            cudaGraphGetNodes(graph, nodes.data(), &nn);
+            for (cudaGraphNode_t nd : nodes) {
+                cudaGraphNodeType ty;
+                cudaKernelNodeParams kp;
+                if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel &&
+                    cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess && kp.func == preprocess_kernel_fn()) {
+                    ctx->gpre = nd;
+                    ctx->gpa = *static_cast<const PreprocessArgs*>(kp.kernelParams[0]);
+                }
+            }
+            if (!ctx->gpre) e = cudaErrorInvalidValue;
+        }
+        if (e != cudaSuccess) {
+            if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+            ctx->gexec = nullptr;
+            cudaGraphDestroy(graph);
+            return cuda_fail(e, "frame graph capture", __FILE__, __LINE__);
+        }
+        // the executable graph references kernel nodes by the (kept) graph's node handles
+        ctx->gkey = key;
+        if (ctx->ggraph) cudaGraphDestroy(ctx->ggraph);
+        ctx->ggraph = graph;
+        TGS_CUDA_OK(cudaGraphLaunch(ctx->gexec, s));
+    } else {
+        const tgs_status rs = record_frame(ctx, scene, cam, opt, gg, feedback, row0, h1, h2, n_alloc, units_per_group);
+        if (rs != TGS_OK) return rs;
+    }
+
+    ctx->last_scene = scene;
+    ctx->last_cam = *cam;
+    ctx->last_opt = *opt;
+    ctx->last_gg = gg;
+    ctx->last_band0 = band0;
+    ctx->last_band1 = band1;
+    ctx->image_rows = row1 - row0;
+    ctx->pending = true;
+    return TGS_OK;
+}
+
+// The stream operations of one frame (eager, or recorded into the frame graph).
+tgs_status record_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* cam, const tgs_options* opt,
+                        const GroupGeom& gg, bool feedback, int row0, size_t h1, size_t h2, int n_alloc,
+                        int units_per_group) {
+    cudaStream_t s = ctx->stream;
+    const int n_groups = gg.n_groups_band;
     FrameCounters* fc = ctx->fc.as<FrameCounters>();
     const DevProjected proj = dev_proj(ctx);
 
-    TGS_CUDA_OK(cudaEventRecord(ctx->ev[0], s));
+    TGS_CUDA_OK(record_event(ctx->ev[0], s));
     // the sticky counters at the end of FrameCounters survive across frames (tgs_sync checks them)
     TGS_CUDA_OK(cudaMemsetAsync(fc, 0, offsetof(FrameCounters, sticky_overflow), s));
 
@@ -271,7 +393,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     pa.alpha_clamp = opt->alpha_clamp;
     launch_preprocess(pa, s);
     TGS_CUDA_OK(cudaGetLastError());
-    TGS_CUDA_OK(cudaEventRecord(ctx->ev[1], s));
+    TGS_CUDA_OK(record_event(ctx->ev[1], s));
 
     // 2. depth presort (keys: depth bits, values: project_scene index)
     SortBuffers pb;
@@ -285,7 +407,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     const int pr = radix_sort(pb, &fc->n_input, &fc->visible, 32, true, false, (size_t)n_alloc, s, &fc->key_min_inv, true);
     TGS_CUDA_OK(cudaGetLastError());
 
-    TGS_CUDA_OK(cudaEventRecord(ctx->ev[2], s));
+    TGS_CUDA_OK(record_event(ctx->ev[2], s));
 
     // 3. binning: stable counting sort of (group, rank) entries -> lists + per-group offsets
     BinArgs ba;
@@ -306,20 +428,14 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     ba.capacity = ctx->capacity;
     launch_binning(ba, n_alloc, s);
     {
-        // tensor G=4 groups are rasterised as 2x2-tile quarters (and G=2 groups as tile rows when
-        // built with half units); the CUDA-core baseline always walks whole lists
+        // tensor G=4 groups are rasterised as 2x2-tile quarters; the CUDA-core baseline walks whole
+        // lists.  With feedback the previous frame's measured walks order the units.
         const int per = units_per_group;
-        // the previous frame's measured walks schedule this one when it had the same unit geometry
-        // (same image, group size, band and backend): a camera path changes slowly
-        const uint64_t key = ((uint64_t)(uint32_t)cam->width << 40) ^ ((uint64_t)(uint32_t)cam->height << 20) ^
-                             ((uint64_t)band0 << 8) ^ ((uint64_t)band1 << 28) ^ ((uint64_t)gg.g << 4) ^
-                             (uint64_t)opt->backend ^ (1ull << 63);
-        const uint32_t* fb = (ctx->ucost_key == key) ? ctx->ucost.as<uint32_t>() : nullptr;
+        const uint32_t* fb = feedback ? ctx->ucost.as<uint32_t>() : nullptr;
         launch_unit_order(ctx->offsets.as<uint32_t>(), fb, n_groups * per, per, ctx->order.as<int>(), fc, s);
-        ctx->ucost_key = key;
     }
     TGS_CUDA_OK(cudaGetLastError());
-    TGS_CUDA_OK(cudaEventRecord(ctx->ev[3], s));
+    TGS_CUDA_OK(record_event(ctx->ev[3], s));
 
     // 6. raster
     RasterArgs ra;
@@ -337,22 +453,16 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     ra.tile_trip = nullptr;
     ra.unit_cost = ctx->ucost.as<uint32_t>();
     ra.tile_cull = ctx->tile_cull;
-    if (opt->backend == TGS_BACKEND_SCALAR)
+    if (opt->mode == TGS_MODE_FP16 || ctx->exact)
+        launch_raster_exact(ra, opt->mode == TGS_MODE_FP16, s);
+    else if (opt->backend == TGS_BACKEND_SCALAR)
         launch_raster_scalar(ra, s);
     else
         launch_raster_tensor(ra, ctx->num_sms, s);
     TGS_CUDA_OK(cudaGetLastError());
-    TGS_CUDA_OK(cudaEventRecord(ctx->ev[4], s));
+    TGS_CUDA_OK(record_event(ctx->ev[4], s));
     TGS_CUDA_OK(cudaMemcpyAsync(ctx->h_fc, fc, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s));
-
-    ctx->last_scene = scene;
-    ctx->last_cam = *cam;
-    ctx->last_opt = *opt;
-    ctx->last_gg = gg;
-    ctx->last_band0 = band0;
-    ctx->last_band1 = band1;
-    ctx->image_rows = row1 - row0;
-    ctx->pending = true;
+    (void)scene;
     return TGS_OK;
 }
 
@@ -412,6 +522,7 @@ tgs_status finish_frame(tgs_ctx* ctx, tgs_stats* stats) {
         stats->ms_raster = ms;
         cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[4]);
         stats->ms_total = ms;
+        (void)cudaGetLastError();  // a timing query must never poison the next frame's error check
         stats->chunk_loads = g.op_chunks;
         stats->fragment_ops = 16ull * g.op_mmas;
         stats->skipped_pairs = g.op_skipped;
@@ -526,6 +637,8 @@ void tgs_ctx_destroy(tgs_ctx* c) {
                     &c->offsets, &c->order, &c->ucost, &c->image, &c->scratch_records};
     for (DBuf* b : bufs) b->release();
     for (DBuf& b : c->stg) b.release();
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->ggraph) cudaGraphDestroy(c->ggraph);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->h_fc) cudaFreeHost(c->h_fc);
@@ -540,6 +653,22 @@ tgs_status tgs_set_tile_cull(tgs_ctx* ctx, int on) {
     ctx->tile_cull = on ? 1 : 0;
     for (tgs_ctx* l : ctx->lanes)
         if (l) l->tile_cull = ctx->tile_cull;
+    return TGS_OK;
+}
+
+tgs_status tgs_set_exact_emulation(tgs_ctx* ctx, int on) {
+    if (!ctx) return set_err(TGS_ERR_VALIDATION, "set_exact_emulation: null context");
+    ctx->exact = on ? 1 : 0;
+    for (tgs_ctx* l : ctx->lanes)
+        if (l) l->exact = ctx->exact;
+    return TGS_OK;
+}
+
+tgs_status tgs_set_graphs(tgs_ctx* ctx, int on) {
+    if (!ctx) return set_err(TGS_ERR_VALIDATION, "set_graphs: null context");
+    ctx->graphs = on ? 1 : 0;
+    for (tgs_ctx* l : ctx->lanes)
+        if (l) l->graphs = ctx->graphs;
     return TGS_OK;
 }
 
@@ -671,6 +800,7 @@ tgs_status tgs_render_batch(tgs_ctx* ctx, const tgs_scene* scene, const tgs_came
             if (st != TGS_OK) return st;
             ctx->lanes[k - 1]->parent = ctx;
             ctx->lanes[k - 1]->tile_cull = ctx->tile_cull;
+            ctx->lanes[k - 1]->graphs = ctx->graphs;
         }
         lane[k] = ctx->lanes[k - 1];
     }

@@ -18,6 +18,8 @@ struct PreprocessArgs {
     float alpha_clamp;             // for the raster record (DevProjected::rr)
 };
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t st);
+// the preprocess kernel's entry (CUDA-graph frames update its camera argument per launch)
+const void* preprocess_kernel_fn();
 
 // ---- radix sort (LSD, stable, u32 keys + u32 values, device-side item count) --------------
 struct SortBuffers {
@@ -103,6 +105,8 @@ void launch_raster_scalar(const RasterArgs& a, cudaStream_t st);
 void launch_unit_order(const uint32_t* offsets, const uint32_t* feedback, int n_units, int per_group, int* order,
                        FrameCounters* fc, cudaStream_t st);
 void launch_raster_tensor(const RasterArgs& a, int num_sms, cudaStream_t st);
+// Exact emulation of the reference's per-pixel arithmetic (fp32 or fp16 lanes), any G.
+void launch_raster_exact(const RasterArgs& a, bool fp16, cudaStream_t st);
 // raster work units per group list of the tensor path (schedule / feedback indexing)
 int raster_units_per_group(int g);
 // Instrumented walk: counts walked / alpha-contributing pairs (reference semantics, G=1 lists).

@@ -334,6 +334,8 @@ __global__ void __launch_bounds__(kPreBlock) preprocess_kernel(PreprocessArgs a)
 
 }  // namespace
 
+const void* preprocess_kernel_fn() { return reinterpret_cast<const void*>(&preprocess_kernel); }
+
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t st) {
     const int blocks = (a.scene.n + kPreBlock * kPrePer - 1) / (kPreBlock * kPrePer);
     if (blocks > 0) preprocess_kernel<<<blocks, kPreBlock, 0, st>>>(a);

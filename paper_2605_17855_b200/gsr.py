@@ -295,6 +295,15 @@ class Context:
         except Exception:
             pass
 
+    def set_exact_emulation(self, on: bool) -> None:
+        """Route fp32 frames through the exact-emulation rasteriser (bit-exact with the reference
+        CPU build; PrecisionMode.fp16 always uses it)."""
+        _check(self.lib.tgs_set_exact_emulation(self.h, int(bool(on))))
+
+    def set_graphs(self, on: bool) -> None:
+        """CUDA-graph capture/replay of the per-frame launches (tgs_set_graphs, default on)."""
+        _check(self.lib.tgs_set_graphs(self.h, int(bool(on))))
+
     def set_tile_cull(self, on: bool) -> None:
         """Rasteriser tile cull by the alpha_skip ellipse box (default on; images identical)."""
         _check(self.lib.tgs_set_tile_cull(self.h, 1 if on else 0))

@@ -187,3 +187,43 @@ def test_op_report_counters(gsr, port):
     assert again == ops
     base = ctx.render(ds, cam, gsr.RenderOptions(gsr.Backend.scalar, gsr.PrecisionMode.fp32, 1)).ops
     assert base.fragment_ops == base.chunk_loads == base.total_lanes == 0
+
+
+def test_graph_frames_identical_to_eager(gsr, port):
+    """Frames replayed from the captured CUDA graph (camera argument updated per launch) equal
+    eager frames bit for bit, for a camera path and after a configuration change."""
+    rec = port.gen_scene(19, 6000, 1.0, 0.01, 0.06, 0)
+    cams = gsr.orbit_cameras(16, 320, 240)
+    opt = gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 2)
+    g, e = gsr.Context(0), gsr.Context(0)
+    try:
+        e.set_graphs(False)
+        dg, de = g.upload(rec), e.upload(rec)
+        for i, cam in enumerate(cams + cams[:4]):
+            o = opt if i < 12 else gsr.RenderOptions(gsr.Backend.scalar, gsr.PrecisionMode.fp32, 1)
+            a = g.render(dg, cam, o)
+            b = e.render(de, cam, o)
+            assert np.array_equal(a.image.rgb.view(np.uint32), b.image.rgb.view(np.uint32)), i
+            assert a.entries == b.entries and a.ops == b.ops
+    finally:
+        g.close()
+        e.close()
+
+
+def test_encode_u8_matches_reference_ppm(gsr, port):
+    """tgs_encode_u8 (the device PPM payload) equals the reference's encode_ppm bytes
+    (scene_io.cpp:253-263: clamp, lrintf(v * 255)) for a rendered frame and for edge values."""
+    rec = port.gen_scene(20, 3000, 1.0, 0.01, 0.08, 0)
+    cam = gsr.make_camera(200, 150)
+    ctx = gsr.default_context(0)
+    res = ctx.render(ctx.upload(rec), cam, gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 2))
+    got = ctx.encode_u8(ctx.image_device_ptr(), res.image.rgb.size)
+    assert np.array_equal(got.reshape(res.image.rgb.shape), port.encode_ppm(res.image.rgb))
+    # half-way and out-of-range values through a device buffer
+    import torch
+    vals = np.array([0.5 / 255, 1.5 / 255, 2.5 / 255, 254.5 / 255, -0.1, 1.2, 0.0, 1.0, 0.2], np.float32)
+    img = np.tile(vals, 3).reshape(1, 9, 3).astype(np.float32)
+    dev = torch.from_numpy(img).cuda()
+    got = ctx.encode_u8(dev.data_ptr(), img.size)
+    torch.cuda.synchronize()
+    assert np.array_equal(got, port.encode_ppm(img).reshape(-1))

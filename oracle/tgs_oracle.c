@@ -782,3 +782,48 @@ int tor_reference_render(const tor_projected* p, int64_t n, int width, int heigh
 void tor_encode_ppm(const float* rgb, int64_t n_floats, uint8_t* out) {
     for (int64_t i = 0; i < n_floats; ++i) out[i] = (uint8_t)lrintf(clamp01(rgb[i]) * 255.0f);
 }
+
+/* glibc 2.39 expf restated (the algorithm the GPU exact-emulation rasteriser runs in
+ * paper_2605_17855_b200/csrc/tgs_expf.cuh): k = round(x 32/ln2) by the 0x1.8p52 shift, a 32-entry
+ * 2^(i/32) table, a cubic in double precision.  tests/test_oracle.py compares it with this host's
+ * libm expf over a dense sweep of the negative floats. */
+static double tor_asdouble(uint64_t u) { double d; memcpy(&d, &u, 8); return d; }
+static uint64_t tor_asuint64(double d) { uint64_t u; memcpy(&u, &d, 8); return u; }
+float tor_expf_glibc(float x) {
+    static uint64_t tab[32];
+    static int init = 0;
+    if (!init) {
+        for (int i = 0; i < 32; ++i) tab[i] = tor_asuint64(exp2((double)i / 32)) - ((uint64_t)i << 47);
+        init = 1;
+    }
+    if (x < -0x1.9fe368p6f) return 0.0f;
+    const double inv = 0x1.71547652b82fep+0 * 32.0, shift = 0x1.8p+52;
+    const double c0 = 0x1.c6af84b912394p-5 / 32.0 / 32.0 / 32.0, c1 = 0x1.ebfce50fac4f3p-3 / 32.0 / 32.0,
+                 c2 = 0x1.62e42ff0c52d6p-1 / 32.0;
+    const double z = inv * (double)x;
+    double kd = z + shift;
+    const uint64_t ki = tor_asuint64(kd);
+    kd -= shift;
+    const double r = z - kd;
+    const double s = tor_asdouble(tab[ki % 32] + (ki << 47));
+    const double zz = c0 * r + c1, r2 = r * r;
+    double y = c2 * r + 1.0;
+    y = zz * r2 + y;
+    return (float)(y * s);
+}
+
+/* count of floats x = -(bits of step*k) in [lo_bits, hi_bits] where tor_expf_glibc(x) != expf(x) */
+int64_t tor_expf_sweep(uint32_t lo_bits, uint32_t hi_bits, uint32_t step, float* first_bad) {
+    int64_t bad = 0;
+    for (uint64_t u = lo_bits; u <= hi_bits; u += step) {
+        float x;
+        const uint32_t b = (uint32_t)u;
+        memcpy(&x, &b, 4);
+        const float a = tor_expf_glibc(x), e = expf(x);
+        if (memcmp(&a, &e, 4) != 0) {
+            if (!bad && first_bad) *first_bad = x;
+            ++bad;
+        }
+    }
+    return bad;
+}

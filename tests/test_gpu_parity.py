@@ -107,19 +107,19 @@ def test_reuse_report_vs_golden_masks(gsr, ctx, golden, name, group):
 @pytest.mark.parametrize("name", list(CASES))
 @pytest.mark.parametrize("backend,group,mode,tag", [
     (0, 1, 0, "scalar_g1"), (1, 1, 0, "tensor_g2"), (1, 2, 0, "tensor_g2"), (1, 4, 0, "tensor_g2"),
-    (1, 2, 1, "tensor_g2"), (1, 4, 1, "tensor_g4_fp16")])
+    (1, 2, 1, "tensor_g4_fp16"), (1, 4, 1, "tensor_g4_fp16"), (0, 1, 1, "tensor_g4_fp16")])
 def test_image_within_tolerance_vs_golden(gsr, ctx, golden, name, backend, group, mode, tag):
     g = golden[name]
     cam = _cam(gsr, CASES[name]["camera"]())
     ds = ctx.upload(g["records"])
     res = ctx.render(ds, cam, _opt(gsr, backend, group, mode))
     ref = g[f"img_{tag}"]
-    if tag == "tensor_g4_fp16":
-        # the reference's emulated fp16 mode differs from its own fp32 image (PSNR >= 40 dB is its
-        # bar, acceptance.cpp:313-336); our fp16 mode runs the same hi/lo contraction as fp32, so
-        # it must meet the fp32 bar against the fp32 image and the reference's bar against fp16.
-        check_image(res.image.rgb, g["img_tensor_g2"], f"{name} fp16 vs fp32")
-        assert gsr.psnr(res.image.rgb, ref) >= 40.0
+    if mode == 1:
+        # fp16 mode runs the exact emulation of the reference's fp16 lanes: bit for bit, for every
+        # backend and G (the reference's fp16 image is G- and backend-invariant itself,
+        # test_raster_tensor.cpp:159-165 and acceptance.cpp:199-238)
+        assert np.array_equal(res.image.rgb.view(np.uint32), ref.astype(np.float32).view(np.uint32))
+        assert gsr.psnr(res.image.rgb, g["img_tensor_g2"]) >= 40.0  # the reference's fp16 bar
     else:
         check_image(res.image.rgb, ref, f"{name} b{backend} g{group} m{mode}")
 
@@ -348,3 +348,47 @@ def test_c3_full_size_properties(gsr, ctx, port):
         assert int(pc) == app
         img = res.image.rgb
         assert np.isfinite(img).all() and img.min() >= 0 and img.max() <= 1
+
+
+# ---------------------------------------------------------------------------------------------
+# Exact-emulation rasteriser: images BIT-EXACT with the reference build (golden fixtures made by
+# oracle/_ref) in fp16 mode (PrecisionMode::fp16 always runs it) and in fp32 mode with
+# tgs_set_exact_emulation — the reference's own acceptance invariants (scalar == tensor, any G,
+# acceptance.cpp:177-238) make one exact kernel cover every backend/G combination.
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("render", ["scalar_g1", "tensor_g2", "tensor_g4_fp16"])
+def test_exact_emulation_bit_exact_vs_reference(gsr, golden, name, render):
+    case, gold = CASES[name], golden[name]
+    c = case["camera"]()
+    r = case["renders"][render]
+    ctx = gsr.Context(0)
+    try:
+        ctx.set_exact_emulation(True)
+        res = ctx.render(ctx.upload(gold["records"]), _cam(gsr, c),
+                         _opt(gsr, r["backend"], r["group_size"], r["mode"]))
+        ref = gold[f"img_{render}"]
+        assert np.array_equal(res.image.rgb.view(np.uint32), ref.astype(np.float32).view(np.uint32)), \
+            f"{name} {render}: {np.count_nonzero(res.image.rgb != ref)} pixels differ"
+    finally:
+        ctx.close()
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_exact_emulation_matches_port_every_group(gsr, port, mode):
+    """Fresh seeds: the exact kernel equals the C restatement (itself pinned to the reference) for
+    G = 1, 2, 4, both precision modes, bit for bit."""
+    rec = port.gen_scene(31, 2500, 1.0, 0.01, 0.08, 5 if mode else 0)
+    c = rotated_camera(176, 136)
+    ctx = gsr.Context(0)
+    try:
+        ctx.set_exact_emulation(True)
+        ds = ctx.upload(rec)
+        proj, _ = port.project(rec, c)
+        for g in (1, 2, 4):
+            backend = 0 if g == 1 else 1
+            res = ctx.render(ds, _cam(gsr, c), _opt(gsr, backend, g, mode))
+            ent, off, _ = port.bin_sort(proj, c.width, c.height, g)
+            img, _ = port.rasterize(ent, off, proj, c.width, c.height, backend=backend, group_size=g, mode=mode)
+            assert np.array_equal(res.image.rgb.view(np.uint32), img.astype(np.float32).view(np.uint32)), (mode, g)
+    finally:
+        ctx.close()

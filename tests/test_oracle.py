@@ -128,3 +128,19 @@ def test_fast_bin_sort_matches_reference_build(port, ref):
         ea, oa, xa = ref.bin_sort(pp, cam.width, cam.height, g)
         eb, ob, xb = port.bin_sort_fast(pp, cam.width, cam.height, g)
         assert np.array_equal(_bits(ea), _bits(eb)) and np.array_equal(oa, ob) and xa == xb
+
+
+def test_expf_restatement_matches_libm(port):
+    """The glibc expf restatement the exact-emulation rasteriser runs on the GPU equals this host's
+    libm expf on every 7th negative float down to -88 (the full sweep, every float, differs in one
+    input, x = -0x1.f8cbb2p+5, whose exp is ~1e-28 — far below any alpha_skip threshold)."""
+    import ctypes as C
+    f = port.lib.tor_expf_sweep
+    f.restype = C.c_int64
+    f.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_float)]
+    first = C.c_float(0)
+    # -0.0 .. -88.0 (0x80000000 .. 0xC2B00000), stride 7
+    bad = f(0x80000000, 0xC2B00000, 7, C.byref(first))
+    assert bad <= 1, (bad, first.value)
+    # the range every alpha >= 1/255 evaluation lives in (power >= ln(1/255) ~ -5.55), every float
+    assert f(0x80000000, 0xC0B20000, 1, C.byref(first)) == 0

@@ -9,3 +9,4 @@ timeout 600 python bench.py --mode bands --steps 5 --warmup 3 > $O/bench_bands.j
 TGS_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29531 bench.py --gpus 2 --steps 6 --warmup 3 --quick > $O/bench_2rank.json 2> $O/bench_2rank.err; tail -2 $O/bench_2rank.err
 TGS_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29532 bench.py --gpus 2 --mode bands --steps 3 --warmup 3 > $O/bench_bands_2rank.json 2> $O/bench_bands_2rank.err; tail -2 $O/bench_bands_2rank.err
 ls -la $O
+timeout 900 python bench.py --mode configs --steps 10 --warmup 3 > $O/bench_configs.jsonl 2> $O/bench_configs.err; tail -2 $O/bench_configs.err

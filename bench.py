@@ -97,12 +97,20 @@ class ClockSampler:
                 self._nv = None if self._nv else self._nv
             self._stop.wait(0.0005 if self._nv else 0.2)
 
+    def _sample_once(self):
+        try:
+            self.samples.append(self._sample_nvml() if self._nv else self._sample_smi())
+        except Exception:
+            pass
+
     def __enter__(self):
+        self._sample_once()  # the timed region can be ~20 ms: bracket it with synchronous samples
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
 
     def __exit__(self, *a):
+        self._sample_once()
         self._stop.set()
         self._t.join(timeout=10)
 

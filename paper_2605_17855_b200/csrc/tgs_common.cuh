@@ -37,6 +37,10 @@ struct DevScene {
     int sh_degree;
 };
 
+#ifndef TGS_RR_PLANE
+#define TGS_RR_PLANE 1  // preprocess writes the raster record plane (DevProjected::rr)
+#endif
+
 // Projected splats, indexed by the compacted (project_scene output) index.
 struct DevProjected {
     float4* mc;   // mean2d.x, mean2d.y, conic_a, conic_b

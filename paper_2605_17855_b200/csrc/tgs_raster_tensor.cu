@@ -125,10 +125,21 @@ struct Smem {
 // Pixel (relative to the unit's top-left) of row l of M-tile m = 2 t + k: member tile t, its
 // 8-column half k; lane quadrant q = l / 32 covers tile rows 4q..4q+3, so warp q of a warpgroup
 // owns a 16x4 pixel strip of its tile (two 8x4 blocks, one per M-tile).
+#ifndef TGS_RR_PLANE
+#define TGS_RR_PLANE 1  // the producer reads the preprocess's raster record (tight rect, log2 o)
+#endif
+#ifndef TGS_RASTER_BLOCK8
+#define TGS_RASTER_BLOCK8 0
+#endif
 __device__ __forceinline__ void lane_pixel(int m, int l, int& x, int& y) {
     const int t = m >> 1, k = m & 1, q = l >> 5, i = l & 31;
-    x = (t & 1) * 16 + k * 8 + (i & 7);
-    y = (t >> 1) * 16 + q * 4 + (i >> 3);
+    if (TGS_RASTER_BLOCK8) {  // warp q: the 8x8 block q of its tile, M-tile k = rows 4k..4k+3 of it
+        x = (t & 1) * 16 + (q & 1) * 8 + (i & 7);
+        y = (t >> 1) * 16 + (q >> 1) * 8 + k * 4 + (i >> 3);
+    } else {
+        x = (t & 1) * 16 + k * 8 + (i & 7);
+        y = (t >> 1) * 16 + q * 4 + (i >> 3);
+    }
 }
 
 // byte offset of (row, k-half) in a K-major no-swizzle operand: 8x16B core matrices
@@ -374,7 +385,7 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                     ptx::cp_async16(&sm.rmc[r][lane], &a.proj.mc[idx]);
                     ptx::cp_async16(&sm.rco[r][lane], &a.proj.co[idx]);
                     ptx::cp_async16(&sm.rcol[r][lane], &a.proj.col[idx]);
-                    ptx::cp_async16(&sm.rrr[r][lane], &a.proj.rr[idx]);
+                    if (TGS_RR_PLANE) ptx::cp_async16(&sm.rrr[r][lane], &a.proj.rr[idx]);
                 }
             };
             struct Rec {
@@ -434,7 +445,8 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                     // record carries that tight rect (preprocess); without the cull, the 3-sigma rect
                     int x0, y0, x1, y1;
                     float cj, lo2;
-                    if (a.tile_cull) {
+                    uint32_t tight = 0xfu;
+                    if (TGS_RR_PLANE && a.tile_cull) {
                         x0 = (int)(cur.rr.x & 0xffffu), x1 = (int)(cur.rr.x >> 16);
                         y0 = (int)(cur.rr.y & 0xffffu), y1 = (int)(cur.rr.y >> 16);
                         lo2 = __uint_as_float(cur.rr.z);
@@ -443,6 +455,7 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                         tile_rect(cur.mc.x, cur.mc.y, __float_as_int(cur.co.w), gg.tiles_x, gg.tiles_y, x0, y0, x1, y1);
                         lo2 = lg2_approx(cur.co.y);
                         cj = fminf(clampv, cur.co.y);
+                        if (a.tile_cull) tight = tight_cover(cur.mc.x, cur.mc.y, cur.col.w, ug.tx0, ug.ty0, SLOTS);
                     }
                     uint32_t cover = 0;
 #pragma unroll
@@ -450,7 +463,7 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                         const int tx = ug.tx0 + (k & 1), ty = ug.ty0 + (k >> 1);
                         if (tx >= x0 && tx <= x1 && ty >= y0 && ty <= y1) cover |= 1u << k;
                     }
-                    cover &= live;
+                    cover &= live & tight;
                     if (cover != 0u && !(cj < skip)) {
                         bt.keep = make_row(cur.mc.x, cur.mc.y, cur.mc.z, cur.mc.w, cur.co.x, lo2, ox, oy, cover, bt.r0,
                                            bt.r1);

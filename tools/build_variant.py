@@ -14,16 +14,20 @@ from paper_2605_17855_b200 import build as B  # noqa: E402
 
 
 def main():
-    name, src, *extra = sys.argv[1:]
+    name, srcs, *extra = sys.argv[1:]
+    srcs = srcs.split(",")  # one or more sources (comma-separated) rebuilt with the extra flags
     B.build()
     out_dir = os.path.join(B.HERE, "variants")
     os.makedirs(out_dir, exist_ok=True)
-    obj = os.path.join(out_dir, f"{name}_{src}.o")
-    cmd = [B.NVCC, *B.ARCH, *B.NVFLAGS, *extra, "-c", os.path.join(B.CSRC, src), "-o", obj]
-    subprocess.run(cmd, check=True)
-    objs = [o for o in sorted(glob.glob(os.path.join(B.OBJ, "*.o"))) if os.path.basename(o) != src + ".o"]
+    vobjs = []
+    for src in srcs:
+        obj = os.path.join(out_dir, f"{name}_{src}.o")
+        cmd = [B.NVCC, *B.ARCH, *B.NVFLAGS, *extra, "-c", os.path.join(B.CSRC, src), "-o", obj]
+        subprocess.run(cmd, check=True)
+        vobjs.append(obj)
+    objs = [o for o in sorted(glob.glob(os.path.join(B.OBJ, "*.o"))) if os.path.basename(o)[:-2] not in srcs]
     lib = os.path.join(out_dir, f"libtgs_{name}.so")
-    subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", lib, obj, *objs, "-lcudart"], check=True)
+    subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", lib, *vobjs, *objs, "-lcudart"], check=True)
     print(lib)
 
 

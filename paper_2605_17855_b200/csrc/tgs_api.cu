@@ -200,7 +200,6 @@ DevProjected dev_proj(tgs_ctx* ctx) {
     p.mc = b;
     p.co = b + ctx->proj_cap;
     p.col = b + 2 * ctx->proj_cap;
-    p.rr = reinterpret_cast<uint4*>(b + 3 * ctx->proj_cap);
     return p;
 }
 
@@ -248,7 +247,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
 
     // ---- buffers ----
     if (ctx->proj_cap < n_alloc) {
-        TGS_CUDA_OK(ctx->proj.ensure((size_t)n_alloc * 4 * sizeof(float4)));
+        TGS_CUDA_OK(ctx->proj.ensure((size_t)n_alloc * 3 * sizeof(float4)));
         ctx->proj_cap = n_alloc;
     }
     for (int i = 0; i < 2; ++i) {
@@ -390,7 +389,6 @@ tgs_status record_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* 
     pa.gg = gg;
     pa.fc = fc;
     pa.alpha_skip = opt->alpha_skip;
-    pa.alpha_clamp = opt->alpha_clamp;
     launch_preprocess(pa, s);
     TGS_CUDA_OK(cudaGetLastError());
     TGS_CUDA_OK(record_event(ctx->ev[1], s));
@@ -756,7 +754,7 @@ tgs_status tgs_group_row_entries(tgs_ctx* ctx, const tgs_scene* scene, const tgs
     if (!counts || cap < gg.groups_y) return TGS_OK;
     const int64_t na = std::max<int64_t>(scene->n, 1);
     if (ctx->proj_cap < na) {
-        TGS_CUDA_OK(ctx->proj.ensure((size_t)na * 4 * sizeof(float4)));
+        TGS_CUDA_OK(ctx->proj.ensure((size_t)na * 3 * sizeof(float4)));
         ctx->proj_cap = na;
     }
     TGS_CUDA_OK(ctx->pre_keys[0].ensure((size_t)na * 4));
@@ -773,7 +771,6 @@ tgs_status tgs_group_row_entries(tgs_ctx* ctx, const tgs_scene* scene, const tgs
     pa.gg = gg;
     pa.fc = fc;
     pa.alpha_skip = opt->alpha_skip;
-    pa.alpha_clamp = opt->alpha_clamp;
     launch_preprocess(pa, ctx->stream);
     launch_row_entries(ctx->rect.as<uint2>(), &fc->n_input, gg, ctx->stg[6].as<unsigned long long>(), ctx->stream);
     TGS_CUDA_OK(cudaGetLastError());
@@ -1070,7 +1067,7 @@ tgs_status tgs_project_scene(tgs_ctx* ctx, const float* records, int64_t count, 
     if (st != TGS_OK) return st;
     const int64_t na = std::max<int64_t>(count, 1);
     if (ctx->proj_cap < na) {
-        TGS_CUDA_OK(ctx->proj.ensure((size_t)na * 4 * sizeof(float4)));
+        TGS_CUDA_OK(ctx->proj.ensure((size_t)na * 3 * sizeof(float4)));
         ctx->proj_cap = na;
     }
     TGS_CUDA_OK(ctx->pre_keys[0].ensure((size_t)na * 4));
@@ -1088,7 +1085,6 @@ tgs_status tgs_project_scene(tgs_ctx* ctx, const float* records, int64_t count, 
     pa.gg = gg;
     pa.fc = fc;
     pa.alpha_skip = 1.0f / 255.0f;
-    pa.alpha_clamp = 0.99f;
     launch_preprocess(pa, ctx->stream);
     TGS_CUDA_OK(cudaGetLastError());
     TGS_CUDA_OK(cudaMemcpyAsync(ctx->h_fc, fc, sizeof(FrameCounters), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1223,7 +1219,7 @@ tgs_status tgs_rasterize_lists(tgs_ctx* ctx, const tgs_group_entry* entries, int
     cudaSetDevice(ctx->device);
     const int64_t na = std::max<int64_t>(n, 1);
     if (ctx->proj_cap < na) {
-        TGS_CUDA_OK(ctx->proj.ensure((size_t)na * 4 * sizeof(float4)));
+        TGS_CUDA_OK(ctx->proj.ensure((size_t)na * 3 * sizeof(float4)));
         ctx->proj_cap = na;
     }
     tgs_projected* dp = nullptr;
@@ -1242,7 +1238,7 @@ tgs_status tgs_rasterize_lists(tgs_ctx* ctx, const tgs_group_entry* entries, int
     TGS_CUDA_OK(cudaMemsetAsync(fc, 0, offsetof(FrameCounters, sticky_overflow), ctx->stream));
     TGS_CUDA_OK(cudaMemsetAsync(flags, 0, 4, ctx->stream));
     const DevProjected planes = dev_proj(ctx);
-    launch_projected_to_planes(dp, n, opt->alpha_skip, opt->alpha_clamp, gg, planes, ctx->stream);
+    launch_projected_to_planes(dp, n, opt->alpha_skip, planes, ctx->stream);
     launch_lists_check(de, doff, ng, dp, n, gg, ctx->list.as<uint32_t>(), flags, ctx->stream);
     uint32_t hflags = 0;
     TGS_CUDA_OK(cudaMemcpyAsync(&hflags, flags, 4, cudaMemcpyDeviceToHost, ctx->stream));

@@ -37,17 +37,11 @@ struct DevScene {
     int sh_degree;
 };
 
-#ifndef TGS_RR_PLANE
-#define TGS_RR_PLANE 1  // preprocess writes the raster record plane (DevProjected::rr)
-#endif
-
 // Projected splats, indexed by the compacted (project_scene output) index.
 struct DevProjected {
     float4* mc;   // mean2d.x, mean2d.y, conic_a, conic_b
     float4* co;   // conic_c, opacity, depth, radius (int bits)
     float4* col;  // color r, g, b, tile-cull extents (half2, tight_extents)
-    uint4* rr;    // raster record of the tensor producer: tight tile rect x0 | x1 << 16,
-                  // y0 | y1 << 16 (x0 > x1: none), log2(opacity), min(alpha_clamp, opacity)
 };
 
 // Device counters / flags of one frame (zeroed per frame).
@@ -190,22 +184,6 @@ __device__ __forceinline__ void tight_span(float m, float e, int lo3, int hi3, i
     hi = min(hi3, (int)floorf((m + e - 0.5f) * 0.0625f));
     if (hi < hi3 && m + e >= (float)((hi + 1) * kTile) + 0.5f) ++hi;
     while (hi >= lo && !(m + e >= (float)(hi * kTile) + 0.5f)) --hi;
-}
-
-// Raster record (DevProjected::rr) of a projected splat: its tight tile rect (tight_span in x and
-// y, inside the 3-sigma rect), log2(opacity) and min(alpha_clamp, opacity).
-__device__ __forceinline__ uint4 raster_record(float mx, float my, float ext, float opacity, float alpha_clamp,
-                                               int x0, int y0, int x1, int y1) {
-    const uint32_t eb = __float_as_uint(ext);
-    const float2 e = __half22float2(*reinterpret_cast<const __half2*>(&eb));
-    int a0 = 1, a1 = 0, b0 = 1, b1 = 0;
-    if (x1 >= x0 && y1 >= y0) {
-        tight_span(mx, e.x, x0, x1, a0, a1);
-        tight_span(my, e.y, y0, y1, b0, b1);
-    }
-    if (a1 < a0 || b1 < b0) a0 = 1, a1 = 0, b0 = 1, b1 = 0;
-    return make_uint4((uint32_t)a0 | ((uint32_t)a1 << 16), (uint32_t)b0 | ((uint32_t)b1 << 16),
-                      __float_as_uint(lg2_approx(opacity)), __float_as_uint(fminf(alpha_clamp, opacity)));
 }
 
 }  // namespace tgs

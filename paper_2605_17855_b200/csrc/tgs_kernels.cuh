@@ -15,7 +15,6 @@ struct PreprocessArgs {
     GroupGeom gg;
     FrameCounters* fc;
     float alpha_skip;              // for the tile-cull extents stored in col.w (tight_extents)
-    float alpha_clamp;             // for the raster record (DevProjected::rr)
 };
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t st);
 // the preprocess kernel's entry (CUDA-graph frames update its camera argument per launch)
@@ -128,8 +127,8 @@ void launch_gather_entries(const tgs_keyed_entry* e, const uint32_t* perm, uint3
                            uint32_t* gid_sorted, cudaStream_t st);
 void launch_offsets_from_sorted(const uint32_t* gid, uint32_t n, uint32_t n_groups, uint32_t* offsets,
                                 cudaStream_t st);
-void launch_projected_to_planes(const tgs_projected* p, int64_t n, float alpha_skip, float alpha_clamp,
-                                const GroupGeom& gg, DevProjected out, cudaStream_t st);
+void launch_projected_to_planes(const tgs_projected* p, int64_t n, float alpha_skip, DevProjected out,
+                                cudaStream_t st);
 // entries per group row of the frame whose splat rects are in `rect` (n = &fc->n_input)
 void launch_row_entries(const uint2* rect, const uint32_t* n, const GroupGeom& gg, unsigned long long* rows,
                         cudaStream_t st);

@@ -244,9 +244,6 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int i, f
             a.depth_keys[i] = __float_as_uint(pr.depth);
             int tx0, ty0, tx1, ty1, gx0, gy0, gx1, gy1;
             const int ng = group_rect(pr.mx, pr.my, pr.radius, a.gg, tx0, ty0, tx1, ty1, gx0, gy0, gx1, gy1);
-#if TGS_RR_PLANE
-            a.out.rr[i] = raster_record(pr.mx, pr.my, ext, po.w, a.alpha_clamp, tx0, ty0, tx1, ty1);
-#endif
             // tile rectangle (binning.cpp:32-44) for the group counting sort; empty -> x0 > x1
             a.rect[i] = (tx1 >= tx0 && ty1 >= ty0)
                             ? make_uint2((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16))

@@ -38,6 +38,9 @@ constexpr int kRadix = 256;
 #define TGS_SWEEP_BLOCKS 3
 #endif
 constexpr int kSweepBlocks = 148 * TGS_SWEEP_BLOCKS;  // persistent one-sweep blocks
+#ifndef TGS_SORT_WIN
+#define TGS_SORT_WIN 8  // look-back predecessors read per round trip
+#endif
 
 
 constexpr uint32_t kFlagAgg = 1u << 30;  // look-back status: tile aggregate published
@@ -212,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
         // kWin predecessors per round trip (independent loads)
         uint32_t prefix = 0;
         if (tile > 0) {
-            constexpr int kWin = 8;
+            constexpr int kWin = TGS_SORT_WIN;
             int j = (int)tile - 1;
             const long long w0 = clock64();
             for (;;) {

@@ -96,16 +96,13 @@ __global__ void offsets_from_sorted_kernel(const uint32_t* __restrict__ gid, uin
 // Caller-provided ProjectedGaussian records -> the rasterisers' SoA planes (mc, co, col; col.w =
 // the tile-cull extents, as preprocess_kernel stores them).
 __global__ void projected_to_planes_kernel(const tgs_projected* __restrict__ p, int64_t n, float alpha_skip,
-                                           float alpha_clamp, GroupGeom gg, DevProjected out) {
+                                           DevProjected out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const tgs_projected r = p[i];
         const float ext = tight_extents(r.conic[0], r.conic[1], r.conic[2], r.opacity, alpha_skip);
         out.mc[i] = make_float4(r.mean2d[0], r.mean2d[1], r.conic[0], r.conic[1]);
         out.co[i] = make_float4(r.conic[2], r.opacity, r.depth, __int_as_float(r.radius));
         out.col[i] = make_float4(r.color[0], r.color[1], r.color[2], ext);
-        int x0, y0, x1, y1;
-        tile_rect(r.mean2d[0], r.mean2d[1], r.radius, gg.tiles_x, gg.tiles_y, x0, y0, x1, y1);
-        out.rr[i] = raster_record(r.mean2d[0], r.mean2d[1], ext, r.opacity, alpha_clamp, x0, y0, x1, y1);
     }
 }
 
@@ -191,9 +188,9 @@ void launch_offsets_from_sorted(const uint32_t* gid, uint32_t n, uint32_t n_grou
                                 cudaStream_t st) {
     offsets_from_sorted_kernel<<<kBlocks, 256, 0, st>>>(gid, n, n_groups, offsets);
 }
-void launch_projected_to_planes(const tgs_projected* p, int64_t n, float alpha_skip, float alpha_clamp,
-                                const GroupGeom& gg, DevProjected out, cudaStream_t st) {
-    if (n > 0) projected_to_planes_kernel<<<kBlocks, 256, 0, st>>>(p, n, alpha_skip, alpha_clamp, gg, out);
+void launch_projected_to_planes(const tgs_projected* p, int64_t n, float alpha_skip, DevProjected out,
+                                cudaStream_t st) {
+    if (n > 0) projected_to_planes_kernel<<<kBlocks, 256, 0, st>>>(p, n, alpha_skip, out);
 }
 void launch_lists_check(const tgs_group_entry* e, const uint32_t* offsets, int n_groups, const tgs_projected* proj,
                         int64_t n_proj, const GroupGeom& gg, uint32_t* list, uint32_t* flags, cudaStream_t st) {

@@ -41,9 +41,6 @@ constexpr int kRowChunks = 148 * 128;  // level-1 chunks (contiguous rank ranges
 #define TGS_STAGE1_WIDE 8192
 #endif
 constexpr int stage1_entries(int kr) { return kr <= 2 ? TGS_STAGE1 : TGS_STAGE1_WIDE; }
-#ifndef TGS_COLS_V1
-#define TGS_COLS_V1 0
-#endif
 #ifndef TGS_SLICE_LEN
 #define TGS_SLICE_LEN 128
 #endif
@@ -417,163 +414,6 @@ __global__ void offsets_kernel(BinArgs a) {
         a.offsets[g] = v;
     }
 }
-
-#if TGS_COLS_V1
-// Group placement.  A block takes one segment (kBinWarps slices of kSliceLen row entries, one per
-// warp); the segment's run of column x is one contiguous global range [base_x, base_x + len_x),
-// inside which warp w's part starts after the parts of warps < w (per-slice column counts, made
-// here in shared memory).  Lane per entry: each lane marks the columns of its entry in a per-warp
-// column bitmask; the entry's slot in column c is the column's running position plus the number of
-// earlier lanes (= earlier entries) that also cover c; after each 32-entry chunk every column
-// advances by its mask's population.  Slots are in the block's shared output buffer (with each
-// slot's column id), flushed with one flat coalesced pass; a block whose output exceeds the buffer
-// writes global slots.
-template <int KC>
-__global__ void __launch_bounds__(kBinWarps * 32) cols_place_v1_kernel(BinArgs a) {
-    constexpr int kPer = kSliceLen / 32;  // row entries per lane
-    // [stage2_entries(KC)] output | [same] u16 column ids | [gx + 1] column global bias |
-    // [kBinWarps][gx + 1] slice counts, column positions, column masks
-    extern __shared__ uint32_t sout[];
-    if (a.fc->overflow) return;
-    const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const uint32_t lanebit = 1u << lane, lt = lanebit - 1u;
-    const uint32_t* rowstart = a.meta;
-    const uint32_t* nsegp = a.meta + rows + 1;
-    const uint32_t* rowbase2 = a.meta + 2 * rows + 2;
-    const uint32_t nq = nsegp[rows], h2 = rowbase2[rows], total = a.fc->n_entries;
-    constexpr int kStage2 = stage2_entries(KC);
-    uint16_t* scol = reinterpret_cast<uint16_t*>(sout + kStage2);
-    uint32_t* gbias = sout + kStage2 + kStage2 / 2;
-    int* cntw = reinterpret_cast<int*>(gbias + gx + 1);
-    int* D = cntw + wib * (gx + 1);
-    uint32_t* cpos = reinterpret_cast<uint32_t*>(cntw) + (kBinWarps + wib) * (gx + 1);
-    uint32_t* cmask = cpos + kBinWarps * (gx + 1);
-    uint32_t* list = a.list;
-    const uint32_t out0 = smem_u32(sout), col0 = smem_u32(scol);
-    auto h2at = [&](uint32_t i) { return i < h2 ? a.hist2[i] : total; };
-    // the segment's group row comes from cols_count's map, loaded one segment ahead
-    uint32_t ynext = blockIdx.x < nq ? __ldg(&a.segmap[blockIdx.x]) : 0u;
-    for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
-        const int y = (int)ynext;
-        if (q + gridDim.x < nq) ynext = __ldg(&a.segmap[q + gridDim.x]);
-        const uint32_t s = q - nsegp[y];
-        const uint32_t nseg = nsegp[y + 1] - nsegp[y];
-        const uint32_t se0 = rowstart[y] + s * kSegLen, se1 = min(rowstart[y + 1], se0 + kSegLen);
-        const uint32_t e0 = min(se1, se0 + (uint32_t)wib * kSliceLen), e1 = min(se1, e0 + kSliceLen);
-        // column runs of the segment, [base, base + len) globally (loads in flight during the counts)
-        uint32_t base[KC], len[KC];
-#pragma unroll
-        for (int k = 0; k < KC; ++k) {
-            const int x = lane + 32 * k;
-            const uint32_t i0 = rowbase2[y] + (uint32_t)x * nseg + s;
-            base[k] = x < gx ? h2at(i0) : 0u;
-            len[k] = x < gx ? h2at(i0 + 1) : 0u;
-        }
-        // this warp's slice, loaded once: per-column counts (difference array -> prefix)
-        uint2 ent[kPer];
-#pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-            const uint32_t e = e0 + lane + 32u * i;
-            ent[i] = e < e1 ? __ldg(&a.rowlist[e]) : make_uint2(0u, 0u);
-        }
-        for (int i = lane; i <= gx; i += 32) D[i] = 0;
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < kPer; ++i)
-            if (e0 + lane + 32u * i < e1) {
-                atomicAdd(&D[ent[i].y & 0xffffu], 1);
-                atomicAdd(&D[(ent[i].y >> 16) + 1], -1);
-            }
-        __syncwarp();
-        {
-            int run = 0;
-            for (int b0 = 0; b0 < gx; b0 += 32) {
-                const int x = b0 + lane;
-                int incl = x < gx ? D[x] : 0;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += t;
-                }
-                if (x < gx) D[x] = run + incl;
-                run += __shfl_sync(0xffffffffu, incl, 31);
-            }
-        }
-        __syncthreads();
-        // local start P of every column run; this warp's part starts off after earlier warps'
-        uint32_t P[KC], off[KC], carry = 0;
-#pragma unroll
-        for (int k = 0; k < KC; ++k) {
-            const int x = lane + 32 * k;
-            len[k] -= base[k];
-            off[k] = 0u;
-            if (x < gx)
-                for (int w = 0; w < wib; ++w) off[k] += (uint32_t)cntw[w * (gx + 1) + x];
-            uint32_t incl = len[k];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            P[k] = carry + incl - len[k];
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        const bool staged = carry <= (uint32_t)kStage2;  // block-uniform
-#pragma unroll
-        for (int k = 0; k < KC; ++k) {
-            const int x = lane + 32 * k;
-            if (x < gx) {
-                cpos[x] = staged ? P[k] + off[k] : base[k] + off[k];
-                cmask[x] = 0u;
-                if (wib == 0) gbias[x] = base[k] - P[k];
-            }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-            if (e0 + 32u * i >= e1) break;  // warp-uniform
-            const uint2 v = ent[i];
-            int x0 = 0, span = 0;
-            if (e0 + lane + 32u * i < e1) {
-                x0 = (int)(v.y & 0xffffu);
-                span = (int)(v.y >> 16) - x0 + 1;
-            }
-            const int ms = (int)__reduce_max_sync(0xffffffffu, (uint32_t)span);
-            for (int t = 0; t < ms; ++t)
-                if (t < span) atomicOr(&cmask[x0 + t], lanebit);
-            __syncwarp();
-            for (int t = 0; t < ms; ++t)
-                if (t < span) {
-                    const uint32_t p = cpos[x0 + t] + __popc(cmask[x0 + t] & lt);
-                    if (staged) {
-                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(out0 + 4u * p), "r"(v.x) : "memory");
-                        asm volatile("st.shared.u16 [%0], %1;" ::"r"(col0 + 2u * p), "h"((unsigned short)(x0 + t)) : "memory");
-                    } else {
-                        list[p] = v.x;
-                    }
-                }
-            __syncwarp();
-            // advance every column by its entries in this chunk (lane-owned columns, race-free)
-            for (int x = lane; x < gx; x += 32) {
-                const uint32_t m = cmask[x];
-                if (m) {
-                    cpos[x] += __popc(m);
-                    cmask[x] = 0u;
-                }
-            }
-            __syncwarp();
-        }
-        __syncthreads();
-        if (staged) {
-            // flush: one flat pass, slot j of column c goes to gbias[c] + j (coalesced runs)
-            for (uint32_t j = threadIdx.x; j < carry; j += kBinWarps * 32) list[gbias[scol[j]] + j] = sout[j];
-            __syncthreads();
-        }
-    }
-}
-
-#endif
 
 // Group placement.  A block takes one segment (kBinWarps slices of kSliceLen row entries, one per
 // warp); the segment's run of column x is one contiguous global range [base_x, base_x + len_x),
@@ -1014,14 +854,8 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     offsets_kernel<<<(gg.n_groups_band + 256) / 256, 256, 0, st>>>(a);
     const int kc = (gx + 31) / 32, t2 = kBinWarps * 32;
     // output stage + column ids, column bias, per-warp slice counts / column positions / masks
-#if TGS_COLS_V1
-    const size_t so = (size_t)stage2_entries(kc) * (sizeof(uint32_t) + sizeof(uint16_t)) +
-                      (size_t)(3 * kBinWarps + 1) * (gx + 1) * sizeof(int);
-#define cols_place_kernel cols_place_v1_kernel
-#else
     // output stage, per-warp slice counts / column positions / masks
     const size_t so = (size_t)stage2_entries(kc) * sizeof(uint32_t) + (size_t)3 * kBinWarps * (gx + 1) * sizeof(int);
-#endif
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)so);
         kern<<<qblocks, t2, so, st>>>(a);
@@ -1036,9 +870,6 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
         launch(cols_place_kernel<8>);
     else
         launch(cols_place_kernel<16>);
-#if TGS_COLS_V1
-#undef cols_place_kernel
-#endif
 }
 
 // ReuseReport of the last frame's group lists (metrics.cpp:45-57) without materialising masks: a

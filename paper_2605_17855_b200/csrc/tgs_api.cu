@@ -103,7 +103,7 @@ struct tgs_ctx {
     DBuf pre_keys[2], pre_vals[2];
     DBuf rect, rrect;   // tile rect per compacted splat / per rank
     DBuf list;          // sorted group lists (splat indices)
-    DBuf rowlist;       // group-row lists (binning level 1)
+    DBuf rowlist;       // group-row lists (binning level 1): splat-index plane, column-range plane
     DBuf hist, bsum;    // counting-sort [group][chunk] matrix and its scan block sums
     DBuf ghist, offsets, order;
     DBuf ucost;         // per unit, list entries the last frame walked (schedule feedback)
@@ -418,7 +418,8 @@ tgs_status record_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* 
     ba.hist2 = ba.hist1 + h1;
     ba.meta = ba.hist2 + h2;
     ba.segmap = ba.meta + bin_meta_elems(gg);
-    ba.rowlist = ctx->rowlist.as<uint2>();
+    ba.rowidx = ctx->rowlist.as<uint32_t>();
+    ba.rowxp = ba.rowidx + std::max<uint32_t>(ctx->capacity, 1u);  // the buffer holds 2 x max(capacity, 1) words
     ba.bsum = ctx->bsum.as<uint32_t>();
     ba.offsets = ctx->offsets.as<uint32_t>();
     ba.list = ctx->list.as<uint32_t>();

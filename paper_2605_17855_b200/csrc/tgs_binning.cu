@@ -9,15 +9,16 @@
 // overlapping it, built by two stable partitions that write each entry once (the level-1 count
 // also gathers the rank-ordered tile rectangles, 8 B per splat, for the placement pass):
 //   level 1: splats -> group-row lists.  Each warp owns a contiguous rank range (chunk); per-row
-//            counts (1D difference array) -> scan over (row, chunk) -> every lane owns some rows
-//            and appends the chunk's splats to them in rank order (8-byte row entries: splat
-//            index, column range);
+//            counts (1D difference array) -> scan over (row, chunk) -> the chunk's splats are
+//            appended to their rows in rank order (row entries: splat index, column range, in two
+//            4-byte planes);
 //   level 2: group-row lists -> group lists.  Each warp owns a segment of one row list; per-column
-//            counts -> scan over (row, column, segment) = group-major -> every lane owns some
-//            columns and appends the segment's splats to them in order.
-// The lane that owns a row / column appends sequentially, so order is stable by construction —
-// no atomics or match on the placement path, and every (row, chunk) / (group, segment) run is a
-// contiguous burst.  Entries carry only the splat index; the member-tile mask
+//            counts -> scan over (row, column, segment) = group-major -> the segment's entries are
+//            appended to their columns in order.
+// Placement is lane per item, 32 items at a time: an item's slot in row / column c is c's running
+// position plus the number of earlier lanes (earlier items) that also cover c, read from a per-warp
+// bitmask of c — so order is stable by construction, with no global atomics, and every
+// (row, chunk) / (group, segment) run is a contiguous burst.  Entries carry only the splat index; the member-tile mask
 // (binning.cpp:56-65) is a pure function of the splat's tile rectangle and the group, so
 // consumers recompute it.
 #include "tgs_common.cuh"
@@ -32,7 +33,10 @@ namespace tgs {
 namespace {
 
 constexpr int kBinWarps = 8;          // warps per binning block (one chunk / segment per warp)
-constexpr int kRowChunks = 148 * 128;  // level-1 chunks (contiguous rank ranges, one warp each)
+#ifndef TGS_ROW_CHUNKS
+#define TGS_ROW_CHUNKS (148 * 128)
+#endif
+constexpr int kRowChunks = TGS_ROW_CHUNKS;  // level-1 chunks (contiguous rank ranges, one warp each)
 // level-1 per-block output staging (row entries), smaller for few rows (more resident blocks)
 #ifndef TGS_STAGE1
 #define TGS_STAGE1 6144
@@ -106,16 +110,16 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_count_kernel(BinArgs a) {
     uint32_t r0, r1;
     chunk_range(*a.visible, kRowChunks, chunk, r0, r1);
     uint32_t ent = 0;
-    for (uint32_t rb = r0 + lane; rb < r1; rb += 32 * 4) {  // 4 gathers in flight per lane
-        uint2 rr[4];
+    for (uint32_t rb = r0 + lane; rb < r1; rb += 32 * 8) {  // 8 gathers in flight per lane
+        uint2 rr[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const uint32_t r = rb + 32u * u;
             // gather the rank-ordered rectangle once here (rows_place reads it back coalesced)
             rr[u] = r < r1 ? __ldg(&a.rect[__ldg(&a.sval[r])]) : make_uint2(0xffffu, 0u);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const uint32_t r = rb + 32u * u;
             if (r >= r1) continue;
             a.rrect[r] = rr[u];
@@ -187,31 +191,50 @@ __global__ void rows_meta_kernel(BinArgs a, const uint32_t* __restrict__ scan1_t
     }
 }
 
-// Bits [lo, hi] of the 32-row/column block k (bit i = row/column 32k + i); 0 if disjoint.
-__device__ __forceinline__ uint32_t range_mask(int lo, int hi, int k) {
-    const int a = max(lo - 32 * k, 0), b = min(hi - 32 * k, 31);
-    return a > b ? 0u : (0xffffffffu >> (31 - b)) & (0xffffffffu << a);
+// Predicated shared-memory reduction / stores (branch-free per-row / per-column loops).
+__device__ __forceinline__ void red_or_if(uint32_t addr, uint32_t v, bool on) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(addr),
+                 "r"(v), "r"((uint32_t)on)
+                 : "memory");
+}
+__device__ __forceinline__ void st_shared_if(uint32_t addr, uint32_t v, bool on) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}" ::"r"(addr),
+                 "r"(v), "r"((uint32_t)on)
+                 : "memory");
+}
+__device__ __forceinline__ void st_shared_v2_if(uint32_t addr, uint32_t x, uint32_t y, bool on) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t@p st.shared.v2.u32 [%0], {%1, %2};\n\t}" ::"r"(addr),
+                 "r"(x), "r"(y), "r"((uint32_t)on)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t ld_shared(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
 }
 
 // Row placement.  A block takes kBinWarps consecutive chunks (one per warp); in the [row][chunk]
-// layout the block's runs of row y are consecutive, i.e. one contiguous global range.  Lane l of
-// every warp owns rows l, l + 32, ... (KR per lane); the warp walks its chunk 32 splats at a time,
-// each lane staging its splat (index, column range, row masks) in shared memory, then splat by
-// splat (broadcast read) every owning lane appends the splat to its row — into the block's shared
-// output buffer at (row run start + the warp's offset in it); every row run is then flushed with
-// coalesced stores.  A block whose output exceeds the buffer writes to global slots directly.
+// layout the block's runs of row y are consecutive, i.e. one contiguous global range inside which
+// warp w's part starts after the parts of warps < w.  Lane per splat: the warp walks its chunk 32
+// splats at a time; each lane marks the group rows of its splat in a per-warp row bitmask, and the
+// splat's slot in row y is the row's running position plus the number of earlier lanes (= earlier
+// ranks) that also cover y; after each batch every row advances by its mask's population.  Slots
+// are in the block's shared output buffer, every row run is then flushed with coalesced stores.  A
+// block whose output exceeds the buffer writes to global slots directly.
 template <int KR>
 __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
-    constexpr int NW = (KR + 2 + 3) / 4;  // uint4 words per staged splat: idx, xp, KR masks
-    __shared__ uint4 stage[kBinWarps][32][NW];
     constexpr int kStage1 = stage1_entries(KR);
-    extern __shared__ uint2 sout1[];      // [kStage1]
+    // [kStage1] output (uint2) | [kBinWarps][rows + 1] row positions | [kBinWarps][rows + 1] row masks
+    extern __shared__ uint2 sout1[];
     if (a.fc->overflow) return;
     const int rows = a.gg.band_gy1 - a.gg.band_gy0;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int c0 = blockIdx.x * kBinWarps, chunk = c0 + wib;
-    const uint32_t lanebit = 1u << lane;
+    const uint32_t lanebit = 1u << lane, lt = lanebit - 1u;
     const uint32_t total = a.meta[rows];  // row entries
+    uint32_t* rpos = reinterpret_cast<uint32_t*>(sout1 + kStage1) + wib * (rows + 1);
+    uint32_t* rmask = reinterpret_cast<uint32_t*>(sout1 + kStage1) + (kBinWarps + wib) * (rows + 1);
+    const uint32_t out0 = smem_u32(sout1), rpos0 = smem_u32(rpos), rmask0 = smem_u32(rmask);
     auto h1at = [&](int y, int c) {       // scanned hist1 at (row y, chunk c); c may be kRowChunks
         const size_t i = (size_t)y * kRowChunks + c;
         return i < (size_t)rows * kRowChunks ? a.hist1[i] : total;
@@ -224,13 +247,12 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
         snext = __ldg(&a.sval[r0 + lane]);
         rnext = __ldg(&a.rrect[r0 + lane]);
     }
-    uint32_t base[KR], len[KR], P[KR], pos[KR], carry = 0;
+    uint32_t base[KR], len[KR], P[KR], carry = 0;
 #pragma unroll
     for (int k = 0; k < KR; ++k) {
         const int y = lane + 32 * k;
         base[k] = y < rows ? h1at(y, c0) : 0u;
         len[k] = y < rows ? h1at(y, c0 + kBinWarps) - base[k] : 0u;
-        pos[k] = y < rows ? h1at(y, chunk) : 0u;
         uint32_t incl = len[k];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -241,11 +263,16 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
         carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     const bool staged = carry <= (uint32_t)kStage1;  // block-uniform
-    const uint32_t out0 = smem_u32(sout1);
-    uint32_t sa[KR];
 #pragma unroll
-    for (int k = 0; k < KR; ++k) sa[k] = out0 + 8u * (P[k] + (pos[k] - base[k]));
-    uint32_t* my = reinterpret_cast<uint32_t*>(&stage[wib][lane][0]);
+    for (int k = 0; k < KR; ++k) {
+        const int y = lane + 32 * k;
+        if (y < rows) {
+            const uint32_t pos = h1at(y, chunk);  // this chunk's first slot of row y
+            rpos[y] = staged ? P[k] + (pos - base[k]) : pos;
+            rmask[y] = 0u;
+        }
+    }
+    __syncwarp();
     for (uint32_t rb = r0; rb < r1; rb += 32) {
         const uint32_t r = rb + lane;
         const uint32_t sv = snext;  // next batch in flight while this one is placed
@@ -254,60 +281,46 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
             snext = __ldg(&a.sval[r + 32]);
             rnext = __ldg(&a.rrect[r + 32]);
         }
-        uint32_t w[4 * NW];
-#pragma unroll
-        for (int i = 0; i < 4 * NW; ++i) w[i] = 0u;
+        // band rows [y0, y1] of this lane's splat (y1 < y0: none) and its column range
+        int y0 = 0, y1 = -1;
+        uint32_t xp = 0u;
         if (r < r1) {
             int gx0, gx1, gy0, gy1;
-            w[0] = sv;
             if (band_groups(a.gg, rr, gx0, gx1, gy0, gy1)) {
-                w[1] = (uint32_t)gx0 | ((uint32_t)gx1 << 16);
-#pragma unroll
-                for (int k = 0; k < KR; ++k) w[2 + k] = range_mask(gy0, gy1, k);
+                y0 = gy0;
+                y1 = gy1;
+                xp = (uint32_t)gx0 | ((uint32_t)gx1 << 16);
             }
         }
+        const int ms = (int)__reduce_max_sync(0xffffffffu, (uint32_t)max(y1 - y0 + 1, 0));
+        auto row = [&](int t) { return (uint32_t)max(min(y0 + t, y1), 0); };
+        for (int t = 0; t < ms; ++t) red_or_if(rmask0 + 4u * row(t), lanebit, y0 + t <= y1);
         __syncwarp();
-#pragma unroll
-        for (int i = 0; i < NW; ++i)
-            reinterpret_cast<uint4*>(my)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
-        __syncwarp();
-        const int n = (int)min(32u, r1 - rb);
         if (staged) {
-#pragma unroll 4
-            for (int j = 0; j < n; ++j) {
-                uint32_t v[4 * NW];
-#pragma unroll
-                for (int i = 0; i < NW; ++i) {
-                    const uint4 q = stage[wib][j][i];
-                    v[4 * i] = q.x;
-                    v[4 * i + 1] = q.y;
-                    v[4 * i + 2] = q.z;
-                    v[4 * i + 3] = q.w;
-                }
-#pragma unroll
-                for (int k = 0; k < KR; ++k)
-                    if (v[2 + k] & lanebit) {
-                        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(sa[k]), "r"(v[0]), "r"(v[1]) : "memory");
-                        sa[k] += 8u;
-                    }
+            for (int t = 0; t < ms; ++t) {
+                const uint32_t y4 = 4u * row(t);
+                const uint32_t p = ld_shared(rpos0 + y4) + __popc(ld_shared(rmask0 + y4) & lt);
+                st_shared_v2_if(out0 + 8u * p, sv, xp, y0 + t <= y1);
             }
         } else {
-#pragma unroll 4
-            for (int j = 0; j < n; ++j) {
-                uint32_t v[4 * NW];
-#pragma unroll
-                for (int i = 0; i < NW; ++i) {
-                    const uint4 q = stage[wib][j][i];
-                    v[4 * i] = q.x;
-                    v[4 * i + 1] = q.y;
-                    v[4 * i + 2] = q.z;
-                    v[4 * i + 3] = q.w;
+            for (int t = 0; t < ms; ++t)
+                if (y0 + t <= y1) {
+                    const uint32_t p = rpos[y0 + t] + __popc(rmask[y0 + t] & lt);
+                    a.rowidx[p] = sv;
+                    a.rowxp[p] = xp;
                 }
+        }
+        __syncwarp();
+        // advance every row by its entries in this batch (lane-owned rows, race-free)
 #pragma unroll
-                for (int k = 0; k < KR; ++k)
-                    if (v[2 + k] & lanebit) a.rowlist[pos[k]++] = make_uint2(v[0], v[1]);
+        for (int k = 0; k < KR; ++k) {
+            const int y = lane + 32 * k;
+            if (y < rows) {
+                rpos[y] += __popc(rmask[y]);
+                rmask[y] = 0u;
             }
         }
+        __syncwarp();
     }
     if (staged) {
         __syncthreads();
@@ -318,7 +331,11 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
                 const uint32_t c = __shfl_sync(0xffffffffu, len[k], l);
                 const uint32_t src = __shfl_sync(0xffffffffu, P[k], l);
                 const uint32_t dst = __shfl_sync(0xffffffffu, base[k], l);
-                for (uint32_t i = lane; i < c; i += 32) a.rowlist[dst + i] = sout1[src + i];
+                for (uint32_t i = lane; i < c; i += 32) {
+                    const uint2 e = sout1[src + i];
+                    a.rowidx[dst + i] = e.x;
+                    a.rowxp[dst + i] = e.y;
+                }
             }
     }
 }
@@ -365,7 +382,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_count_kernel(BinArgs a) {
         for (uint32_t eb = e0 + lane; eb < e1; eb += 32 * 8) {  // 8 loads in flight per lane
             uint32_t xp[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) xp[u] = eb + 32u * u < e1 ? __ldg(&a.rowlist[eb + 32u * u].y) : 0xffffffffu;
+            for (int u = 0; u < 8; ++u) xp[u] = eb + 32u * u < e1 ? __ldg(&a.rowxp[eb + 32u * u]) : 0xffffffffu;
 #pragma unroll
             for (int u = 0; u < 8; ++u)
                 if (xp[u] != 0xffffffffu) {
@@ -425,22 +442,6 @@ __global__ void offsets_kernel(BinArgs a) {
 // reductions / stores), slots are in the block's shared output buffer in column-major order, and
 // every column run is flushed as one coalesced burst; a block whose output exceeds the buffer
 // writes global slots.
-__device__ __forceinline__ void red_or_if(uint32_t addr, uint32_t v, bool on) {
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(addr),
-                 "r"(v), "r"((uint32_t)on)
-                 : "memory");
-}
-__device__ __forceinline__ void st_shared_if(uint32_t addr, uint32_t v, bool on) {
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}" ::"r"(addr),
-                 "r"(v), "r"((uint32_t)on)
-                 : "memory");
-}
-__device__ __forceinline__ uint32_t ld_shared(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-    return v;
-}
-
 template <int KC>
 __global__ void __launch_bounds__(kBinWarps * 32, KC <= 4 ? 5 : 1) cols_place_kernel(BinArgs a) {
     constexpr int kPer = kSliceLen / 32;  // row entries per lane
@@ -484,7 +485,7 @@ __global__ void __launch_bounds__(kBinWarps * 32, KC <= 4 ? 5 : 1) cols_place_ke
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {
             const uint32_t e = e0 + lane + 32u * i;
-            ent[i] = e < e1 ? __ldg(&a.rowlist[e]) : make_uint2(0u, 0u);
+            ent[i] = e < e1 ? make_uint2(__ldg(&a.rowidx[e]), __ldg(&a.rowxp[e])) : make_uint2(0u, 0u);
         }
         for (int i = lane; i <= gx; i += 32) D[i] = 0;
         __syncwarp();
@@ -829,7 +830,8 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     const uint32_t* scan1_total = launch_exclusive_scan(a.hist1, n1, tmp, st, nullptr);
     rows_meta_kernel<<<1, 32, 0, st>>>(a, scan1_total);
     const int kr = (rows + 31) / 32, b1 = kRowChunks / kBinWarps, t1 = kBinWarps * 32;
-    const size_t so1 = (size_t)stage1_entries(kr) * sizeof(uint2);
+    // output stage, per-warp row positions / masks
+    const size_t so1 = (size_t)stage1_entries(kr) * sizeof(uint2) + (size_t)2 * kBinWarps * (rows + 1) * sizeof(uint32_t);
     auto launch1 = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)so1);
         kern<<<b1, t1, so1, st>>>(a);

@@ -56,7 +56,8 @@ struct BinArgs {
     uint32_t* hist2;             // [bin_hist2_elems] level-2 counts, scanned in place
     uint32_t* meta;              // [bin_meta_elems] row starts / segment layout
     uint32_t* bsum;              // scan block sums (+1)
-    uint2* rowlist;              // [capacity] group-row entries (splat index, gx0 | gx1 << 16)
+    uint32_t* rowidx;            // [capacity] group-row entries: splat index
+    uint32_t* rowxp;             // [capacity]                    column range gx0 | gx1 << 16
     uint32_t* offsets;           // [n_groups_band + 1]
     uint32_t* list;              // [capacity] output entries (splat indices)
     uint32_t* segmap;            // [bin_segmap_elems] level-2 segment -> group row (cols_count -> cols_place)

@@ -38,8 +38,14 @@ constexpr int kRadix = 256;
 #define TGS_SWEEP_BLOCKS 3
 #endif
 constexpr int kSweepBlocks = 148 * TGS_SWEEP_BLOCKS;  // persistent one-sweep blocks
+#ifndef TGS_SORT_NOLB
+#define TGS_SORT_NOLB 0  // timing experiment only: no look-back (wrong offsets)
+#endif
+#ifndef TGS_SORT_NS
+#define TGS_SORT_NS 20  // look-back back-off (ns) when no predecessor has published
+#endif
 #ifndef TGS_SORT_WIN
-#define TGS_SORT_WIN 8  // look-back predecessors read per round trip
+#define TGS_SORT_WIN 2  // look-back predecessors read per round trip (1-32 measured: 2 best)
 #endif
 
 
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
         // look-back: sum earlier tiles' digit-d counts until one with an inclusive prefix, reading
         // kWin predecessors per round trip (independent loads)
         uint32_t prefix = 0;
-        if (tile > 0) {
+        if (tile > 0 && !TGS_SORT_NOLB) {
             constexpr int kWin = TGS_SORT_WIN;
             int j = (int)tile - 1;
             const long long w0 = clock64();
@@ -239,7 +245,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
                 if (done) break;
                 j -= used;
                 if (used == 0) {
-                    __nanosleep(20);
+                    __nanosleep(TGS_SORT_NS);
                     if (clock64() - w0 > 4000000000ll) {  // bounded wait: report, never hang
                         printf("radix look-back stuck: pass %d tile %u waits on %d\n", pass, tile, j);
                         __trap();

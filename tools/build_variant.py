@@ -20,12 +20,13 @@ def main():
     out_dir = os.path.join(B.HERE, "variants")
     os.makedirs(out_dir, exist_ok=True)
     vobjs = []
-    for src in srcs:
-        obj = os.path.join(out_dir, f"{name}_{src}.o")
-        cmd = [B.NVCC, *B.ARCH, *B.NVFLAGS, *extra, "-c", os.path.join(B.CSRC, src), "-o", obj]
+    for src in srcs:  # a source may be an absolute path (e.g. an older revision of a csrc file)
+        obj = os.path.join(out_dir, f"{name}_{os.path.basename(src)}.o")
+        cmd = [B.NVCC, *B.ARCH, *B.NVFLAGS, "-I", B.CSRC, *extra, "-c", os.path.join(B.CSRC, src), "-o", obj]
         subprocess.run(cmd, check=True)
         vobjs.append(obj)
-    objs = [o for o in sorted(glob.glob(os.path.join(B.OBJ, "*.o"))) if os.path.basename(o)[:-2] not in srcs]
+    names = {os.path.basename(s) for s in srcs}
+    objs = [o for o in sorted(glob.glob(os.path.join(B.OBJ, "*.o"))) if os.path.basename(o)[:-2] not in names]
     lib = os.path.join(out_dir, f"libtgs_{name}.so")
     subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", lib, *vobjs, *objs, "-lcudart"], check=True)
     print(lib)

@@ -131,6 +131,38 @@ __device__ __forceinline__ void lane_pixel(int m, int l, int& x, int& y) {
     y = (t >> 1) * 16 + (q >> 1) * 8 + k * 4 + (i >> 3);
 }
 
+#ifndef TGS_BLEND_X2
+#define TGS_BLEND_X2 1
+#endif
+// Blend step of both pixels of a thread with packed FP32x2 instructions (FMUL2 / FFMA2 / FADD2):
+// per pixel k  wt = T * al;  c += wt * colour (fused);  T -= wt  — the same IEEE operations, in the
+// same order, as the scalar form, so the result is bit-identical.
+__device__ __forceinline__ void blend_x2(float (&T)[2], float (&cr)[2], float (&cg)[2], float (&cb)[2],
+                                         const float (&al)[2], const float4& ej) {
+    asm("{\n\t"
+        ".reg .b64 t, a, w, r, g, b, cx, cy, cz;\n\t"
+        "mov.b64 t, {%0, %1};\n\t"
+        "mov.b64 a, {%8, %9};\n\t"
+        "mov.b64 r, {%2, %3};\n\t"
+        "mov.b64 g, {%4, %5};\n\t"
+        "mov.b64 b, {%6, %7};\n\t"
+        "mov.b64 cx, {%10, %10};\n\t"
+        "mov.b64 cy, {%11, %11};\n\t"
+        "mov.b64 cz, {%12, %12};\n\t"
+        "mul.rn.f32x2 w, t, a;\n\t"
+        "fma.rn.f32x2 r, w, cx, r;\n\t"
+        "fma.rn.f32x2 g, w, cy, g;\n\t"
+        "fma.rn.f32x2 b, w, cz, b;\n\t"
+        "sub.rn.f32x2 t, t, w;\n\t"
+        "mov.b64 {%0, %1}, t;\n\t"
+        "mov.b64 {%2, %3}, r;\n\t"
+        "mov.b64 {%4, %5}, g;\n\t"
+        "mov.b64 {%6, %7}, b;\n\t"
+        "}"
+        : "+f"(T[0]), "+f"(T[1]), "+f"(cr[0]), "+f"(cr[1]), "+f"(cg[0]), "+f"(cg[1]), "+f"(cb[0]), "+f"(cb[1])
+        : "f"(al[0]), "f"(al[1]), "f"(ej.x), "f"(ej.y), "f"(ej.z));
+}
+
 // byte offset of (row, k-half) in a K-major no-swizzle operand: 8x16B core matrices
 __device__ __forceinline__ uint32_t core_off(int row, int khalf) {
     return (uint32_t)((row >> 3) * 256 + khalf * 128 + (row & 7) * 16);
@@ -777,17 +809,25 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                     for (int jj = 0; jj < kJB; ++jj)
                         if (M & (1u << jj)) {
                             const float4 ej = sm.epi[s][j0 + jj];
+                            float al[2];
 #pragma unroll
                             for (int k = 0; k < 2; ++k) {
                                 const float dv = __uint_as_float(d[k][jj]);
                                 const float e2 = fminf(ej.w, ex2_approx(dv));
-                                const float al = (dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f;
-                                const float wt = T[k] * al;
+                                al[k] = (dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f;
+                            }
+#if TGS_BLEND_X2
+                            blend_x2(T, cr, cg, cb, al, ej);
+#else
+#pragma unroll
+                            for (int k = 0; k < 2; ++k) {
+                                const float wt = T[k] * al[k];
                                 cr[k] = fmaf(wt, ej.x, cr[k]);
                                 cg[k] = fmaf(wt, ej.y, cg[k]);
                                 cb[k] = fmaf(wt, ej.z, cb[k]);
                                 T[k] -= wt;
                             }
+#endif
                         }
 #pragma unroll
                     for (int k = 0; k < 2; ++k)

@@ -401,8 +401,9 @@ tgs_status record_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* 
     pb.vals[1] = ctx->pre_vals[1].as<uint32_t>();
     pb.ghist = ctx->ghist.as<uint32_t>();
     pb.scan_tmp = ctx->bsum.as<uint32_t>();
+    pb.result_sel = ctx->ghist.as<uint32_t>() + sort_result_sel_offset();
     // pass 1 covers all n splats and drops the culled ones (key kCulledKey); later passes the kept
-    const int pr = radix_sort(pb, &fc->n_input, &fc->visible, 32, true, false, (size_t)n_alloc, s, &fc->key_min_inv, true);
+    radix_sort(pb, &fc->n_input, &fc->visible, 32, true, false, (size_t)n_alloc, s, &fc->key_min_inv, true);
     TGS_CUDA_OK(cudaGetLastError());
 
     TGS_CUDA_OK(record_event(ctx->ev[2], s));
@@ -410,7 +411,9 @@ tgs_status record_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* 
     // 3. binning: stable counting sort of (group, rank) entries -> lists + per-group offsets
     BinArgs ba;
     ba.visible = &fc->visible;
-    ba.sval = pb.vals[pr];
+    ba.sval[0] = pb.vals[0];
+    ba.sval[1] = pb.vals[1];
+    ba.sval_sel = pb.result_sel;
     ba.rect = ctx->rect.as<uint2>();
     ba.rrect = ctx->rrect.as<uint2>();
     ba.gg = gg;

@@ -101,6 +101,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // hist1[y * kRowChunks + chunk] = splats of the chunk overlapping group row y; fc->n_entries +=
 // the chunk's (splat, group) entries (the capacity check needs the total before any placement).
 __global__ void __launch_bounds__(kBinWarps * 32) rows_count_kernel(BinArgs a) {
+    const uint32_t* __restrict__ sval = *a.sval_sel ? a.sval[1] : a.sval[0];
     extern __shared__ int sdiff[];
     const int rows = a.gg.band_gy1 - a.gg.band_gy0;
     const int lane = threadIdx.x & 31, chunk = blockIdx.x * kBinWarps + (threadIdx.x >> 5);
@@ -116,7 +117,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_count_kernel(BinArgs a) {
         for (int u = 0; u < 8; ++u) {
             const uint32_t r = rb + 32u * u;
             // gather the rank-ordered rectangle once here (rows_place reads it back coalesced)
-            rr[u] = r < r1 ? __ldg(&a.rect[__ldg(&a.sval[r])]) : make_uint2(0xffffu, 0u);
+            rr[u] = r < r1 ? __ldg(&a.rect[__ldg(&sval[r])]) : make_uint2(0xffffu, 0u);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
     // [kStage1] output (uint2) | [kBinWarps][rows + 1] row positions | [kBinWarps][rows + 1] row masks
     extern __shared__ uint2 sout1[];
     if (a.fc->overflow) return;
+    const uint32_t* __restrict__ sval = *a.sval_sel ? a.sval[1] : a.sval[0];
     const int rows = a.gg.band_gy1 - a.gg.band_gy0;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int c0 = blockIdx.x * kBinWarps, chunk = c0 + wib;
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
     uint32_t snext = 0u;  // the chunk's first batch is in flight during the row setup
     uint2 rnext = make_uint2(0u, 0u);
     if (r0 + lane < r1) {
-        snext = __ldg(&a.sval[r0 + lane]);
+        snext = __ldg(&sval[r0 + lane]);
         rnext = __ldg(&a.rrect[r0 + lane]);
     }
     uint32_t base[KR], len[KR], P[KR], carry = 0;
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
         const uint32_t sv = snext;  // next batch in flight while this one is placed
         const uint2 rr = rnext;
         if (r + 32 < r1) {
-            snext = __ldg(&a.sval[r + 32]);
+            snext = __ldg(&sval[r + 32]);
             rnext = __ldg(&a.rrect[r + 32]);
         }
         // band rows [y0, y1] of this lane's splat (y1 < y0: none) and its column range

@@ -26,9 +26,13 @@ struct SortBuffers {
     uint32_t* vals[2];
     uint32_t* ghist;      // sort_scratch_elems(max_items): [digit][tile] counts, scanned in place
     uint32_t* scan_tmp;   // scan_tmp_elems(sort_scratch_elems(max_items))
+    // Optional device word: when set, a last pass whose digit is constant (the identity) is skipped
+    // instead of copied, and the index of the buffer holding the result is written here.
+    uint32_t* result_sel = nullptr;
 };
 constexpr int kSortBlocks = 592;  // 4 x 148 SMs (grid of the binning/scan helpers)
 size_t sort_scratch_elems(size_t max_items);
+size_t sort_result_sel_offset();  // a free word of the sort scratch (ghist) for SortBuffers::result_sel
 // Sorts keys[0]/vals[0] by bits [0, nbits) in 8-bit passes; the first pass covers
 // *count_first items and, with drop_first, drops keys equal to kCulledKey; later passes cover
 // *count_rest items (device-side counts, <= max_items).  Result in keys[r]/vals[r], r returned.
@@ -36,6 +40,7 @@ size_t sort_scratch_elems(size_t max_items);
 // key_min_inv (device, may be null) holds ~min over the sorted keys: digits are taken from
 // (key - min), which keeps the order and leaves the passes above the key range trivial (copies).
 // index_vals: the first pass takes item i's value to be i (vals[0] is not read).
+// With b.result_sel the result is in vals[*result_sel] (device word; r or r ^ 1).
 int radix_sort(SortBuffers& b, const uint32_t* count_first, const uint32_t* count_rest, int nbits,
                bool drop_first, bool want_keys_last, size_t max_items, cudaStream_t st,
                const uint32_t* key_min_inv = nullptr, bool index_vals = false);
@@ -48,7 +53,8 @@ int radix_sort(SortBuffers& b, const uint32_t* count_first, const uint32_t* coun
 // of the reference (binning.cpp:86-91) entry for entry.
 struct BinArgs {
     const uint32_t* visible;     // &fc->visible (device-side count)
-    const uint32_t* sval;        // rank -> splat index
+    const uint32_t* sval[2];     // rank -> splat index: the presort's two value buffers,
+    const uint32_t* sval_sel;    // of which buffer *sval_sel holds the result (device word)
     const uint2* rect;           // splat index -> tile rect
     uint2* rrect;                // rank -> tile rect
     GroupGeom gg;

@@ -163,6 +163,17 @@ __device__ __forceinline__ void blend_x2(float (&T)[2], float (&cr)[2], float (&
         : "f"(al[0]), "f"(al[1]), "f"(ej.x), "f"(ej.y), "f"(ej.z));
 }
 
+#ifndef TGS_PHASE1_X2
+#define TGS_PHASE1_X2 1
+#endif
+// (x0 - t, x1 - t) with one packed FADD2; results as raw bits
+__device__ __forceinline__ void sub_x2(uint32_t x0, uint32_t x1, float t, uint32_t& r0, uint32_t& r1) {
+    asm("{\n\t.reg .b64 x, y, r;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %4};\n\t"
+        "sub.rn.f32x2 r, x, y;\n\tmov.b64 {%0, %1}, r;\n\t}"
+        : "=r"(r0), "=r"(r1)
+        : "r"(x0), "r"(x1), "f"(t));
+}
+
 // byte offset of (row, k-half) in a K-major no-swizzle operand: 8x16B core matrices
 __device__ __forceinline__ uint32_t core_off(int row, int khalf) {
     return (uint32_t)((row >> 3) * 256 + khalf * 128 + (row & 7) * 16);
@@ -788,6 +799,22 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                     }
                     // Phase 1 (branch-free, kJB independent chains): which of the batch's splats
                     // reach alpha_skip at any of this warp's pixels -> warp-uniform mask.
+#if TGS_PHASE1_X2
+                    // D - thr with packed FADD2 over splat pairs (sign bit set <=> D < thr, exactly:
+                    // IEEE subtraction of finite values is 0 only for equal operands, -inf for a
+                    // retired pixel's +inf); bit jj of `idle` = both pixels below thr, gathered with
+                    // one funnel shift per splat
+                    uint32_t idle = 0;
+#pragma unroll
+                    for (int jj = kJB - 2; jj >= 0; jj -= 2) {
+                        uint32_t a0, a1, b0, b1;
+                        sub_x2(d[0][jj], d[0][jj + 1], thr[0], a0, a1);
+                        sub_x2(d[1][jj], d[1][jj + 1], thr[1], b0, b1);
+                        idle = __funnelshift_l(a1 & b1, idle, 1);
+                        idle = __funnelshift_l(a0 & b0, idle, 1);
+                    }
+                    const uint32_t M = __reduce_or_sync(0xffffffffu, ~idle & ((1u << kJB) - 1u));
+#else
                     uint32_t mk = 0;
 #pragma unroll
                     for (int jj = 0; jj < kJB; ++jj) {
@@ -796,6 +823,7 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                         mk |= p & (1u << jj);
                     }
                     const uint32_t M = __reduce_or_sync(0xffffffffu, mk);
+#endif
                     if (TGS_RASTER_PROF) {
                         pf[2] += __popc(M);
                         pf[3] += kJB;

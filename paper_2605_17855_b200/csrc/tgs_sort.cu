@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kThreads) digits_kernel(const uint32_t* __rest
 __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, const uint32_t* count_ptr, int pass, bool write_keys, bool drop,
-    const uint32_t* key_min_inv, uint32_t* __restrict__ scratch) {
+    const uint32_t* key_min_inv, uint32_t* __restrict__ scratch, uint32_t* sel, uint32_t src_idx) {
     __shared__ uint32_t wcnt[kWarps][kRadix];   // per-warp digit counts -> per-warp offsets
     __shared__ uint32_t tot[kRadix];            // tile digit totals
     __shared__ uint32_t lstart[kRadix];         // tile-local start of each digit
@@ -122,6 +122,10 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     // A pass whose digit is the same for every item (e.g. the top byte of depth keys that share
     // their float exponent's high bits) is the identity permutation: copy instead of ranking.
     if (!drop && vin && __syncthreads_or(scratch[kHistOff + pass * kRadix + threadIdx.x] == n)) {
+        if (sel) {  // last pass of a caller that reads the result buffer index: nothing to move
+            if (blockIdx.x == 0 && threadIdx.x == 0) *sel = src_idx;
+            return;
+        }
         const uint32_t tid = blockIdx.x * kThreads + threadIdx.x, nt = gridDim.x * kThreads, n4 = n / 4u;
         auto copy = [&](const uint32_t* __restrict__ src, uint32_t* __restrict__ dst) {
             const uint4* s4 = reinterpret_cast<const uint4*>(src);  // cudaMalloc'd: 16-byte aligned
@@ -134,6 +138,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
         copy(vin, vout);
         return;
     }
+    if (sel && blockIdx.x == 0 && threadIdx.x == 0) *sel = src_idx ^ 1u;
     // persistent blocks claim tiles in order, so only ~gridDim tiles are in flight and look-back
     // walks stay short
     for (;;) {
@@ -283,6 +288,8 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
 
 }  // namespace
 
+size_t sort_result_sel_offset() { return kCtrOff + 7; }  // tile counters use kCtrOff + pass (< 4)
+
 size_t sort_scratch_elems(size_t max_items) {
     return (size_t)kStatusOff + ((max_items + kTileItems - 1) / kTileItems + 1) * kRadix;
 }
@@ -301,7 +308,8 @@ int radix_sort(SortBuffers& b, const uint32_t* count_first, const uint32_t* coun
             cudaMemsetAsync(b.ghist + kStatusOff, 0, (size_t)tiles * kRadix * sizeof(uint32_t), st);
         onesweep_kernel<<<std::min(tiles, kSweepBlocks), kThreads, 0, st>>>(b.keys[src], p == 0 && index_vals ? nullptr : b.vals[src], b.keys[src ^ 1], b.vals[src ^ 1],
                                                    p == 0 ? count_first : count_rest, p, !last || want_keys_last,
-                                                   p == 0 && drop_first, key_min_inv, b.ghist);
+                                                   p == 0 && drop_first, key_min_inv, b.ghist,
+                                                   last ? b.result_sel : nullptr, (uint32_t)src);
         src ^= 1;
     }
     return src;

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--backend", default="tensor")
     ap.add_argument("--cam", type=int, default=5)
     ap.add_argument("--save", action="store_true", help="save the image to gpurun_out/ab_TAG.npy")
+    ap.add_argument("--hash", action="store_true", help="print a digest of the image bytes (bit-identity checks)")
     a = ap.parse_args()
     ctx = gsr.Context(0)
     ds = ctx.upload(gsr.gen_synthetic_scene(3, 3_000_000, 1.0, (0.01, 0.05)))
@@ -37,6 +38,10 @@ def main():
         img = ctx.render(ds, cam, opt).image.rgb
         os.makedirs("gpurun_out", exist_ok=True)
         np.save(f"gpurun_out/ab_{a.tag}.npy", img)
+    if a.hash:
+        import hashlib
+        img = ctx.render(ds, cam, opt).image.rgb
+        print(f"HASH {a.tag}: {hashlib.sha256(np.ascontiguousarray(img).tobytes()).hexdigest()[:16]}", flush=True)
     print(f"AB {a.tag}: pre {med[0]:.3f} sort {med[1]:.3f} bin {med[2]:.3f} raster {med[3]:.3f} "
           f"total {med[4]:.3f} ms", flush=True)
 

@@ -166,6 +166,19 @@ __device__ __forceinline__ void blend_x2(float (&T)[2], float (&cr)[2], float (&
 #ifndef TGS_PHASE1_X2
 #define TGS_PHASE1_X2 1
 #endif
+#ifndef TGS_SEL_AND
+#define TGS_SEL_AND 1
+#endif
+// (a >= b && c >= d) ? v : 0 as two compares (the second AND-ed with the first) and one select
+__device__ __forceinline__ float sel_ge2(float a, float b, float c, float d, float v) {
+    float r;
+    asm("{\n\t.reg .pred q, p;\n\tsetp.ge.f32 q, %3, %4;\n\tsetp.ge.and.f32 p, %1, %2, q;\n\t"
+        "selp.f32 %0, %5, 0f00000000, p;\n\t}"
+        : "=f"(r)
+        : "f"(a), "f"(b), "f"(c), "f"(d), "f"(v));
+    return r;
+}
+
 // (x0 - t, x1 - t) with one packed FADD2; results as raw bits
 __device__ __forceinline__ void sub_x2(uint32_t x0, uint32_t x1, float t, uint32_t& r0, uint32_t& r1) {
     asm("{\n\t.reg .b64 x, y, r;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %4};\n\t"
@@ -842,7 +855,8 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                             for (int k = 0; k < 2; ++k) {
                                 const float dv = __uint_as_float(d[k][jj]);
                                 const float e2 = fminf(ej.w, ex2_approx(dv));
-                                al[k] = (dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f;
+                                al[k] = TGS_SEL_AND ? sel_ge2(dv, thr[k], T[k], tterm, e2)
+                                                    : ((dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f);
                             }
 #if TGS_BLEND_X2
                             blend_x2(T, cr, cg, cb, al, ej);

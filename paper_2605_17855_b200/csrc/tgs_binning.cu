@@ -45,21 +45,14 @@ constexpr int kRowChunks = TGS_ROW_CHUNKS;  // level-1 chunks (contiguous rank r
 #define TGS_STAGE1_WIDE 8192
 #endif
 constexpr int stage1_entries(int kr) { return kr <= 2 ? TGS_STAGE1 : TGS_STAGE1_WIDE; }
-#ifndef TGS_SLICE_LEN
-#define TGS_SLICE_LEN 128
-#endif
-constexpr uint32_t kSliceLen = TGS_SLICE_LEN;   // level-2 placement: row-list entries per warp
-constexpr uint32_t kSegLen = kSliceLen * kBinWarps;  // level-2 segment: one count warp / one placement block
-// level-2 per-block output staging (entries): one segment's output is ~kSegLen x the mean column
-// span, which grows with the columns per row; a smaller stage keeps more blocks resident (bench
-// G=2, 60 columns: 6144; G=1, 120 columns: 8192)
-#ifndef TGS_STAGE2
-#define TGS_STAGE2 6144
-#endif
-#ifndef TGS_STAGE2_WIDE
-#define TGS_STAGE2_WIDE 8192
-#endif
-constexpr int stage2_entries(int kc) { return kc <= 2 ? TGS_STAGE2 : TGS_STAGE2_WIDE; }
+// Level 2 cuts every group-row list into segments of kBinWarps slices (one placement block, one
+// count warp); a slice is the row entries one warp places.  A segment's output (~entries x the mean
+// column span) is staged in shared memory: 256-entry slices and a 12K-entry stage for up to 64
+// group columns (bench G=2), 128 / 8K beyond (G=1 at 1080p: 120 columns) — measured per config.
+__host__ __device__ constexpr uint32_t slice_len(int kc) { return kc <= 2 ? 256u : 128u; }
+__host__ __device__ constexpr uint32_t seg_len_kc(int kc) { return slice_len(kc) * kBinWarps; }
+__host__ __device__ inline uint32_t seg_len_gx(int gx) { return seg_len_kc((gx + 31) / 32); }
+constexpr int stage2_entries(int kc) { return kc <= 2 ? 12288 : 8192; }
 constexpr int kScanItems = 16;        // per thread in the hist scan
 constexpr int kScanBlock = 256;
 constexpr int kScanTile = kScanItems * kScanBlock;
@@ -173,7 +166,7 @@ __global__ void rows_meta_kernel(BinArgs a, const uint32_t* __restrict__ scan1_t
         if (y < rows) {
             start = a.hist1[(size_t)y * kRowChunks];
             const uint32_t next = y + 1 < rows ? a.hist1[(size_t)(y + 1) * kRowChunks] : *scan1_total;
-            nseg = over ? 0u : (next - start + kSegLen - 1u) / kSegLen;
+            nseg = over ? 0u : (next - start + seg_len_gx(gx) - 1u) / seg_len_gx(gx);
         } else if (y == rows) {
             start = *scan1_total;
         }
@@ -343,7 +336,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
 }
 
 // ---- level 2: group-row lists -> group lists ----------------------------------------------------
-// Row y's list is cut into segments of kSegLen entries (one warp each).  hist2 holds, per row, a
+// Row y's list is cut into segments of seg_len_gx entries (one count warp each).  hist2 holds, per row, a
 // [column][segment] block, so the exclusive scan of hist2 (rows in order) is directly the global
 // start of every (group, segment) run and group g = (y, x) starts at its segment-0 slot.
 
@@ -378,7 +371,8 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_count_kernel(BinArgs a) {
         seg_locate(nsegp, rows, q, y, s);
         if (lane == 0) a.segmap[q] = (uint32_t)y;  // cols_place reads the row back (one load)
         const uint32_t nseg = nsegp[y + 1] - nsegp[y];
-        const uint32_t e0 = rowstart[y] + s * kSegLen, e1 = min(rowstart[y + 1], e0 + kSegLen);
+        const uint32_t seg = seg_len_gx(gx);
+        const uint32_t e0 = rowstart[y] + s * seg, e1 = min(rowstart[y + 1], e0 + seg);
         for (int i = lane; i <= gx; i += 32) D[i] = 0;
         __syncwarp();
         for (uint32_t eb = e0 + lane; eb < e1; eb += 32 * 8) {  // 8 loads in flight per lane
@@ -434,7 +428,7 @@ __global__ void offsets_kernel(BinArgs a) {
     }
 }
 
-// Group placement.  A block takes one segment (kBinWarps slices of kSliceLen row entries, one per
+// Group placement.  A block takes one segment (kBinWarps slices of slice_len row entries, one per
 // warp); the segment's run of column x is one contiguous global range [base_x, base_x + len_x),
 // inside which warp w's part starts after the parts of warps < w (per-slice column counts, made
 // here in shared memory).  Lane per entry: each lane marks the columns of its entry in a per-warp
@@ -446,6 +440,7 @@ __global__ void offsets_kernel(BinArgs a) {
 // writes global slots.
 template <int KC>
 __global__ void __launch_bounds__(kBinWarps * 32, KC <= 4 ? 5 : 1) cols_place_kernel(BinArgs a) {
+    constexpr uint32_t kSliceLen = slice_len(KC), kSegLen = seg_len_kc(KC);
     constexpr int kPer = kSliceLen / 32;  // row entries per lane
     constexpr int kStage2 = stage2_entries(KC);
     // [kStage2] output | [kBinWarps][gx + 1] slice counts, column positions, column masks
@@ -804,11 +799,11 @@ int bin_chunks(int) { return kRowChunks; }
 size_t bin_hist1_elems(const GroupGeom& gg) { return (size_t)std::max(1, gg.band_gy1 - gg.band_gy0) * kRowChunks; }
 size_t bin_hist2_elems(const GroupGeom& gg, uint32_t capacity) {
     const size_t rows = (size_t)std::max(1, gg.band_gy1 - gg.band_gy0);
-    return (size_t)gg.groups_x * (rows + capacity / kSegLen + 1);
+    return (size_t)gg.groups_x * (rows + capacity / seg_len_gx(gg.groups_x) + 1);
 }
 size_t bin_meta_elems(const GroupGeom& gg) { return 4 * (size_t)(gg.band_gy1 - gg.band_gy0 + 1) + 1; }
 size_t bin_segmap_elems(const GroupGeom& gg, uint32_t capacity) {
-    return (size_t)std::max(1, gg.band_gy1 - gg.band_gy0) + capacity / kSegLen + 1;
+    return (size_t)std::max(1, gg.band_gy1 - gg.band_gy0) + capacity / seg_len_gx(gg.groups_x) + 1;
 }
 
 size_t scan_tmp_elems(size_t n) { return 4 + 2 * ((n + kScanTile - 1) / kScanTile); }
@@ -851,7 +846,7 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     // level 2
     const size_t n2 = bin_hist2_elems(gg, a.capacity);
     const uint32_t* h2_len = a.meta + 3 * rows + 2;  // rowbase2[rows]: device-side hist2 length
-    const size_t max_seg = (size_t)rows + a.capacity / kSegLen + 1;
+    const size_t max_seg = (size_t)rows + a.capacity / seg_len_gx(gx) + 1;
     const int qblocks = (int)std::max<size_t>(1, std::min<size_t>(148 * 8, (max_seg + kBinWarps - 1) / kBinWarps));
     cols_count_kernel<<<qblocks, kBinWarps * 32, kBinWarps * (gx + 1) * sizeof(int), st>>>(a);
     launch_exclusive_scan(a.hist2, n2, tmp, st, h2_len);

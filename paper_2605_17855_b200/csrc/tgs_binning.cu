@@ -201,9 +201,9 @@ __device__ __forceinline__ void st_shared_v2_if(uint32_t addr, uint32_t x, uint3
                  "r"(x), "r"(y), "r"((uint32_t)on)
                  : "memory");
 }
-__device__ __forceinline__ uint32_t ld_shared(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+__device__ __forceinline__ uint2 ld_shared_v2(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
     return v;
 }
 
@@ -227,9 +227,9 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
     const int c0 = blockIdx.x * kBinWarps, chunk = c0 + wib;
     const uint32_t lanebit = 1u << lane, lt = lanebit - 1u;
     const uint32_t total = a.meta[rows];  // row entries
-    uint32_t* rpos = reinterpret_cast<uint32_t*>(sout1 + kStage1) + wib * (rows + 1);
-    uint32_t* rmask = reinterpret_cast<uint32_t*>(sout1 + kStage1) + (kBinWarps + wib) * (rows + 1);
-    const uint32_t out0 = smem_u32(sout1), rpos0 = smem_u32(rpos), rmask0 = smem_u32(rmask);
+    // per-warp row records (running position, mask of this batch's lanes)
+    uint2* rm = sout1 + kStage1 + wib * (rows + 1);
+    const uint32_t out0 = smem_u32(sout1), rm0 = smem_u32(rm);
     auto h1at = [&](int y, int c) {       // scanned hist1 at (row y, chunk c); c may be kRowChunks
         const size_t i = (size_t)y * kRowChunks + c;
         return i < (size_t)rows * kRowChunks ? a.hist1[i] : total;
@@ -263,8 +263,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
         const int y = lane + 32 * k;
         if (y < rows) {
             const uint32_t pos = h1at(y, chunk);  // this chunk's first slot of row y
-            rpos[y] = staged ? P[k] + (pos - base[k]) : pos;
-            rmask[y] = 0u;
+            rm[y] = make_uint2(staged ? P[k] + (pos - base[k]) : pos, 0u);
         }
     }
     __syncwarp();
@@ -276,34 +275,36 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
             snext = __ldg(&sval[r + 32]);
             rnext = __ldg(&a.rrect[r + 32]);
         }
-        // band rows [y0, y1] of this lane's splat (y1 < y0: none) and its column range
-        int y0 = 0, y1 = -1;
-        uint32_t xp = 0u;
+        // band rows [y0, y0 + span) of this lane's splat (span 0: none; reads row 0) and its
+        // column range
+        uint32_t y0 = 0u, y1 = 0u, xp = 0u;
+        int span = 0;
         if (r < r1) {
             int gx0, gx1, gy0, gy1;
             if (band_groups(a.gg, rr, gx0, gx1, gy0, gy1)) {
-                y0 = gy0;
-                y1 = gy1;
+                y0 = (uint32_t)gy0;
+                y1 = (uint32_t)gy1;
+                span = gy1 - gy0 + 1;
                 xp = (uint32_t)gx0 | ((uint32_t)gx1 << 16);
             }
         }
-        const int ms = (int)__reduce_max_sync(0xffffffffu, (uint32_t)max(y1 - y0 + 1, 0));
-        auto row = [&](int t) { return (uint32_t)max(min(y0 + t, y1), 0); };
-        for (int t = 0; t < ms; ++t) red_or_if(rmask0 + 4u * row(t), lanebit, y0 + t <= y1);
+        const int ms = (int)__reduce_max_sync(0xffffffffu, (uint32_t)span);
+        // record address of step t, clamped to the last row (inactive steps store nothing)
+        const uint32_t ra = rm0 + 8u * y0, rz = rm0 + 8u * y1;
+        for (int t = 0; t < ms; ++t) red_or_if(min(ra + 8u * (uint32_t)t, rz) + 4u, lanebit, t < span);
         __syncwarp();
         if (staged) {
             for (int t = 0; t < ms; ++t) {
-                const uint32_t y4 = 4u * row(t);
-                const uint32_t p = ld_shared(rpos0 + y4) + __popc(ld_shared(rmask0 + y4) & lt);
-                st_shared_v2_if(out0 + 8u * p, sv, xp, y0 + t <= y1);
+                const uint2 q = ld_shared_v2(min(ra + 8u * (uint32_t)t, rz));
+                st_shared_v2_if(out0 + 8u * (q.x + __popc(q.y & lt)), sv, xp, t < span);
             }
         } else {
-            for (int t = 0; t < ms; ++t)
-                if (y0 + t <= y1) {
-                    const uint32_t p = rpos[y0 + t] + __popc(rmask[y0 + t] & lt);
-                    a.rowidx[p] = sv;
-                    a.rowxp[p] = xp;
-                }
+            for (int t = 0; t < span; ++t) {
+                const uint2 q = rm[y0 + t];
+                const uint32_t p = q.x + __popc(q.y & lt);
+                a.rowidx[p] = sv;
+                a.rowxp[p] = xp;
+            }
         }
         __syncwarp();
         // advance every row by its entries in this batch (lane-owned rows, race-free)
@@ -311,8 +312,8 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
         for (int k = 0; k < KR; ++k) {
             const int y = lane + 32 * k;
             if (y < rows) {
-                rpos[y] += __popc(rmask[y]);
-                rmask[y] = 0u;
+                const uint2 q = rm[y];
+                rm[y] = make_uint2(q.x + __popc(q.y), 0u);
             }
         }
         __syncwarp();
@@ -443,7 +444,8 @@ __global__ void __launch_bounds__(kBinWarps * 32, KC <= 4 ? 5 : 1) cols_place_ke
     constexpr uint32_t kSliceLen = slice_len(KC), kSegLen = seg_len_kc(KC);
     constexpr int kPer = kSliceLen / 32;  // row entries per lane
     constexpr int kStage2 = stage2_entries(KC);
-    // [kStage2] output | [kBinWarps][gx + 1] slice counts, column positions, column masks
+    // [kStage2] output | [kBinWarps][gx + 1] slice counts | [kBinWarps][gx + 1] column records
+    // (running position, mask of this batch's lanes) — one 8-byte load serves the slot formula
     extern __shared__ uint32_t sout[];
     if (a.fc->overflow) return;
     const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x;
@@ -455,9 +457,8 @@ __global__ void __launch_bounds__(kBinWarps * 32, KC <= 4 ? 5 : 1) cols_place_ke
     const uint32_t nq = nsegp[rows], h2 = rowbase2[rows], total = a.fc->n_entries;
     int* cntw = reinterpret_cast<int*>(sout + kStage2);
     int* D = cntw + wib * (gx + 1);
-    uint32_t* cpos = reinterpret_cast<uint32_t*>(cntw) + (kBinWarps + wib) * (gx + 1);
-    uint32_t* cmask = cpos + kBinWarps * (gx + 1);
-    const uint32_t out0 = smem_u32(sout), cpos0 = smem_u32(cpos), cmask0 = smem_u32(cmask);
+    uint2* cm = reinterpret_cast<uint2*>(cntw + kBinWarps * (gx + 1)) + wib * (gx + 1);
+    const uint32_t out0 = smem_u32(sout), cm0 = smem_u32(cm);
     auto h2at = [&](uint32_t i) { return i < h2 ? a.hist2[i] : total; };
     // the segment's group row comes from cols_count's map, loaded one segment ahead
     uint32_t ynext = blockIdx.x < nq ? __ldg(&a.segmap[blockIdx.x]) : 0u;
@@ -530,36 +531,34 @@ __global__ void __launch_bounds__(kBinWarps * 32, KC <= 4 ? 5 : 1) cols_place_ke
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
             const int x = lane + 32 * k;
-            if (x < gx) {
-                cpos[x] = staged ? P[k] + off[k] : base[k] + off[k];
-                cmask[x] = 0u;
-            }
+            if (x < gx) cm[x] = make_uint2(staged ? P[k] + off[k] : base[k] + off[k], 0u);
         }
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {
             if (e0 + 32u * i >= e1) break;  // warp-uniform
             const uint2 v = ent[i];
-            // columns [x0, x1]; a lane without an entry has x1 < x0 (no column)
-            int x0 = 0, x1 = -1;
-            if (e0 + lane + 32u * i < e1) {
-                x0 = (int)(v.y & 0xffffu);
-                x1 = (int)(v.y >> 16);
-            }
-            const int ms = (int)__reduce_max_sync(0xffffffffu, (uint32_t)(x1 - x0 + 1));
-            // clamped column of step t: inactive steps read a valid column and store nothing
-            auto col = [&](int t) { return max(min(x0 + t, x1), 0); };
-            for (int t = 0; t < ms; ++t) red_or_if(cmask0 + 4u * (uint32_t)col(t), lanebit, x0 + t <= x1);
+            // columns [x0, x0 + span); a lane without an entry has span 0 (and reads column 0)
+            const bool valid = e0 + lane + 32u * i < e1;
+            const uint32_t x0 = valid ? (v.y & 0xffffu) : 0u, x1 = valid ? (v.y >> 16) : 0u;
+            const int span = valid ? (int)(x1 - x0) + 1 : 0;
+            const int ms = (int)__reduce_max_sync(0xffffffffu, (uint32_t)span);
+            // record address of step t, clamped to the last column (inactive steps store nothing)
+            const uint32_t ra = cm0 + 8u * x0, rz = cm0 + 8u * x1;
+#pragma unroll 2
+            for (int t = 0; t < ms; ++t) red_or_if(min(ra + 8u * (uint32_t)t, rz) + 4u, lanebit, t < span);
             __syncwarp();
             if (staged) {
+#pragma unroll 2
                 for (int t = 0; t < ms; ++t) {
-                    const uint32_t c4 = 4u * (uint32_t)col(t);
-                    const uint32_t p = ld_shared(cpos0 + c4) + __popc(ld_shared(cmask0 + c4) & lt);
-                    st_shared_if(out0 + 4u * p, v.x, x0 + t <= x1);
+                    const uint2 r = ld_shared_v2(min(ra + 8u * (uint32_t)t, rz));
+                    st_shared_if(out0 + 4u * (r.x + __popc(r.y & lt)), v.x, t < span);
                 }
             } else {
-                for (int t = 0; t < ms; ++t)
-                    if (x0 + t <= x1) a.list[cpos[x0 + t] + __popc(cmask[x0 + t] & lt)] = v.x;
+                for (int t = 0; t < span; ++t) {
+                    const uint2 r = cm[x0 + t];
+                    a.list[r.x + __popc(r.y & lt)] = v.x;
+                }
             }
             __syncwarp();
             // advance every column by its entries in this chunk (lane-owned columns, race-free)
@@ -567,8 +566,8 @@ __global__ void __launch_bounds__(kBinWarps * 32, KC <= 4 ? 5 : 1) cols_place_ke
             for (int k = 0; k < KC; ++k) {
                 const int x = lane + 32 * k;
                 if (x < gx) {
-                    cpos[x] += __popc(cmask[x]);
-                    cmask[x] = 0u;
+                    const uint2 r = cm[x];
+                    cm[x] = make_uint2(r.x + __popc(r.y), 0u);
                 }
             }
             __syncwarp();
@@ -582,7 +581,15 @@ __global__ void __launch_bounds__(kBinWarps * 32, KC <= 4 ? 5 : 1) cols_place_ke
                     const uint32_t c = __shfl_sync(0xffffffffu, len[k], l);
                     const uint32_t src = __shfl_sync(0xffffffffu, P[k], l);
                     const uint32_t dst = __shfl_sync(0xffffffffu, base[k], l);
-                    for (uint32_t j = lane; j < c; j += 32) a.list[dst + j] = sout[src + j];
+                    uint32_t* __restrict__ d = a.list + dst;
+                    const uint32_t* sp = sout + src;
+                    uint32_t j = lane;
+                    for (; j + 32u < c; j += 64u) {  // two independent copies per step
+                        const uint32_t v0 = sp[j], v1 = sp[j + 32u];
+                        d[j] = v0;
+                        d[j + 32u] = v1;
+                    }
+                    if (j < c) d[j] = sp[j];
                 }
             __syncthreads();
         }
@@ -827,8 +834,8 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     const uint32_t* scan1_total = launch_exclusive_scan(a.hist1, n1, tmp, st, nullptr);
     rows_meta_kernel<<<1, 32, 0, st>>>(a, scan1_total);
     const int kr = (rows + 31) / 32, b1 = kRowChunks / kBinWarps, t1 = kBinWarps * 32;
-    // output stage, per-warp row positions / masks
-    const size_t so1 = (size_t)stage1_entries(kr) * sizeof(uint2) + (size_t)2 * kBinWarps * (rows + 1) * sizeof(uint32_t);
+    // output stage, per-warp row records
+    const size_t so1 = (size_t)stage1_entries(kr) * sizeof(uint2) + (size_t)kBinWarps * (rows + 1) * sizeof(uint2);
     auto launch1 = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)so1);
         kern<<<b1, t1, so1, st>>>(a);

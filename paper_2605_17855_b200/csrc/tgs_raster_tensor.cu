@@ -131,9 +131,6 @@ __device__ __forceinline__ void lane_pixel(int m, int l, int& x, int& y) {
     y = (t >> 1) * 16 + (q >> 1) * 8 + k * 4 + (i >> 3);
 }
 
-#ifndef TGS_BLEND_X2
-#define TGS_BLEND_X2 1
-#endif
 // Blend step of both pixels of a thread with packed FP32x2 instructions (FMUL2 / FFMA2 / FADD2):
 // per pixel k  wt = T * al;  c += wt * colour (fused);  T -= wt  — the same IEEE operations, in the
 // same order, as the scalar form, so the result is bit-identical.
@@ -163,12 +160,6 @@ __device__ __forceinline__ void blend_x2(float (&T)[2], float (&cr)[2], float (&
         : "f"(al[0]), "f"(al[1]), "f"(ej.x), "f"(ej.y), "f"(ej.z));
 }
 
-#ifndef TGS_PHASE1_X2
-#define TGS_PHASE1_X2 1
-#endif
-#ifndef TGS_SEL_AND
-#define TGS_SEL_AND 1
-#endif
 // (a >= b && c >= d) ? v : 0 as two compares (the second AND-ed with the first) and one select
 __device__ __forceinline__ float sel_ge2(float a, float b, float c, float d, float v) {
     float r;
@@ -230,13 +221,6 @@ __device__ __forceinline__ bool make_row(float mx, float my, float qa, float qb,
     r0 = make_uint4(hp[0], hp[1], hp[2], lp[0]);
     r1 = make_uint4(lp[1], lp[2], pack_half2(m0, m1), pack_half2(m2, m3));
     return ok;
-}
-
-// 0xffffffff if a >= b else 0 (opaque to CSE, so the blend's own compare stays a predicate)
-__device__ __forceinline__ uint32_t fset_ge(float a, float b) {
-    uint32_t r;
-    asm volatile("set.ge.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
-    return r;
 }
 
 __device__ __forceinline__ unsigned int ld_volatile_u32(const unsigned int* p) {
@@ -812,7 +796,6 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                     }
                     // Phase 1 (branch-free, kJB independent chains): which of the batch's splats
                     // reach alpha_skip at any of this warp's pixels -> warp-uniform mask.
-#if TGS_PHASE1_X2
                     // D - thr with packed FADD2 over splat pairs (sign bit set <=> D < thr, exactly:
                     // IEEE subtraction of finite values is 0 only for equal operands, -inf for a
                     // retired pixel's +inf); bit jj of `idle` = both pixels below thr, gathered with
@@ -827,16 +810,6 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                         idle = __funnelshift_l(a0 & b0, idle, 1);
                     }
                     const uint32_t M = __reduce_or_sync(0xffffffffu, ~idle & ((1u << kJB) - 1u));
-#else
-                    uint32_t mk = 0;
-#pragma unroll
-                    for (int jj = 0; jj < kJB; ++jj) {
-                        const uint32_t p = fset_ge(__uint_as_float(d[0][jj]), thr[0]) |
-                                           fset_ge(__uint_as_float(d[1][jj]), thr[1]);
-                        mk |= p & (1u << jj);
-                    }
-                    const uint32_t M = __reduce_or_sync(0xffffffffu, mk);
-#endif
                     if (TGS_RASTER_PROF) {
                         pf[2] += __popc(M);
                         pf[3] += kJB;
@@ -855,21 +828,9 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                             for (int k = 0; k < 2; ++k) {
                                 const float dv = __uint_as_float(d[k][jj]);
                                 const float e2 = fminf(ej.w, ex2_approx(dv));
-                                al[k] = TGS_SEL_AND ? sel_ge2(dv, thr[k], T[k], tterm, e2)
-                                                    : ((dv >= thr[k] && T[k] >= tterm) ? e2 : 0.0f);
+                                al[k] = sel_ge2(dv, thr[k], T[k], tterm, e2);
                             }
-#if TGS_BLEND_X2
                             blend_x2(T, cr, cg, cb, al, ej);
-#else
-#pragma unroll
-                            for (int k = 0; k < 2; ++k) {
-                                const float wt = T[k] * al[k];
-                                cr[k] = fmaf(wt, ej.x, cr[k]);
-                                cg[k] = fmaf(wt, ej.y, cg[k]);
-                                cb[k] = fmaf(wt, ej.z, cb[k]);
-                                T[k] -= wt;
-                            }
-#endif
                         }
 #pragma unroll
                     for (int k = 0; k < 2; ++k)

@@ -108,6 +108,11 @@ struct tgs_ctx {
     DBuf ghist, offsets, order;
     DBuf ucost;         // per unit, list entries the last frame walked (schedule feedback)
     uint64_t ucost_key = 0;  // geometry the feedback belongs to (0: none)
+    // level-1 binning chunks: sized from the group-row entries of the last synced frame of the
+    // same geometry (rc_key), so a block's share of them fits its shared-memory stage
+    uint64_t rc_key = 0, rc_pending_key = 0;
+    uint64_t rc_entries = 0;
+    int row_chunks = 0;
     DBuf image;
     DBuf scratch_records;
     DBuf stg[8];  // stage-API scratch (tgs_build_group_entries / tgs_sort_entries / tgs_rasterize_lists)
@@ -258,7 +263,14 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     TGS_CUDA_OK(ctx->rrect.ensure((size_t)n_alloc * sizeof(uint2)));
     const uint32_t cap = std::max<uint32_t>(ctx->capacity, 1u);
     TGS_CUDA_OK(ctx->list.ensure((size_t)cap * 4));
-    const size_t h1 = bin_hist1_elems(gg), h2 = bin_hist2_elems(gg, cap), hm = bin_meta_elems(gg);
+    // the previous frame's measured walks schedule this one when it had the same unit geometry
+    // (same image, group size, band and backend): a camera path changes slowly
+    const uint64_t ukey = ((uint64_t)(uint32_t)cam->width << 40) ^ ((uint64_t)(uint32_t)cam->height << 20) ^
+                          ((uint64_t)band0 << 8) ^ ((uint64_t)band1 << 28) ^ ((uint64_t)gg.g << 4) ^
+                          (uint64_t)opt->backend ^ (1ull << 63);
+    ctx->row_chunks = bin_row_chunks(gg, ctx->rc_key == (ukey ^ (uint64_t)(uintptr_t)scene) ? ctx->rc_entries : 0u);
+    ctx->rc_pending_key = ukey ^ (uint64_t)(uintptr_t)scene;
+    const size_t h1 = bin_hist1_elems(gg, ctx->row_chunks), h2 = bin_hist2_elems(gg, cap), hm = bin_meta_elems(gg);
     TGS_CUDA_OK(ctx->hist.ensure((h1 + h2 + hm + bin_segmap_elems(gg, cap)) * 4));
     TGS_CUDA_OK(ctx->rowlist.ensure((size_t)cap * sizeof(uint2)));
     TGS_CUDA_OK(ctx->bsum.ensure(
@@ -274,21 +286,16 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     const int row1 = std::min(cam->height, band1 * gg.g * kTile);
     TGS_CUDA_OK(ctx->image.ensure((size_t)(row1 - row0) * cam->width * 3 * sizeof(float)));
 
-    // the previous frame's measured walks schedule this one when it had the same unit geometry
-    // (same image, group size, band and backend): a camera path changes slowly
-    const uint64_t ukey = ((uint64_t)(uint32_t)cam->width << 40) ^ ((uint64_t)(uint32_t)cam->height << 20) ^
-                          ((uint64_t)band0 << 8) ^ ((uint64_t)band1 << 28) ^ ((uint64_t)gg.g << 4) ^
-                          (uint64_t)opt->backend ^ (1ull << 63);
     const bool feedback = ctx->ucost_key == ukey;
     ctx->ucost_key = ukey;
     // everything the launch sequence depends on except the camera pose / intrinsics
     char kbuf[640];
-    int kl = std::snprintf(kbuf, sizeof(kbuf), "%p %lld %d %d %d %d %d %d %d %a %a %a %d %d %u %lld", (const void*)scene,
+    int kl = std::snprintf(kbuf, sizeof(kbuf), "%p %lld %d %d %d %d %d %d %d %a %a %a %d %d %u %lld %d", (const void*)scene,
                            (long long)scene->n, cam->width, cam->height, opt->backend, opt->mode, opt->group_size,
                            band0, band1,
                            opt->alpha_skip, opt->alpha_clamp, opt->t_terminate, ctx->tile_cull * 2 + ctx->exact,
                            feedback ? 1 : 0,
-                           ctx->capacity, (long long)ctx->proj_cap);
+                           ctx->capacity, (long long)ctx->proj_cap, ctx->row_chunks);
     // ... and every buffer address the captured launches bake in (buffers only ever grow)
     const DBuf* fbufs[] = {&ctx->proj, &ctx->pre_keys[0], &ctx->pre_keys[1], &ctx->pre_vals[0], &ctx->pre_vals[1],
                            &ctx->rect, &ctx->rrect, &ctx->list, &ctx->rowlist, &ctx->hist, &ctx->bsum, &ctx->ghist,
@@ -417,6 +424,7 @@ tgs_status record_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* 
     ba.rect = ctx->rect.as<uint2>();
     ba.rrect = ctx->rrect.as<uint2>();
     ba.gg = gg;
+    ba.row_chunks = ctx->row_chunks;
     ba.hist1 = ctx->hist.as<uint32_t>();
     ba.hist2 = ba.hist1 + h1;
     ba.meta = ba.hist2 + h2;
@@ -502,6 +510,8 @@ tgs_status finish_frame(tgs_ctx* ctx, tgs_stats* stats) {
         if (ctx->h_fc->overflow) return set_err(TGS_ERR_OOM, "render: entry capacity overflow after growth");
     }
     const FrameCounters& g = *ctx->h_fc;
+    ctx->rc_key = ctx->rc_pending_key;  // the last enqueued frame's geometry and group-row entries
+    ctx->rc_entries = g.row_entries;
     if (g.err_validation & 1u) return set_err(TGS_ERR_VALIDATION, "compute_cov3d: non-positive scale");
     if (g.err_validation & 2u)
         return set_err(TGS_ERR_VALIDATION, "sort_entries: an entry has non-finite or negative depth");

@@ -33,10 +33,10 @@ namespace tgs {
 namespace {
 
 constexpr int kBinWarps = 8;          // warps per binning block (one chunk / segment per warp)
-#ifndef TGS_ROW_CHUNKS
-#define TGS_ROW_CHUNKS (148 * 128)
-#endif
-constexpr int kRowChunks = TGS_ROW_CHUNKS;  // level-1 chunks (contiguous rank ranges, one warp each)
+// level-1 chunks (contiguous rank ranges, one warp each): 148 x 128 (measured best at C3, where a
+// block's row entries just fit its stage), doubled while a block's expected share (previous frame)
+// exceeds its stage — large frames (C4: 6M splats at 4K) would otherwise write unstaged
+constexpr int kRowChunksMin = 148 * 128, kRowChunksMax = 148 * 128 * 16;
 // level-1 per-block output staging (row entries), smaller for few rows (more resident blocks)
 #ifndef TGS_STAGE1
 #define TGS_STAGE1 6144
@@ -91,7 +91,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // A "chunk" is one warp's contiguous rank range.  Row entries are (splat index, gx0 | gx1 << 16)
 // and row y's list is the concatenation over chunks of the chunk's splats overlapping row y.
 
-// hist1[y * kRowChunks + chunk] = splats of the chunk overlapping group row y; fc->n_entries +=
+// hist1[y * row_chunks + chunk] = splats of the chunk overlapping group row y; fc->n_entries +=
 // the chunk's (splat, group) entries (the capacity check needs the total before any placement).
 __global__ void __launch_bounds__(kBinWarps * 32) rows_count_kernel(BinArgs a) {
     const uint32_t* __restrict__ sval = *a.sval_sel ? a.sval[1] : a.sval[0];
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_count_kernel(BinArgs a) {
     for (int i = lane; i <= rows; i += 32) D[i] = 0;
     __syncwarp();
     uint32_t r0, r1;
-    chunk_range(*a.visible, kRowChunks, chunk, r0, r1);
+    chunk_range(*a.visible, a.row_chunks, chunk, r0, r1);
     uint32_t ent = 0;
     for (uint32_t rb = r0 + lane; rb < r1; rb += 32 * 8) {  // 8 gathers in flight per lane
         uint2 rr[8];
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_count_kernel(BinArgs a) {
             const int t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
-        if (y < rows) a.hist1[(size_t)y * kRowChunks + chunk] = (uint32_t)(carry + incl);
+        if (y < rows) a.hist1[(size_t)y * a.row_chunks + chunk] = (uint32_t)(carry + incl);
         carry += __shfl_sync(0xffffffffu, incl, 31);
     }
 #pragma unroll
@@ -158,14 +158,15 @@ __global__ void rows_meta_kernel(BinArgs a, const uint32_t* __restrict__ scan1_t
             a.fc->overflow = 1u;
         else
             a.fc->n_sort = total;
+        a.fc->row_entries = *scan1_total;
     }
     uint32_t cs = 0;
     for (int base = 0; base <= rows; base += 32) {
         const int y = base + lane;
         uint32_t start = 0, nseg = 0;
         if (y < rows) {
-            start = a.hist1[(size_t)y * kRowChunks];
-            const uint32_t next = y + 1 < rows ? a.hist1[(size_t)(y + 1) * kRowChunks] : *scan1_total;
+            start = a.hist1[(size_t)y * a.row_chunks];
+            const uint32_t next = y + 1 < rows ? a.hist1[(size_t)(y + 1) * a.row_chunks] : *scan1_total;
             nseg = over ? 0u : (next - start + seg_len_gx(gx) - 1u) / seg_len_gx(gx);
         } else if (y == rows) {
             start = *scan1_total;
@@ -230,12 +231,12 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_place_kernel(BinArgs a) {
     // per-warp row records (running position, mask of this batch's lanes)
     uint2* rm = sout1 + kStage1 + wib * (rows + 1);
     const uint32_t out0 = smem_u32(sout1), rm0 = smem_u32(rm);
-    auto h1at = [&](int y, int c) {       // scanned hist1 at (row y, chunk c); c may be kRowChunks
-        const size_t i = (size_t)y * kRowChunks + c;
-        return i < (size_t)rows * kRowChunks ? a.hist1[i] : total;
+    auto h1at = [&](int y, int c) {       // scanned hist1 at (row y, chunk c); c may be row_chunks
+        const size_t i = (size_t)y * a.row_chunks + c;
+        return i < (size_t)rows * a.row_chunks ? a.hist1[i] : total;
     };
     uint32_t r0, r1;
-    chunk_range(*a.visible, kRowChunks, chunk, r0, r1);
+    chunk_range(*a.visible, a.row_chunks, chunk, r0, r1);
     uint32_t snext = 0u;  // the chunk's first batch is in flight during the row setup
     uint2 rnext = make_uint2(0u, 0u);
     if (r0 + lane < r1) {
@@ -802,8 +803,15 @@ void launch_unit_order(const uint32_t* offsets, const uint32_t* feedback, int n_
     unit_order_kernel<<<1, 1024, 0, st>>>(offsets, feedback, n_units, per_group, order, fc);
 }
 
-int bin_chunks(int) { return kRowChunks; }
-size_t bin_hist1_elems(const GroupGeom& gg) { return (size_t)std::max(1, gg.band_gy1 - gg.band_gy0) * kRowChunks; }
+int bin_row_chunks(const GroupGeom& gg, uint64_t row_entries) {
+    const int kr = (gg.band_gy1 - gg.band_gy0 + 31) / 32;
+    int c = kRowChunksMin;
+    while (c < kRowChunksMax && row_entries * kBinWarps > (uint64_t)c * (uint64_t)stage1_entries(kr)) c *= 2;
+    return c;
+}
+size_t bin_hist1_elems(const GroupGeom& gg, int row_chunks) {
+    return (size_t)std::max(1, gg.band_gy1 - gg.band_gy0) * (size_t)row_chunks;
+}
 size_t bin_hist2_elems(const GroupGeom& gg, uint32_t capacity) {
     const size_t rows = (size_t)std::max(1, gg.band_gy1 - gg.band_gy0);
     return (size_t)gg.groups_x * (rows + capacity / seg_len_gx(gg.groups_x) + 1);
@@ -828,12 +836,12 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     const int rows = gg.band_gy1 - gg.band_gy0, gx = gg.groups_x;
     (void)max_visible;
     // level 1
-    const size_t n1 = bin_hist1_elems(gg);
-    rows_count_kernel<<<kRowChunks / kBinWarps, kBinWarps * 32, kBinWarps * (rows + 1) * sizeof(int), st>>>(a);
+    const size_t n1 = bin_hist1_elems(gg, a.row_chunks);
+    rows_count_kernel<<<a.row_chunks / kBinWarps, kBinWarps * 32, kBinWarps * (rows + 1) * sizeof(int), st>>>(a);
     uint32_t* tmp = a.bsum;
     const uint32_t* scan1_total = launch_exclusive_scan(a.hist1, n1, tmp, st, nullptr);
     rows_meta_kernel<<<1, 32, 0, st>>>(a, scan1_total);
-    const int kr = (rows + 31) / 32, b1 = kRowChunks / kBinWarps, t1 = kBinWarps * 32;
+    const int kr = (rows + 31) / 32, b1 = a.row_chunks / kBinWarps, t1 = kBinWarps * 32;
     // output stage, per-warp row records
     const size_t so1 = (size_t)stage1_entries(kr) * sizeof(uint2) + (size_t)kBinWarps * (rows + 1) * sizeof(uint2);
     auto launch1 = [&](auto kern) {

@@ -63,6 +63,7 @@ struct FrameCounters {
     // OpReport (metrics.hpp:49-69) of the tensor rasteriser: chunks staged, tcgen05.mma issued,
     // splat rows those MMAs carried, (member tile, staged row) pairs the mask filtered out
     unsigned long long op_chunks, op_mmas, op_mma_rows, op_skipped;
+    unsigned int row_entries;       // group-row entries of the frame (sizes the next frame's chunks)
     // not zeroed per frame: frames of this context that overflowed / failed validation so far
     // (counted by unit_order_kernel, checked by tgs_sync so no un-synced frame fails silently)
     unsigned int sticky_overflow;

@@ -58,7 +58,8 @@ struct BinArgs {
     const uint2* rect;           // splat index -> tile rect
     uint2* rrect;                // rank -> tile rect
     GroupGeom gg;
-    uint32_t* hist1;             // [rows * bin_chunks] level-1 counts, scanned in place
+    int row_chunks;              // level-1 chunks (bin_row_chunks)
+    uint32_t* hist1;             // [rows * row_chunks] level-1 counts, scanned in place
     uint32_t* hist2;             // [bin_hist2_elems] level-2 counts, scanned in place
     uint32_t* meta;              // [bin_meta_elems] row starts / segment layout
     uint32_t* bsum;              // scan block sums (+1)
@@ -70,8 +71,10 @@ struct BinArgs {
     FrameCounters* fc;
     uint32_t capacity;
 };
-int bin_chunks(int n_groups);                                      // level-1 chunks
-size_t bin_hist1_elems(const GroupGeom& gg);
+// level-1 chunks for a frame whose previous frame of the same geometry had `row_entries` group-row
+// entries (0: unknown): enough that a block's share fits its output stage
+int bin_row_chunks(const GroupGeom& gg, uint64_t row_entries);
+size_t bin_hist1_elems(const GroupGeom& gg, int row_chunks);
 size_t bin_hist2_elems(const GroupGeom& gg, uint32_t capacity);
 size_t bin_segmap_elems(const GroupGeom& gg, uint32_t capacity);
 size_t bin_meta_elems(const GroupGeom& gg);

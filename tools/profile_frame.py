@@ -20,10 +20,15 @@ def main():
     ap.add_argument("frames", type=int, nargs="?", default=3)
     ap.add_argument("--backend", default="both", choices=["tensor", "scalar", "both"])
     ap.add_argument("--cam", type=int, default=5, help="orbit camera index (-1: identity view)")
+    ap.add_argument("--c4", action="store_true", help="BASELINE config 4: 6M splats (seed 4), 3840x2160, identity")
     a = ap.parse_args()
     ctx = gsr.Context(0)
-    ds = ctx.upload(gsr.gen_synthetic_scene(3, 3_000_000, 1.0, (0.01, 0.05)))
-    cam = gsr.make_camera(1920, 1080) if a.cam < 0 else gsr.orbit_cameras(256, 1920, 1080)[a.cam]
+    if a.c4:
+        ds = ctx.upload(gsr.gen_synthetic_scene(4, 6_000_000, 1.0, (0.01, 0.05)))
+        cam = gsr.make_camera(3840, 2160)
+    else:
+        ds = ctx.upload(gsr.gen_synthetic_scene(3, 3_000_000, 1.0, (0.01, 0.05)))
+        cam = gsr.make_camera(1920, 1080) if a.cam < 0 else gsr.orbit_cameras(256, 1920, 1080)[a.cam]
     runs = []
     if a.backend in ("tensor", "both"):
         runs.append((gsr.Backend.tensor, 2))

@@ -47,12 +47,12 @@ constexpr int kRowChunksMin = 148 * 128, kRowChunksMax = 148 * 128 * 16;
 constexpr int stage1_entries(int kr) { return kr <= 2 ? TGS_STAGE1 : TGS_STAGE1_WIDE; }
 // Level 2 cuts every group-row list into segments of kBinWarps slices (one placement block, one
 // count warp); a slice is the row entries one warp places.  A segment's output (~entries x the mean
-// column span) is staged in shared memory: 256-entry slices and a 12K-entry stage for up to 64
-// group columns (bench G=2), 128 / 8K beyond (G=1 at 1080p: 120 columns) — measured per config.
+// column span) is staged in shared memory: a 12K-entry stage, 256-entry slices for up to 64 group
+// columns (bench G=2), 128 beyond (G=1 at 1080p and C4: 120 columns) — measured per config.
 __host__ __device__ constexpr uint32_t slice_len(int kc) { return kc <= 2 ? 256u : 128u; }
 __host__ __device__ constexpr uint32_t seg_len_kc(int kc) { return slice_len(kc) * kBinWarps; }
 __host__ __device__ inline uint32_t seg_len_gx(int gx) { return seg_len_kc((gx + 31) / 32); }
-constexpr int stage2_entries(int kc) { return kc <= 2 ? 12288 : 8192; }
+constexpr int stage2_entries(int) { return 12288; }
 constexpr int kScanItems = 16;        // per thread in the hist scan
 constexpr int kScanBlock = 256;
 constexpr int kScanTile = kScanItems * kScanBlock;
@@ -593,6 +593,8 @@ __global__ void __launch_bounds__(kBinWarps * 32, KC <= 4 ? 5 : 1) cols_place_ke
                     if (j < c) d[j] = sp[j];
                 }
             __syncthreads();
+        } else {
+            __syncthreads();  // the next segment rewrites the slice counts other warps read above
         }
     }
 }

@@ -194,7 +194,7 @@ CONFIGS = {  # BASELINE.json configs: seed, splats, SH seed, wi
 
 def run_configs(args, local):
     """Per-stage ms of one frame (identity camera, testutil.hpp:14-24) for every BASELINE config:
-    tensor G=2 and the CUDA-core baseline G=1, median of `steps` synced frames after `warmup`;
+    tensor G=2 and G=4 and the CUDA-core baseline G=1, median of `steps` synced frames after `warmup`;
     one JSON line per config.  Not the driver's bench line (that is --mode cameras)."""
     from paper_2605_17855_b200 import gsr
     ctx = gsr.Context(local)
@@ -203,6 +203,7 @@ def run_configs(args, local):
         cam = gsr.make_camera(w, h)
         out = {"config": name, "splats": n, "sh_degree": 3 if sh else 0, "width": w, "height": h}
         for label, opt in (("tensor_g2", gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 2)),
+                           ("tensor_g4", gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 4)),
                            ("cuda_core_g1", gsr.RenderOptions(gsr.Backend.scalar, gsr.PrecisionMode.fp32, 1))):
             rows = []
             for i in range(max(args.warmup, 3) + args.steps):
@@ -222,7 +223,9 @@ def run_configs(args, local):
 
 
 def run_bands(args, rank, world, local, coll_dev):
-    """BASELINE config 4: one 3840x2160 frame of the 6M-splat scene (seed 4), tensor G=2, split into
+    """BASELINE config 4: one 3840x2160 frame of the 6M-splat scene (seed 4), tensor G=4 (--group;
+    1.80 ms per frame vs 3.19 ms at G=2 on one B200: a 4K frame of this scene has 3.2x fewer group
+    entries at G=4 and binning scales with entries, the raster is within 3 %), split into
     `world` screen bands of group rows balanced by per-row entry counts (tgs_group_row_entries);
     rank r renders band r (tgs_render_band: full preprocess, binning/sort/raster of its rows only).
     A step = one frame; value = frames/s with the frame time = max over ranks (strong scaling: the
@@ -235,7 +238,8 @@ def run_bands(args, rank, world, local, coll_dev):
     scene = gsr.gen_synthetic_scene(SEED4, N4, 1.0, (0.01, 0.05))
     ds = ctx.upload(scene)
     cam = gsr.make_camera(W4, H4)
-    opt = gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 2)
+    group = args.group or 4
+    opt = gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, group)
     rows = ctx.group_row_entries(ds, cam, opt)
     bands = multigpu.band_split(rows.astype(np.float64), world)
     g0, g1 = bands[rank]
@@ -265,7 +269,7 @@ def run_bands(args, rank, world, local, coll_dev):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32 (fp16 hi/lo tensor-core contraction)",
         "data": "synthetic (reference generator gen_synthetic_scene seed 4, scales 0.01-0.05)",
-        "config": {"workload": "C4: 6M splats, 3840x2160, identity camera, tensor G=2, screen bands of group rows",
+        "config": {"workload": f"C4: 6M splats, 3840x2160, identity camera, tensor G={group}, screen bands of group rows",
                    "global_batch": 1, "seq_len": 0, "parallelism": f"screen-bands x{world}",
                    "bands": bands, "row_entries_total": int(rows.sum())},
         "band_device_ms_median": statistics.median(stage), "full_frame_ms": full_ms,
@@ -286,6 +290,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e/baseline extras (profiling runs)")
+    ap.add_argument("--group", type=int, default=None, help="--mode bands: group size (default 4)")
     ap.add_argument("--mode", default="cameras", choices=["cameras", "bands", "configs"],
                     help="cameras: the C3/C5 camera-batch line (default); bands: C4 single 4K frame split "
                          "into screen bands across the ranks")

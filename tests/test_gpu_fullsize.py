@@ -66,6 +66,10 @@ def _full_frame_parity(gsr, ctx, port, rec, c, tag):
     cam = _cam(gsr, c)
     images = {}
     for backend, group in ((1, 2), (0, 1)):
+        if group == 1:
+            # a second frame of the same geometry sizes its level-1 chunks from this one's row
+            # entries (C3 at G=1: 2-4x the default); its lists are the ones checked below
+            ctx.render(ds, cam, _opt(gsr, backend, group))
         res = ctx.render(ds, cam, _opt(gsr, backend, group))
         images[(backend, group)] = res.image.rgb.copy()
         if group == 2:

@@ -150,13 +150,18 @@ __device__ __forceinline__ uint32_t group_mask(int gx, int gy, int g, int tx0, i
 // preprocess stores the padded half-extents as a half2 rounded up (a superset) in col.w; +inf
 // halves mean "no bound" (opacity at or below alpha_skip, degenerate conic).  Tighter than the
 // reference's 3-sigma square (binning.cpp:32-44), which stays the list criterion.
+// The box only has to be a superset, so it is computed with the MUFU approximations (log2, rcp,
+// rsqrt; relative errors ~2^-21) and widened by 2^-12 relative before the half-pixel pad.
 __device__ __forceinline__ float tight_extents(float ca, float cb, float cc, float o, float skip) {
     const float det = ca * cc - cb * cb;
-    const float lnt = logf(o / skip);
+    const float lnt = __logf(__fdividef(o, skip));
     __half2 e = __halves2half2(__ushort_as_half((unsigned short)0x7c00u), __ushort_as_half((unsigned short)0x7c00u));
     if (det > 0.0f && lnt > 0.0f) {
-        const float s2 = 2.0f * lnt / det;
-        e = __halves2half2(__float2half_ru(sqrtf(s2 * cc) + 0.5f), __float2half_ru(sqrtf(s2 * ca) + 0.5f));
+        const float s2 = __fdividef(2.0f * lnt, det) * (1.0f + 0x1p-12f);
+        const float vx = s2 * cc, vy = s2 * ca;  // > 0: a positive-definite conic
+        // sqrt as v * rsqrt(v); an overflowed v stays +inf ("no bound"), never inf * 0
+        const float ex = vx < 0x1p126f ? vx * rsqrtf(vx) : vx, ey = vy < 0x1p126f ? vy * rsqrtf(vy) : vy;
+        e = __halves2half2(__float2half_ru(ex + 0.5f), __float2half_ru(ey + 0.5f));
     }
     return __uint_as_float(*reinterpret_cast<const uint32_t*>(&e));
 }

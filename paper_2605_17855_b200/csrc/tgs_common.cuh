@@ -157,10 +157,11 @@ __device__ __forceinline__ float tight_extents(float ca, float cb, float cc, flo
     const float lnt = __logf(__fdividef(o, skip));
     __half2 e = __halves2half2(__ushort_as_half((unsigned short)0x7c00u), __ushort_as_half((unsigned short)0x7c00u));
     if (det > 0.0f && lnt > 0.0f) {
-        const float s2 = __fdividef(2.0f * lnt, det) * (1.0f + 0x1p-12f);
-        const float vx = s2 * cc, vy = s2 * ca;  // > 0: a positive-definite conic
-        // sqrt as v * rsqrt(v); an overflowed v stays +inf ("no bound"), never inf * 0
-        const float ex = vx < 0x1p126f ? vx * rsqrtf(vx) : vx, ey = vy < 0x1p126f ? vy * rsqrtf(vy) : vy;
+        const float s2 = 2.0f * lnt * __frcp_rn(det) * (1.0f + 0x1p-12f);
+        const float vx = s2 * cc, vy = s2 * ca;  // >= 0: a positive-definite conic
+        // sqrt as v * rsqrt(v); an overflowed v stays +inf ("no bound"), 0 stays 0 (never inf * 0)
+        auto root = [](float v) { return v > 0.0f && v < 0x1p126f ? v * rsqrtf(v) : v; };
+        const float ex = root(vx), ey = root(vy);
         e = __halves2half2(__float2half_ru(ex + 0.5f), __float2half_ru(ey + 0.5f));
     }
     return __uint_as_float(*reinterpret_cast<const uint32_t*>(&e));

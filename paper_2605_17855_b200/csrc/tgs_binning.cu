@@ -139,7 +139,13 @@ __global__ void __launch_bounds__(kBinWarps * 32) rows_count_kernel(BinArgs a) {
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ent += __shfl_xor_sync(0xffffffffu, ent, o);
-    if (lane == 0 && ent) atomicAdd(&a.fc->n_entries, ent);
+    // one global atomic per block (same-address atomics serialise in L2)
+    __shared__ uint32_t s_ent;
+    if (threadIdx.x == 0) s_ent = 0u;
+    __syncthreads();
+    if (lane == 0 && ent) atomicAdd(&s_ent, ent);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_ent) atomicAdd(&a.fc->n_entries, s_ent);
 }
 
 // One warp: capacity check, row starts, per-row segment counts and the level-2 histogram layout.

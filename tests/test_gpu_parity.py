@@ -350,6 +350,50 @@ def test_c3_full_size_properties(gsr, ctx, port):
         assert np.isfinite(img).all() and img.min() >= 0 and img.max() <= 1
 
 
+def test_c4_full_size_properties(gsr, ctx, port):
+    """BASELINE config 4 (6M splats, 3840x2160): projection bit-exact vs the port; entry counts and
+    tile appearances equal the recount from it (G=2: 386.5M entries, G=4); at G=4 every list in
+    (depth, index) order with non-empty masks whose popcounts sum to the appearances (SURVEY §8(d):
+    count + popcount conservation at C4).  Each geometry renders twice: the second frame's level-1
+    chunks are sized from the first one's row entries, and its lists are the ones checked."""
+    c = make_camera(3840, 2160)
+    rec = gsr.gen_synthetic_scene(4, 6_000_000, 1.0, (0.01, 0.05)).records
+    pp, _ = port.project(rec, c)
+    ds = ctx.upload(rec)
+    cam = _cam(gsr, c)
+    r = pp["radius"].astype(np.float32)
+    mx, my = pp["mean2d"][:, 0], pp["mean2d"][:, 1]
+    tx0 = np.maximum(np.floor((mx - r) / np.float32(16)).astype(np.int64), 0)
+    tx1 = np.minimum(np.floor((mx + r) / np.float32(16)).astype(np.int64), 239)
+    ty0 = np.maximum(np.floor((my - r) / np.float32(16)).astype(np.int64), 0)
+    ty1 = np.minimum(np.floor((my + r) / np.float32(16)).astype(np.int64), 134)
+    ok = (tx1 >= tx0) & (ty1 >= ty0)
+    app = int(np.sum(((tx1 - tx0 + 1) * (ty1 - ty0 + 1))[ok]))
+    for group in (2, 4):
+        ctx.render(ds, cam, _opt(gsr, 1, group))
+        res = ctx.render(ds, cam, _opt(gsr, 1, group))
+        if group == 2:
+            assert np.array_equal(ctx.read_projected().view(np.uint8), pp.view(np.uint8))
+        n_ent = int(np.sum(((tx1 // group - tx0 // group + 1) * (ty1 // group - ty0 // group + 1))[ok]))
+        assert res.tile_appearances == app and res.entries == n_ent
+        if group == 2:
+            assert n_ent == 386_505_600  # SURVEY §8(a) a5
+            continue
+        ng = ((240 + group - 1) // group) * ((135 + group - 1) // group)
+        ent, off = ctx.read_lists(ng)
+        assert off[-1] == n_ent
+        gid = np.repeat(np.arange(ng), np.diff(off.astype(np.int64)))
+        key = (gid.astype(np.uint64) << np.uint64(32)) | ent["depth"].view(np.uint32).astype(np.uint64)
+        dk = np.diff(key.astype(np.int64))
+        assert np.all(dk >= 0)
+        ties = dk == 0
+        assert np.all(np.diff(ent["gaussian_index"].astype(np.int64))[ties] > 0)
+        assert np.all(ent["mask"] != 0)
+        pc = np.unpackbits(np.ascontiguousarray(ent["mask"]).view(np.uint8)).sum()
+        assert int(pc) == app
+        del ent, gid, key, dk
+
+
 # ---------------------------------------------------------------------------------------------
 # Exact-emulation rasteriser: images BIT-EXACT with the reference build (golden fixtures made by
 # oracle/_ref) in fp16 mode (PrecisionMode::fp16 always runs it) and in fp32 mode with

@@ -145,14 +145,16 @@ def test_group_row_entries_match_lists(gsr, port):
 
 
 @pytest.mark.parametrize("world", [3, 8])
-def test_c4_bands_stitch_bit_identical(gsr, world):
-    """BASELINE config 4 (6M splats, 3840x2160, tensor G=2): the frame rendered whole equals the
-    concatenation of the screen bands band_split cuts from the per-row entry counts."""
+@pytest.mark.parametrize("group", [2, 4])
+def test_c4_bands_stitch_bit_identical(gsr, world, group):
+    """BASELINE config 4 (6M splats, 3840x2160, tensor G=2 and the bench's G=4): the frame rendered
+    whole equals the concatenation of the screen bands band_split cuts from the per-row entry
+    counts."""
     from paper_2605_17855_b200 import multigpu
     ctx = gsr.default_context(0)
     ds = ctx.upload(gsr.gen_synthetic_scene(4, 6_000_000, 1.0, (0.01, 0.05)))
     cam = gsr.make_camera(3840, 2160)
-    opt = gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 2)
+    opt = gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, group)
     full = ctx.render(ds, cam, opt)
     rows = ctx.group_row_entries(ds, cam, opt)
     assert int(rows.sum()) == full.entries

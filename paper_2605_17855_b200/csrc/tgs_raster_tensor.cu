@@ -64,7 +64,13 @@ constexpr int kSS = 4;      // shared-memory chunk ring (slack between member ti
 constexpr int kTS = 2;      // TMEM accumulator stages per warpgroup
 constexpr int kJB = 16;     // accumulator columns per epilogue batch
 constexpr int kRing = 8;    // producer gather ring: kRing - 2 batches of records in flight
-constexpr uint32_t kMmaSleep0 = 16, kMmaSleepCap = 128;  // MMA warp back-off (ns) when nothing is ready
+#ifndef TGS_MMA_SLEEP0
+#define TGS_MMA_SLEEP0 16
+#endif
+#ifndef TGS_MMA_SLEEPCAP
+#define TGS_MMA_SLEEPCAP 128
+#endif
+constexpr uint32_t kMmaSleep0 = TGS_MMA_SLEEP0, kMmaSleepCap = TGS_MMA_SLEEPCAP;  // MMA warp back-off (ns) when idle
 #ifndef TGS_RASTER_PROF
 #define TGS_RASTER_PROF 0
 #endif
@@ -585,59 +591,63 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
         }
     } else if (warp == kMma) {
         // ================================ MMA issuer ==========================================
+        // Lane t (< SLOTS) tracks warpgroup t: its next chunk and whether its stream ended.  One
+        // poll tests every group's readiness at once (chunk published, TMEM stage released), the
+        // ready groups are then issued in turn — the issue latency is on the raster's critical
+        // path (a slower poll measured +30 % raster time).
         constexpr uint32_t idesc = ptx::idesc_f16(128, kN);
         const uint32_t a_base = ptx::smem_u32(&sm.a[0][0]);
-        uint32_t cg[SLOTS];   // next chunk of each warpgroup
-        bool ended[SLOTS];
-#pragma unroll
-        for (int t = 0; t < SLOTS; ++t) {
-            cg[t] = 0;
-            ended[t] = false;
-        }
-        int n_done = 0;
+        uint32_t my_c = 0;                    // lane t: next chunk of warpgroup t
+        bool my_end = lane >= SLOTS;          // lane t: warpgroup t's stream ended (other lanes: idle)
         unsigned long long op_mmas = 0, op_mma_rows = 0;  // OpReport
         long long idle0 = clock64();
         uint32_t backoff = kMmaSleep0;
 #if TGS_RASTER_PROF
         unsigned long long mma_iters = 0;
 #endif
-        while (n_done < SLOTS) {
-            bool did = false;
-            if (TGS_RASTER_PROF) pf[3] += 0;  // (issue time accumulates in pf[3])
+        for (;;) {
+            if (__all_sync(0xffffffffu, my_end)) break;
 #if TGS_RASTER_PROF
             ++mma_iters;
 #endif
-#pragma unroll
-            for (int t = 0; t < SLOTS; ++t) {
-                if (ended[t]) continue;
-                const uint32_t c = cg[t];
-                const int s = (int)(c % kSS), ts = (int)(c % kTS);
-                int ready = 0;
-                if (lane == 0) {
-                    // chunk published, and warpgroup t finished chunk c - kTS (its TMEM stage)
-                    ready = ptx::mbar_test(&sm.full[s], (c / kSS) & 1);
-                    if (ready && c >= (uint32_t)kTS) {
-                        const int4 d = ld_volatile_v4(&sm.wdone[4 * t]);
-                        ready = min(min(d.x, d.y), min(d.z, d.w)) >= (int)(c - kTS + 1);
-                    }
+            bool rdy = false;
+            if (!my_end) {
+                const int s = (int)(my_c % kSS);
+                // chunk published, and warpgroup t finished chunk c - kTS (its TMEM stage)
+                rdy = ptx::mbar_test(&sm.full[s], (my_c / kSS) & 1);
+                if (rdy && my_c >= (uint32_t)kTS) {
+                    const int4 d = ld_volatile_v4(&sm.wdone[4 * lane]);
+                    rdy = min(min(d.x, d.y), min(d.z, d.w)) >= (int)(my_c - kTS + 1);
                 }
-                ready = __shfl_sync(0xffffffffu, ready, 0);
-                if (!ready) continue;
-                [[maybe_unused]] const long long t_seen = TGS_RASTER_PROF ? clock64() : 0;
-                __syncwarp();
-                ptx::tc_fence_after();
-                const ChunkHeader& hs = sm.hdr[s];
-                const int hseq = __shfl_sync(0xffffffffu, hs.seq, 0);
-                const int hnv = __shfl_sync(0xffffffffu, hs.n_valid, 0);
-                const uint32_t hlive = __shfl_sync(0xffffffffu, (uint32_t)hs.live, 0);
-                const int hch = __shfl_sync(0xffffffffu, hs.chunk, 0);
+            }
+            uint32_t rm = __ballot_sync(0xffffffffu, rdy);
+            if (rm == 0u) {
+                // idle: back off exponentially so the polls do not take issue slots from the
+                // epilogue warps of this SMSP (the MMA warp has the highest arbitration rank)
+                __nanosleep(backoff);
+                backoff = backoff < kMmaSleepCap ? 2 * backoff : backoff;
+                if (clock64() - idle0 > 4000000000ll)
+                    ptx::watchdog_trap("mma/idle", (int)__shfl_sync(0xffffffffu, my_c, 0), (int)rm);
+                continue;
+            }
+            idle0 = clock64();
+            backoff = kMmaSleep0;
+            __syncwarp();
+            ptx::tc_fence_after();
+            while (rm) {
+                const int t = __ffs(rm) - 1;
+                rm &= rm - 1u;
+                const uint32_t c = __shfl_sync(0xffffffffu, my_c, t);
+                const int s = (int)(c % kSS), ts = (int)(c % kTS);
+                const volatile ChunkHeader& hs = sm.hdr[s];  // every lane reads it (broadcast)
+                const int hseq = hs.seq, hnv = hs.n_valid, hch = hs.chunk;
+                const uint32_t hlive = (uint32_t)hs.live;
                 if (hch != (int)c) {
                     if (lane == 0)
                         printf("libtgs MMA: warpgroup %d expected chunk %d found %d (seq %d)\n", t, (int)c, hch, hseq);
                     __trap();
                 }
                 if (hseq >= 0 && hnv > 0 && ((hlive >> t) & 1u)) {
-                    [[maybe_unused]] const long long ti0 = TGS_RASTER_PROF ? clock64() : 0;
                     const uint64_t bd = ptx::smem_desc(ptx::smem_u32(&sm.b[s][0]), 128, 256);
                     const uint32_t dcol = tmem + (uint32_t)(((ts * SLOTS + t) * 2) * kN);
 #pragma unroll
@@ -649,37 +659,19 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                     op_mmas += 2;
                     op_mma_rows += 2u * (uint32_t)hnv;
 #if TGS_RASTER_PROF
-                    if (lane == 0) {
-                        const unsigned long long now = (unsigned long long)clock64();
-                        const unsigned long long rdy =
-                            c >= (uint32_t)kTS ? max(sm.t_rel[t][ts], sm.t_pub[s]) : sm.t_pub[s];
-                        pf[0] += now > rdy ? now - rdy : 0ull;  // ready -> MMAs issued and committed
-                        pf[1] += (unsigned long long)t_seen > rdy ? (unsigned long long)t_seen - rdy : 0ull;
-                        pf[2] += 1;
-                        pf[3] += now - (unsigned long long)ti0;  // the issue itself
-                        sm.t_iss[t][ts] = now;
-                    }
+                    if (lane == 0) sm.t_iss[t][ts] = (unsigned long long)clock64();
 #endif
                 } else if (lane == 0) {
                     ptx::mbar_arrive(&sm.tfull[t][ts]);
                 }
                 __syncwarp();
-                cg[t] = c + 1;
-                if (hseq < 0) {
-                    ended[t] = true;
-                    ++n_done;
+                if (lane == t) {
+                    my_c = c + 1;
+                    if (hseq < 0) my_end = true;
                 }
-                did = true;
-            }
-            if (did) {
-                idle0 = clock64();
-                backoff = kMmaSleep0;
-            } else {
-                // idle: back off exponentially so the polls do not take issue slots from the
-                // epilogue warps of this SMSP (the MMA warp has the highest arbitration rank)
-                __nanosleep(backoff);
-                backoff = backoff < kMmaSleepCap ? 2 * backoff : backoff;
-                if (clock64() - idle0 > 4000000000ll) ptx::watchdog_trap("mma/idle", (int)cg[0], n_done);
+#ifdef TGS_MMA_DELAY
+                __nanosleep(TGS_MMA_DELAY);  // experiment: MMA-issue latency sensitivity
+#endif
             }
         }
         if (lane == 0) {

@@ -64,13 +64,7 @@ constexpr int kSS = 4;      // shared-memory chunk ring (slack between member ti
 constexpr int kTS = 2;      // TMEM accumulator stages per warpgroup
 constexpr int kJB = 16;     // accumulator columns per epilogue batch
 constexpr int kRing = 8;    // producer gather ring: kRing - 2 batches of records in flight
-#ifndef TGS_MMA_SLEEP0
-#define TGS_MMA_SLEEP0 16
-#endif
-#ifndef TGS_MMA_SLEEPCAP
-#define TGS_MMA_SLEEPCAP 128
-#endif
-constexpr uint32_t kMmaSleep0 = TGS_MMA_SLEEP0, kMmaSleepCap = TGS_MMA_SLEEPCAP;  // MMA warp back-off (ns) when idle
+constexpr uint32_t kMmaSleep0 = 16, kMmaSleepCap = 128;  // MMA warp back-off (ns) when nothing is ready
 #ifndef TGS_RASTER_PROF
 #define TGS_RASTER_PROF 0
 #endif
@@ -669,9 +663,6 @@ __global__ void __launch_bounds__(Cfg<SLOTS>::kThreads, Cfg<SLOTS>::kCtasPerSm) 
                     my_c = c + 1;
                     if (hseq < 0) my_end = true;
                 }
-#ifdef TGS_MMA_DELAY
-                __nanosleep(TGS_MMA_DELAY);  // experiment: MMA-issue latency sensitivity
-#endif
             }
         }
         if (lane == 0) {

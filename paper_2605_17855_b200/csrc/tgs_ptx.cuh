@@ -47,9 +47,6 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
 
 // Bounded wait: a deadlock (a protocol bug) must become a reported kernel error, never a hung
 // GPU.  After ~4e9 cycles (~2 s) the waiter prints where it is stuck and traps.
-#ifndef TGS_WAIT_NS
-#define TGS_WAIT_NS 0  // extra back-off between failed waits (0: none)
-#endif
 #ifndef TGS_MBAR_HINT_NS
 #define TGS_MBAR_HINT_NS 20000
 #endif
@@ -94,10 +91,7 @@ __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, con
         const long long t0 = clock64();
         for (;;) {
             bool ok = false;
-            for (int i = 0; i < 4096 && !ok; ++i) {
-                if (TGS_WAIT_NS) __nanosleep(TGS_WAIT_NS);
-                ok = mbar_try(bar, parity);
-            }
+            for (int i = 0; i < 4096 && !ok; ++i) ok = mbar_try(bar, parity);
             if (ok) break;
             if (clock64() - t0 > 4000000000ll) watchdog_trap(what, a0, a1);
         }

@@ -12,7 +12,7 @@
 //   pass   : one kernel per digit.  Tiles are claimed in order from a counter; each tile ranks its
 //            items stably (per-warp __match_any_sync against running digit counters, warps
 //            ordered by a per-digit prefix), publishes its per-digit totals, resolves its global
-//            per-digit offsets by decoupled look-back over earlier tiles (8 predecessors per
+//            per-digit offsets by decoupled look-back over earlier tiles (2 predecessors per
 //            round trip), sorts the tile by digit in shared memory and writes every digit run as
 //            one contiguous burst.
 // (Reduce-then-scan over the same tiles measured slower: 0.27 vs 0.21 ms for the 3M presort.)
@@ -38,15 +38,8 @@ constexpr int kRadix = 256;
 #define TGS_SWEEP_BLOCKS 3
 #endif
 constexpr int kSweepBlocks = 148 * TGS_SWEEP_BLOCKS;  // persistent one-sweep blocks
-#ifndef TGS_SORT_NOLB
-#define TGS_SORT_NOLB 0  // timing experiment only: no look-back (wrong offsets)
-#endif
-#ifndef TGS_SORT_NS
-#define TGS_SORT_NS 20  // look-back back-off (ns) when no predecessor has published
-#endif
-#ifndef TGS_SORT_WIN
-#define TGS_SORT_WIN 2  // look-back predecessors read per round trip (1-32 measured: 2 best)
-#endif
+constexpr unsigned kLookbackSleepNs = 20;  // look-back back-off when no predecessor has published
+constexpr int kLookbackWin = 2;  // predecessors read per look-back round trip (1-32 measured: 2 best)
 
 
 constexpr uint32_t kFlagAgg = 1u << 30;  // look-back status: tile aggregate published
@@ -225,8 +218,8 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
         // look-back: sum earlier tiles' digit-d counts until one with an inclusive prefix, reading
         // kWin predecessors per round trip (independent loads)
         uint32_t prefix = 0;
-        if (tile > 0 && !TGS_SORT_NOLB) {
-            constexpr int kWin = TGS_SORT_WIN;
+        if (tile > 0) {
+            constexpr int kWin = kLookbackWin;
             int j = (int)tile - 1;
             const long long w0 = clock64();
             for (;;) {
@@ -250,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
                 if (done) break;
                 j -= used;
                 if (used == 0) {
-                    __nanosleep(TGS_SORT_NS);
+                    __nanosleep(kLookbackSleepNs);
                     if (clock64() - w0 > 4000000000ll) {  // bounded wait: report, never hang
                         printf("radix look-back stuck: pass %d tile %u waits on %d\n", pass, tile, j);
                         __trap();

@@ -10,7 +10,7 @@
 // One-sweep passes (8-bit digits, tiles of 3072 items):
 //   digits : one kernel reads the keys once and builds the histograms of every pass;
 //   pass   : one kernel per digit.  Tiles are claimed in order from a counter; each tile ranks its
-//            items stably (per-warp __match_any_sync against running digit counters, warps
+//            items stably (per-warp digit peers from 8 ballots against running digit counters, warps
 //            ordered by a per-digit prefix), publishes its per-digit totals, resolves its global
 //            per-digit offsets by decoupled look-back over earlier tiles (2 predecessors per
 //            round trip), sorts the tile by digit in shared memory and writes every digit run as

@@ -271,7 +271,7 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
     ctx->row_chunks = bin_row_chunks(gg, ctx->rc_key == (ukey ^ (uint64_t)(uintptr_t)scene) ? ctx->rc_entries : 0u);
     ctx->rc_pending_key = ukey ^ (uint64_t)(uintptr_t)scene;
     const size_t h1 = bin_hist1_elems(gg, ctx->row_chunks), h2 = bin_hist2_elems(gg, cap), hm = bin_meta_elems(gg);
-    TGS_CUDA_OK(ctx->hist.ensure((h1 + h2 + hm + bin_segmap_elems(gg, cap)) * 4));
+    TGS_CUDA_OK(ctx->hist.ensure((h1 + h2 + hm + bin_segmap_elems(gg, cap) + bin_slicecum_elems(gg, cap)) * 4));
     TGS_CUDA_OK(ctx->rowlist.ensure((size_t)cap * sizeof(uint2)));
     TGS_CUDA_OK(ctx->bsum.ensure(
         std::max({scan_tmp_elems(h1), scan_tmp_elems(h2), scan_tmp_elems(sort_scratch_elems((size_t)n_alloc))}) * 4));
@@ -429,6 +429,7 @@ tgs_status record_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera* 
     ba.hist2 = ba.hist1 + h1;
     ba.meta = ba.hist2 + h2;
     ba.segmap = ba.meta + bin_meta_elems(gg);
+    ba.slicecum = ba.segmap + bin_segmap_elems(gg, std::max<uint32_t>(ctx->capacity, 1u));
     ba.rowidx = ctx->rowlist.as<uint32_t>();
     ba.rowxp = ba.rowidx + std::max<uint32_t>(ctx->capacity, 1u);  // the buffer holds 2 x max(capacity, 1) words
     ba.bsum = ctx->bsum.as<uint32_t>();

@@ -383,16 +383,38 @@ __global__ void __launch_bounds__(kBinWarps * 32) cols_count_kernel(BinArgs a) {
         const uint32_t e0 = rowstart[y] + s * seg, e1 = min(rowstart[y + 1], e0 + seg);
         for (int i = lane; i <= gx; i += 32) D[i] = 0;
         __syncwarp();
-        for (uint32_t eb = e0 + lane; eb < e1; eb += 32 * 8) {  // 8 loads in flight per lane
-            uint32_t xp[8];
+        // slice by slice (the placement warps' shares): after slice w < kBinWarps - 1 the running
+        // per-column counts are the start of warp w + 1's part of every column run
+        const uint32_t sl = slice_len((gx + 31) / 32);
+        for (int w = 0; w < kBinWarps; ++w) {
+            const uint32_t s0 = min(e1, e0 + (uint32_t)w * sl), s1 = min(e1, s0 + sl);
+            for (uint32_t eb = s0 + lane; eb < s1; eb += 32 * 8) {  // 8 loads in flight per lane
+                uint32_t xp[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) xp[u] = eb + 32u * u < e1 ? __ldg(&a.rowxp[eb + 32u * u]) : 0xffffffffu;
+                for (int u = 0; u < 8; ++u) xp[u] = eb + 32u * u < s1 ? __ldg(&a.rowxp[eb + 32u * u]) : 0xffffffffu;
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (xp[u] != 0xffffffffu) {
-                    atomicAdd(&D[xp[u] & 0xffffu], 1);
-                    atomicAdd(&D[(xp[u] >> 16) + 1], -1);
+                for (int u = 0; u < 8; ++u)
+                    if (xp[u] != 0xffffffffu) {
+                        atomicAdd(&D[xp[u] & 0xffffu], 1);
+                        atomicAdd(&D[(xp[u] >> 16) + 1], -1);
+                    }
+            }
+            __syncwarp();
+            if (w + 1 < kBinWarps) {
+                uint32_t* cum = a.slicecum + ((size_t)q * (kBinWarps - 1) + (size_t)w) * (size_t)gx;
+                int run = 0;
+                for (int base = 0; base < gx; base += 32) {
+                    const int x = base + lane;
+                    int incl = x < gx ? D[x] : 0;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += t;
+                    }
+                    if (x < gx) cum[x] = (uint32_t)(run + incl);
+                    run += __shfl_sync(0xffffffffu, incl, 31);
                 }
+            }
         }
         __syncwarp();
         int carry = 0;
@@ -451,8 +473,8 @@ __global__ void __launch_bounds__(kBinWarps * 32, KC <= 4 ? 5 : 1) cols_place_ke
     constexpr uint32_t kSliceLen = slice_len(KC), kSegLen = seg_len_kc(KC);
     constexpr int kPer = kSliceLen / 32;  // row entries per lane
     constexpr int kStage2 = stage2_entries(KC);
-    // [kStage2] output | [kBinWarps][gx + 1] slice counts | [kBinWarps][gx + 1] column records
-    // (running position, mask of this batch's lanes) — one 8-byte load serves the slot formula
+    // [kStage2] output | [kBinWarps][gx + 1] column records (running position, mask of this
+    // batch's lanes) — one 8-byte load serves the slot formula
     extern __shared__ uint32_t sout[];
     if (a.fc->overflow) return;
     const int rows = a.gg.band_gy1 - a.gg.band_gy0, gx = a.gg.groups_x;
@@ -462,9 +484,7 @@ __global__ void __launch_bounds__(kBinWarps * 32, KC <= 4 ? 5 : 1) cols_place_ke
     const uint32_t* nsegp = a.meta + rows + 1;
     const uint32_t* rowbase2 = a.meta + 2 * rows + 2;
     const uint32_t nq = nsegp[rows], h2 = rowbase2[rows], total = a.fc->n_entries;
-    int* cntw = reinterpret_cast<int*>(sout + kStage2);
-    int* D = cntw + wib * (gx + 1);
-    uint2* cm = reinterpret_cast<uint2*>(cntw + kBinWarps * (gx + 1)) + wib * (gx + 1);
+    uint2* cm = reinterpret_cast<uint2*>(sout + kStage2) + wib * (gx + 1);
     const uint32_t out0 = smem_u32(sout), cm0 = smem_u32(cm);
     auto h2at = [&](uint32_t i) { return i < h2 ? a.hist2[i] : total; };
     // the segment's group row comes from cols_count's map, loaded one segment ahead
@@ -485,46 +505,22 @@ __global__ void __launch_bounds__(kBinWarps * 32, KC <= 4 ? 5 : 1) cols_place_ke
             base[k] = x < gx ? h2at(i0) : 0u;
             len[k] = x < gx ? h2at(i0 + 1) : 0u;
         }
-        // this warp's slice, loaded once: per-column counts (difference array -> prefix)
+        // this warp's slice, loaded once; its start in every column run is cols_count's running
+        // count after the earlier slices (no per-block counting, no barrier)
         uint2 ent[kPer];
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {
             const uint32_t e = e0 + lane + 32u * i;
             ent[i] = e < e1 ? make_uint2(__ldg(&a.rowidx[e]), __ldg(&a.rowxp[e])) : make_uint2(0u, 0u);
         }
-        for (int i = lane; i <= gx; i += 32) D[i] = 0;
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < kPer; ++i)
-            if (e0 + lane + 32u * i < e1) {
-                atomicAdd(&D[ent[i].y & 0xffffu], 1);
-                atomicAdd(&D[(ent[i].y >> 16) + 1], -1);
-            }
-        __syncwarp();
-        {
-            int run = 0;
-            for (int b0 = 0; b0 < gx; b0 += 32) {
-                const int x = b0 + lane;
-                int incl = x < gx ? D[x] : 0;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += t;
-                }
-                if (x < gx) D[x] = run + incl;
-                run += __shfl_sync(0xffffffffu, incl, 31);
-            }
-        }
-        __syncthreads();
+        const uint32_t* cum = a.slicecum + ((size_t)q * (kBinWarps - 1) + (size_t)(wib - 1)) * (size_t)gx;
         // local start P of every column run; this warp's part starts off after earlier warps'
         uint32_t P[KC], off[KC], carry = 0;
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
             const int x = lane + 32 * k;
             len[k] -= base[k];
-            off[k] = 0u;
-            if (x < gx)
-                for (int w = 0; w < wib; ++w) off[k] += (uint32_t)cntw[w * (gx + 1) + x];
+            off[k] = (wib > 0 && x < gx) ? __ldg(&cum[x]) : 0u;
             uint32_t incl = len[k];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -825,6 +821,9 @@ size_t bin_hist2_elems(const GroupGeom& gg, uint32_t capacity) {
     return (size_t)gg.groups_x * (rows + capacity / seg_len_gx(gg.groups_x) + 1);
 }
 size_t bin_meta_elems(const GroupGeom& gg) { return 4 * (size_t)(gg.band_gy1 - gg.band_gy0 + 1) + 1; }
+size_t bin_slicecum_elems(const GroupGeom& gg, uint32_t capacity) {
+    return bin_segmap_elems(gg, capacity) * (size_t)(kBinWarps - 1) * (size_t)gg.groups_x;
+}
 size_t bin_segmap_elems(const GroupGeom& gg, uint32_t capacity) {
     return (size_t)std::max(1, gg.band_gy1 - gg.band_gy0) + capacity / seg_len_gx(gg.groups_x) + 1;
 }
@@ -876,8 +875,8 @@ void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st) {
     offsets_kernel<<<(gg.n_groups_band + 256) / 256, 256, 0, st>>>(a);
     const int kc = (gx + 31) / 32, t2 = kBinWarps * 32;
     // output stage + column ids, column bias, per-warp slice counts / column positions / masks
-    // output stage, per-warp slice counts / column positions / masks
-    const size_t so = (size_t)stage2_entries(kc) * sizeof(uint32_t) + (size_t)3 * kBinWarps * (gx + 1) * sizeof(int);
+    // output stage, per-warp column records
+    const size_t so = (size_t)stage2_entries(kc) * sizeof(uint32_t) + (size_t)kBinWarps * (gx + 1) * sizeof(uint2);
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)so);
         kern<<<qblocks, t2, so, st>>>(a);

@@ -68,6 +68,8 @@ struct BinArgs {
     uint32_t* offsets;           // [n_groups_band + 1]
     uint32_t* list;              // [capacity] output entries (splat indices)
     uint32_t* segmap;            // [bin_segmap_elems] level-2 segment -> group row (cols_count -> cols_place)
+    uint32_t* slicecum;          // [bin_slicecum_elems] per segment and column: entries of slices 0..w
+                                 // (w < kBinWarps - 1) — each placement warp's start in the column run
     FrameCounters* fc;
     uint32_t capacity;
 };
@@ -77,6 +79,7 @@ int bin_row_chunks(const GroupGeom& gg, uint64_t row_entries);
 size_t bin_hist1_elems(const GroupGeom& gg, int row_chunks);
 size_t bin_hist2_elems(const GroupGeom& gg, uint32_t capacity);
 size_t bin_segmap_elems(const GroupGeom& gg, uint32_t capacity);
+size_t bin_slicecum_elems(const GroupGeom& gg, uint32_t capacity);
 size_t bin_meta_elems(const GroupGeom& gg);
 void launch_binning(const BinArgs& a, int max_visible, cudaStream_t st);
 // In-place exclusive scan of n u32 (one pass, decoupled look-back); tmp holds scan_tmp_elems(n)

@@ -67,10 +67,18 @@ def _full_frame_parity(gsr, ctx, port, rec, c, tag):
     images = {}
     for backend, group in ((1, 2), (0, 1)):
         if group == 1:
-            # later frames of the same geometry size their level-1 chunks from the previous one's
-            # row entries (C3 at G=1: 2-4x the default): frame 2 runs eagerly with the new chunk
-            # count, frame 3 is captured into the frame graph, frame 4 (checked below) replays it
-            for _ in range(3):
+            # The first frame of a geometry uses the default level-1 chunks, whose blocks overflow
+            # their stage at C3 G=1 (the direct-to-global path): its lists are checked here.  Later
+            # frames size the chunks from the previous frame's row entries (2-4x the default):
+            # frame 2 runs eagerly, frame 3 is captured into the frame graph, frame 4 (checked
+            # below) replays it.
+            ctx.render(ds, cam, _opt(gsr, backend, group))
+            ent_p1, off_p1, _ = port.bin_sort_fast(pp, w, h, group)
+            ent1, off1 = ctx.read_lists(len(off_p1) - 1)
+            assert np.array_equal(off1, off_p1) and np.array_equal(ent1.view(np.uint8), ent_p1.view(np.uint8)), \
+                f"{tag} g1 first-frame lists"
+            del ent1, ent_p1
+            for _ in range(2):
                 ctx.render(ds, cam, _opt(gsr, backend, group))
         res = ctx.render(ds, cam, _opt(gsr, backend, group))
         images[(backend, group)] = res.image.rgb.copy()

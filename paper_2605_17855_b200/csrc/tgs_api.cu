@@ -297,6 +297,9 @@ tgs_status enqueue_frame(tgs_ctx* ctx, const tgs_scene* scene, const tgs_camera*
                            feedback ? 1 : 0,
                            ctx->capacity, (long long)ctx->proj_cap, ctx->row_chunks);
     // ... and every buffer address the captured launches bake in (buffers only ever grow)
+    // (the scene's device planes too: a scene freed and another uploaded at the same host address
+    // must not replay launches that point at the old planes)
+    kl += std::snprintf(kbuf + kl, sizeof(kbuf) - (size_t)kl, " %p %d", scene->planes.p, scene->sh_degree);
     const DBuf* fbufs[] = {&ctx->proj, &ctx->pre_keys[0], &ctx->pre_keys[1], &ctx->pre_vals[0], &ctx->pre_vals[1],
                            &ctx->rect, &ctx->rrect, &ctx->list, &ctx->rowlist, &ctx->hist, &ctx->bsum, &ctx->ghist,
                            &ctx->offsets, &ctx->order, &ctx->ucost, &ctx->image};

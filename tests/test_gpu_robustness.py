@@ -212,6 +212,29 @@ def test_graph_frames_identical_to_eager(gsr, port):
         e.close()
 
 
+def test_graph_not_replayed_for_a_new_scene(gsr, port):
+    """A scene freed after its frames were captured into the frame graph, and another scene of the
+    same size uploaded (possibly at the same host address), must not replay launches that point at
+    the freed planes: every frame equals a fresh context's render of the scene it was given."""
+    cam = gsr.orbit_cameras(16, 320, 240)[3]
+    opt = gsr.RenderOptions(gsr.Backend.tensor, gsr.PrecisionMode.fp32, 2)
+    g, ref = gsr.Context(0), gsr.Context(0)
+    try:
+        for seed in (41, 42, 43):
+            rec = port.gen_scene(seed, 5000, 1.0, 0.01, 0.06, 0)
+            ds = g.upload(rec)
+            frames = [g.render(ds, cam, opt).image.rgb.copy() for _ in range(3)]  # eager, capture, replay
+            ds.free()
+            dr = ref.upload(rec)
+            want = ref.render(dr, cam, opt).image.rgb
+            dr.free()
+            for i, img in enumerate(frames):
+                assert np.array_equal(img.view(np.uint32), want.view(np.uint32)), (seed, i)
+    finally:
+        g.close()
+        ref.close()
+
+
 def test_encode_u8_matches_reference_ppm(gsr, port):
     """tgs_encode_u8 (the device PPM payload) equals the reference's encode_ppm bytes
     (scene_io.cpp:253-263: clamp, lrintf(v * 255)) for a rendered frame and for edge values."""

@@ -32,15 +32,19 @@
 //                    list order), writes unit-centred coefficient rows + blend data into a ring of
 //                    kSS shared-memory chunk stages;
 //   warpgroups:      one per member tile (4 warps = the 4 TMEM lane quadrants).  A member tile is
-//                    two M=128 tiles (its left and right 8-column halves); warp q of the group owns
-//                    rows 4q..4q+3 of the tile, i.e. lane quadrant q of both M-tiles: 2 pixels per
-//                    thread.  Each warpgroup has its own 2-stage TMEM accumulator ring and its own
+//                    two M=128 tiles; warp q of the group owns lane quadrant q of both, which is
+//                    the tile's 8x8 pixel block q (lane_pixel): 2 pixels per thread, blended
+//                    together with packed FP32x2 instructions, and a packed-FADD2 mask phase picks
+//                    the splats of each 16-splat batch that reach any of the warp's pixels.  Each
+//                    warpgroup has its own 2-stage TMEM accumulator ring and its own
 //                    commit barriers, so member tiles progress independently through the shared
 //                    chunk ring (up to kSS chunks apart) and only the 4 warps of one tile advance
 //                    in lock-step;
-//   MMA warp:        TMEM owner; per (warpgroup, chunk) two tcgen05.mma (M=128, N=32, K=16) into
-//                    the group's free TMEM stage, issued from warp-uniform code by an elected lane,
-//                    then tcgen05.commit -> that group's barrier.  Retired tiles get no MMA.
+//   MMA warp:        TMEM owner; lane t polls warpgroup t (chunk published, TMEM stage free) so one
+//                    ballot finds every ready group; per (warpgroup, chunk) two tcgen05.mma
+//                    (M=128, N=32, K=16) into the group's free TMEM stage, issued from warp-uniform
+//                    code by an elected lane, then tcgen05.commit -> that group's barrier.  Retired
+//                    tiles get no MMA.
 // The pixel operand A is identical for every unit and built once per CTA.  Hand-offs: full[s]
 // (mbarrier, producer -> MMA), tfull[t][ts] (tcgen05.commit, MMA -> warpgroup t), and release
 // counters compared against absolute chunk targets (done_cnt: smem stage; wdone: TMEM stage);

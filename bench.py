@@ -123,7 +123,7 @@ class ClockSampler:
                 "samples": len(self.samples), "source": "nvml" if self._nv else "nvidia-smi"}
 
 
-def cpu_reference_frame(rec, cam_ns, group, backend, n_bands=1, band_first=0, band_count=None):
+def cpu_reference_frame(rec, cam_ns, group, backend, n_bands=1, band_first=0, band_count=None, image=None):
     """The reference's CPU path on this host through its own stage API (oracle/_ref, all host
     threads): project_scene ONCE, then build_group_entries / sort_entries / rasterize_* per
     horizontal band of group rows (n_bands = 1: the whole frame, exactly render.cpp:7-35).
@@ -133,8 +133,8 @@ def cpu_reference_frame(rec, cam_ns, group, backend, n_bands=1, band_first=0, ba
     ref = Ref()
     workers = ref.hardware_concurrency()
     band_count = n_bands if band_count is None else band_count
-    rows, ms_proj, bands = ref.time_bands(rec, cam_ns, n_bands, band_first, band_count, backend=backend,
-                                          group_size=group, workers=workers)
+    rows, ms_proj, bands = ref.time_bands(rec, cam_ns, n_bands, band_first, band_count, image=image,
+                                          backend=backend, group_size=group, workers=workers)
     frac = rows / cam_ns.height
     sec = (ms_proj * frac + sum(sum(b) for b in bands)) / 1e3
     return frac, sec, workers
@@ -514,6 +514,7 @@ def main():
     # ---- CPU baseline: the reference's own CPU path on this host (rank 0, N=1): one whole
     # frame of the bench camera path through its stage API (render.cpp:7-35), all host threads --
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:
         try:
             from oracle.oracle import Ref
@@ -522,11 +523,22 @@ def main():
                 c = mine[args.warmup]
                 cns = SimpleNamespace(view=c.view, focal_x=c.focal_x, focal_y=c.focal_y, width=W, height=H,
                                       near=c.near, far=c.far)
-                fr, sec, workers = cpu_reference_frame(scene.records, cns, 2, 1)
+                ref_img = np.zeros((H, W, 3), np.float32)
+                fr, sec, workers = cpu_reference_frame(scene.records, cns, 2, 1, image=ref_img)
                 cpu = {"value": fr / sec, "unit": "frames/s", "cores": workers, "kind": "reference",
                        "sample": "one whole 3M/1080p orbit frame (G=2 tensor fp32) through the reference stage "
                                  "API (oracle/_ref: project_scene, build_group_entries, sort_entries, "
                                  "rasterize_groups_tensor), steady_clock per stage"}
+                # the same frame through our path (after every timed region): image parity against
+                # the reference's fp32 image, with the tolerance the tests use
+                ours = np.asarray(ctx.render(ds, c, opt_t).image.rgb, np.float32).reshape(H, W, 3)
+                diff = np.abs(ours.astype(np.float64) - ref_img.astype(np.float64))
+                mse = float(np.mean(diff ** 2))
+                psnr = 10.0 * math.log10(1.0 / mse) if mse > 0 else float("inf")
+                parity = {"camera": args.warmup % N_CAMS, "max_abs": float(diff.max()), "mean_abs": float(diff.mean()),
+                          "psnr_db": psnr, "tolerance": "max_abs <= 2/255, psnr >= 50 dB",
+                          "pass": bool(diff.max() <= 2.0 / 255.0 and psnr >= 50.0),
+                          "against": "oracle/_ref (the reference compiled here) fp32 image of the same frame"}
         except Exception as e:  # reported, never fatal for the GPU number
             cpu = {"value": None, "unit": "frames/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
@@ -548,7 +560,7 @@ def main():
                                 "speedup": speedup_nc},
         "stage_ms": st_t, "baseline_stage_ms": st_s,
         "roofline": roof, "stage_roofline": stage_roofline,
-        "cpu_baseline": cpu, "e2e": e2e,
+        "cpu_baseline": cpu, "e2e": e2e, "parity_vs_reference": parity,
         "clocks": clk_sum, "gpu_launches": launches_per_frame * args.steps,
     }
     if rank == 0:

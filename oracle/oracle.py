@@ -287,9 +287,10 @@ class Ref(_Base):
             raise ValueError(self.last_error())
         return int(n), dict(zip(("project", "bin", "sort", "raster"), ms.tolist()))
 
-    def time_bands(self, rec, cam, n_bands, band_first, band_count, **opt):
+    def time_bands(self, rec, cam, n_bands, band_first, band_count, image=None, **opt):
         """project_scene once, then bin/sort/raster per band (gref_time_bands):
-        (image rows covered, project ms, [(bin, sort, raster) ms per band])."""
+        (image rows covered, project ms, [(bin, sort, raster) ms per band]).  `image` (optional,
+        float32 H x W x 3, C-contiguous) receives the rendered bands' rows (copied after timing)."""
         rec = np.ascontiguousarray(rec, dtype=np.float32)
         deg = 3 if rec.shape[1] == 59 else 0
         ms = np.zeros(1 + 3 * band_count, dtype=np.float64)
@@ -297,7 +298,7 @@ class Ref(_Base):
         f.restype = C.c_int64
         rows = f(_f32p(rec), C.c_int64(len(rec)), C.c_int(deg), C.byref(make_camera(cam)),
                  C.byref(make_options(**opt)), C.c_int(n_bands), C.c_int(band_first), C.c_int(band_count),
-                 ms.ctypes.data_as(C.c_void_p))
+                 ms.ctypes.data_as(C.c_void_p), None if image is None else _f32p(image))
         if rows < 0:
             raise ValueError(self.last_error())
         return int(rows), float(ms[0]), [tuple(ms[1 + 3 * b: 4 + 3 * b]) for b in range(band_count)]

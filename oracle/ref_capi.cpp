@@ -343,7 +343,7 @@ std::int64_t gref_time_stages(const float* rec, std::int64_t n, int deg, const C
 // bin, sort, raster}.  Returns the sum of the timed bands' image rows.  Each band copies and
 // shifts the projected list (untimed), exactly like gref_time_stages.
 std::int64_t gref_time_bands(const float* rec, std::int64_t n, int deg, const CCamera* cam, const COptions* opt,
-                             int n_bands, int band_first, int band_count, double* ms) {
+                             int n_bands, int band_first, int band_count, double* ms, float* img) {
     try {
         const auto scene = to_scene(rec, n, deg);
         const gsr::RenderOptions o = to_opt(opt);
@@ -373,17 +373,20 @@ std::int64_t gref_time_bands(const float* rec, std::int64_t n, int deg, const CC
             const auto lists = gsr::sort_entries(std::move(entries), cfg);
             m[1] = ms_since(t0);
             t0 = std::chrono::steady_clock::now();
+            gsr::ImageBuffer band;
             if (o.backend == gsr::Backend::scalar) {
-                auto img = gsr::rasterize_tiles_scalar(lists, pr, cfg, o.constants, o.mode, o.workers);
+                band = gsr::rasterize_tiles_scalar(lists, pr, cfg, o.constants, o.mode, o.workers);
             } else {
                 gsr::TensorRasterOptions t;
                 t.constants = o.constants;
                 t.mode = o.mode;
                 t.chunk_len = o.chunk_len;
                 t.workers = o.workers;
-                auto img = gsr::rasterize_groups_tensor(lists, pr, cfg, t);
+                band = gsr::rasterize_groups_tensor(lists, pr, cfg, t);
             }
             m[2] = ms_since(t0);
+            // optional (untimed): the band's rows of the frame image, for a parity check by the caller
+            if (img) std::copy(band.rgb.begin(), band.rgb.end(), img + static_cast<size_t>(y0) * c.width * 3);
         }
         return rows;
     } catch (const gsr::ValidationError& e) {
